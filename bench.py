@@ -1,0 +1,445 @@
+"""Benchmark: Ulysses attention layer (fwd+bwd) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N)
+
+Workload (BASELINE.json): at N = 1, config 2 -- local attention fwd+bwd of
+one GPT-1.3B layer shape (16 heads x 128), N = 8192 tokens, bf16, causal.
+At N > 1 the same layer runs as a Ulysses group of N ranks with the sequence
+scaled with the group (N_seq = 8192 * P, weak scaling in the paper's sense:
+tokens per GPU fixed); the seq->head / head->seq exchanges run on the
+peer-memory kernels (csrc/a2a.cu), no NCCL on the data path.
+
+One JSON line on rank 0.  `value` = tokens/s of the whole job with inputs
+resident in HBM (device time from CUDA events, max over ranks; L2 flushed
+before every timed step).  `e2e` = the same through the public API from
+pinned host buffers (H2D q,k,v,dO + D2H of the loss scalar every step).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEQ_PER_GPU = 8192
+HEADS = 16
+HEAD_DIM = 128
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    try:
+        with open(MEASURED_PEAKS) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return FALLBACK_PEAKS, "fallback"
+
+
+def attn_flops(n_seq, heads, hd, causal=True):
+    """fwd 4*H*N^2*hd*c, bwd 8*H*N^2*hd*c, c = 1/2 causal."""
+    c = 0.5 if causal else 1.0
+    return 4.0 * heads * n_seq * n_seq * hd * c, 8.0 * heads * n_seq * n_seq * hd * c
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle restatement of the reference algorithm
+# ---------------------------------------------------------------------------
+
+def _cpu_sample_worker(args):
+    n_s, hd, seed = args
+    import numpy as np
+    from oracle import ulysses_oracle as O
+    q, k, v, do = (O.make_tensor((n_s, 1, hd), seed, s) for s in (1, 2, 3, 4))
+    t0 = time.perf_counter()
+    scale = 1.0 / math.sqrt(hd)
+    O.attention_head(q, k, v, "causal", scale)               # kernels.py:31-52 (fixed-order matmul)
+    O.attention_head_backward(q, k, v, do, "causal", scale)  # kernels.py:89-111
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(n_seq, heads, hd, procs=1, n_sample=1024):
+    """Time the reference algorithm (oracle port, fixed-order f64 matmul) on
+    `procs` host processes, one head of N=n_sample each, and extrapolate by
+    N^2 * hd * heads to the full workload (the reference is O(N^2 hd) per head
+    with full n x n scores, kernels.py:37)."""
+    import multiprocessing as mp
+    if procs <= 1:
+        dt = _cpu_sample_worker((n_sample, hd, 0))
+        per_head = dt
+        wall = dt
+    else:
+        ctx = mp.get_context("fork")
+        with ctx.Pool(procs) as pool:
+            t0 = time.perf_counter()
+            pool.map(_cpu_sample_worker, [(n_sample, hd, i) for i in range(procs)])
+            wall = time.perf_counter() - t0
+        per_head = wall / procs            # throughput-equivalent seconds per sampled head
+    scale = (n_seq / n_sample) ** 2 * heads
+    t_full = per_head * scale
+    return {"tokens_per_s": n_seq / t_full, "seconds_full_extrapolated": t_full, "sample_wall_s": wall,
+            "sample": f"{procs} x causal fwd+bwd head of N={n_sample}, hd={hd} (f64, reference fixed-order "
+                      f"matmul); extrapolated by N^2*hd*heads to N={n_seq}, {heads} heads"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2309_14509_b200 as U
+    from paper_2309_14509_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P = world
+    n_seq = args.seq if args.seq else SEQ_PER_GPU * P
+    H, hd = args.heads, HEAD_DIM
+    nl = n_seq // P
+    causal = True
+
+    # synthetic inputs: N(0,1), seed 2024, per-rank contiguous shard
+    g = torch.Generator(device=dev)
+    g.manual_seed(2024 + rank)
+    mk = lambda: torch.randn((nl, 1, H, hd), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    q, k, v, do = mk(), mk(), mk(), mk()
+    if P > 1:
+        slot = 3 * nl * H * hd * 2 + (1 << 20)
+        group = U.SequenceGroup.from_process_group(None, slot_bytes=slot, device=local_rank)
+    else:
+        group = U.SequenceGroup.single(local_rank)
+    attn = U.FlashAttention("causal")
+    layer = U.DistributedAttention(attn, group)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def step(qq, kk, vv, dd):
+        qq.requires_grad_(True)
+        kk.requires_grad_(True)
+        vv.requires_grad_(True)
+        o = layer(qq, kk, vv)
+        torch.autograd.backward([o], [dd])
+        return o
+
+    # ---- device-resident timing -------------------------------------------
+    for _ in range(args.warmup):
+        step(q.detach(), k.detach(), v.detach(), do)
+    torch.cuda.synchronize()
+    if P > 1:
+        dist.barrier()
+    launches0 = _lib.total_launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        if P > 1:
+            dist.barrier()
+        for i in range(args.steps):
+            flush.zero_()                                  # untimed L2 flush
+            ev[i][0].record()
+            step(q.detach(), k.detach(), v.detach(), do)
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        if P > 1:
+            dist.barrier()
+    launches = _lib.total_launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t_ms = sum(step_ms)
+    if P > 1:
+        tt = torch.tensor([t_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    ms_per_step = t_ms / args.steps
+    tokens_per_s = n_seq / (ms_per_step / 1e3)
+    f_fwd, f_bwd = attn_flops(n_seq, H // P, hd, causal)
+    tflops_per_gpu = (f_fwd + f_bwd) / (ms_per_step / 1e3) / 1e12
+
+    # ---- per-kernel split (dominant kernel roofline) --------------------
+    kt = kernel_split(attn, q, k, v, do, args, dev)
+
+    # ---- e2e through the public API from pinned host buffers ----------
+    e2e = run_e2e(layer, q, k, v, do, args, P, dev)
+
+    pk, src = peaks()
+    result = None
+    if rank == 0:
+        dom = max(kt["kernels"], key=lambda x: x["ms"])
+        peak = pk["bf16_tflops"]
+        ach = dom["alg_flops"] / (dom["ms"] / 1e3) / 1e12
+        clocks = clk.summary()
+        result = {
+            "metric": "Ulysses attn tokens/s (fwd+bwd layer), TFLOPs/GPU, all-to-all GB/s",
+            "value": round(tokens_per_s, 1),
+            "unit": "tokens/s",
+            "n_gpus": P,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic N(0,1) q/k/v/dO, seed 2024 (no dataset)",
+            "config": {
+                "workload": ("config2: single-GPU local attention fwd+bwd, GPT-1.3B layer 16 heads x 128, "
+                             f"N={n_seq} bf16 causal" if P == 1 else
+                             f"Ulysses DistributedAttention fwd+bwd, P={P}, 16 heads x 128, N={n_seq} "
+                             f"(= {SEQ_PER_GPU} x P) bf16 causal"),
+                "seq_len": n_seq, "heads": H, "head_dim": hd, "batch": 1, "parallelism": f"ulysses-sp{P}",
+                "causal": True, "l2": "flushed (256 MB write) before every timed step, flush untimed",
+            },
+            "tflops_per_gpu": round(tflops_per_gpu, 1),
+            "tflops_per_gpu_fa_convention": round(
+                (f_fwd * 3.5) / (ms_per_step / 1e3) / 1e12, 1),
+            "roofline": {
+                "bound": "tensor", "kernel": dom["name"], "achieved": round(ach, 1),
+                "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({src}, burst)",
+                "frac_of_sustained": round(ach / pk.get("bf16_tflops_sustained", peak), 4),
+                "traffic": None,
+                "alg_flops_per_launch": dom["alg_flops"],
+                "layer_frac": round(tflops_per_gpu / peak, 4),
+            },
+            "kernels": kt["kernels"],
+            "a2a": kt.get("a2a"),
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+    if args.cpu_baseline and rank == 0:
+        cb = cpu_baseline(n_seq, H, hd, procs=1, n_sample=args.cpu_sample)
+        result["cpu_baseline"] = {"value": round(cb["tokens_per_s"], 4), "unit": "tokens/s", "cores": 1,
+                                  "kind": "port", "sample": cb["sample"],
+                                  "sample_wall_s": round(cb["sample_wall_s"], 2)}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if P > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def kernel_split(attn, q, k, v, do, args, dev):
+    """Per-kernel device time of the local attention (P = this rank's heads)
+    with CUDA events on the launching stream, L2 flushed before each."""
+    import torch
+    from paper_2309_14509_b200 import _lib
+    n, b, h, hd = q.shape[0], q.shape[1], q.shape[2], q.shape[3]
+    lib = _lib.lib()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    o = torch.empty_like(q)
+    lse = torch.empty((b, h, n), dtype=torch.float32, device=dev)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    wsb = int(lib.ul_attn_bwd_workspace_bytes(n, b, h, h, hd, 1))
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    scale = 1.0 / math.sqrt(hd)
+    names = ["attn_fwd_sm100", "attn_bwd_prep", "attn_bwd_dkdv_sm100", "attn_bwd_dq_sm100"]
+    times = {nm: [] for nm in names}
+    f_fwd, f_bwd = attn_flops(n, h, hd, True)
+    # algorithmic FLOPs credited per kernel: fwd = QK^T + PV; dkdv produces dP, dV, dK
+    # (3 of the 4 backward GEMMs, 6*N^2*hd*c); dq produces dQ (2*N^2*hd*c).
+    alg = {"attn_fwd_sm100": f_fwd, "attn_bwd_prep": 0.0, "attn_bwd_dkdv_sm100": f_bwd * 0.75,
+           "attn_bwd_dq_sm100": f_bwd * 0.25}
+
+    def run(nm):
+        if nm == "attn_fwd_sm100":
+            _lib.check(lib.ul_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(),
+                                       n, b, h, h, hd, 1, 1, scale, stream))
+        else:
+            stage = {"attn_bwd_prep": 1, "attn_bwd_dkdv_sm100": 2, "attn_bwd_dq_sm100": 4}[nm]
+            _lib.check(lib.ul_attn_bwd_stages(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                              do.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(),
+                                              dv.data_ptr(), ws.data_ptr(), wsb, n, b, h, h, hd, 1, 1, scale,
+                                              stage, stream))
+
+    reps = max(3, min(args.steps, 10))
+    for it in range(args.warmup + reps):
+        for nm in names:
+            flush.zero_()
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            run(nm)
+            e.record()
+            if it >= args.warmup:
+                times[nm].append((a, e))
+    torch.cuda.synchronize()
+    out = []
+    for nm in names:
+        ms = statistics.mean(a.elapsed_time(e) for a, e in times[nm])
+        rec = {"name": nm, "ms": round(ms, 4), "alg_flops": alg[nm]}
+        if alg[nm]:
+            rec["tflops"] = round(alg[nm] / (ms / 1e3) / 1e12, 1)
+        out.append(rec)
+    return {"kernels": out}
+
+
+def run_e2e(layer, q, k, v, do, args, P, dev):
+    import torch
+    import torch.distributed as dist
+    hq = [t.detach().cpu().pin_memory() for t in (q, k, v, do)]
+    h2d = sum(t.numel() * t.element_size() for t in hq)
+
+    def step():
+        qq, kk, vv, dd = (t.to(dev, non_blocking=True) for t in hq)
+        for t in (qq, kk, vv):
+            t.requires_grad_(True)
+        o = layer(qq, kk, vv)
+        torch.autograd.backward([o], [dd])
+        loss = (o.float() * dd.float()).sum()        # the step's scalar result
+        return loss.to("cpu", non_blocking=False)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if P > 1:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    t = s.elapsed_time(e)
+    if P > 1:
+        tt = torch.tensor([t], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    n_seq = q.shape[0] * P
+    return {"value": round(n_seq / (t / args.steps / 1e3), 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": 4, "ms_per_step": round(t / args.steps, 4),
+            "path": "DistributedAttention fwd+backward from pinned host q/k/v/dO, D2H loss scalar"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference algorithm on the host cores
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    P = world
+    n_seq = args.seq if args.seq else SEQ_PER_GPU * P
+    cores = os.cpu_count() or 1
+    procs = max(1, min(cores, 16))
+    for _ in range(args.warmup):
+        cpu_baseline(n_seq, args.heads, HEAD_DIM, procs=procs, n_sample=args.cpu_sample // 2)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(n_seq, args.heads, HEAD_DIM, procs=procs, n_sample=args.cpu_sample))
+    wall = time.perf_counter() - t0
+    tok = statistics.mean(v["tokens_per_s"] for v in vals)
+    ms_per_step = n_seq / tok * 1e3
+    res = {
+        "impl": "reference",
+        "metric": "Ulysses attn tokens/s (fwd+bwd layer), TFLOPs/GPU, all-to-all GB/s",
+        "value": round(tok, 4), "unit": "tokens/s", "n_gpus": P, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic N(0,1), seed-derived",
+        "config": {"workload": f"reference algorithm (seqlab kernels.py fixed-order f64) for N={n_seq}, "
+                               f"{args.heads} heads x {HEAD_DIM}, causal fwd+bwd", "seq_len": n_seq},
+        "cpu_baseline": {"value": round(tok, 4), "unit": "tokens/s", "cores": procs, "kind": "port",
+                         "sample": vals[0]["sample"]},
+        "e2e": {"value": round(tok, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": round(wall, 1),
+    }
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seq", type=int, default=0, help="override total sequence length")
+    ap.add_argument("--heads", type=int, default=HEADS)
+    ap.add_argument("--cpu-sample", type=int, default=1024)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,164 @@
+/*
+ * ulysses_b200.h -- C-ABI of the B200-native Ulysses sequence-parallel
+ * attention path (DeepSpeed-Ulysses, arXiv 2309.14509).
+ *
+ * Plain pointers and sizes only; no torch types.  Every entry point returns
+ * an int status (UL_OK or a negative UL_ERR_*), never throws or aborts,
+ * and is stream-ordered on the caller's cudaStream_t (passed as void*).
+ * ul_last_error() returns a thread-local message naming the offending
+ * rank / tensor / dimension, worded like the reference's exceptions.
+ *
+ * Reference interface each entry point replaces (paths relative to
+ * /root/reference/pkg/src/seqlab):
+ *
+ *   ul_all_to_all            RankContext.all_to_all          simgroup.py:453-456
+ *                            -> RankGroup._all_to_all        simgroup.py:313-335
+ *                            -> RankGroup._exchange          simgroup.py:251-304
+ *                            as used by seq_to_head / _to_head (split 2, concat 0)
+ *                            ulysses.py:104-111, 161-164 and head_to_seq /
+ *                            _to_seq (split 0, concat 2) ulysses.py:114-124, 167-169
+ *   ul_comm_*                RankGroup / RankContext identity + rendezvous
+ *                            simgroup.py:198-224, 444-451 (ranks are processes/GPUs
+ *                            here, not threads)
+ *   ul_comm_status           GroupDesyncError poisoning     simgroup.py:228-243, 265-298
+ *   ul_attn_fwd              kernel plugin kernel(q,k,v,mask,scale) -> context
+ *                            dense_kernel / causal_kernel kernels.py:43-52 over
+ *                            _masked_attention kernels.py:31-40 (plus LSE, new)
+ *   ul_attn_bwd              masked_attention_backward     kernels.py:89-111
+ *   ul_ulysses_volume        costmodel.ulysses_volume       costmodel.py:82-87
+ *
+ * Tensor layouts are the reference's sequence-major [s, b, h, hd]
+ * (ulysses.py:47-48), row-major and contiguous.
+ */
+#ifndef ULYSSES_B200_H
+#define ULYSSES_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UL_ABI_VERSION 1
+
+/* ---- status codes: one per reference exception type ------------------ */
+#define UL_OK                 0
+#define UL_ERR_DIVISIBILITY  -1  /* ShardError simgroup.py:62 / DivisibilityError tensor.py:27 */
+#define UL_ERR_DESYNC        -2  /* GroupDesyncError simgroup.py:66 (signature mismatch, timeout) */
+#define UL_ERR_KERNEL        -3  /* KernelError kernels.py:22 (mask / dtype / head_dim unsupported) */
+#define UL_ERR_STATE         -4  /* ForwardStateError ulysses.py:39 (missing LSE / shape mismatch) */
+#define UL_ERR_SHAPE         -5  /* ShapeError tensor.py:23 */
+#define UL_ERR_DEGENERATE    -6  /* DegenerateRowError tensor.py:31 */
+#define UL_ERR_CUDA          -7  /* CUDA runtime / driver failure */
+#define UL_ERR_ARG           -8  /* ValueError (bad argument) */
+
+/* ---- element types -------------------------------------------------- */
+#define UL_DTYPE_F32   0   /* fp32 mode: SIMT FFMA kernels, rtol 1e-5 vs the f64 oracle */
+#define UL_DTYPE_BF16  1   /* bf16 mode: tcgen05/TMEM/TMA kernels, fp32 accumulation */
+
+/* ---- masks (Mask.kind, tensor.py:109-149) ----------------------------- */
+#define UL_MASK_NONE   0   /* Mask.none()   -> dense_kernel  kernels.py:43-46 */
+#define UL_MASK_CAUSAL 1   /* Mask.causal() -> causal_kernel kernels.py:49-52 */
+
+#define UL_MAX_RANKS        16
+#define UL_MAX_FUSED         4   /* tensors per fused all-to-all launch (Q, K, V, ...) */
+#define UL_IPC_HANDLE_BYTES 128  /* cudaIpcMemHandle_t + workspace geometry */
+
+int         ul_abi_version(void);
+const char* ul_last_error(void);
+
+/* ======================================================================
+ * Sequence-parallel group: one process per GPU.  Each rank owns a
+ * workspace of two receive slots (ping-pong by call parity) plus per-slot
+ * signal words; peers map it through CUDA IPC (NVLink/NVSwitch P2P).
+ * ==================================================================== */
+typedef struct ul_comm ul_comm;
+
+/* Allocate this rank's workspace (2 x slot_bytes + signals) on `device`. */
+int ul_comm_create(int rank, int world, int device, size_t slot_bytes, ul_comm** out);
+/* Serialise this rank's IPC handle + geometry into handle_out[UL_IPC_HANDLE_BYTES]. */
+int ul_comm_export_handle(const ul_comm* comm, void* handle_out);
+/* Map every peer's workspace from world * UL_IPC_HANDLE_BYTES handle bytes
+ * (gathered in rank order); validates world size and slot geometry. */
+int ul_comm_open_peers(ul_comm* comm, const void* all_handles);
+/* In-process group (one process driving `world` comms on one device, each
+ * on its own stream): wires peer pointers directly.  Used by the 1-GPU
+ * parity tests so the same kernels run at P = 2/4/8. */
+int ul_comm_link_local(ul_comm* const* comms, int world);
+int ul_comm_destroy(ul_comm* comm);
+int ul_comm_rank(const ul_comm* comm);
+int ul_comm_world(const ul_comm* comm);
+size_t ul_comm_slot_bytes(const ul_comm* comm);
+/* Bound on every device-side flag wait; a timeout is reported as
+ * UL_ERR_DESYNC ("timeout in collective ... waiting on ranks [...]"). */
+int ul_comm_set_timeout_ms(ul_comm* comm, int64_t ms);
+/* Asynchronous error word (written by the device into mapped host memory):
+ * UL_OK, or UL_ERR_DESYNC with a message naming the peer, the call label
+ * and both signatures (simgroup.py:265-276).  Cleared by reading. */
+int ul_comm_status(ul_comm* comm, char* msg, size_t msg_len);
+/* Per-rank egress bytes / calls metered by this comm since creation
+ * (CommLedger, simgroup.py:88-172). */
+int ul_comm_ledger(const ul_comm* comm, uint64_t* calls, uint64_t* egress_bytes,
+                   uint64_t* aggregate_bytes);
+
+/* Fused all-to-all of n_tensors row-major tensors (each of rank `ndim`
+ * <= 4, shape given per tensor in shapes[t*4 .. t*4+ndim)), identical
+ * split/concat axes:  out_i = concat_j( split(in_j, P, split_axis)[i],
+ * concat_axis ).  Bit-exact byte routing.  comm == NULL means P = 1 (a
+ * local copy).  `label_hash` joins the call signature checked across ranks.
+ * Launches: one push kernel (local chunk -> out, remote chunks -> peers'
+ * receive slot, then release-signal), one flag wait, one slot drain. */
+int ul_all_to_all(ul_comm* comm, int n_tensors, const void* const* in, void* const* out,
+                  const int64_t* shapes, int ndim, int dtype, int split_axis,
+                  int concat_axis, uint64_t label_hash, void* stream);
+
+/* Bytes of receive slot ul_all_to_all needs for these tensors. */
+size_t ul_all_to_all_slot_bytes(int n_tensors, const int64_t* shapes, int ndim, int dtype,
+                                int split_axis, int concat_axis, int world);
+
+/* ======================================================================
+ * Local attention (the `local_attn` plugin after seq->head):
+ *   q  [n, b, hq,  hd]      k, v [n, b, hkv, hd]     (hkv | hq, GQA)
+ *   o  [n, b, hq,  hd]      lse  [b, hq, n] float32, natural log
+ * mask UL_MASK_NONE / UL_MASK_CAUSAL on global indices (kv <= q).
+ * bf16: hd in {64, 128}; fp32: hd <= 256.
+ * ==================================================================== */
+int ul_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
+                int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
+                int dtype, int mask, float scale, void* stream);
+
+/* dq [n,b,hq,hd], dk/dv [n,b,hkv,hd] (dk/dv summed over each kv head's
+ * query group).  workspace >= ul_attn_bwd_workspace_bytes(...). */
+size_t ul_attn_bwd_workspace_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
+                                   int dtype);
+int ul_attn_bwd(const void* q, const void* k, const void* v, const void* o,
+                const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                void* workspace, size_t workspace_bytes,
+                int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
+                int dtype, int mask, float scale, void* stream);
+
+/* Same as ul_attn_bwd restricted to a subset of its launches (bit 0: D/LSE
+ * pre-pass, bit 1: dK/dV kernel, bit 2: dQ kernel), in that order; the
+ * stages must run in order over one workspace.  Lets callers time or
+ * overlap the stages; ul_attn_bwd == stage_mask 7. */
+int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* o,
+                       const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                       void* workspace, size_t workspace_bytes,
+                       int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
+                       int dtype, int mask, float scale, int stage_mask, void* stream);
+
+/* Number of kernel launches the last ul_* call on this thread issued, and
+ * the cumulative count since the library was loaded (all threads). */
+int ul_last_launch_count(void);
+uint64_t ul_total_launch_count(void);
+
+/* costmodel.py:82-87 -- per-link a2a elements of one layer's forward,
+ * as an exact fraction num/den.  convention 0 = exact, 1 = paper_asymptotic. */
+int ul_ulysses_volume(int64_t n, int64_t b, int64_t d, int64_t p, int convention,
+                      int64_t* num, int64_t* den);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ULYSSES_B200_H */

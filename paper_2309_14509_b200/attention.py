@@ -1,0 +1,273 @@
+"""DistributedAttention / seq_all_to_all and the local-attention plugins.
+
+API surface (DeepSpeed-Ulysses, arXiv 2309.14509):
+
+    seq_all_to_all(input, scatter_idx, gather_idx, group)
+    DistributedAttention(local_attn, sequence_process_group, scatter_idx=2, gather_idx=0)
+
+mapped onto the reference's semantics (paths relative to
+/root/reference/pkg/src/seqlab):
+
+  * ``seq_all_to_all`` == ``RankContext.all_to_all(local, split_axis=
+    scatter_idx, concat_axis=gather_idx)`` (simgroup.py:453-456,
+    313-335).  Its backward is the same call with the indices swapped --
+    the reference's self-inverse law (test_simgroup.py:166-176).
+  * ``DistributedAttention.forward(q, k, v)`` == the core of
+    ``ulysses_attention_forward_with_state`` between the projections
+    (ulysses.py:144-154): 3x seq->head, per-head ``kernel``, 1x head->seq.
+    Its backward mirrors ``ulysses_attention_backward`` (ulysses.py:
+    213-226): dctx seq->head, per-head backward, 3x head->seq.
+  * ``local_attn`` is the kernel plugin ``kernel(q, k, v, mask, scale)``
+    (kernels.py:31-52, registry kernels.py:114-128); ``FlashAttention``
+    is this framework's implementation on full-sequence, head-sharded
+    ``[n, b, h/P, hd]`` tensors (bf16: tcgen05/TMEM/TMA; fp32: SIMT).
+
+Inputs are the reference's sequence-major ``[s/P, b, h, hd]`` shards
+(ulysses.py:47-48).  When ``local_attn`` is a ``FlashAttention`` the whole
+layer runs as one autograd node with fused launches: Q, K and V share one
+seq->head exchange; dQ, dK and dV share one head->seq exchange.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _lib
+from .comm import SequenceGroup
+from .errors import DivisibilityError, ForwardStateError, KernelError
+
+_ATTN_DTYPES = {torch.float32: _lib.DTYPE_F32, torch.bfloat16: _lib.DTYPE_BF16}
+
+
+def _stream(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _group(group) -> SequenceGroup:
+    if group is None:
+        return SequenceGroup.single()
+    if not isinstance(group, SequenceGroup):
+        raise TypeError("sequence_process_group must be a SequenceGroup "
+                        "(SequenceGroup.from_process_group(torch.distributed group))")
+    return group
+
+
+# ---------------------------------------------------------------------------
+# seq_all_to_all
+# ---------------------------------------------------------------------------
+
+class _SeqAllToAll(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, group, x, scatter_idx, gather_idx, label):
+        ctx.group, ctx.scatter_idx, ctx.gather_idx, ctx.label = group, scatter_idx, gather_idx, label
+        return group.all_to_all([x], scatter_idx, gather_idx, label=label)[0]
+
+    @staticmethod
+    def backward(ctx, grad):
+        g = _SeqAllToAll.apply(ctx.group, grad.contiguous(), ctx.gather_idx, ctx.scatter_idx,
+                               ctx.label + ".bwd")
+        return None, g, None, None, None
+
+
+def seq_all_to_all(input: torch.Tensor, scatter_idx: int, gather_idx: int, group=None,
+                   label: str = "all_to_all") -> torch.Tensor:
+    """All-to-all over the sequence-parallel group: split ``input`` into P
+    chunks along ``scatter_idx``, send chunk i to rank i, concatenate the
+    received chunks in rank order along ``gather_idx`` (simgroup.py:322-327).
+    Bit-exact routing; differentiable (backward swaps the indices)."""
+    return _SeqAllToAll.apply(_group(group), input, scatter_idx, gather_idx, label)
+
+
+# ---------------------------------------------------------------------------
+# local attention plugin
+# ---------------------------------------------------------------------------
+
+class FlashAttention:
+    """Local-attention plugin on head-sharded ``[n, b, h, hd]`` tensors.
+
+    ``mask`` is "causal" (causal_kernel, kernels.py:49-52) or "none"
+    (dense_kernel, kernels.py:43-46); ``scale`` defaults to 1/sqrt(hd)
+    (AttentionSpec.scale, layers.py:51).  K/V may carry fewer heads than Q
+    (GQA: query head h reads kv head h // (hq/hkv)).
+    """
+
+    def __init__(self, mask: str = "causal", scale: float | None = None):
+        if mask not in ("causal", "none"):
+            raise KernelError(f"kernel supports dense/causal masks only, got {mask!r}")
+        self.mask = mask
+        self.scale = scale
+
+    @property
+    def mask_code(self) -> int:
+        return _lib.MASK_CAUSAL if self.mask == "causal" else _lib.MASK_NONE
+
+    def _check(self, q, k, v):
+        if q.dim() != 4 or k.dim() != 4 or v.dim() != 4:
+            raise KernelError(f"kernel needs (n, b, h, hdim) tensors, got {tuple(q.shape)}, "
+                              f"{tuple(k.shape)}, {tuple(v.shape)}")
+        n, b, hq, hd = q.shape
+        if k.shape != v.shape or k.shape[0] != n or k.shape[1] != b or k.shape[3] != hd:
+            raise KernelError(f"kernel needs matching (n, b, hdim) views, got {tuple(q.shape)}, "
+                              f"{tuple(k.shape)}, {tuple(v.shape)}")
+        if q.dtype not in _ATTN_DTYPES or k.dtype != q.dtype or v.dtype != q.dtype:
+            raise KernelError(f"attention computes in float32 or bfloat16, got {q.dtype}")
+        if k.shape[2] < 1 or hq % k.shape[2] != 0:
+            raise DivisibilityError(f"kv head count {k.shape[2]} does not divide query head count {hq}")
+        if not (q.is_cuda and k.is_cuda and v.is_cuda):
+            raise KernelError("FlashAttention runs on CUDA tensors only (no CPU path)")
+        return n, b, hq, k.shape[2], hd
+
+    def _scale(self, hd):
+        return float(self.scale) if self.scale is not None else 1.0 / math.sqrt(hd)
+
+    def forward_with_lse(self, q, k, v):
+        n, b, hq, hkv, hd = self._check(q, k, v)
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        o = torch.empty_like(q)
+        lse = torch.empty((b, hq, n), dtype=torch.float32, device=q.device)
+        _lib.check(_lib.lib().ul_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                          lse.data_ptr(), n, b, hq, hkv, hd, _ATTN_DTYPES[q.dtype],
+                                          self.mask_code, self._scale(hd), _stream(q)))
+        return o, lse
+
+    def backward(self, q, k, v, o, lse, do):
+        if lse is None:
+            raise ForwardStateError("backward needs the state saved by the forward pass")
+        n, b, hq, hkv, hd = self._check(q, k, v)
+        if o.shape != q.shape or do.shape != q.shape or tuple(lse.shape) != (b, hq, n):
+            raise ForwardStateError(f"grad shape {tuple(do.shape)} does not match saved forward "
+                                    f"shape {tuple(o.shape)}")
+        q, k, v, o, do = (x.contiguous() for x in (q, k, v, o, do))
+        dq = torch.empty_like(q)
+        dk = torch.empty_like(k)
+        dv = torch.empty_like(v)
+        dt = _ATTN_DTYPES[q.dtype]
+        wsb = int(_lib.lib().ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dt))
+        ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=q.device)
+        _lib.check(_lib.lib().ul_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                          do.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(),
+                                          dv.data_ptr(), ws.data_ptr(), ws.numel(), n, b, hq, hkv, hd,
+                                          dt, self.mask_code, self._scale(hd), _stream(q)))
+        return dq, dk, dv
+
+    def __call__(self, q, k, v):
+        return _LocalAttnFn.apply(self, q, k, v)
+
+
+class _LocalAttnFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, attn, q, k, v):
+        o, lse = attn.forward_with_lse(q, k, v)
+        ctx.attn = attn
+        ctx.save_for_backward(q, k, v, o, lse)
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, o, lse = ctx.saved_tensors
+        dq, dk, dv = ctx.attn.backward(q, k, v, o, lse, do)
+        return None, dq, dk, dv
+
+
+KERNELS = {"dense": FlashAttention("none"), "causal": FlashAttention("causal")}
+
+
+def get_kernel(name: str) -> FlashAttention:
+    """kernels.py:124-128."""
+    try:
+        return KERNELS[name]
+    except KeyError:
+        raise KernelError(f"unknown kernel {name!r}, expected one of {sorted(KERNELS)}") from None
+
+
+# ---------------------------------------------------------------------------
+# DistributedAttention
+# ---------------------------------------------------------------------------
+
+class _UlyssesAttnFn(torch.autograd.Function):
+    """Whole-layer node: fused QKV seq->head, local attention, O head->seq."""
+
+    @staticmethod
+    def forward(ctx, group, attn, scatter_idx, gather_idx, q, k, v):
+        if group.world > 1:
+            q4, k4, v4 = group.all_to_all([q, k, v], scatter_idx, gather_idx, label="attn.qkv.seq2head",
+                                          labels=["attn.q.seq2head", "attn.k.seq2head", "attn.v.seq2head"])
+        else:
+            q4, k4, v4 = q.contiguous(), k.contiguous(), v.contiguous()
+        o4, lse = attn.forward_with_lse(q4, k4, v4)
+        if group.world > 1:
+            (o,) = group.all_to_all([o4], gather_idx, scatter_idx, label="attn.ctx.head2seq")
+        else:
+            o = o4
+        ctx.group, ctx.attn, ctx.idx = group, attn, (scatter_idx, gather_idx)
+        ctx.save_for_backward(q4, k4, v4, o4, lse)
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        group, attn = ctx.group, ctx.attn
+        scatter_idx, gather_idx = ctx.idx
+        q4, k4, v4, o4, lse = ctx.saved_tensors
+        do = do.contiguous()
+        if group.world > 1:
+            (do4,) = group.all_to_all([do], scatter_idx, gather_idx, label="bwd.ctx.seq2head")
+        else:
+            do4 = do
+        dq4, dk4, dv4 = attn.backward(q4, k4, v4, o4, lse, do4)
+        if group.world > 1:
+            dq, dk, dv = group.all_to_all([dq4, dk4, dv4], gather_idx, scatter_idx, label="bwd.qkv.head2seq",
+                                          labels=["bwd.q.head2seq", "bwd.k.head2seq", "bwd.v.head2seq"])
+        else:
+            dq, dk, dv = dq4, dk4, dv4
+        return None, None, None, None, dq, dk, dv
+
+
+class DistributedAttention(torch.nn.Module):
+    """Ulysses sequence-parallel attention (arXiv 2309.14509 section 3.1).
+
+    ``forward(query, key, value)`` takes this rank's sequence shards
+    ``[s/P, b, h, hd]`` (key/value may have ``h_kv`` heads, GQA) and returns
+    the context shard ``[s/P, b, h, hd]``.
+    """
+
+    def __init__(self, local_attention, sequence_process_group=None, scatter_idx: int = 2,
+                 gather_idx: int = 0):
+        super().__init__()
+        self.local_attn = local_attention
+        self.spg = _group(sequence_process_group)
+        self.scatter_idx = scatter_idx
+        self.gather_idx = gather_idx
+
+    def _check(self, q, k, v):
+        p = self.spg.world
+        if q.dim() != 4:
+            raise KernelError(f"DistributedAttention needs [s/P, b, h, hd] shards, got {tuple(q.shape)}")
+        h = q.shape[self.scatter_idx]
+        n = q.shape[self.gather_idx] * p
+        if n % p != 0:                                  # layers.py:53-57
+            raise DivisibilityError(f"p={p} does not divide sequence length n={n}")
+        if h % p != 0:
+            raise DivisibilityError(f"p={p} does not divide head count {h}")
+        hkv = k.shape[self.scatter_idx]
+        if hkv % p != 0:
+            raise DivisibilityError(f"p={p} does not divide kv head count {hkv}")
+
+    def forward(self, query, key, value):
+        self._check(query, key, value)
+        fused_layout = (self.scatter_idx, self.gather_idx) == (2, 0) or \
+            ((self.scatter_idx, self.gather_idx) == (2, 1) and query.shape[0] == 1)
+        if isinstance(self.local_attn, FlashAttention) and fused_layout:
+            if (self.scatter_idx, self.gather_idx) == (2, 1):      # [1, s, h, d] == [s, 1, h, d]
+                q, k, v = (x.reshape(x.shape[1], 1, x.shape[2], x.shape[3]) for x in (query, key, value))
+                o = _UlyssesAttnFn.apply(self.spg, self.local_attn, 2, 0, q, k, v)
+                return o.reshape(1, o.shape[0], o.shape[2], o.shape[3])
+            return _UlyssesAttnFn.apply(self.spg, self.local_attn, self.scatter_idx, self.gather_idx,
+                                        query, key, value)
+        # generic plugin: any callable local_attn(q, k, v) on head-sharded tensors
+        q4 = seq_all_to_all(query, self.scatter_idx, self.gather_idx, self.spg, "attn.q.seq2head")
+        k4 = seq_all_to_all(key, self.scatter_idx, self.gather_idx, self.spg, "attn.k.seq2head")
+        v4 = seq_all_to_all(value, self.scatter_idx, self.gather_idx, self.spg, "attn.v.seq2head")
+        ctx = self.local_attn(q4, k4, v4)
+        return seq_all_to_all(ctx, self.gather_idx, self.scatter_idx, self.spg, "attn.ctx.head2seq")

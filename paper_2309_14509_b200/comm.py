@@ -1,0 +1,220 @@
+"""The sequence-parallel group: identity, peer-mapped workspace, all-to-all.
+
+``SequenceGroup`` is this framework's ``sequence_process_group``.  It plays
+the role of the reference's ``RankContext`` over a ``RankGroup``
+(simgroup.py:198-224, 444-468), except that ranks are processes on
+different GPUs (``from_process_group``) -- or, for single-GPU parity tests,
+``world`` ranks driven from one process on one device, each on its own
+CUDA stream (``local_group``).  Both run the same native kernels: fused
+permute + NVLink peer stores + release/acquire flags (csrc/a2a.cu).
+
+Plumbing only goes through torch.distributed (exchanging IPC handles at
+setup); the data path never calls NCCL.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .errors import GroupDesyncError, ShardError
+
+_DTYPES = {torch.float32: _lib.DTYPE_F32, torch.bfloat16: _lib.DTYPE_BF16}
+
+DEFAULT_SLOT_BYTES = 64 << 20
+
+
+def label_hash(label: str) -> int:
+    h = 1469598103934665603
+    for ch in label.encode():
+        h ^= ch
+        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def dtype_code(dtype: torch.dtype) -> int:
+    try:
+        return _DTYPES[dtype]
+    except KeyError:
+        from .errors import KernelError
+        raise KernelError(f"all_to_all supports float32/bfloat16 payloads, got {dtype}") from None
+
+
+def a2a_out_shape(shape, p: int, split_axis: int, concat_axis: int) -> tuple:
+    """Output shape of simgroup.py:322-327's combine for one rank."""
+    shape = list(shape)
+    if shape[split_axis] % p != 0:
+        raise ShardError(f"all_to_all split axis {split_axis} (length {shape[split_axis]}) "
+                         f"not divisible by p={p}")
+    shape[split_axis] //= p
+    if split_axis != concat_axis:
+        shape[concat_axis] *= p
+    return tuple(shape)
+
+
+@dataclass(frozen=True)
+class CommRecord:
+    """One logical all_to_all, as the reference ledger records it
+    (CommRecord, simgroup.py:70-85), in elements."""
+    collective: str
+    step_label: str
+    aggregate_elements: int
+    per_rank_egress_elements: int
+
+
+class SequenceGroup:
+    """One rank of a P-way Ulysses sequence-parallel group."""
+
+    def __init__(self, rank: int, world: int, device: int, handle, slot_bytes: int,
+                 stream: torch.cuda.Stream | None = None, pg=None):
+        self.rank = rank
+        self.world = world
+        self.p = world                      # reference spelling (RankContext.p)
+        self.device = device
+        self._handle = handle               # ul_comm* (None for world == 1)
+        self.slot_bytes = slot_bytes
+        self.stream = stream
+        self._pg = pg
+        self.records: list[CommRecord] = []
+
+    # -- construction ------------------------------------------------------
+    @staticmethod
+    def _create(rank, world, device, slot_bytes):
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().ul_comm_create(rank, world, device, slot_bytes, ctypes.byref(h)))
+        return h
+
+    @classmethod
+    def single(cls, device: int | None = None) -> "SequenceGroup":
+        """P = 1: the seq<->head flips are identities (ulysses.py:104-111 at P=1)."""
+        if device is None:
+            device = torch.cuda.current_device()
+        return cls(0, 1, device, None, 0)
+
+    @classmethod
+    def from_process_group(cls, pg=None, slot_bytes: int = DEFAULT_SLOT_BYTES,
+                           device: int | None = None, timeout_ms: int | None = None) -> "SequenceGroup":
+        """Collective: every rank of ``pg`` (a torch.distributed group, any
+        backend) allocates its workspace and maps every peer's over CUDA IPC."""
+        import torch.distributed as dist
+        rank = dist.get_rank(pg)
+        world = dist.get_world_size(pg)
+        if device is None:
+            device = torch.cuda.current_device()
+        if world == 1:
+            return cls.single(device)
+        h = cls._create(rank, world, device, slot_bytes)
+        blob = ctypes.create_string_buffer(_lib.IPC_HANDLE_BYTES)
+        _lib.check(_lib.lib().ul_comm_export_handle(h, blob))
+        gathered = [None] * world
+        dist.all_gather_object(gathered, bytes(blob.raw), group=pg)
+        allb = ctypes.create_string_buffer(b"".join(gathered), world * _lib.IPC_HANDLE_BYTES)
+        _lib.check(_lib.lib().ul_comm_open_peers(h, allb))
+        g = cls(rank, world, device, h, int(_lib.lib().ul_comm_slot_bytes(h)), pg=pg)
+        if timeout_ms:
+            g.set_timeout_ms(timeout_ms)
+        dist.barrier(group=pg)
+        return g
+
+    @classmethod
+    def local_group(cls, world: int, slot_bytes: int = DEFAULT_SLOT_BYTES,
+                    device: int | None = None) -> list["SequenceGroup"]:
+        """``world`` ranks in this process on one GPU, one stream each.  The
+        peer pointers are plain device pointers, so the exact kernels of the
+        multi-GPU path (incl. flag waits) run at P = 2/4/8 on one B200.
+        Calls of different ranks must be issued on their own ``stream``."""
+        if device is None:
+            device = torch.cuda.current_device()
+        if world == 1:
+            return [cls.single(device)]
+        handles = [cls._create(r, world, device, slot_bytes) for r in range(world)]
+        arr = (ctypes.c_void_p * world)(*[h.value for h in handles])
+        _lib.check(_lib.lib().ul_comm_link_local(arr, world))
+        sb = int(_lib.lib().ul_comm_slot_bytes(handles[0]))
+        return [cls(r, world, device, handles[r], sb, stream=torch.cuda.Stream(device=device))
+                for r in range(world)]
+
+    def set_timeout_ms(self, ms: int):
+        if self._handle is not None:
+            _lib.check(_lib.lib().ul_comm_set_timeout_ms(self._handle, int(ms)))
+
+    def destroy(self):
+        if self._handle is not None:
+            _lib.lib().ul_comm_destroy(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    # -- status / metering -------------------------------------------------
+    def check(self):
+        """Raise GroupDesyncError if a device-side wait saw a signature
+        mismatch or timed out (simgroup.py:265-298).  Errors are reported
+        asynchronously, like NCCL's: poll after a synchronize."""
+        if self._handle is None:
+            return
+        buf = ctypes.create_string_buffer(512)
+        st = _lib.lib().ul_comm_status(self._handle, buf, 512)
+        if st != _lib.UL_OK:
+            raise GroupDesyncError(buf.value.decode(errors="replace"))
+
+    def native_ledger(self) -> dict:
+        if self._handle is None:
+            return {"calls": 0, "egress_bytes": 0, "aggregate_bytes": 0}
+        c, e, a = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        _lib.check(_lib.lib().ul_comm_ledger(self._handle, ctypes.byref(c), ctypes.byref(e), ctypes.byref(a)))
+        return {"calls": c.value, "egress_bytes": e.value, "aggregate_bytes": a.value}
+
+    def total_egress(self) -> int:
+        return sum(r.per_rank_egress_elements for r in self.records)
+
+    def total_aggregate(self) -> int:
+        return sum(r.aggregate_elements for r in self.records)
+
+    # -- the collective ----------------------------------------------------
+    def all_to_all(self, tensors, split_axis: int, concat_axis: int, label: str = "all_to_all",
+                   labels=None):
+        """Fused all-to-all of 1..4 contiguous tensors with the same rank,
+        dtype and axes (RankContext.all_to_all, simgroup.py:453-456).
+        Returns freshly allocated outputs (no aliasing across ranks, like the
+        reference's np.concatenate results, simgroup.py:322-327)."""
+        tensors = list(tensors)
+        if not tensors or len(tensors) > _lib.MAX_FUSED:
+            raise ValueError(f"all_to_all fuses 1..{_lib.MAX_FUSED} tensors, got {len(tensors)}")
+        ndim = tensors[0].dim()
+        if ndim < 1 or ndim > 4:
+            raise ValueError(f"all_to_all supports tensors of rank 1..4, got {ndim}")
+        split_axis = split_axis % ndim
+        concat_axis = concat_axis % ndim
+        p = self.world
+        dt = dtype_code(tensors[0].dtype)
+        outs = []
+        shapes = (ctypes.c_int64 * (4 * len(tensors)))()
+        for t, x in enumerate(tensors):
+            if x.dim() != ndim or x.dtype != tensors[0].dtype:
+                raise ValueError("fused all_to_all needs tensors of one rank and dtype")
+            if not x.is_cuda:
+                raise ValueError("all_to_all operates on CUDA tensors")
+            outs.append(torch.empty(a2a_out_shape(x.shape, p, split_axis, concat_axis),
+                                    dtype=x.dtype, device=x.device))
+            for k in range(ndim):
+                shapes[4 * t + k] = x.shape[k]
+        labels = labels or [label] * len(tensors)
+        for x, lab in zip(tensors, labels):
+            n = x.numel()
+            self.records.append(CommRecord("all_to_all", lab, p * n, n // p * (p - 1)))
+        ins = [x.contiguous() for x in tensors]
+        inp = (ctypes.c_void_p * len(ins))(*[x.data_ptr() for x in ins])
+        outp = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        stream = torch.cuda.current_stream(tensors[0].device).cuda_stream
+        # P = 1 passes a NULL comm: a local copy (the reference returns a fresh array too)
+        _lib.check(_lib.lib().ul_all_to_all(self._handle, len(ins), inp, outp, shapes, ndim, dt,
+                                            split_axis, concat_axis, label_hash(label), stream),
+                   exc_override={-1: ShardError})
+        return outs

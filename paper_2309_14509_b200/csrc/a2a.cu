@@ -1,0 +1,637 @@
+// K1/K2: the Ulysses all-to-all over NVLink/NVSwitch peer memory.
+//
+// Replaces RankGroup._all_to_all (simgroup.py:313-335) + _exchange
+// (simgroup.py:251-304) as called by seq_to_head (split 2, concat 0,
+// ulysses.py:104-111) and head_to_seq (split 0, concat 2, ulysses.py:114-124).
+//
+// Semantics (combine, simgroup.py:322-327): out_i = concat_j(split(in_j, P,
+// split_axis)[i], concat_axis).  Each (tensor, destination) pair is a 4-D
+// box copy whose innermost `run` bytes are contiguous on both sides, so the
+// permute is fused into the exchange: a warp streams one run with 16-byte
+// vector loads (coalesced, local HBM) and 16-byte stores straight into the
+// destination -- `out` for the local chunk, the peer's receive slot over
+// NVLink for remote chunks.  The last CTA to finish publishes a per-slot
+// signature and an epoch flag into every peer with st.release.sys; the
+// receiver's wait kernel acquires the flags (bounded spin -> DESYNC error
+// instead of a hang, simgroup.py:292-297) and compares signatures
+// (simgroup.py:265-276); a drain kernel then moves the P-1 remote chunks
+// from the slot into `out`.  Two slots alternate by call parity, which
+// makes one barrier per call sufficient.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ul {
+
+struct ErrWord {
+  volatile int32_t code;   // 0 or UL_ERR_DESYNC
+  volatile int32_t kind;   // 1 signature mismatch, 2 timeout
+  volatile int32_t peer;
+  volatile int32_t pad;
+  volatile uint64_t epoch;
+  volatile uint64_t expect_sig;
+  volatile uint64_t got;   // peer signature, or bitmask of missing ranks
+};
+
+struct Signals {           // lives at base + 2*slot_bytes on every rank
+  uint64_t flags[2][UL_MAX_RANKS];
+  uint64_t sigs[2][UL_MAX_RANKS];
+  unsigned int counter[2];
+  unsigned int pad[2];
+  ErrWord err;              // device-side error accumulator (local use)
+};
+
+struct Box {               // one (tensor, peer) chunk of a fused all-to-all
+  const char* src;
+  char* dst;
+  int64_t rows;            // product of the outer extents
+  int64_t run;             // contiguous bytes per row (both sides)
+  int64_t ext[3];          // outer extents (slowest first); unused dims = 1
+  int64_t sst[3], dstr[3]; // byte strides of the outer dims
+  int32_t vec;             // access width: 16, 8, 4 or 2 bytes
+  int32_t pad;
+};
+
+constexpr int kMaxBoxes = UL_MAX_FUSED * UL_MAX_RANKS;
+
+struct CopyParams {
+  Box box[kMaxBoxes];
+  int nbox;
+  // signalling (push kernel only)
+  int signal;               // 1 -> last CTA publishes sig + epoch to peers
+  int rank, world, slot;
+  uint64_t epoch, sig;
+  Signals* peer_sig[UL_MAX_RANKS];
+  unsigned int* counter;    // local, reset by the last CTA
+};
+
+}  // namespace ul
+
+struct ul_comm {
+  int rank = 0, world = 1, device = 0;
+  size_t slot_bytes = 0;
+  char* base = nullptr;
+  char* peer_base[UL_MAX_RANKS] = {};
+  bool ipc_opened[UL_MAX_RANKS] = {};
+  uint64_t epoch = 0;
+  int64_t timeout_ns = 60ll * 1000 * 1000 * 1000;   // RankGroup default 60 s (simgroup.py:207-208)
+  ul::ErrWord* err_host = nullptr;
+  ul::ErrWord* err_dev = nullptr;
+  uint64_t calls = 0, egress = 0, aggregate = 0;
+  uint64_t last_label = 0;
+};
+
+namespace ul {
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int V>
+struct VecT;
+template <> struct VecT<16> { using T = int4; };
+template <> struct VecT<8>  { using T = int2; };
+template <> struct VecT<4>  { using T = int;  };
+template <> struct VecT<2>  { using T = short; };
+
+// one warp per row, lanes stride over the row's vectors, 4 loads in flight
+template <int V>
+__device__ __forceinline__ void copy_box(const Box& bx, int64_t warp0, int64_t nwarps, int lane) {
+  using T = typename VecT<V>::T;
+  const int64_t nvec = bx.run / V;
+  const int64_t e1 = bx.ext[1], e2 = bx.ext[2];
+  for (int64_t r = warp0; r < bx.rows; r += nwarps) {
+    int64_t c2 = r % e2;
+    int64_t t = r / e2;
+    int64_t c1 = t % e1;
+    int64_t c0 = t / e1;
+    const T* s = reinterpret_cast<const T*>(bx.src + c0 * bx.sst[0] + c1 * bx.sst[1] + c2 * bx.sst[2]);
+    T* d = reinterpret_cast<T*>(bx.dst + c0 * bx.dstr[0] + c1 * bx.dstr[1] + c2 * bx.dstr[2]);
+    int64_t i = lane;
+    for (; i + 96 < nvec; i += 128) {
+      T a0 = __ldcs(s + i), a1 = __ldcs(s + i + 32), a2 = __ldcs(s + i + 64), a3 = __ldcs(s + i + 96);
+      d[i] = a0; d[i + 32] = a1; d[i + 64] = a2; d[i + 96] = a3;
+    }
+    for (; i < nvec; i += 32) d[i] = __ldcs(s + i);
+  }
+}
+
+// grid (blocks_per_box, nbox); 256 threads
+__global__ void __launch_bounds__(256) a2a_copy_kernel(const __grid_constant__ CopyParams p) {
+  const Box& bx = p.box[blockIdx.y];
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t w0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  switch (bx.vec) {
+    case 16: copy_box<16>(bx, w0, nwarps, lane); break;
+    case 8:  copy_box<8>(bx, w0, nwarps, lane); break;
+    case 4:  copy_box<4>(bx, w0, nwarps, lane); break;
+    default: copy_box<2>(bx, w0, nwarps, lane); break;
+  }
+  if (!p.signal) return;
+  // make this CTA's peer stores visible system-wide, then count CTAs
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int total = gridDim.x * gridDim.y;
+    unsigned int ticket = atomicAdd(p.counter, 1u);
+    if (ticket == total - 1) {
+      *p.counter = 0;  // every CTA has arrived; safe to rearm for the next call
+      __threadfence_system();
+      for (int i = 0; i < p.world; ++i) {
+        if (i == p.rank) continue;
+        Signals* s = p.peer_sig[i];
+        st_relaxed_sys(&s->sigs[p.slot][p.rank], p.sig);
+        st_release_sys(&s->flags[p.slot][p.rank], p.epoch);
+      }
+    }
+  }
+}
+
+// one warp: lane j waits for rank j's epoch flag in this slot.  Errors are
+// combined with device-memory atomics (`dev`), then lane 0 mirrors the word
+// into mapped host memory (`host`) with plain stores so the host can poll
+// it without a device sync.
+__global__ void a2a_wait_kernel(Signals* mine, int rank, int world, int slot, uint64_t epoch,
+                                uint64_t sig, int64_t timeout_ns, ErrWord* dev, ErrWord* host) {
+  const int j = threadIdx.x;
+  if (j < world && j != rank) {
+    bool ok = true;
+    const uint64_t t0 = globaltimer();
+    uint32_t spins = 0;
+    while (ld_acquire_sys(&mine->flags[slot][j]) < epoch) {
+      if ((++spins & 255u) == 0 && (int64_t)(globaltimer() - t0) > timeout_ns) {
+        ok = false;
+        break;
+      }
+      __nanosleep(100);
+    }
+    if (!ok) {
+      if (atomicCAS((int*)&dev->code, 0, UL_ERR_DESYNC) == 0) {
+        dev->kind = 2;
+        dev->peer = j;
+        dev->epoch = epoch;
+        dev->expect_sig = sig;
+      }
+      atomicOr((unsigned long long*)&dev->got, 1ull << j);
+    } else {
+      uint64_t got = ld_relaxed_sys(&mine->sigs[slot][j]);
+      if (got != sig && atomicCAS((int*)&dev->code, 0, UL_ERR_DESYNC) == 0) {
+        dev->kind = 1;
+        dev->peer = j;
+        dev->epoch = epoch;
+        dev->expect_sig = sig;
+        dev->got = got;
+      }
+    }
+  }
+  __syncwarp();
+  __threadfence();
+  if (j == 0 && dev->code != 0 && host->code == 0) {
+    host->kind = dev->kind;
+    host->peer = dev->peer;
+    host->epoch = dev->epoch;
+    host->expect_sig = dev->expect_sig;
+    host->got = dev->got;
+    __threadfence_system();
+    host->code = dev->code;
+    dev->code = 0;   // re-arm (host keeps the first error until read)
+    dev->got = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+static uint64_t fnv(uint64_t h, uint64_t v) {
+  for (int i = 0; i < 8; ++i) {
+    h ^= (v >> (8 * i)) & 0xff;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Geom {                 // one tensor of a fused call, padded to 4-D
+  int64_t S[4], So[4];        // in / out shapes
+  int64_t ss[4], so[4];       // byte strides
+  int split, concat;
+  size_t in_bytes, out_bytes;
+};
+
+static int make_geom(int ndim, const int64_t* shape, int esz, int split, int concat, int P, Geom* g) {
+  const int pad = 4 - ndim;
+  for (int k = 0; k < 4; ++k) g->S[k] = k < pad ? 1 : shape[k - pad];
+  for (int k = 0; k < 4; ++k)
+    if (g->S[k] < 0) return fail(UL_ERR_SHAPE, "all_to_all: negative dimension in shape");
+  g->split = split + pad;
+  g->concat = concat + pad;
+  if (g->S[g->split] % P != 0)
+    return fail(UL_ERR_DIVISIBILITY, "all_to_all split axis %d (length %lld) not divisible by p=%d",
+                split, (long long)g->S[g->split], P);
+  for (int k = 0; k < 4; ++k) g->So[k] = g->S[k];
+  g->So[g->split] /= P;
+  if (g->split != g->concat) g->So[g->concat] *= P;
+  g->ss[3] = esz;
+  g->so[3] = esz;
+  for (int k = 2; k >= 0; --k) {
+    g->ss[k] = g->ss[k + 1] * g->S[k + 1];
+    g->so[k] = g->so[k + 1] * g->So[k + 1];
+  }
+  g->in_bytes = (size_t)(g->ss[0] * g->S[0]);
+  g->out_bytes = (size_t)(g->so[0] * g->So[0]);
+  return UL_OK;
+}
+
+// chunk for destination `dst_rank` sent by `src_rank`: box in the source
+// tensor (layout S) and the same box placed in out_dst (layout So)
+// drain=true: the chunk already sits in a receive slot laid out like out_dst,
+// so both sides use the output layout and offset.
+static void make_box(const Geom& g, int src_rank, int dst_rank, int P, const char* src, char* dst,
+                     Box* b, bool drain = false) {
+  int64_t E[4], os[4] = {0, 0, 0, 0}, od[4] = {0, 0, 0, 0};
+  for (int k = 0; k < 4; ++k) E[k] = g.S[k];
+  const int64_t L = g.S[g.split] / P;
+  E[g.split] = L;
+  os[g.split] = (int64_t)dst_rank * L;
+  if (g.split == g.concat) od[g.concat] = (int64_t)src_rank * L;
+  else od[g.concat] = (int64_t)src_rank * g.S[g.concat];
+  const int m = g.split > g.concat ? g.split : g.concat;
+  int64_t run = g.ss[3] * E[m];
+  for (int k = m + 1; k < 4; ++k) run *= E[k];
+  b->run = run;
+  int64_t off_s = 0, off_d = 0;
+  for (int k = 0; k < 4; ++k) {
+    off_s += drain ? od[k] * g.so[k] : os[k] * g.ss[k];
+    off_d += od[k] * g.so[k];
+  }
+  b->src = src + off_s;
+  b->dst = dst + off_d;
+  // outer dims k < m, right-aligned into ext[0..2]
+  for (int i = 0; i < 3; ++i) {
+    b->ext[i] = 1;
+    b->sst[i] = 0;
+    b->dstr[i] = 0;
+  }
+  for (int k = 0; k < m; ++k) {
+    const int i = 3 - m + k;
+    b->ext[i] = E[k];
+    b->sst[i] = drain ? g.so[k] : g.ss[k];
+    b->dstr[i] = g.so[k];
+  }
+  b->rows = b->ext[0] * b->ext[1] * b->ext[2];
+  if (run == 0) b->rows = 0;
+  uint64_t al = (uint64_t)run | (uint64_t)(uintptr_t)b->src | (uint64_t)(uintptr_t)b->dst;
+  for (int i = 0; i < 3; ++i) al |= (uint64_t)b->sst[i] | (uint64_t)b->dstr[i];
+  b->vec = (al % 16 == 0) ? 16 : (al % 8 == 0) ? 8 : (al % 4 == 0) ? 4 : 2;
+}
+
+static int launch_copy(CopyParams& p, cudaStream_t st, const char* name) {
+  if (p.nbox == 0) return UL_OK;
+  int64_t maxwork = 0;
+  for (int i = 0; i < p.nbox; ++i) {
+    int64_t w = p.box[i].rows * ((p.box[i].run + 511) / 512);
+    if (w > maxwork) maxwork = w;
+  }
+  // ~one 512-byte warp-row per warp per pass; cap the grid at a few waves
+  const int warps_per_block = 8;
+  int64_t bpb = (maxwork + warps_per_block - 1) / warps_per_block;
+  const int64_t cap = (int64_t)sm_count() * 8 / p.nbox + 1;
+  if (bpb > cap) bpb = cap;
+  if (bpb < 1) bpb = 1;
+  dim3 grid((unsigned)bpb, (unsigned)p.nbox);
+  a2a_copy_kernel<<<grid, 256, 0, st>>>(p);
+  return launched(name);
+}
+
+}  // namespace ul
+
+using namespace ul;
+
+extern "C" {
+
+int ul_comm_create(int rank, int world, int device, size_t slot_bytes, ul_comm** out) {
+  if (!out) return fail(UL_ERR_ARG, "ul_comm_create: out is NULL");
+  *out = nullptr;
+  if (world < 1 || world > UL_MAX_RANKS)
+    return fail(UL_ERR_ARG, "group size must be in [1, %d], got %d", UL_MAX_RANKS, world);
+  if (rank < 0 || rank >= world) return fail(UL_ERR_ARG, "rank %d outside group of %d", rank, world);
+  UL_CUDA(cudaSetDevice(device));
+  ul_comm* c = new ul_comm();
+  c->rank = rank;
+  c->world = world;
+  c->device = device;
+  c->slot_bytes = align_up(slot_bytes ? slot_bytes : 256, 4096);
+  const size_t total = 2 * c->slot_bytes + align_up(sizeof(Signals), 4096);
+  cudaError_t e = cudaMalloc(&c->base, total);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(UL_ERR_CUDA, "ul_comm_create: cudaMalloc(%zu): %s", total, cudaGetErrorString(e));
+  }
+  e = cudaMemset(c->base + 2 * c->slot_bytes, 0, sizeof(Signals));
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&c->err_host, sizeof(ErrWord), cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    memset((void*)c->err_host, 0, sizeof(ErrWord));
+    e = cudaHostGetDevicePointer((void**)&c->err_dev, (void*)c->err_host, 0);
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaFree(c->base);
+    delete c;
+    return fail(UL_ERR_CUDA, "ul_comm_create: %s", cudaGetErrorString(e));
+  }
+  c->peer_base[rank] = c->base;
+  *out = c;
+  return UL_OK;
+}
+
+struct HandleBlob {
+  cudaIpcMemHandle_t h;   // 64 bytes
+  uint64_t magic;
+  uint64_t slot_bytes;
+  int32_t rank, world;
+};
+static_assert(sizeof(HandleBlob) <= UL_IPC_HANDLE_BYTES, "blob too large");
+static const uint64_t kMagic = 0x554c595353455332ull;  // "ULYSSES2"
+
+int ul_comm_export_handle(const ul_comm* c, void* handle_out) {
+  if (!c || !handle_out) return fail(UL_ERR_ARG, "ul_comm_export_handle: NULL argument");
+  HandleBlob b;
+  memset(&b, 0, sizeof(b));
+  UL_CUDA(cudaSetDevice(c->device));
+  UL_CUDA(cudaIpcGetMemHandle(&b.h, c->base));
+  b.magic = kMagic;
+  b.slot_bytes = c->slot_bytes;
+  b.rank = c->rank;
+  b.world = c->world;
+  memset(handle_out, 0, UL_IPC_HANDLE_BYTES);
+  memcpy(handle_out, &b, sizeof(b));
+  return UL_OK;
+}
+
+int ul_comm_open_peers(ul_comm* c, const void* all) {
+  if (!c || !all) return fail(UL_ERR_ARG, "ul_comm_open_peers: NULL argument");
+  UL_CUDA(cudaSetDevice(c->device));
+  const char* p = (const char*)all;
+  for (int r = 0; r < c->world; ++r) {
+    HandleBlob b;
+    memcpy(&b, p + (size_t)r * UL_IPC_HANDLE_BYTES, sizeof(b));
+    if (b.magic != kMagic)
+      return fail(UL_ERR_DESYNC, "group desync: rank %d sent a malformed comm handle", r);
+    if (b.rank != r || b.world != c->world)
+      return fail(UL_ERR_DESYNC, "group desync: rank %d reports rank %d of %d, expected %d of %d", r,
+                  b.rank, b.world, r, c->world);
+    if (b.slot_bytes != c->slot_bytes)
+      return fail(UL_ERR_DESYNC, "group desync: rank %d workspace slot %llu bytes, rank %d has %llu", r,
+                  (unsigned long long)b.slot_bytes, c->rank, (unsigned long long)c->slot_bytes);
+    if (r == c->rank) continue;
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, b.h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return fail(UL_ERR_CUDA, "rank %d: cudaIpcOpenMemHandle(peer %d): %s", c->rank, r,
+                  cudaGetErrorString(e));
+    c->peer_base[r] = (char*)ptr;
+    c->ipc_opened[r] = true;
+  }
+  return UL_OK;
+}
+
+int ul_comm_link_local(ul_comm* const* comms, int world) {
+  if (!comms || world < 1) return fail(UL_ERR_ARG, "ul_comm_link_local: bad arguments");
+  for (int r = 0; r < world; ++r) {
+    if (!comms[r] || comms[r]->world != world || comms[r]->rank != r)
+      return fail(UL_ERR_DESYNC, "group desync: comm %d is not rank %d of %d", r, r, world);
+    if (comms[r]->slot_bytes != comms[0]->slot_bytes)
+      return fail(UL_ERR_DESYNC, "group desync: rank %d workspace slot differs from rank 0", r);
+  }
+  for (int r = 0; r < world; ++r)
+    for (int s = 0; s < world; ++s) comms[r]->peer_base[s] = comms[s]->base;
+  return UL_OK;
+}
+
+int ul_comm_destroy(ul_comm* c) {
+  if (!c) return UL_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int r = 0; r < c->world; ++r)
+    if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->peer_base[r]);
+  cudaFree(c->base);
+  if (c->err_host) cudaFreeHost((void*)c->err_host);
+  delete c;
+  return UL_OK;
+}
+
+int ul_comm_rank(const ul_comm* c) { return c ? c->rank : 0; }
+int ul_comm_world(const ul_comm* c) { return c ? c->world : 1; }
+size_t ul_comm_slot_bytes(const ul_comm* c) { return c ? c->slot_bytes : 0; }
+
+int ul_comm_set_timeout_ms(ul_comm* c, int64_t ms) {
+  if (!c || ms <= 0) return fail(UL_ERR_ARG, "ul_comm_set_timeout_ms: bad arguments");
+  c->timeout_ns = ms * 1000000ll;
+  return UL_OK;
+}
+
+int ul_comm_status(ul_comm* c, char* msg, size_t len) {
+  if (!c) return fail(UL_ERR_ARG, "ul_comm_status: NULL comm");
+  const int code = c->err_host->code;
+  if (code == 0) {
+    if (msg && len) msg[0] = 0;
+    return UL_OK;
+  }
+  char buf[512];
+  if (c->err_host->kind == 2) {
+    std::string missing;
+    for (int r = 0; r < c->world; ++r)
+      if (c->err_host->got & (1ull << r)) missing += (missing.empty() ? "" : ", ") + std::to_string(r);
+    snprintf(buf, sizeof(buf),
+             "group desync: timeout in collective 'all_to_all' (call %llu) on rank %d waiting on ranks [%s]",
+             (unsigned long long)c->err_host->epoch, c->rank, missing.c_str());
+  } else {
+    snprintf(buf, sizeof(buf),
+             "group desync: rank %d entered collective 'all_to_all' (call %llu, signature %016llx) while rank "
+             "%d entered 'all_to_all' (signature %016llx)",
+             c->err_host->peer, (unsigned long long)c->err_host->epoch,
+             (unsigned long long)c->err_host->got, c->rank, (unsigned long long)c->err_host->expect_sig);
+  }
+  if (msg && len) {
+    strncpy(msg, buf, len - 1);
+    msg[len - 1] = 0;
+  }
+  last_error() = buf;
+  memset((void*)c->err_host, 0, sizeof(ErrWord));
+  return code;
+}
+
+int ul_comm_ledger(const ul_comm* c, uint64_t* calls, uint64_t* egress, uint64_t* aggregate) {
+  if (!c) return fail(UL_ERR_ARG, "ul_comm_ledger: NULL comm");
+  if (calls) *calls = c->calls;
+  if (egress) *egress = c->egress;
+  if (aggregate) *aggregate = c->aggregate;
+  return UL_OK;
+}
+
+size_t ul_all_to_all_slot_bytes(int n, const int64_t* shapes, int ndim, int dtype, int split,
+                                int concat, int world) {
+  size_t tot = 0;
+  for (int t = 0; t < n; ++t) {
+    Geom g;
+    if (make_geom(ndim, shapes + 4 * t, (int)dtype_size(dtype), split, concat, world, &g) != UL_OK)
+      return 0;
+    tot += align_up(g.out_bytes, 256);
+  }
+  return tot;
+}
+
+int ul_all_to_all(ul_comm* c, int n, const void* const* in, void* const* out, const int64_t* shapes,
+                  int ndim, int dtype, int split, int concat, uint64_t label, void* stream) {
+  launch_count() = 0;
+  if (n < 1 || n > UL_MAX_FUSED)
+    return fail(UL_ERR_ARG, "all_to_all: fuses 1..%d tensors, got %d", UL_MAX_FUSED, n);
+  if (ndim < 1 || ndim > 4) return fail(UL_ERR_SHAPE, "all_to_all: tensors of rank 1..4, got %d", ndim);
+  if (dtype != UL_DTYPE_F32 && dtype != UL_DTYPE_BF16)
+    return fail(UL_ERR_KERNEL, "all_to_all: unsupported dtype %d", dtype);
+  if (split < 0 || split >= ndim || concat < 0 || concat >= ndim)
+    return fail(UL_ERR_ARG, "all_to_all: axes (%d, %d) out of range for rank %d", split, concat, ndim);
+  if (!in || !out || !shapes) return fail(UL_ERR_ARG, "all_to_all: NULL argument");
+  const int P = c ? c->world : 1;
+  const int me = c ? c->rank : 0;
+  const int esz = (int)dtype_size(dtype);
+  cudaStream_t st = (cudaStream_t)stream;
+
+  Geom g[UL_MAX_FUSED];
+  size_t slot_off[UL_MAX_FUSED];
+  size_t slot_need = 0;
+  uint64_t sig = 1469598103934665603ull;
+  sig = fnv(sig, (uint64_t)n);
+  sig = fnv(sig, (uint64_t)ndim);
+  sig = fnv(sig, (uint64_t)dtype);
+  sig = fnv(sig, (uint64_t)split);
+  sig = fnv(sig, (uint64_t)concat);
+  sig = fnv(sig, label);
+  uint64_t in_total = 0;
+  for (int t = 0; t < n; ++t) {
+    UL_TRY(make_geom(ndim, shapes + 4 * t, esz, split, concat, P, &g[t]));
+    if (!in[t] || !out[t]) return fail(UL_ERR_ARG, "all_to_all: NULL tensor %d", t);
+    for (int k = 0; k < ndim; ++k) sig = fnv(sig, (uint64_t)shapes[4 * t + k]);
+    slot_off[t] = slot_need;
+    slot_need += align_up(g[t].out_bytes, 256);
+    in_total += g[t].in_bytes;
+  }
+  if (P > 1 && slot_need > c->slot_bytes)
+    return fail(UL_ERR_ARG, "all_to_all: call needs %zu receive-slot bytes, workspace has %zu", slot_need,
+                c->slot_bytes);
+  for (int r = 0; P > 1 && r < P; ++r)
+    if (!c->peer_base[r])
+      return fail(UL_ERR_STATE, "all_to_all: rank %d has no mapping for peer %d (open_peers not called)",
+                  me, r);
+
+  uint64_t epoch = 0;
+  int slot = 0;
+  if (c) {
+    epoch = ++c->epoch;
+    slot = (int)(epoch & 1);
+    c->calls += 1;
+    c->aggregate += (uint64_t)P * in_total;
+    c->egress += in_total / P * (P - 1);
+  }
+
+  // push: local chunk -> out (local HBM), remote chunks -> peer slots (NVLink)
+  CopyParams cp;
+  memset(&cp, 0, sizeof(cp));
+  for (int t = 0; t < n; ++t) {
+    for (int k = 0; k < P; ++k) {
+      const int i = (me + k) % P;  // rotate destinations to spread switch load
+      char* dst = (i == me) ? (char*)out[t] : c->peer_base[i] + (size_t)slot * c->slot_bytes + slot_off[t];
+      make_box(g[t], me, i, P, (const char*)in[t], dst, &cp.box[cp.nbox]);
+      if (cp.box[cp.nbox].rows > 0) ++cp.nbox;
+    }
+  }
+  if (P > 1) {
+    cp.signal = 1;
+    cp.rank = me;
+    cp.world = P;
+    cp.slot = slot;
+    cp.epoch = epoch;
+    cp.sig = sig;
+    for (int r = 0; r < P; ++r) cp.peer_sig[r] = (Signals*)(c->peer_base[r] + 2 * c->slot_bytes);
+    cp.counter = &((Signals*)(c->base + 2 * c->slot_bytes))->counter[slot];
+    if (cp.nbox == 0) {  // nothing to move (empty tensors) -- still signal
+      make_box(g[0], me, me, P, (const char*)in[0], (char*)out[0], &cp.box[0]);
+      cp.box[0].rows = 0;
+      cp.nbox = 1;
+    }
+  }
+  UL_TRY(launch_copy(cp, st, "a2a_push"));
+  if (P == 1) return UL_OK;
+
+  Signals* mine = (Signals*)(c->base + 2 * c->slot_bytes);
+  a2a_wait_kernel<<<1, 32, 0, st>>>(mine, me, P, slot, epoch, sig, c->timeout_ns, &mine->err,
+                                      c->err_dev);
+  UL_TRY(launched("a2a_wait"));
+
+  CopyParams dp;
+  memset(&dp, 0, sizeof(dp));
+  for (int t = 0; t < n; ++t) {
+    for (int j = 0; j < P; ++j) {
+      if (j == me) continue;
+      // the chunk rank j sent sits in my slot exactly where it belongs in out
+      Box b;
+      const char* slot_img = c->base + (size_t)slot * c->slot_bytes + slot_off[t];
+      make_box(g[t], j, me, P, slot_img, (char*)out[t], &b, /*drain=*/true);
+      if (b.rows > 0) dp.box[dp.nbox++] = b;
+    }
+  }
+  UL_TRY(launch_copy(dp, st, "a2a_drain"));
+  return UL_OK;
+}
+
+int ul_ulysses_volume(int64_t n, int64_t b, int64_t d, int64_t p, int convention, int64_t* num,
+                      int64_t* den) {
+  if (!num || !den || n < 1 || b < 1 || d < 1 || p < 1)
+    return fail(UL_ERR_ARG, "ul_ulysses_volume: bad arguments");
+  if (n % p != 0) return fail(UL_ERR_DIVISIBILITY, "p=%lld does not divide n=%lld", (long long)p, (long long)n);
+  const int64_t m = 4 * n * b * d;
+  int64_t nu, de;
+  if (convention == 1) {
+    nu = m;
+    de = p;
+  } else {
+    nu = m * (p - 1);
+    de = p * p;
+  }
+  int64_t a = nu, bb = de;
+  while (bb) {
+    int64_t t = a % bb;
+    a = bb;
+    bb = t;
+  }
+  if (a == 0) a = 1;
+  *num = nu / a;
+  *den = de / a;
+  return UL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// extern "C" entry points for the local-attention plugin (ul_attn_*) and
+// library-level utilities.  Argument validation mirrors the reference's
+// error taxonomy (kernels.py:22-28, layers.py:53-57, tensor.py:23-32).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <string>
+
+#include "common.cuh"
+
+namespace ul {
+
+std::string& last_error() {
+  static thread_local std::string s;
+  return s;
+}
+int& launch_count() {
+  static thread_local int n = 0;
+  return n;
+}
+static std::atomic<uint64_t> g_total_launches{0};
+void count_launch() { g_total_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int simt_fwd(const float* q, const float* k, const float* v, float* o, float* lse, int64_t n, int64_t b,
+             int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st);
+int simt_bwd(const float* q, const float* k, const float* v, const float* o, const float* dout,
+             const float* lse, float* dq, float* dk, float* dv, float* Dws, int64_t n, int64_t b, int64_t hq,
+             int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st);
+int sm100_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
+              int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st);
+int sm100_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
+              void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n, int64_t b, int64_t hq,
+              int64_t hkv, int64_t hd, int causal, float scale, int stages, cudaStream_t st);
+size_t sm100_bwd_workspace(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd);
+
+static int check_attn(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask) {
+  if (mask != UL_MASK_NONE && mask != UL_MASK_CAUSAL)
+    return fail(UL_ERR_KERNEL, "kernel supports dense/causal masks only, got mask kind %d", mask);
+  if (dtype != UL_DTYPE_F32 && dtype != UL_DTYPE_BF16)
+    return fail(UL_ERR_KERNEL, "unsupported attention dtype %d", dtype);
+  if (n < 0 || b < 0 || hq < 0 || hkv < 0 || hd < 1)
+    return fail(UL_ERR_SHAPE, "kernel needs (n, b, heads, hdim) >= 0 with hdim >= 1, got (%lld, %lld, %lld, %lld)",
+                (long long)n, (long long)b, (long long)hq, (long long)hd);
+  if (hkv < 1 || hq % hkv != 0)
+    return fail(UL_ERR_DIVISIBILITY, "kv head count %lld does not divide query head count %lld", (long long)hkv,
+                (long long)hq);
+  if (dtype == UL_DTYPE_F32 && hd > 256)
+    return fail(UL_ERR_KERNEL, "fp32 attention supports head_dim <= 256, got %lld", (long long)hd);
+  return UL_OK;
+}
+
+}  // namespace ul
+
+using namespace ul;
+
+extern "C" {
+
+int ul_abi_version(void) { return UL_ABI_VERSION; }
+const char* ul_last_error(void) { return last_error().c_str(); }
+int ul_last_launch_count(void) { return launch_count(); }
+uint64_t ul_total_launch_count(void) { return g_total_launches.load(); }
+
+int ul_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
+                int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask, float scale, void* stream) {
+  launch_count() = 0;
+  UL_TRY(check_attn(n, b, hq, hkv, hd, dtype, mask));
+  if (!q || !k || !v || !o || !lse) {
+    if (n * b * hq == 0) return UL_OK;
+    return fail(UL_ERR_ARG, "ul_attn_fwd: NULL tensor");
+  }
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(UL_ERR_ARG, "scale must be finite and > 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int causal = mask == UL_MASK_CAUSAL;
+  if (dtype == UL_DTYPE_F32)
+    return simt_fwd((const float*)q, (const float*)k, (const float*)v, (float*)o, lse, n, b, hq, hkv, hd, causal,
+                    scale, st);
+  return sm100_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, causal, scale, st);
+}
+
+size_t ul_attn_bwd_workspace_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype) {
+  const size_t dvec = (size_t)n * b * hq * sizeof(float);
+  if (dtype == UL_DTYPE_F32) return dvec;
+  return sm100_bwd_workspace(n, b, hq, hkv, hd);
+}
+
+int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* o, const void* dout,
+                       const float* lse, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n,
+                       int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask, float scale,
+                       int stages, void* stream) {
+  launch_count() = 0;
+  UL_TRY(check_attn(n, b, hq, hkv, hd, dtype, mask));
+  if (n * b * hq == 0) return UL_OK;
+  if (!q || !k || !v || !o || !dout || !dq || !dk || !dv)
+    return fail(UL_ERR_ARG, "ul_attn_bwd: NULL tensor");
+  if (!lse) return fail(UL_ERR_STATE, "backward needs the LSE saved by the forward pass");
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(UL_ERR_ARG, "scale must be finite and > 0");
+  if (stages < 1 || stages > 7) return fail(UL_ERR_ARG, "stage mask must be in [1, 7], got %d", stages);
+  const size_t need = ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dtype);
+  if (!ws || ws_bytes < need)
+    return fail(UL_ERR_ARG, "ul_attn_bwd: workspace of %zu bytes < required %zu", ws_bytes, need);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int causal = mask == UL_MASK_CAUSAL;
+  if (dtype == UL_DTYPE_F32) {
+    if (stages != 7) return fail(UL_ERR_KERNEL, "fp32 backward runs all stages together");
+    return simt_bwd((const float*)q, (const float*)k, (const float*)v, (const float*)o, (const float*)dout, lse,
+                    (float*)dq, (float*)dk, (float*)dv, (float*)ws, n, b, hq, hkv, hd, causal, scale, st);
+  }
+  return sm100_bwd(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, causal, scale, stages, st);
+}
+
+int ul_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
+                void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n, int64_t b, int64_t hq,
+                int64_t hkv, int64_t hd, int dtype, int mask, float scale, void* stream) {
+  return ul_attn_bwd_stages(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, dtype, mask, scale,
+                            7, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,53 @@
+"""Shared test helpers (GPU-side runners for in-process sequence groups)."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+
+def to_dev(x, dtype=torch.float32, device="cuda"):
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float64).to(dtype).to(device).contiguous()
+
+
+def to_np(t):
+    return t.detach().to(torch.float64).cpu().numpy()
+
+
+def run_ranks(groups, fn):
+    """Issue fn(rank) for every rank of an in-process group, each on its own
+    stream (ranks of a local group must not share a stream: their device
+    waits would serialise), then synchronise and surface desync errors."""
+    torch.cuda.synchronize()
+    out = []
+    for g in groups:
+        s = g.stream if g.stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            out.append(fn(g.rank))
+    torch.cuda.synchronize()
+    for g in groups:
+        g.check()
+    return out
+
+
+def rel_max_err(a, ref):
+    a = np.asarray(a, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    return float(np.abs(a - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+# fp32-mode tolerance (north star: rtol 1e-5), with an absolute floor of
+# 1e-6 * max|o| for entries that are near zero by cancellation.
+FP32_RTOL = 1e-5
+FP32_ATOL_REL = 1e-6
+# bf16-mode tolerance (north star): max|a - o| <= 2e-2 * max|o|, o in f64.
+BF16_MAXREL = 2e-2
+
+
+def assert_rtol(a, ref, rtol=FP32_RTOL, atol_rel=FP32_ATOL_REL):
+    """fp32-mode contract: |a - o| <= rtol*|o| + atol_rel*max|o|."""
+    a = np.asarray(a, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    tol = rtol * np.abs(ref) + atol_rel * max(np.abs(ref).max(), 1e-30)
+    bad = np.abs(a - ref) > tol
+    assert not bad.any(), f"{bad.sum()} elements out of tolerance; max err {np.abs(a - ref).max():.3e}"

@@ -1,0 +1,146 @@
+"""K3/K4 local attention on the GPU vs the f64 oracle.
+
+bf16 mode (tcgen05/TMEM/TMA): max|a - o| <= 2e-2 * max|o| (north star),
+o = oracle in float64 on the same bf16-rounded inputs.
+fp32 mode (SIMT): |a - o| <= 1e-5 |o| + 1e-6 max|o|.
+Mirrors test_kernels.py (n=1, causal row 0, FD-checked backward) and
+test_oracle.py (causality probe) at GPU sizes.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import BF16_MAXREL, assert_rtol, rel_max_err, to_dev, to_np
+from oracle import ulysses_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def U():
+    import paper_2309_14509_b200 as mod
+    return mod
+
+
+def inputs(n, b, hq, hkv, hd, dtype, seed=0):
+    dt = "bfloat16" if dtype == torch.bfloat16 else "float32"
+    q = O.make_tensor((n, b, hq, hd), seed, 1, dt)
+    k = O.make_tensor((n, b, hkv, hd), seed, 2, dt)
+    v = O.make_tensor((n, b, hkv, hd), seed, 3, dt)
+    do = O.make_tensor((n, b, hq, hd), seed, 4, dt)
+    return q, k, v, do
+
+
+FWD_CASES = [
+    # n, b, hq, hkv, hd, mask
+    (1, 1, 1, 1, 64, "none"),
+    (5, 1, 2, 2, 64, "causal"),
+    (128, 1, 2, 2, 128, "causal"),
+    (200, 2, 4, 2, 128, "causal"),
+    (256, 1, 2, 1, 64, "none"),
+    (384, 1, 4, 4, 128, "none"),
+    (1000, 1, 2, 2, 128, "causal"),
+    (1024, 1, 8, 8, 64, "causal"),
+]
+
+
+@pytest.mark.parametrize("n,b,hq,hkv,hd,mask", FWD_CASES)
+def test_fwd_bf16_vs_oracle(n, b, hq, hkv, hd, mask):
+    q, k, v, _ = inputs(n, b, hq, hkv, hd, torch.bfloat16, seed=n + hd)
+    kind = "causal" if mask == "causal" else "none"
+    ref, ref_lse = O.local_attention(q, k, v, kind, exact=False)
+    attn = U().FlashAttention(mask)
+    o, lse = attn.forward_with_lse(*(to_dev(x, torch.bfloat16) for x in (q, k, v)))
+    torch.cuda.synchronize()
+    assert rel_max_err(to_np(o), ref) <= BF16_MAXREL
+    assert np.abs(to_np(lse) - ref_lse).max() <= 2e-2
+
+
+@pytest.mark.parametrize("n,b,hq,hkv,hd,mask", [(1, 1, 1, 1, 8, "none"), (7, 2, 4, 2, 3, "causal"),
+                                                (64, 1, 4, 4, 16, "none"), (300, 1, 4, 1, 64, "causal"),
+                                                (129, 2, 2, 2, 128, "causal")])
+def test_fwd_bwd_fp32_vs_oracle(n, b, hq, hkv, hd, mask):
+    q, k, v, do = inputs(n, b, hq, hkv, hd, torch.float32, seed=7 + n)
+    kind = "causal" if mask == "causal" else "none"
+    ref, ref_lse = O.local_attention(q, k, v, kind, exact=False)
+    dq_r, dk_r, dv_r = O.local_attention_backward(q, k, v, do, kind, exact=False)
+    attn = U().FlashAttention(mask)
+    tq, tk, tv, tdo = (to_dev(x) for x in (q, k, v, do))
+    o, lse = attn.forward_with_lse(tq, tk, tv)
+    dq, dk, dv = attn.backward(tq, tk, tv, o, lse, tdo)
+    torch.cuda.synchronize()
+    assert_rtol(to_np(o), ref)
+    assert np.abs(to_np(lse) - ref_lse).max() <= 1e-5
+    assert_rtol(to_np(dq), dq_r)
+    assert_rtol(to_np(dk), dk_r)
+    assert_rtol(to_np(dv), dv_r)
+
+
+def test_single_token_context_is_v():
+    # test_kernels.py:32-35
+    for dt in (torch.float32, torch.bfloat16):
+        q, k, v, _ = inputs(1, 2, 2, 2, 64, dt, seed=3)
+        o, _ = U().FlashAttention("none").forward_with_lse(*(to_dev(x, dt) for x in (q, k, v)))
+        assert np.array_equal(to_np(o), v)
+
+
+def test_causal_first_row_is_v0():
+    # test_kernels.py:37-40
+    for dt in (torch.float32, torch.bfloat16):
+        q, k, v, _ = inputs(300, 1, 2, 2, 128 if dt == torch.bfloat16 else 32, dt, seed=4)
+        o, _ = U().FlashAttention("causal").forward_with_lse(*(to_dev(x, dt) for x in (q, k, v)))
+        assert np.array_equal(to_np(o)[0], v[0])
+
+
+def test_causality_probe_bf16():
+    # test_oracle.py:83-93: perturbing key/value row j must not change rows < j
+    n, hd = 512, 128
+    q, k, v, _ = inputs(n, 1, 2, 2, hd, torch.bfloat16, seed=5)
+    attn = U().FlashAttention("causal")
+    base, _ = attn.forward_with_lse(*(to_dev(x, torch.bfloat16) for x in (q, k, v)))
+    k2, v2 = k.copy(), v.copy()
+    k2[300] += 4.0
+    v2[300] += 4.0
+    bumped, _ = attn.forward_with_lse(*(to_dev(x, torch.bfloat16) for x in (q, k2, v2)))
+    assert torch.equal(base[:300], bumped[:300])
+    assert (base[300:] - bumped[300:]).abs().max().item() > 1e-3
+
+
+def test_deterministic_and_longest_first_order_independent():
+    q, k, v, _ = inputs(1024, 1, 4, 4, 128, torch.bfloat16, seed=6)
+    attn = U().FlashAttention("causal")
+    tq, tk, tv = (to_dev(x, torch.bfloat16) for x in (q, k, v))
+    a, la = attn.forward_with_lse(tq, tk, tv)
+    b, lb = attn.forward_with_lse(tq, tk, tv)
+    assert torch.equal(a, b) and torch.equal(la, lb)
+
+
+def test_kernel_errors():
+    attn = U().FlashAttention("causal")
+    x = torch.zeros(4, 1, 2, 96, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(U().KernelError):
+        attn.forward_with_lse(x, x, x)
+    with pytest.raises(U().KernelError):
+        U().get_kernel("blocked")
+    y = torch.zeros(4, 1, 4, 64, device="cuda", dtype=torch.bfloat16)
+    z = torch.zeros(4, 1, 3, 64, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(U().DivisibilityError):
+        attn.forward_with_lse(y, z, z)
+    with pytest.raises(U().ForwardStateError):
+        attn.backward(y, y, y, y, None, y)
+
+
+@pytest.mark.parametrize("n", [8192])
+def test_fwd_bf16_large_sampled_rows(n):
+    # full-size config-2 shape; oracle on sampled query-row blocks (row_offset)
+    hq, hd = 4, 128
+    q, k, v, _ = inputs(n, 1, hq, hq, hd, torch.bfloat16, seed=9)
+    o, lse = U().FlashAttention("causal").forward_with_lse(*(to_dev(x, torch.bfloat16) for x in (q, k, v)))
+    o = to_np(o)
+    lse = to_np(lse)
+    for r0 in (0, 4000, n - 128):
+        ref, ref_lse = O.local_attention(q, k, v, "causal", exact=False, rows=(r0, r0 + 128))
+        assert rel_max_err(o[r0:r0 + 128], ref) <= BF16_MAXREL
+        assert np.abs(lse[:, :, r0:r0 + 128] - ref_lse).max() <= 2e-2
