@@ -82,6 +82,10 @@ int ul_comm_export_handle(const ul_comm* comm, void* handle_out);
 /* Map every peer's workspace from world * UL_IPC_HANDLE_BYTES handle bytes
  * (gathered in rank order); validates world size and slot geometry. */
 int ul_comm_open_peers(ul_comm* comm, const void* all_handles);
+/* Host-only check of gathered handles (magic, rank order, world size, slot
+ * geometry) -- the signature check of simgroup.py:265-276 applied to the
+ * group's setup; ul_comm_open_peers runs it first. */
+int ul_comm_validate_handles(const void* all_handles, int world, int rank, size_t slot_bytes);
 /* In-process group (one process driving `world` comms on one device, each
  * on its own stream): wires peer pointers directly.  Used by the 1-GPU
  * parity tests so the same kernels run at P = 2/4/8. */

@@ -27,7 +27,7 @@ IPC_HANDLE_BYTES = 128
 # every symbol include/ulysses_b200.h declares (tests check the exports)
 EXPORTS = (
     "ul_abi_version", "ul_last_error", "ul_comm_create", "ul_comm_export_handle",
-    "ul_comm_open_peers", "ul_comm_link_local", "ul_comm_destroy", "ul_comm_rank",
+    "ul_comm_open_peers", "ul_comm_validate_handles", "ul_comm_link_local", "ul_comm_destroy", "ul_comm_rank",
     "ul_comm_world", "ul_comm_slot_bytes", "ul_comm_set_timeout_ms", "ul_comm_status",
     "ul_comm_ledger", "ul_all_to_all", "ul_all_to_all_slot_bytes", "ul_attn_fwd",
     "ul_attn_bwd_workspace_bytes", "ul_attn_bwd", "ul_attn_bwd_stages", "ul_last_launch_count",
@@ -49,6 +49,7 @@ def _declare(lib):
                                           P(c_vp)]),
         "ul_comm_export_handle": (ctypes.c_int, [c_vp, c_vp]),
         "ul_comm_open_peers": (ctypes.c_int, [c_vp, c_vp]),
+        "ul_comm_validate_handles": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_size_t]),
         "ul_comm_link_local": (ctypes.c_int, [P(c_vp), ctypes.c_int]),
         "ul_comm_destroy": (ctypes.c_int, [c_vp]),
         "ul_comm_rank": (ctypes.c_int, [c_vp]),

@@ -15,6 +15,7 @@ setup); the data path never calls NCCL.
 from __future__ import annotations
 
 import ctypes
+import struct
 from dataclasses import dataclass
 
 import torch
@@ -25,6 +26,33 @@ from .errors import GroupDesyncError, ShardError
 _DTYPES = {torch.float32: _lib.DTYPE_F32, torch.bfloat16: _lib.DTYPE_BF16}
 
 DEFAULT_SLOT_BYTES = 64 << 20
+
+# layout of one rank's handle blob (csrc/a2a.cu HandleBlob): IPC handle,
+# magic, slot bytes, rank, world -- padded to UL_IPC_HANDLE_BYTES
+HANDLE_STRUCT = struct.Struct("<64sQQii")
+HANDLE_MAGIC = 0x554C595353455332
+
+
+def pack_handle(ipc_handle: bytes, slot_bytes: int, rank: int, world: int) -> bytes:
+    blob = HANDLE_STRUCT.pack(ipc_handle.ljust(64, b"\0")[:64], HANDLE_MAGIC, slot_bytes, rank, world)
+    return blob.ljust(_lib.IPC_HANDLE_BYTES, b"\0")
+
+
+def gather_handles(blob: bytes, pg=None) -> bytes:
+    """Rendezvous: every rank contributes its handle blob; returns all blobs
+    concatenated in rank order (the only collective on the setup path)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(pg)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, bytes(blob), group=pg)
+    return b"".join(gathered)
+
+
+def validate_handles(all_blobs: bytes, world: int, rank: int, slot_bytes: int):
+    """Raise GroupDesyncError if the gathered blobs disagree (rank order,
+    group size, workspace geometry)."""
+    buf = ctypes.create_string_buffer(bytes(all_blobs), len(all_blobs))
+    _lib.check(_lib.lib().ul_comm_validate_handles(buf, world, rank, slot_bytes))
 
 
 def label_hash(label: str) -> int:
@@ -109,9 +137,8 @@ class SequenceGroup:
         h = cls._create(rank, world, device, slot_bytes)
         blob = ctypes.create_string_buffer(_lib.IPC_HANDLE_BYTES)
         _lib.check(_lib.lib().ul_comm_export_handle(h, blob))
-        gathered = [None] * world
-        dist.all_gather_object(gathered, bytes(blob.raw), group=pg)
-        allb = ctypes.create_string_buffer(b"".join(gathered), world * _lib.IPC_HANDLE_BYTES)
+        all_blobs = gather_handles(blob.raw, pg)
+        allb = ctypes.create_string_buffer(all_blobs, world * _lib.IPC_HANDLE_BYTES)
         _lib.check(_lib.lib().ul_comm_open_peers(h, allb))
         g = cls(rank, world, device, h, int(_lib.lib().ul_comm_slot_bytes(h)), pg=pg)
         if timeout_ms:

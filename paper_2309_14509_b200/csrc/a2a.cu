@@ -392,22 +392,34 @@ int ul_comm_export_handle(const ul_comm* c, void* handle_out) {
   return UL_OK;
 }
 
-int ul_comm_open_peers(ul_comm* c, const void* all) {
-  if (!c || !all) return fail(UL_ERR_ARG, "ul_comm_open_peers: NULL argument");
-  UL_CUDA(cudaSetDevice(c->device));
+int ul_comm_validate_handles(const void* all, int world, int rank, size_t slot_bytes) {
+  if (!all || world < 1 || world > UL_MAX_RANKS || rank < 0 || rank >= world)
+    return fail(UL_ERR_ARG, "ul_comm_validate_handles: bad arguments");
   const char* p = (const char*)all;
-  for (int r = 0; r < c->world; ++r) {
+  for (int r = 0; r < world; ++r) {
     HandleBlob b;
     memcpy(&b, p + (size_t)r * UL_IPC_HANDLE_BYTES, sizeof(b));
     if (b.magic != kMagic)
       return fail(UL_ERR_DESYNC, "group desync: rank %d sent a malformed comm handle", r);
-    if (b.rank != r || b.world != c->world)
-      return fail(UL_ERR_DESYNC, "group desync: rank %d reports rank %d of %d, expected %d of %d", r,
-                  b.rank, b.world, r, c->world);
-    if (b.slot_bytes != c->slot_bytes)
+    if (b.rank != r || b.world != world)
+      return fail(UL_ERR_DESYNC, "group desync: rank %d reports rank %d of %d, expected %d of %d", r, b.rank,
+                  b.world, r, world);
+    if (b.slot_bytes != slot_bytes)
       return fail(UL_ERR_DESYNC, "group desync: rank %d workspace slot %llu bytes, rank %d has %llu", r,
-                  (unsigned long long)b.slot_bytes, c->rank, (unsigned long long)c->slot_bytes);
+                  (unsigned long long)b.slot_bytes, rank, (unsigned long long)slot_bytes);
+  }
+  return UL_OK;
+}
+
+int ul_comm_open_peers(ul_comm* c, const void* all) {
+  if (!c || !all) return fail(UL_ERR_ARG, "ul_comm_open_peers: NULL argument");
+  UL_TRY(ul_comm_validate_handles(all, c->world, c->rank, c->slot_bytes));
+  UL_CUDA(cudaSetDevice(c->device));
+  const char* p = (const char*)all;
+  for (int r = 0; r < c->world; ++r) {
     if (r == c->rank) continue;
+    HandleBlob b;
+    memcpy(&b, p + (size_t)r * UL_IPC_HANDLE_BYTES, sizeof(b));
     void* ptr = nullptr;
     cudaError_t e = cudaIpcOpenMemHandle(&ptr, b.h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess)

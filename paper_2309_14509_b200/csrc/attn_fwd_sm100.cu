@@ -225,7 +225,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // P_j over the consumed S_j columns [0, BN/2)
 #pragma unroll
       for (int c = 0; c < BN / 64; ++c) tmem_st32(tS[j & 1] + lane_off + c * 32, pk + c * 32);
-      if (rescale) {
+      // tcgen05.ld/st are warp-collective: rescale if any row of the warp
+      // needs it (rows that do not keep alpha == 1)
+      if (__any_sync(0xffffffffu, rescale)) {
         // O must hold the complete sum through PV_{j-1} before it is rescaled
         mbar_wait(o_done, (j - 1) & 1);
         tc_fence_after();
@@ -269,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
+    __syncwarp();
     tc_fence_after();
     tmem_dealloc<512>(tbase);
   }
