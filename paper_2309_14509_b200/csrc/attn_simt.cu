@@ -1,5 +1,6 @@
-// fp32 mode of the local-attention plugin: SIMT FFMA kernels with fp32
-// inputs/outputs and accurate expf/logf, for the reference's fp32 parity
+// fp32 mode of the local-attention plugin: SIMT kernels with fp32
+// inputs/outputs and float64 accumulation/exp/log inside (fp32 outputs then
+// carry only their final rounding), for the reference's fp32 parity
 // contract (rtol 1e-5 vs the f64 oracle; BASELINE config 1).  tcgen05 has
 // no fp32 (only tf32) datapath, so this is the fp32 specialisation of the
 // same plugin, not a second backend.  bf16 runs on attn_fwd_sm100.cu /
@@ -26,12 +27,12 @@ namespace simt {
 constexpr int kWarps = 4;
 constexpr int kMaxT = 8;  // hd <= 256
 
-__device__ __forceinline__ float warp_max(float v) {
+__device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
-__device__ __forceinline__ float warp_sum(float v) {
+__device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
@@ -49,10 +50,10 @@ __device__ __forceinline__ int64_t rowoff(int64_t row, int64_t bb, int64_t head,
   return ((row * b + bb) * h + head) * hd;
 }
 
-__device__ __forceinline__ float dot_row(const float* __restrict__ a_smem, const float* __restrict__ b,
+__device__ __forceinline__ double dot_row(const float* __restrict__ a_smem, const float* __restrict__ b,
                                          int hd) {
-  float s = 0.f;
-  for (int d = 0; d < hd; ++d) s = fmaf(a_smem[d], b[d], s);
+  double s = 0.0;
+  for (int d = 0; d < hd; ++d) s = fma((double)a_smem[d], (double)b[d], s);
   return s;
 }
 
@@ -76,45 +77,45 @@ __global__ void __launch_bounds__(kWarps * 32) fwd_kernel(const float* __restric
   const float* qrow = q + rowoff(i, bb, h, D.b, D.hq, hd);
   for (int d = lane; d < hd; d += 32) qs[d] = qrow[d];
   __syncwarp();
-  float acc[kMaxT];
+  double acc[kMaxT];
 #pragma unroll
-  for (int t = 0; t < kMaxT; ++t) acc[t] = 0.f;
-  float m = -INFINITY, l = 0.f;
+  for (int t = 0; t < kMaxT; ++t) acc[t] = 0.0;
+  double m = -INFINITY, l = 0.0;
   const int64_t jmax = D.causal ? i + 1 : D.n;
   const int64_t kvstride = D.b * D.hkv * hd;
   const float* kbase = k + rowoff(0, bb, g, D.b, D.hkv, hd);
   const float* vbase = v + rowoff(0, bb, g, D.b, D.hkv, hd);
   for (int64_t j0 = 0; j0 < jmax; j0 += 32) {
     const int64_t j = j0 + lane;
-    float s = -INFINITY;
-    if (j < jmax) s = dot_row(qs, kbase + j * kvstride, hd) * D.scale;
-    const float cmax = warp_max(s);
-    const float mnew = fmaxf(m, cmax);
-    const float p = (j < jmax) ? expf(s - mnew) : 0.f;
-    const float alpha = (m == -INFINITY) ? 0.f : expf(m - mnew);
+    double s = -INFINITY;
+    if (j < jmax) s = dot_row(qs, kbase + j * kvstride, hd) * (double)D.scale;
+    const double cmax = warp_max(s);
+    const double mnew = fmax(m, cmax);
+    const double p = (j < jmax) ? exp(s - mnew) : 0.0;
+    const double alpha = (m == -INFINITY) ? 0.0 : exp(m - mnew);
     l = l * alpha + warp_sum(p);
     m = mnew;
 #pragma unroll
     for (int t = 0; t < kMaxT; ++t) acc[t] *= alpha;
     const int cnt = (int)(jmax - j0 < 32 ? jmax - j0 : 32);
     for (int jj = 0; jj < cnt; ++jj) {
-      const float pj = __shfl_sync(0xffffffffu, p, jj);
+      const double pj = __shfl_sync(0xffffffffu, p, jj);
       const float* vr = vbase + (j0 + jj) * kvstride;
 #pragma unroll
       for (int t = 0; t < kMaxT; ++t) {
         const int d = lane + 32 * t;
-        if (d < hd) acc[t] = fmaf(pj, vr[d], acc[t]);
+        if (d < hd) acc[t] = fma(pj, (double)vr[d], acc[t]);
       }
     }
   }
-  const float inv = 1.f / l;
+  const double inv = 1.0 / l;
   float* orow = o + rowoff(i, bb, h, D.b, D.hq, hd);
 #pragma unroll
   for (int t = 0; t < kMaxT; ++t) {
     const int d = lane + 32 * t;
-    if (d < hd) orow[d] = acc[t] * inv;
+    if (d < hd) orow[d] = (float)(acc[t] * inv);
   }
-  if (lane == 0) lse[(bb * D.hq + h) * D.n + i] = m + logf(l);
+  if (lane == 0) lse[(bb * D.hq + h) * D.n + i] = (float)(m + log(l));
 }
 
 // ---- backward pre-pass: D_i = rowsum(dO_i * O_i) ---------------------------
@@ -126,10 +127,10 @@ __global__ void __launch_bounds__(kWarps * 32) dot_kernel(const float* __restric
   if (gw >= D.n * D.b * D.hq) return;
   const int64_t h = gw % D.hq, bb = (gw / D.hq) % D.b, i = gw / (D.hq * D.b);
   const int64_t off = rowoff(i, bb, h, D.b, D.hq, D.hd);
-  float s = 0.f;
-  for (int d = lane; d < D.hd; d += 32) s = fmaf(o[off + d], dout[off + d], s);
+  double s = 0.0;
+  for (int d = lane; d < D.hd; d += 32) s = fma((double)o[off + d], (double)dout[off + d], s);
   s = warp_sum(s);
-  if (lane == 0) Dv[(bb * D.hq + h) * D.n + i] = s;
+  if (lane == 0) Dv[(bb * D.hq + h) * D.n + i] = (float)s;
 }
 
 // ---- dQ: warp per query row -------------------------------------------------
@@ -155,39 +156,39 @@ __global__ void __launch_bounds__(kWarps * 32) dq_kernel(const float* __restrict
     ds_[d] = dout[off + d];
   }
   __syncwarp();
-  const float L = lse[(bb * D.hq + h) * D.n + i];
-  const float Di = Dv[(bb * D.hq + h) * D.n + i];
-  float acc[kMaxT];
+  const double L = lse[(bb * D.hq + h) * D.n + i];
+  const double Di = Dv[(bb * D.hq + h) * D.n + i];
+  double acc[kMaxT];
 #pragma unroll
-  for (int t = 0; t < kMaxT; ++t) acc[t] = 0.f;
+  for (int t = 0; t < kMaxT; ++t) acc[t] = 0.0;
   const int64_t jmax = D.causal ? i + 1 : D.n;
   const int64_t kvstride = D.b * D.hkv * hd;
   const float* kbase = k + rowoff(0, bb, g, D.b, D.hkv, hd);
   const float* vbase = v + rowoff(0, bb, g, D.b, D.hkv, hd);
   for (int64_t j0 = 0; j0 < jmax; j0 += 32) {
     const int64_t j = j0 + lane;
-    float dsc = 0.f;
+    double dsc = 0.0;
     if (j < jmax) {
-      const float s = dot_row(qs, kbase + j * kvstride, hd) * D.scale;
-      const float p = expf(s - L);
-      const float dp = dot_row(ds_, vbase + j * kvstride, hd);
+      const double s = dot_row(qs, kbase + j * kvstride, hd) * (double)D.scale;
+      const double p = exp(s - L);
+      const double dp = dot_row(ds_, vbase + j * kvstride, hd);
       dsc = p * (dp - Di);
     }
     const int cnt = (int)(jmax - j0 < 32 ? jmax - j0 : 32);
     for (int jj = 0; jj < cnt; ++jj) {
-      const float x = __shfl_sync(0xffffffffu, dsc, jj);
+      const double x = __shfl_sync(0xffffffffu, dsc, jj);
       const float* kr = kbase + (j0 + jj) * kvstride;
 #pragma unroll
       for (int t = 0; t < kMaxT; ++t) {
         const int d = lane + 32 * t;
-        if (d < hd) acc[t] = fmaf(x, kr[d], acc[t]);
+        if (d < hd) acc[t] = fma(x, (double)kr[d], acc[t]);
       }
     }
   }
 #pragma unroll
   for (int t = 0; t < kMaxT; ++t) {
     const int d = lane + 32 * t;
-    if (d < hd) dq[off + d] = acc[t] * D.scale;
+    if (d < hd) dq[off + d] = (float)(acc[t] * (double)D.scale);
   }
 }
 
@@ -214,9 +215,9 @@ __global__ void __launch_bounds__(kWarps * 32) dkdv_kernel(const float* __restri
     vs[d] = v[off + d];
   }
   __syncwarp();
-  float ak[kMaxT], av[kMaxT];
+  double ak[kMaxT], av[kMaxT];
 #pragma unroll
-  for (int t = 0; t < kMaxT; ++t) ak[t] = av[t] = 0.f;
+  for (int t = 0; t < kMaxT; ++t) ak[t] = av[t] = 0.0;
   const int64_t group = D.hq / D.hkv;
   const int64_t qstride = D.b * D.hq * hd;
   const int64_t i0 = D.causal ? j : 0;
@@ -228,25 +229,25 @@ __global__ void __launch_bounds__(kWarps * 32) dkdv_kernel(const float* __restri
     const float* Db = Dv + (bb * D.hq + h) * D.n;
     for (int64_t c0 = i0; c0 < D.n; c0 += 32) {
       const int64_t i = c0 + lane;
-      float p = 0.f, dsc = 0.f;
+      double p = 0.0, dsc = 0.0;
       if (i < D.n) {
-        const float s = dot_row(ks, qb + i * qstride, hd) * D.scale;
-        p = expf(s - Lb[i]);
-        const float dp = dot_row(vs, db + i * qstride, hd);
-        dsc = p * (dp - Db[i]);
+        const double s = dot_row(ks, qb + i * qstride, hd) * (double)D.scale;
+        p = exp(s - (double)Lb[i]);
+        const double dp = dot_row(vs, db + i * qstride, hd);
+        dsc = p * (dp - (double)Db[i]);
       }
       const int cnt = (int)(D.n - c0 < 32 ? D.n - c0 : 32);
       for (int ii = 0; ii < cnt; ++ii) {
-        const float pi = __shfl_sync(0xffffffffu, p, ii);
-        const float si = __shfl_sync(0xffffffffu, dsc, ii);
+        const double pi = __shfl_sync(0xffffffffu, p, ii);
+        const double si = __shfl_sync(0xffffffffu, dsc, ii);
         const float* qr = qb + (c0 + ii) * qstride;
         const float* dr = db + (c0 + ii) * qstride;
 #pragma unroll
         for (int t = 0; t < kMaxT; ++t) {
           const int d = lane + 32 * t;
           if (d < hd) {
-            av[t] = fmaf(pi, dr[d], av[t]);
-            ak[t] = fmaf(si, qr[d], ak[t]);
+            av[t] = fma(pi, (double)dr[d], av[t]);
+            ak[t] = fma(si, (double)qr[d], ak[t]);
           }
         }
       }
@@ -256,8 +257,8 @@ __global__ void __launch_bounds__(kWarps * 32) dkdv_kernel(const float* __restri
   for (int t = 0; t < kMaxT; ++t) {
     const int d = lane + 32 * t;
     if (d < hd) {
-      dk[off + d] = ak[t] * D.scale;
-      dv[off + d] = av[t];
+      dk[off + d] = (float)(ak[t] * (double)D.scale);
+      dv[off + d] = (float)av[t];
     }
   }
 }

@@ -34,9 +34,11 @@ def run_layer(p, q, k, v, do, mask, dtype, backward=True, slot_bytes=16 << 20):
     attn = U().FlashAttention(mask)
     layers = [U().DistributedAttention(attn, g) for g in groups]
     sh = lambda x, r: to_dev(x[r * nl:(r + 1) * nl], dtype).requires_grad_(backward)
-    ins = [[sh(x, r) for x in (q, k, v)] for r in range(p)]
-    dos = [to_dev(do[r * nl:(r + 1) * nl], dtype) for r in range(p)]
-    torch.cuda.synchronize()
+    # every rank's tensors (leaves and incoming grads) live on that rank's
+    # stream, so autograd never couples two ranks' streams (a rank's device
+    # wait would then block its peer's push on a shared stream)
+    ins = run_ranks(groups, lambda r: [sh(x, r) for x in (q, k, v)])
+    dos = run_ranks(groups, lambda r: to_dev(do[r * nl:(r + 1) * nl], dtype))
 
     def fwd(r):
         return layers[r](*ins[r])
