@@ -67,6 +67,12 @@ extern "C" {
 
 int         ul_abi_version(void);
 const char* ul_last_error(void);
+/* Load every kernel of the library into the current context now.  CUDA's
+ * lazy loading would otherwise load a kernel at its first launch, which can
+ * stall the launching thread while one of this rank's flag-wait kernels
+ * spins -- a deadlock when several ranks share one process (local groups).
+ * ul_comm_create calls it. */
+int         ul_preload_kernels(void);
 
 /* ======================================================================
  * Sequence-parallel group: one process per GPU.  Each rank owns a

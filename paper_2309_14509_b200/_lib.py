@@ -26,7 +26,7 @@ IPC_HANDLE_BYTES = 128
 
 # every symbol include/ulysses_b200.h declares (tests check the exports)
 EXPORTS = (
-    "ul_abi_version", "ul_last_error", "ul_comm_create", "ul_comm_export_handle",
+    "ul_abi_version", "ul_last_error", "ul_preload_kernels", "ul_comm_create", "ul_comm_export_handle",
     "ul_comm_open_peers", "ul_comm_validate_handles", "ul_comm_link_local", "ul_comm_destroy", "ul_comm_rank",
     "ul_comm_world", "ul_comm_slot_bytes", "ul_comm_set_timeout_ms", "ul_comm_status",
     "ul_comm_ledger", "ul_all_to_all", "ul_all_to_all_slot_bytes", "ul_attn_fwd",
@@ -45,6 +45,7 @@ def _declare(lib):
     sig = {
         "ul_abi_version": (ctypes.c_int, []),
         "ul_last_error": (ctypes.c_char_p, []),
+        "ul_preload_kernels": (ctypes.c_int, []),
         "ul_comm_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_size_t,
                                           P(c_vp)]),
         "ul_comm_export_handle": (ctypes.c_int, [c_vp, c_vp]),

@@ -327,11 +327,20 @@ static int launch_copy(CopyParams& p, cudaStream_t st, const char* name) {
   return launched(name);
 }
 
+int preload_a2a() {
+  cudaFuncAttributes a;
+  UL_CUDA(cudaFuncGetAttributes(&a, a2a_copy_kernel));
+  UL_CUDA(cudaFuncGetAttributes(&a, a2a_wait_kernel));
+  return UL_OK;
+}
+
 }  // namespace ul
 
 using namespace ul;
 
 extern "C" {
+
+int ul_preload_kernels(void);
 
 int ul_comm_create(int rank, int world, int device, size_t slot_bytes, ul_comm** out) {
   if (!out) return fail(UL_ERR_ARG, "ul_comm_create: out is NULL");
@@ -340,6 +349,7 @@ int ul_comm_create(int rank, int world, int device, size_t slot_bytes, ul_comm**
     return fail(UL_ERR_ARG, "group size must be in [1, %d], got %d", UL_MAX_RANKS, world);
   if (rank < 0 || rank >= world) return fail(UL_ERR_ARG, "rank %d outside group of %d", rank, world);
   UL_CUDA(cudaSetDevice(device));
+  UL_TRY(ul_preload_kernels());
   ul_comm* c = new ul_comm();
   c->rank = rank;
   c->world = world;

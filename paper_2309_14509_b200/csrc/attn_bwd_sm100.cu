@@ -11,13 +11,16 @@
 // Three launches, no atomics (deterministic, so results are P-invariant
 // bit for bit):
 //   bwd_prep   D = rowsum(dO*O) and LSE*log2(e) into padded f32 rows
-//   bwd_dkdv   one CTA per (kv tile, kv head): loops over the group's
-//              query heads and the visible query tiles; S^T = K Q^T and
-//              dP^T = V dO^T land in TMEM (kv rows on lanes), softmax warps
-//              write P^T / dS^T back to TMEM as bf16, then
-//              dV += P^T dO and dK += dS^T Q (TS MMAs) accumulate in TMEM.
-//   bwd_dq     one CTA per (query tile, head): S = Q K^T, dP = dO V^T,
-//              dS -> TMEM, dQ += dS K.
+//   bwd_dkdv   one CTA per (128-row kv tile, kv head); loops over the
+//              group's query heads and the visible 64-row query sub-tiles.
+//              S^T = K Q^T and dP^T = V dO^T (SS, M = 128 kv rows, N = 64)
+//              go to one of two TMEM buffers; softmax warps (thread = kv
+//              row) write P^T / dS^T back over them as bf16; dV += P^T dO
+//              and dK += dS^T Q are TS MMAs.  Double-buffered TMEM lets the
+//              MMAs of sub-tile i+1 run while the softmax of sub-tile i does.
+//   bwd_dq     one CTA per (128-row query tile, head): 64-row kv sub-tiles,
+//              S = Q K^T, dP = dO V^T (double-buffered), dS -> TMEM,
+//              dQ += dS K.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -33,10 +36,12 @@ namespace bwd {
 
 using namespace sm100;
 
-constexpr int BM = 128;   // query tile
-constexpr int BN = 128;   // key tile
+constexpr int BT = 128;           // the tile a CTA owns (kv tile for dkdv, q tile for dq)
+constexpr int BS = 64;            // the sub-tile streamed against it
+constexpr int NST = 3;            // streamed-operand pipeline stages
 constexpr int kThreads = 192;
-constexpr int kAtom = 128 * 128;  // SW128 atom column of a 128-row tile
+constexpr int kAtomT = BT * 128;  // SW128 atom column of a 128-row tile (16 KB)
+constexpr int kAtomS = BS * 128;  // ... of a 64-row sub-tile (8 KB)
 
 struct Params {
   int n, n_pad, b, hq, hkv;
@@ -94,17 +99,39 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
   }
 }
 
+// TMEM epilogue: a 128-lane x HD fp32 accumulator -> bf16 rows (x mul)
+template <int HD>
+__device__ __forceinline__ void store_acc_rows(uint32_t tacc, uint32_t lane_off, float mul, __nv_bfloat16* dst,
+                                               bool valid) {
+#pragma unroll
+  for (int c = 0; c < HD / 32; ++c) {
+    uint32_t v[32];
+    tmem_ld32(tacc + lane_off + c * 32, v);   // warp-collective: every lane executes it
+    tmem_wait_ld();
+    uint32_t pkd[16];
+#pragma unroll
+    for (int x = 0; x < 16; ++x)
+      pkd[x] = pack_bf16(__uint_as_float(v[2 * x]) * mul, __uint_as_float(v[2 * x + 1]) * mul);
+    if (valid) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+      for (int x = 0; x < 4; ++x) d4[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+    }
+  }
+}
+
 // ---- dK / dV -----------------------------------------------------------------
 template <int HD>
 struct DkdvSmem {
-  static constexpr int kTile = (HD / 64) * kAtom;
+  static constexpr int kTileT = (HD / 64) * kAtomT;   // 128 x HD
+  static constexpr int kTileS = (HD / 64) * kAtomS;   // 64 x HD
   static constexpr int kK = 0;
-  static constexpr int kV = kK + kTile;
-  static constexpr int kQ = kV + kTile;          // [2] stages
-  static constexpr int kO = kQ + 2 * kTile;      // dO [2]
-  static constexpr int kL = kO + 2 * kTile;      // [2][BM] f32
-  static constexpr int kD = kL + 2 * BM * 4;     // [2][BM] f32
-  static constexpr int kBar = kD + 2 * BM * 4;
+  static constexpr int kV = kK + kTileT;
+  static constexpr int kQ = kV + kTileT;              // [NST]
+  static constexpr int kO = kQ + NST * kTileS;        // dO [NST]
+  static constexpr int kL = kO + NST * kTileS;        // [NST][BS] f32
+  static constexpr int kD = kL + NST * BS * 4;        // [NST][BS] f32
+  static constexpr int kBar = kD + NST * BS * 4;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
 
@@ -124,35 +151,36 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* sD = reinterpret_cast<float*>(smem + S::kD);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint64_t* kv_full = bars + 0;
-  uint64_t* q_full = bars + 1;   // [2]
-  uint64_t* q_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_full = bars + 6;
-  uint64_t* m_done = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* q_full = bars + 1;                 // [NST]
+  uint64_t* q_empty = bars + 1 + NST;          // [NST]
+  uint64_t* s_full = bars + 1 + 2 * NST;       // [2]
+  uint64_t* p_full = bars + 3 + 2 * NST;       // [2]
+  uint64_t* buf_free = bars + 5 + 2 * NST;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 2 * NST);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkv = (p.n + BN - 1) / BN;
   const int heads = p.b * p.hkv;
   const int kt = (int)(blockIdx.x / heads);      // ascending kv tile == longest first (causal)
   const int bg = (int)(blockIdx.x % heads);
   const int bb = bg / p.hkv, g = bg % p.hkv;
   const int group = p.hq / p.hkv;
-  const int kv0 = kt * BN;
-  const int nq = (p.n + BM - 1) / BM;
-  const int i0 = p.causal ? kv0 / BM : 0;
-  const int per_head = nq - i0;
+  const int kv0 = kt * BT;
+  const int nsub = (p.n + BS - 1) / BS;
+  const int i0 = p.causal ? kv0 / BS : 0;
+  const int per_head = nsub - i0;
   const int total = per_head * group;
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
-    mbar_init(m_done, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 128);
+      mbar_init(&buf_free[s], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -160,8 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t tSt = tbase, tdPt = tbase + 128, tdV = tbase + 256, tdK = tbase + 256 + HD;
-  (void)nkv;
+  // TMEM: S^T[2] at 0/64, dP^T[2] at 128/192, dV at 256, dK at 256+HD
+  const uint32_t tdV = tbase + 256, tdK = tbase + 256 + HD;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -169,64 +197,72 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
       tma_prefetch_desc(&tmO);
-      mbar_expect_tx(kv_full, 2 * BN * HD * 2);
+      mbar_expect_tx(kv_full, 2 * BT * HD * 2);
 #pragma unroll
       for (int a = 0; a < HD / 64; ++a) {
-        tma_load_3d(sK + a * kAtom, &tmK, kv_full, a * 64, bb * p.hkv + g, kv0);
-        tma_load_3d(sV + a * kAtom, &tmV, kv_full, a * 64, bb * p.hkv + g, kv0);
+        tma_load_3d(sK + a * kAtomT, &tmK, kv_full, a * 64, bb * p.hkv + g, kv0);
+        tma_load_3d(sV + a * kAtomT, &tmV, kv_full, a * 64, bb * p.hkv + g, kv0);
       }
       for (int it = 0; it < total; ++it) {
         const int h = g * group + it / per_head;
         const int qi = i0 + it % per_head;
-        const int s = it & 1;
-        mbar_wait(&q_empty[s], ((it >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[s], 2 * BM * HD * 2 + 2 * BM * 4);
+        const int s = it % NST;
+        mbar_wait(&q_empty[s], ((it / NST) & 1) ^ 1);
+        mbar_expect_tx(&q_full[s], 2 * BS * HD * 2 + 2 * BS * 4);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a) {
-          tma_load_3d(sQ + s * S::kTile + a * kAtom, &tmQ, &q_full[s], a * 64, bb * p.hq + h, qi * BM);
-          tma_load_3d(sO + s * S::kTile + a * kAtom, &tmO, &q_full[s], a * 64, bb * p.hq + h, qi * BM);
+          tma_load_3d(sQ + s * S::kTileS + a * kAtomS, &tmQ, &q_full[s], a * 64, bb * p.hq + h, qi * BS);
+          tma_load_3d(sO + s * S::kTileS + a * kAtomS, &tmO, &q_full[s], a * 64, bb * p.hq + h, qi * BS);
         }
-        const int64_t roff = ((int64_t)bb * p.hq + h) * p.n_pad + qi * BM;
-        bulk_load(sL + s * BM, p.L2 + roff, BM * 4, &q_full[s]);
-        bulk_load(sD + s * BM, p.Dv + roff, BM * 4, &q_full[s]);
+        const int64_t roff = ((int64_t)bb * p.hq + h) * p.n_pad + qi * BS;
+        bulk_load(sL + s * BS, p.L2 + roff, BS * 4, &q_full[s]);
+        bulk_load(sD + s * BS, p.Dv + roff, BS * 4, &q_full[s]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t kIdS = idesc_bf16(BN, BM, 0, 0);   // M = kv rows, N = q rows
-      constexpr uint32_t kIdG = idesc_bf16(BN, HD, 0, 1);   // M = kv rows, N = hd, B MN-major
+      constexpr uint32_t kIdS = idesc_bf16(BT, BS, 0, 0);   // M = kv rows, N = 64 q rows
+      constexpr uint32_t kIdG = idesc_bf16(BT, HD, 0, 1);   // M = kv rows, N = hd, B MN-major
       const uint32_t kaddr = smem_u32(sK), vaddr = smem_u32(sV);
+      auto issue_grads = [&](int i) {
+        const int b = i & 1, s = i % NST;
+        const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
+        mbar_wait(&p_full[b], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t qaddr = smem_u32(sQ + s * S::kTileS), oaddr = smem_u32(sO + s * S::kTileS);
+#pragma unroll
+        for (int kk = 0; kk < BS / 16; ++kk)
+          mma_ts(tdV, tSt + kk * 8, sdesc(oaddr + kk * 2048, kAtomS, 1024), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < BS / 16; ++kk)
+          mma_ts(tdK, tdPt + kk * 8, sdesc(qaddr + kk * 2048, kAtomS, 1024), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&q_empty[s]);
+        mma_commit(&buf_free[b]);
+      };
       mbar_wait(kv_full, 0);
       for (int it = 0; it < total; ++it) {
-        const int s = it & 1;
-        if (it > 0) mbar_wait(m_done, (it - 1) & 1);
-        mbar_wait(&q_full[s], (it >> 1) & 1);
+        const int b = it & 1, s = it % NST;
+        const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
+        if (it >= 2) mbar_wait(&buf_free[b], ((it - 2) >> 1) & 1);
+        mbar_wait(&q_full[s], (it / NST) & 1);
         tc_fence_after();
-        const uint32_t qaddr = smem_u32(sQ + s * S::kTile), oaddr = smem_u32(sO + s * S::kTile);
+        const uint32_t qaddr = smem_u32(sQ + s * S::kTileS), oaddr = smem_u32(sO + s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
-          mma_ss(tSt, sdesc(kaddr + off, 16, 1024), sdesc(qaddr + off, 16, 1024), kIdS, kk > 0 ? 1u : 0u);
+          const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
+          const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
+          mma_ss(tSt, sdesc(kaddr + offT, 16, 1024), sdesc(qaddr + offS, 16, 1024), kIdS, kk > 0 ? 1u : 0u);
         }
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
-          mma_ss(tdPt, sdesc(vaddr + off, 16, 1024), sdesc(oaddr + off, 16, 1024), kIdS, kk > 0 ? 1u : 0u);
+          const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
+          const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
+          mma_ss(tdPt, sdesc(vaddr + offT, 16, 1024), sdesc(oaddr + offS, 16, 1024), kIdS, kk > 0 ? 1u : 0u);
         }
-        mma_commit(s_full);
-        mbar_wait(p_full, it & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < BM / 16; ++kk) {
-          mma_ts(tdV, tSt + kk * 8, sdesc(oaddr + kk * 2048, kAtom, 1024), kIdG, (it > 0 || kk > 0) ? 1u : 0u);
-        }
-#pragma unroll
-        for (int kk = 0; kk < BM / 16; ++kk) {
-          mma_ts(tdK, tdPt + kk * 8, sdesc(qaddr + kk * 2048, kAtom, 1024), kIdG, (it > 0 || kk > 0) ? 1u : 0u);
-        }
-        mma_commit(&q_empty[s]);
-        mma_commit(m_done);
+        mma_commit(&s_full[b]);
+        if (it >= 1) issue_grads(it - 1);
       }
+      issue_grads(total - 1);
     }
   } else {
     const int quarter = warp & 3;
@@ -234,20 +270,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int kvrow = kv0 + row;
     for (int it = 0; it < total; ++it) {
-      const int s = it & 1;
-      const int qi = i0 + it % per_head;
-      const int q0 = qi * BM;
-      mbar_wait(&q_full[s], (it >> 1) & 1);
-      mbar_wait(s_full, it & 1);
+      const int b = it & 1, s = it % NST;
+      const int q0 = (i0 + it % per_head) * BS;
+      const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
+      mbar_wait(&q_full[s], (it / NST) & 1);
+      mbar_wait(&s_full[b], (it >> 1) & 1);
       tc_fence_after();
-      const float* L = sL + s * BM;
-      const float* Dd = sD + s * BM;
-      // visible query columns: q >= kv (causal)
-      const int first = p.causal ? kvrow - q0 : 0;   // columns c < first are masked
+      const float* L = sL + s * BS;
+      const float* Dd = sD + s * BS;
+      const int first = p.causal ? kvrow - q0 : 0;   // query columns c < first are masked (q < kv)
       // 32-column chunks: P^T / dS^T of chunk c overwrite TMEM columns
-      // [16c, 16c+16), which were consumed by chunk c' <= c
+      // [16c, 16c+16) of the same buffer, already consumed by chunk c' <= c
 #pragma unroll
-      for (int c = 0; c < BM / 32; ++c) {
+      for (int c = 0; c < BS / 32; ++c) {
         uint32_t r[32], d[32];
         tmem_ld32(tSt + lane_off + c * 32, r);
         tmem_ld32(tdPt + lane_off + c * 32, d);
@@ -268,34 +303,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[b]);
     }
     // epilogue: dV, dK * scale -> bf16 rows of kv head g
-    mbar_wait(m_done, (total - 1) & 1);
+    mbar_wait(&buf_free[(total - 1) & 1], ((total - 1) >> 1) & 1);
     tc_fence_after();
     const bool valid = kvrow < p.n;
     const int64_t off = (((int64_t)kvrow * p.b + bb) * p.hkv + g) * HD;
-#pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      const uint32_t tacc = which == 0 ? tdV : tdK;
-      const float mul = which == 0 ? 1.f : p.scale;
-      __nv_bfloat16* dst = (which == 0 ? p.dv : p.dk) + off;
-#pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(tacc + lane_off + c * 32, v);
-        tmem_wait_ld();
-        uint32_t pkd[16];
-#pragma unroll
-        for (int x = 0; x < 16; ++x)
-          pkd[x] = pack_bf16(__uint_as_float(v[2 * x]) * mul, __uint_as_float(v[2 * x + 1]) * mul);
-        if (valid) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-          for (int x = 0; x < 4; ++x) d4[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
-        }
-      }
-    }
+    store_acc_rows<HD>(tdV, lane_off, 1.f, p.dv + off, valid);
+    store_acc_rows<HD>(tdK, lane_off, p.scale, p.dk + off, valid);
   }
   tc_fence_before();
   __syncthreads();
@@ -309,12 +325,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ---- dQ ------------------------------------------------------------------------
 template <int HD>
 struct DqSmem {
-  static constexpr int kTile = (HD / 64) * kAtom;
+  static constexpr int kTileT = (HD / 64) * kAtomT;
+  static constexpr int kTileS = (HD / 64) * kAtomS;
   static constexpr int kQ = 0;
-  static constexpr int kO = kQ + kTile;
-  static constexpr int kK = kO + kTile;          // [2]
-  static constexpr int kV = kK + 2 * kTile;      // [2]
-  static constexpr int kBar = kV + 2 * kTile;
+  static constexpr int kO = kQ + kTileT;
+  static constexpr int kK = kO + kTileT;          // [NST]
+  static constexpr int kV = kK + NST * kTileS;    // [NST]
+  static constexpr int kBar = kV + NST * kTileS;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
 
@@ -332,33 +349,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sV = smem + S::kV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* p_full = bars + 6;
-  uint64_t* m_done = bars + 7;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* kv_full = bars + 1;                // [NST]
+  uint64_t* kv_empty = bars + 1 + NST;         // [NST]
+  uint64_t* s_full = bars + 1 + 2 * NST;       // [2]
+  uint64_t* p_full = bars + 3 + 2 * NST;       // [2]
+  uint64_t* buf_free = bars + 5 + 2 * NST;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 2 * NST);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int heads = p.b * p.hq;
-  const int qtiles = (p.n + BM - 1) / BM;
+  const int qtiles = (p.n + BT - 1) / BT;
   const int qt = qtiles - 1 - (int)(blockIdx.x / heads);   // longest first
   const int bh = (int)(blockIdx.x % heads);
   const int bb = bh / p.hq, h = bh % p.hq;
   const int g = h / (p.hq / p.hkv);
-  const int q0 = qt * BM;
-  const int nkv_all = (p.n + BN - 1) / BN;
-  const int nkv = p.causal ? min(nkv_all, (q0 + BM - 1) / BN + 1) : nkv_all;
+  const int q0 = qt * BT;
+  const int nsub_all = (p.n + BS - 1) / BS;
+  const int nsub = p.causal ? min(nsub_all, (q0 + BT - 1) / BS + 1) : nsub_all;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
-    mbar_init(m_done, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 128);
+      mbar_init(&buf_free[s], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -366,7 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t tS = tbase, tdP = tbase + 128, tdQ = tbase + 256;
+  // TMEM: S[2] at 0/64, dP[2] at 128/192 (dS written over dP), dQ at 256
+  const uint32_t tdQ = tbase + 256;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -374,54 +394,64 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
       tma_prefetch_desc(&tmO);
-      mbar_expect_tx(q_full, 2 * BM * HD * 2);
+      mbar_expect_tx(q_full, 2 * BT * HD * 2);
 #pragma unroll
       for (int a = 0; a < HD / 64; ++a) {
-        tma_load_3d(sQ + a * kAtom, &tmQ, q_full, a * 64, bb * p.hq + h, q0);
-        tma_load_3d(sO + a * kAtom, &tmO, q_full, a * 64, bb * p.hq + h, q0);
+        tma_load_3d(sQ + a * kAtomT, &tmQ, q_full, a * 64, bb * p.hq + h, q0);
+        tma_load_3d(sO + a * kAtomT, &tmO, q_full, a * 64, bb * p.hq + h, q0);
       }
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j & 1;
-        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[s], 2 * BN * HD * 2);
+      for (int j = 0; j < nsub; ++j) {
+        const int s = j % NST;
+        mbar_wait(&kv_empty[s], ((j / NST) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[s], 2 * BS * HD * 2);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a) {
-          tma_load_3d(sK + s * S::kTile + a * kAtom, &tmK, &kv_full[s], a * 64, bb * p.hkv + g, j * BN);
-          tma_load_3d(sV + s * S::kTile + a * kAtom, &tmV, &kv_full[s], a * 64, bb * p.hkv + g, j * BN);
+          tma_load_3d(sK + s * S::kTileS + a * kAtomS, &tmK, &kv_full[s], a * 64, bb * p.hkv + g, j * BS);
+          tma_load_3d(sV + s * S::kTileS + a * kAtomS, &tmV, &kv_full[s], a * 64, bb * p.hkv + g, j * BS);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t kIdS = idesc_bf16(BM, BN, 0, 0);
-      constexpr uint32_t kIdG = idesc_bf16(BM, HD, 0, 1);
+      constexpr uint32_t kIdS = idesc_bf16(BT, BS, 0, 0);
+      constexpr uint32_t kIdG = idesc_bf16(BT, HD, 0, 1);
       const uint32_t qaddr = smem_u32(sQ), oaddr = smem_u32(sO);
-      mbar_wait(q_full, 0);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j & 1;
-        if (j > 0) mbar_wait(m_done, (j - 1) & 1);
-        mbar_wait(&kv_full[s], (j >> 1) & 1);
+      auto issue_dq = [&](int i) {
+        const int b = i & 1, s = i % NST;
+        const uint32_t tdP = tbase + 128 + b * 64;
+        mbar_wait(&p_full[b], (i >> 1) & 1);
         tc_fence_after();
-        const uint32_t kaddr = smem_u32(sK + s * S::kTile), vaddr = smem_u32(sV + s * S::kTile);
+        const uint32_t kaddr = smem_u32(sK + s * S::kTileS);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
-          mma_ss(tS, sdesc(qaddr + off, 16, 1024), sdesc(kaddr + off, 16, 1024), kIdS, kk > 0 ? 1u : 0u);
-        }
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
-          mma_ss(tdP, sdesc(oaddr + off, 16, 1024), sdesc(vaddr + off, 16, 1024), kIdS, kk > 0 ? 1u : 0u);
-        }
-        mma_commit(s_full);
-        mbar_wait(p_full, j & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)
-          mma_ts(tdQ, tdP + kk * 8, sdesc(kaddr + kk * 2048, kAtom, 1024), kIdG, (j > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < BS / 16; ++kk)
+          mma_ts(tdQ, tdP + kk * 8, sdesc(kaddr + kk * 2048, kAtomS, 1024), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&kv_empty[s]);
-        mma_commit(m_done);
+        mma_commit(&buf_free[b]);
+      };
+      mbar_wait(q_full, 0);
+      for (int j = 0; j < nsub; ++j) {
+        const int b = j & 1, s = j % NST;
+        const uint32_t tS = tbase + b * 64, tdP = tbase + 128 + b * 64;
+        if (j >= 2) mbar_wait(&buf_free[b], ((j - 2) >> 1) & 1);
+        mbar_wait(&kv_full[s], (j / NST) & 1);
+        tc_fence_after();
+        const uint32_t kaddr = smem_u32(sK + s * S::kTileS), vaddr = smem_u32(sV + s * S::kTileS);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
+          const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
+          mma_ss(tS, sdesc(qaddr + offT, 16, 1024), sdesc(kaddr + offS, 16, 1024), kIdS, kk > 0 ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
+          const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
+          mma_ss(tdP, sdesc(oaddr + offT, 16, 1024), sdesc(vaddr + offS, 16, 1024), kIdS, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[b]);
+        if (j >= 1) issue_dq(j - 1);
       }
+      issue_dq(nsub - 1);
     }
   } else {
     const int quarter = warp & 3;
@@ -431,13 +461,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t roff = ((int64_t)bb * p.hq + h) * p.n_pad + qrow;
     const float L = p.L2[roff];
     const float Dr = p.Dv[roff];
-    for (int j = 0; j < nkv; ++j) {
-      const int kv0 = j * BN;
-      mbar_wait(s_full, j & 1);
+    for (int j = 0; j < nsub; ++j) {
+      const int b = j & 1;
+      const int kv0 = j * BS;
+      const uint32_t tS = tbase + b * 64, tdP = tbase + 128 + b * 64;
+      mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
-      const int limit = p.causal ? qrow - kv0 + 1 : BN;   // columns c >= limit are masked
+      const int limit = p.causal ? qrow - kv0 + 1 : BS;   // columns c >= limit are masked
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < BS / 32; ++c) {
         uint32_t r[32], d[32];
         tmem_ld32(tS + lane_off + c * 32, r);
         tmem_ld32(tdP + lane_off + c * 32, d);
@@ -456,27 +488,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[b]);
     }
-    mbar_wait(m_done, (nkv - 1) & 1);
+    mbar_wait(&buf_free[(nsub - 1) & 1], ((nsub - 1) >> 1) & 1);
     tc_fence_after();
-    const bool valid = qrow < p.n;
-    __nv_bfloat16* dst = p.dq + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD;
-#pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld32(tdQ + lane_off + c * 32, v);   // warp-collective: executed by every lane
-      tmem_wait_ld();
-      uint32_t pkd[16];
-#pragma unroll
-      for (int x = 0; x < 16; ++x)
-        pkd[x] = pack_bf16(__uint_as_float(v[2 * x]) * p.scale, __uint_as_float(v[2 * x + 1]) * p.scale);
-      if (valid) {
-        uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-        for (int x = 0; x < 4; ++x) d4[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
-      }
-    }
+    store_acc_rows<HD>(tdQ, lane_off, p.scale, p.dq + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD,
+                       qrow < p.n);
   }
   tc_fence_before();
   __syncthreads();
@@ -503,11 +520,6 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
                                                 (int)n, (int)npad, (int)b, (int)hq);
     UL_TRY(launched("attn_bwd_prep"));
   }
-  CUtensorMap mq, mk, mv, mo;
-  UL_TRY(make_tmap_bhsd(&mq, q, n, b * hq, HD, 128));
-  UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, 128));
-  UL_TRY(make_tmap_bhsd(&mv, v, n, b * hkv, HD, 128));
-  UL_TRY(make_tmap_bhsd(&mo, dout, n, b * hq, HD, 128));
   Params p;
   p.n = (int)n;
   p.n_pad = (int)npad;
@@ -529,12 +541,24 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
     UL_CUDA(cudaFuncSetAttribute(bwd_dq_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqSmem<HD>::kBytes));
     attr = true;
   }
-  const int64_t tiles = (n + 127) / 128;
+  const int64_t tiles = (n + BT - 1) / BT;
   if (stages & 2) {
+    // dkdv: the kv tile is resident (128-row boxes), query sub-tiles stream (64-row boxes)
+    CUtensorMap mq, mk, mv, mo;
+    UL_TRY(make_tmap_bhsd(&mq, q, n, b * hq, HD, BS));
+    UL_TRY(make_tmap_bhsd(&mo, dout, n, b * hq, HD, BS));
+    UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, BT));
+    UL_TRY(make_tmap_bhsd(&mv, v, n, b * hkv, HD, BT));
     bwd_dkdv_kernel<HD><<<(unsigned)(tiles * b * hkv), kThreads, DkdvSmem<HD>::kBytes, st>>>(mq, mk, mv, mo, p);
     UL_TRY(launched("attn_bwd_dkdv_sm100"));
   }
   if (stages & 4) {
+    // dq: the query tile is resident, key/value sub-tiles stream
+    CUtensorMap mq, mk, mv, mo;
+    UL_TRY(make_tmap_bhsd(&mq, q, n, b * hq, HD, BT));
+    UL_TRY(make_tmap_bhsd(&mo, dout, n, b * hq, HD, BT));
+    UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, BS));
+    UL_TRY(make_tmap_bhsd(&mv, v, n, b * hkv, HD, BS));
     bwd_dq_kernel<HD><<<(unsigned)(tiles * b * hq), kThreads, DqSmem<HD>::kBytes, st>>>(mq, mk, mv, mo, p);
     UL_TRY(launched("attn_bwd_dq_sm100"));
   }
@@ -542,6 +566,17 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
 }
 
 }  // namespace bwd
+
+int preload_bwd() {
+  cudaFuncAttributes a;
+  UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_prep_kernel<64>));
+  UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_prep_kernel<128>));
+  UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dkdv_kernel<64>));
+  UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dkdv_kernel<128>));
+  UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dq_kernel<64>));
+  UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dq_kernel<128>));
+  return UL_OK;
+}
 
 size_t sm100_bwd_workspace(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd) {
   (void)hkv;
@@ -556,7 +591,8 @@ int sm100_bwd(const void* q, const void* k, const void* v, const void* o, const 
   if (n > INT32_MAX / 2) return fail(UL_ERR_SHAPE, "attention: sequence too long (n=%lld)", (long long)n);
   switch (hd) {
     case 64: return bwd::launch<64>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, st);
-    case 128: return bwd::launch<128>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, st);
+    case 128:
+      return bwd::launch<128>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, st);
     default:
       return fail(UL_ERR_KERNEL, "bf16 attention supports head_dim 64 or 128, got %lld", (long long)hd);
   }

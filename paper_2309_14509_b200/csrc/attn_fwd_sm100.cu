@@ -307,6 +307,13 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
 
 }  // namespace fwd
 
+int preload_fwd() {
+  cudaFuncAttributes a;
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_kernel<64>));
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_kernel<128>));
+  return UL_OK;
+}
+
 int sm100_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
               int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st) {
   if (n == 0 || b == 0 || hq == 0) return UL_OK;

@@ -263,9 +263,20 @@ __global__ void __launch_bounds__(kWarps * 32) dkdv_kernel(const float* __restri
   }
 }
 
+int preload() {
+  cudaFuncAttributes a;
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd_kernel));
+  UL_CUDA(cudaFuncGetAttributes(&a, dot_kernel));
+  UL_CUDA(cudaFuncGetAttributes(&a, dq_kernel));
+  UL_CUDA(cudaFuncGetAttributes(&a, dkdv_kernel));
+  return UL_OK;
+}
+
 static unsigned blocks_for(int64_t warps) { return (unsigned)((warps + kWarps - 1) / kWarps); }
 
 }  // namespace simt
+
+int preload_simt() { return simt::preload(); }
 
 int simt_fwd(const float* q, const float* k, const float* v, float* o, float* lse, int64_t n, int64_t b,
              int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st) {

@@ -33,6 +33,10 @@ int sm100_bwd(const void* q, const void* k, const void* v, const void* o, const 
               void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n, int64_t b, int64_t hq,
               int64_t hkv, int64_t hd, int causal, float scale, int stages, cudaStream_t st);
 size_t sm100_bwd_workspace(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd);
+int preload_a2a();
+int preload_simt();
+int preload_fwd();
+int preload_bwd();
 
 static int check_attn(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask) {
   if (mask != UL_MASK_NONE && mask != UL_MASK_CAUSAL)
@@ -60,6 +64,13 @@ int ul_abi_version(void) { return UL_ABI_VERSION; }
 const char* ul_last_error(void) { return last_error().c_str(); }
 int ul_last_launch_count(void) { return launch_count(); }
 uint64_t ul_total_launch_count(void) { return g_total_launches.load(); }
+
+int ul_preload_kernels(void) {
+  UL_TRY(preload_a2a());
+  UL_TRY(preload_simt());
+  UL_TRY(preload_fwd());
+  return preload_bwd();
+}
 
 int ul_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
                 int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask, float scale, void* stream) {

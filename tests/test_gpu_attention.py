@@ -58,6 +58,36 @@ def test_fwd_bf16_vs_oracle(n, b, hq, hkv, hd, mask):
     assert np.abs(to_np(lse) - ref_lse).max() <= 2e-2
 
 
+BWD_CASES = [
+    # n, b, hq, hkv, hd, mask
+    (1, 1, 1, 1, 64, "causal"),
+    (64, 1, 2, 2, 128, "causal"),
+    (130, 1, 2, 1, 128, "none"),
+    (256, 2, 4, 2, 64, "causal"),
+    (512, 1, 4, 4, 128, "causal"),
+    (640, 1, 4, 1, 128, "none"),
+    (1000, 1, 2, 2, 128, "causal"),
+]
+
+
+@pytest.mark.parametrize("n,b,hq,hkv,hd,mask", BWD_CASES)
+def test_bwd_bf16_vs_oracle(n, b, hq, hkv, hd, mask):
+    q, k, v, do = inputs(n, b, hq, hkv, hd, torch.bfloat16, seed=100 + n + hd)
+    kind = "causal" if mask == "causal" else "none"
+    dq_r, dk_r, dv_r = O.local_attention_backward(q, k, v, do, kind, exact=False)
+    attn = U().FlashAttention(mask)
+    tq, tk, tv, tdo = (to_dev(x, torch.bfloat16) for x in (q, k, v, do))
+    o, lse = attn.forward_with_lse(tq, tk, tv)
+    dq, dk, dv = attn.backward(tq, tk, tv, o, lse, tdo)
+    torch.cuda.synchronize()
+    for name, got, ref in (("dq", dq, dq_r), ("dk", dk, dk_r), ("dv", dv, dv_r)):
+        err = rel_max_err(to_np(got), ref)
+        assert err <= BF16_MAXREL, f"{name}: max-abs / max|ref| = {err:.3e}"
+    # deterministic: a second backward is bitwise identical (no atomics)
+    dq2, dk2, dv2 = attn.backward(tq, tk, tv, o, lse, tdo)
+    assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)
+
+
 @pytest.mark.parametrize("n,b,hq,hkv,hd,mask", [(1, 1, 1, 1, 8, "none"), (7, 2, 4, 2, 3, "causal"),
                                                 (64, 1, 4, 4, 16, "none"), (300, 1, 4, 1, 64, "causal"),
                                                 (129, 2, 2, 2, 128, "causal")])

@@ -100,6 +100,22 @@ def test_bf16_forward_vs_oracle_and_p_invariance(p):
     assert np.array_equal(o, o1)
 
 
+@pytest.mark.parametrize("p,hq,hkv", [(2, 8, 8), (4, 8, 4), (8, 16, 8)])
+def test_bf16_forward_backward_vs_oracle(p, hq, hkv):
+    n, b, hd = 1024, 1, 128
+    q, k, v, do = (O.make_tensor((n, b, hh, hd), 51 + p, s, "bfloat16") for s, hh in
+                   ((1, hq), (2, hkv), (3, hkv), (4, hq)))
+    ref, _ = O.local_attention(q, k, v, "causal", exact=False)
+    gref = O.local_attention_backward(q, k, v, do, "causal", exact=False)
+    o, grads, groups = run_layer(p, q, k, v, do, "causal", torch.bfloat16, backward=True)
+    assert rel_max_err(o, ref) <= BF16_MAXREL
+    for name, got, r in zip(("dq", "dk", "dv"), grads, gref):
+        err = rel_max_err(got, r)
+        assert err <= BF16_MAXREL, f"{name}: {err:.3e}"
+    # 4 native exchange calls per fwd+bwd (QKV fused, O, dO, dQdKdV fused)
+    assert groups[0].native_ledger()["calls"] == 4
+
+
 def test_bf16_gqa_forward_p4():
     n, b, hq, hkv, hd = 512, 1, 8, 4, 128
     q, k, v, do = (O.make_tensor((n, b, hh, hd), 41, s, "bfloat16") for s, hh in
