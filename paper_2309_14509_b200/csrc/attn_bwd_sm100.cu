@@ -39,9 +39,19 @@ using namespace sm100;
 constexpr int BT = 128;           // the tile a CTA owns (kv tile for dkdv, q tile for dq)
 constexpr int BS = 64;            // the sub-tile streamed against it
 constexpr int NST = 3;            // streamed-operand pipeline stages
-constexpr int kThreads = 192;
+// warp 0 TMA, warp 1 MMA, warps 2..9 softmax: two warps per TMEM lane
+// quarter, each owning one 32-column half of the 64-column sub-tile, so
+// every SMSP interleaves two independent softmax streams
+constexpr int kSoftWarps = 8;
+constexpr int kSoftThreads = kSoftWarps * 32;
+constexpr int kThreads = 64 + kSoftThreads;
 constexpr int kAtomT = BT * 128;  // SW128 atom column of a 128-row tile (16 KB)
 constexpr int kAtomS = BS * 128;  // ... of a 64-row sub-tile (8 KB)
+
+// TMEM column of the bf16 A operand (P^T, dS^T or dS) for K-step kk (16
+// elements = 8 packed columns): softmax half h packs its 32 elements into
+// columns [32h + 16, 32h + 32) of the buffer it read them from.
+__device__ __forceinline__ uint32_t a_col(int kk) { return (kk >> 1) * 32 + 16 + (kk & 1) * 8; }
 
 struct Params {
   int n, n_pad, b, hq, hkv;
@@ -178,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 128);
+      mbar_init(&p_full[s], kSoftThreads);
       mbar_init(&buf_free[s], 1);
     }
     fence_barrier_init();
@@ -220,24 +230,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp runs the issue loop; one elected lane issues
       constexpr uint32_t kIdS = idesc_bf16(BT, BS, 0, 0);   // M = kv rows, N = 64 q rows
       constexpr uint32_t kIdG = idesc_bf16(BT, HD, 0, 1);   // M = kv rows, N = hd, B MN-major
-      const uint32_t kaddr = smem_u32(sK), vaddr = smem_u32(sV);
+      // base descriptors, built once: K/V (K-major A), Q/dO stage 0 as
+      // K-major B (for S^T, dP^T) and as MN-major B (for dK, dV)
+      const uint64_t dK0 = sdesc(smem_u32(sK), 16, 1024), dV0 = sdesc(smem_u32(sV), 16, 1024);
+      const uint64_t dQk0 = sdesc(smem_u32(sQ), 16, 1024), dOk0 = sdesc(smem_u32(sO), 16, 1024);
+      const uint64_t dQm0 = sdesc(smem_u32(sQ), kAtomS, 1024), dOm0 = sdesc(smem_u32(sO), kAtomS, 1024);
       auto issue_grads = [&](int i) {
         const int b = i & 1, s = i % NST;
         const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
         mbar_wait(&p_full[b], (i >> 1) & 1);
         tc_fence_after();
-        const uint32_t qaddr = smem_u32(sQ + s * S::kTileS), oaddr = smem_u32(sO + s * S::kTileS);
+        const uint64_t dOm = dadd(dOm0, s * S::kTileS), dQm = dadd(dQm0, s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < BS / 16; ++kk)
-          mma_ts(tdV, tSt + kk * 8, sdesc(oaddr + kk * 2048, kAtomS, 1024), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_ts_w(tdV, tSt + a_col(kk), dadd(dOm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < BS / 16; ++kk)
-          mma_ts(tdK, tdPt + kk * 8, sdesc(qaddr + kk * 2048, kAtomS, 1024), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&q_empty[s]);
-        mma_commit(&buf_free[b]);
+          mma_ts_w(tdK, tdPt + a_col(kk), dadd(dQm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+        mma_commit_w(&q_empty[s]);
+        mma_commit_w(&buf_free[b]);
       };
       mbar_wait(kv_full, 0);
       for (int it = 0; it < total; ++it) {
@@ -246,29 +260,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (it >= 2) mbar_wait(&buf_free[b], ((it - 2) >> 1) & 1);
         mbar_wait(&q_full[s], (it / NST) & 1);
         tc_fence_after();
-        const uint32_t qaddr = smem_u32(sQ + s * S::kTileS), oaddr = smem_u32(sO + s * S::kTileS);
+        const uint64_t dQk = dadd(dQk0, s * S::kTileS), dOk = dadd(dOk0, s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
           const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ss(tSt, sdesc(kaddr + offT, 16, 1024), sdesc(qaddr + offS, 16, 1024), kIdS, kk > 0 ? 1u : 0u);
+          mma_ss_w(tSt, dadd(dK0, offT), dadd(dQk, offS), kIdS, kk > 0 ? 1u : 0u);
         }
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
           const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ss(tdPt, sdesc(vaddr + offT, 16, 1024), sdesc(oaddr + offS, 16, 1024), kIdS, kk > 0 ? 1u : 0u);
+          mma_ss_w(tdPt, dadd(dV0, offT), dadd(dOk, offS), kIdS, kk > 0 ? 1u : 0u);
         }
-        mma_commit(&s_full[b]);
+        mma_commit_w(&s_full[b]);
         if (it >= 1) issue_grads(it - 1);
       }
       issue_grads(total - 1);
     }
   } else {
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;        // which 32-column half of the sub-tile
     const int row = quarter * 32 + lane;     // kv row within the tile
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int kvrow = kv0 + row;
+    const int c0 = half * 32;
     for (int it = 0; it < total; ++it) {
       const int b = it & 1, s = it % NST;
       const int q0 = (i0 + it % per_head) * BS;
@@ -276,42 +292,58 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&q_full[s], (it / NST) & 1);
       mbar_wait(&s_full[b], (it >> 1) & 1);
       tc_fence_after();
-      const float* L = sL + s * BS;
-      const float* Dd = sD + s * BS;
-      const int first = p.causal ? kvrow - q0 : 0;   // query columns c < first are masked (q < kv)
-      // 32-column chunks: P^T / dS^T of chunk c overwrite TMEM columns
-      // [16c, 16c+16) of the same buffer, already consumed by chunk c' <= c
+      uint32_t r[32], d[32];
+      tmem_ld32(tSt + lane_off + c0, r);
+      tmem_ld32(tdPt + lane_off + c0, d);
+      // per-column LSE / D of this half: broadcast 16-byte smem reads
+      float Lc[32], Dc[32];
+      const float4* L4 = reinterpret_cast<const float4*>(sL + s * BS + c0);
+      const float4* D4 = reinterpret_cast<const float4*>(sD + s * BS + c0);
 #pragma unroll
-      for (int c = 0; c < BS / 32; ++c) {
-        uint32_t r[32], d[32];
-        tmem_ld32(tSt + lane_off + c * 32, r);
-        tmem_ld32(tdPt + lane_off + c * 32, d);
-        tmem_wait_ld();
-        uint32_t pk[16], dsk[16];
+      for (int x = 0; x < 8; ++x) {
+        const float4 a = L4[x], e = D4[x];
+        Lc[4 * x] = a.x; Lc[4 * x + 1] = a.y; Lc[4 * x + 2] = a.z; Lc[4 * x + 3] = a.w;
+        Dc[4 * x] = e.x; Dc[4 * x + 1] = e.y; Dc[4 * x + 2] = e.z; Dc[4 * x + 3] = e.w;
+      }
+      tmem_wait_ld();
+      uint32_t pk[16], dsk[16];
+      // only sub-tiles overlapping the kv tile's diagonal need the causal mask
+      if (p.causal && q0 + c0 < kv0 + BT) {
+        const int first = kvrow - q0 - c0;   // columns x < first are masked (q < kv)
 #pragma unroll
         for (int x = 0; x < 32; x += 2) {
-          const int col = c * 32 + x;
-          float p0 = fast_exp2(__uint_as_float(r[x]) * p.scale_log2 - L[col]);
-          float p1 = fast_exp2(__uint_as_float(r[x + 1]) * p.scale_log2 - L[col + 1]);
-          if (col < first) p0 = 0.f;
-          if (col + 1 < first) p1 = 0.f;
+          float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -Lc[x]));
+          float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -Lc[x + 1]));
+          p0 = x < first ? 0.f : p0;
+          p1 = x + 1 < first ? 0.f : p1;
           pk[x / 2] = pack_bf16(p0, p1);
-          dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dd[col]), p1 * (__uint_as_float(d[x + 1]) - Dd[col + 1]));
+          dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dc[x]), p1 * (__uint_as_float(d[x + 1]) - Dc[x + 1]));
         }
-        tmem_st16(tSt + lane_off + c * 16, pk);
-        tmem_st16(tdPt + lane_off + c * 16, dsk);
+      } else {
+#pragma unroll
+        for (int x = 0; x < 32; x += 2) {
+          const float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -Lc[x]));
+          const float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -Lc[x + 1]));
+          pk[x / 2] = pack_bf16(p0, p1);
+          dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dc[x]), p1 * (__uint_as_float(d[x + 1]) - Dc[x + 1]));
+        }
       }
+      // packed P^T / dS^T of this half go to the upper 16 of the 32 columns
+      // this warp just consumed (never into the other half's unread columns);
+      // the TS MMAs address K-step kk at a_col(kk)
+      tmem_st16(tSt + lane_off + c0 + 16, pk);
+      tmem_st16(tdPt + lane_off + c0 + 16, dsk);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[b]);
     }
-    // epilogue: dV, dK * scale -> bf16 rows of kv head g
+    // epilogue: half 0 stores dV, half 1 stores dK * scale (bf16 rows of kv head g)
     mbar_wait(&buf_free[(total - 1) & 1], ((total - 1) >> 1) & 1);
     tc_fence_after();
     const bool valid = kvrow < p.n;
     const int64_t off = (((int64_t)kvrow * p.b + bb) * p.hkv + g) * HD;
-    store_acc_rows<HD>(tdV, lane_off, 1.f, p.dv + off, valid);
-    store_acc_rows<HD>(tdK, lane_off, p.scale, p.dk + off, valid);
+    if (half == 0) store_acc_rows<HD>(tdV, lane_off, 1.f, p.dv + off, valid);
+    else store_acc_rows<HD>(tdK, lane_off, p.scale, p.dk + off, valid);
   }
   tc_fence_before();
   __syncthreads();
@@ -375,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 128);
+      mbar_init(&p_full[s], kSoftThreads);
       mbar_init(&buf_free[s], 1);
     }
     fence_barrier_init();
@@ -412,21 +444,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp runs the issue loop; one elected lane issues
       constexpr uint32_t kIdS = idesc_bf16(BT, BS, 0, 0);
       constexpr uint32_t kIdG = idesc_bf16(BT, HD, 0, 1);
-      const uint32_t qaddr = smem_u32(sQ), oaddr = smem_u32(sO);
+      const uint64_t dQ0 = sdesc(smem_u32(sQ), 16, 1024), dO0 = sdesc(smem_u32(sO), 16, 1024);
+      const uint64_t dKk0 = sdesc(smem_u32(sK), 16, 1024), dVk0 = sdesc(smem_u32(sV), 16, 1024);
+      const uint64_t dKm0 = sdesc(smem_u32(sK), kAtomS, 1024);
       auto issue_dq = [&](int i) {
         const int b = i & 1, s = i % NST;
         const uint32_t tdP = tbase + 128 + b * 64;
         mbar_wait(&p_full[b], (i >> 1) & 1);
         tc_fence_after();
-        const uint32_t kaddr = smem_u32(sK + s * S::kTileS);
+        const uint64_t dKm = dadd(dKm0, s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < BS / 16; ++kk)
-          mma_ts(tdQ, tdP + kk * 8, sdesc(kaddr + kk * 2048, kAtomS, 1024), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&kv_empty[s]);
-        mma_commit(&buf_free[b]);
+          mma_ts_w(tdQ, tdP + a_col(kk), dadd(dKm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+        mma_commit_w(&kv_empty[s]);
+        mma_commit_w(&buf_free[b]);
       };
       mbar_wait(q_full, 0);
       for (int j = 0; j < nsub; ++j) {
@@ -435,65 +469,89 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j >= 2) mbar_wait(&buf_free[b], ((j - 2) >> 1) & 1);
         mbar_wait(&kv_full[s], (j / NST) & 1);
         tc_fence_after();
-        const uint32_t kaddr = smem_u32(sK + s * S::kTileS), vaddr = smem_u32(sV + s * S::kTileS);
+        const uint64_t dKk = dadd(dKk0, s * S::kTileS), dVk = dadd(dVk0, s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
           const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ss(tS, sdesc(qaddr + offT, 16, 1024), sdesc(kaddr + offS, 16, 1024), kIdS, kk > 0 ? 1u : 0u);
+          mma_ss_w(tS, dadd(dQ0, offT), dadd(dKk, offS), kIdS, kk > 0 ? 1u : 0u);
         }
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
           const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ss(tdP, sdesc(oaddr + offT, 16, 1024), sdesc(vaddr + offS, 16, 1024), kIdS, kk > 0 ? 1u : 0u);
+          mma_ss_w(tdP, dadd(dO0, offT), dadd(dVk, offS), kIdS, kk > 0 ? 1u : 0u);
         }
-        mma_commit(&s_full[b]);
+        mma_commit_w(&s_full[b]);
         if (j >= 1) issue_dq(j - 1);
       }
       issue_dq(nsub - 1);
     }
   } else {
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;        // which 32-column half of the kv sub-tile
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int qrow = q0 + row;
+    const int c0 = half * 32;
     const int64_t roff = ((int64_t)bb * p.hq + h) * p.n_pad + qrow;
     const float L = p.L2[roff];
     const float Dr = p.Dv[roff];
     for (int j = 0; j < nsub; ++j) {
       const int b = j & 1;
-      const int kv0 = j * BS;
+      const int kv0 = j * BS + c0;
       const uint32_t tS = tbase + b * 64, tdP = tbase + 128 + b * 64;
       mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
-      const int limit = p.causal ? qrow - kv0 + 1 : BS;   // columns c >= limit are masked
-#pragma unroll
-      for (int c = 0; c < BS / 32; ++c) {
-        uint32_t r[32], d[32];
-        tmem_ld32(tS + lane_off + c * 32, r);
-        tmem_ld32(tdP + lane_off + c * 32, d);
-        tmem_wait_ld();
-        uint32_t dsk[16];
+      uint32_t r[32], d[32];
+      tmem_ld32(tS + lane_off + c0, r);
+      tmem_ld32(tdP + lane_off + c0, d);
+      tmem_wait_ld();
+      uint32_t dsk[16];
+      if (p.causal && kv0 + 31 > q0) {       // only the diagonal sub-tiles need the mask
+        const int limit = qrow - kv0 + 1;     // columns x >= limit are masked (kv > q)
 #pragma unroll
         for (int x = 0; x < 32; x += 2) {
-          const int col = c * 32 + x;
-          float p0 = fast_exp2(__uint_as_float(r[x]) * p.scale_log2 - L);
-          float p1 = fast_exp2(__uint_as_float(r[x + 1]) * p.scale_log2 - L);
-          if (col >= limit) p0 = 0.f;
-          if (col + 1 >= limit) p1 = 0.f;
+          float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -L));
+          float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -L));
+          p0 = x >= limit ? 0.f : p0;
+          p1 = x + 1 >= limit ? 0.f : p1;
           dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dr), p1 * (__uint_as_float(d[x + 1]) - Dr));
         }
-        tmem_st16(tdP + lane_off + c * 16, dsk);   // dS over consumed dP columns
+      } else {
+#pragma unroll
+        for (int x = 0; x < 32; x += 2) {
+          const float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -L));
+          const float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -L));
+          dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dr), p1 * (__uint_as_float(d[x + 1]) - Dr));
+        }
       }
+      tmem_st16(tdP + lane_off + c0 + 16, dsk);   // dS over this warp's consumed dP columns
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&p_full[b]);
     }
     mbar_wait(&buf_free[(nsub - 1) & 1], ((nsub - 1) >> 1) & 1);
     tc_fence_after();
-    store_acc_rows<HD>(tdQ, lane_off, p.scale, p.dq + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD,
-                       qrow < p.n);
+    // each half stores HD/2 columns of dQ * scale
+    const bool valid = qrow < p.n;
+    __nv_bfloat16* dst = p.dq + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 64; ++c) {
+      const int col = half * (HD / 2) + c * 32;
+      uint32_t v[32];
+      tmem_ld32(tdQ + lane_off + col, v);
+      tmem_wait_ld();
+      uint32_t pkd[16];
+#pragma unroll
+      for (int x = 0; x < 16; ++x)
+        pkd[x] = pack_bf16(__uint_as_float(v[2 * x]) * p.scale, __uint_as_float(v[2 * x + 1]) * p.scale);
+      if (valid) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + col);
+#pragma unroll
+        for (int x = 0; x < 4; ++x) d4[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();

@@ -1,0 +1,350 @@
+// K3 (v2): FlashAttention-style forward on sm_100a, two query tiles per CTA.
+//
+// Same contract as attn_fwd_sm100.cu (_masked_attention kernels.py:31-40 +
+// LSE), restructured so the tensor core never waits on a softmax:
+//   * a CTA owns two 128-row query tiles (A, B) of one (batch, head); every
+//     K_j / V_j tile brought in by TMA serves both (half the smem/L2 traffic
+//     per FLOP of one tile per CTA);
+//   * TMEM = S_A | S_B | O_A | O_B (128 + 128 + hd + hd columns);
+//   * the single MMA thread issues   PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
+//     so softmax A of tile j+1 overlaps PV_B(j)/S_B(j+1) and vice versa.
+//     tcgen05.mma ops of one thread execute in issue order, so S_A(j+1) may
+//     overwrite the TMEM columns PV_A(j) reads P_A(j) from without a wait;
+//     and tcgen05.commit tracks every earlier MMA of the thread, so "S_A(j)
+//     ready" also means "PV_A(j-1) done" -- the (rare, lazy) O rescale needs
+//     no extra barrier;
+//   * warps 2-5 run softmax A, warps 6-9 softmax B (two independent softmax
+//     streams per SMSP); one query row per thread, exp2 domain, masking only
+//     on diagonal/tail tiles, FFMA-fused exponent, ILP'd max/sum chains, P
+//     packed to bf16 and stored 32 columns at a time over consumed S.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "common.cuh"
+#include "sm100.cuh"
+#include "tmap.cuh"
+
+namespace ul {
+namespace fwd2 {
+
+using namespace sm100;
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int NS = 2;               // K/V pipeline stages
+constexpr int kThreads = 320;       // TMA, MMA, 2 x 4 softmax warps
+constexpr float kLazy = 8.0f;       // log2 headroom before O is rescaled
+constexpr int kAtom = 128 * 128;    // SW128 atom column of a 128-row tile
+
+template <int HD>
+struct Smem {
+  static constexpr int kTile = (HD / 64) * kAtom;
+  static constexpr int kQ = 0;                    // [2] (tile A, tile B)
+  static constexpr int kK = kQ + 2 * kTile;       // [NS]
+  static constexpr int kV = kK + NS * kTile;      // [NS]
+  static constexpr int kBar = kV + NS * kTile;
+  static constexpr int kBytes = kBar + 256 + 1024;
+};
+
+struct Params {
+  int n, b, hq, hkv;
+  int causal;
+  int qtiles, pairs;
+  float scale_log2;
+  __nv_bfloat16* o;
+  float* lse;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const Params p) {
+  using S = Smem<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + S::kQ;
+  uint8_t* sK = smem + S::kK;
+  uint8_t* sV = smem + S::kV;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;              // [NS]
+  uint64_t* k_empty = bars + 1 + NS;        // [NS]
+  uint64_t* v_full = bars + 1 + 2 * NS;     // [NS]
+  uint64_t* v_empty = bars + 1 + 3 * NS;    // [NS]
+  uint64_t* s_full = bars + 1 + 4 * NS;     // [2] per tile
+  uint64_t* p_full = bars + 3 + 4 * NS;     // [2] per tile
+  uint64_t* o_done = bars + 5 + 4 * NS;     // [2] per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 4 * NS);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  const int heads = p.b * p.hq;
+  const int pair = p.pairs - 1 - (int)(blockIdx.x / heads);   // longest (causal) pairs first
+  const int bh = (int)(blockIdx.x % heads);
+  const int bb = bh / p.hq, h = bh % p.hq;
+  const int g = h / (p.hq / p.hkv);
+  const int nkv_all = (p.n + BN - 1) / BN;
+  int nkvT[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int qt = 2 * pair + t;
+    nkvT[t] = qt >= p.qtiles ? 0 : (p.causal ? min(nkv_all, (qt * BM + BM - 1) / BN + 1) : nkv_all);
+  }
+  const int nkv = max(nkvT[0], nkvT[1]);
+  const int ntiles = nkvT[1] > 0 ? 2 : 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_done[t], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  // TMEM columns: S_A 0, S_B 128, O_A 256, O_B 256 + HD
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      mbar_expect_tx(q_full, ntiles * BM * HD * 2);
+      for (int t = 0; t < ntiles; ++t)
+#pragma unroll
+        for (int a = 0; a < HD / 64; ++a)
+          tma_load_3d(sQ + t * S::kTile + a * kAtom, &tmQ, q_full, a * 64, bb * p.hq + h, (2 * pair + t) * BM);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % NS;
+        const uint32_t ph = (j / NS) & 1;
+        mbar_wait(&k_empty[s], ph ^ 1);
+        mbar_expect_tx(&k_full[s], BN * HD * 2);
+#pragma unroll
+        for (int a = 0; a < HD / 64; ++a)
+          tma_load_3d(sK + s * S::kTile + a * kAtom, &tmK, &k_full[s], a * 64, bb * p.hkv + g, j * BN);
+        mbar_wait(&v_empty[s], ph ^ 1);
+        mbar_expect_tx(&v_full[s], BN * HD * 2);
+#pragma unroll
+        for (int a = 0; a < HD / 64; ++a)
+          tma_load_3d(sV + s * S::kTile + a * kAtom, &tmV, &v_full[s], a * 64, bb * p.hkv + g, j * BN);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    {  // the whole warp runs the issue loop; one elected lane issues
+      constexpr uint32_t kIdQK = idesc_bf16(BM, BN, 0, 0);
+      constexpr uint32_t kIdPV = idesc_bf16(BM, HD, 0, 1);
+      // base descriptors built once; per-MMA cost is a constant add
+      const uint64_t dQ0 = sdesc(smem_u32(sQ), 16, 1024);
+      const uint64_t dK0 = sdesc(smem_u32(sK), 16, 1024);
+      const uint64_t dV0 = sdesc(smem_u32(sV), kAtom, 1024);
+      auto issue_s = [&](int t, int j) {   // S_t = Q_t K_j^T
+        const uint64_t dk = dadd(dK0, (j % NS) * S::kTile);
+        const uint64_t dq = dadd(dQ0, t * S::kTile);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
+          mma_ss_w(tbase + t * 128, dadd(dq, off), dadd(dk, off), kIdQK, kk > 0 ? 1u : 0u);
+        }
+        mma_commit_w(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j
+        mbar_wait(&p_full[t], j & 1);
+        tc_fence_after();
+        const uint64_t dv = dadd(dV0, (j % NS) * S::kTile);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk)
+          mma_ts_w(tbase + 256 + t * HD, tbase + t * 128 + kk * 8, dadd(dv, kk * 2048), kIdPV,
+                 (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit_w(&o_done[t]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      if (nkvT[0] > 0) issue_s(0, 0);
+      if (nkvT[1] > 0) issue_s(1, 0);
+      mma_commit_w(&k_empty[0]);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % NS;
+        const bool next = j + 1 < nkv;
+        mbar_wait(&v_full[s], (j / NS) & 1);
+        if (next) mbar_wait(&k_full[(j + 1) % NS], ((j + 1) / NS) & 1);
+        tc_fence_after();
+        if (j < nkvT[0]) issue_pv(0, j);
+        if (next && j + 1 < nkvT[0]) issue_s(0, j + 1);
+        if (j < nkvT[1]) issue_pv(1, j);
+        if (next && j + 1 < nkvT[1]) issue_s(1, j + 1);
+        mma_commit_w(&v_empty[s]);
+        if (next) mma_commit_w(&k_empty[(j + 1) % NS]);
+      }
+    }
+  } else {
+    // ---------------- softmax / correction / epilogue ----------------
+    const int t = (warp - 2) >> 2;            // query tile of this warpgroup
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tbase + t * 128 + lane_off;
+    const uint32_t tO = tbase + 256 + t * HD + lane_off;
+    const int q0 = (2 * pair + t) * BM;
+    const int qrow = q0 + row;
+    const int my_nkv = nkvT[t];
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < my_nkv; ++j) {
+      const int kv0 = j * BN;
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      uint32_t r[BN];
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, r + c * 32);
+      tmem_wait_ld();
+      if ((p.causal && kv0 + BN - 1 > q0) || kv0 + BN > p.n) {
+        int limit = p.n - kv0;
+        if (p.causal) limit = min(limit, qrow - kv0 + 1);
+#pragma unroll
+        for (int c = 0; c < BN; ++c)
+          if (c >= limit) r[c] = __float_as_uint(-INFINITY);
+      }
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < BN; c += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mx[u] = fmaxf(mx[u], __uint_as_float(r[c + u]));
+      }
+      const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
+      float alpha = 1.f;
+      bool rescale = false;
+      if (mt > m + kLazy) {
+        alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - mt);
+        rescale = (j > 0);
+        m = mt;
+      }
+      const float mu = (m == -INFINITY) ? 0.f : m;
+      float rsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int x = 0; x < 32; x += 2) {
+          const float e0 = fast_exp2(fmaf(__uint_as_float(r[c * 32 + x]), p.scale_log2, -mu));
+          const float e1 = fast_exp2(fmaf(__uint_as_float(r[c * 32 + x + 1]), p.scale_log2, -mu));
+          rsum[(x >> 1) & 7] += e0 + e1;
+          pk[x / 2] = pack_bf16(e0, e1);
+        }
+        tmem_st16(tS + c * 16, pk);   // P over S columns already in registers
+      }
+      l = l * alpha + (((rsum[0] + rsum[1]) + (rsum[2] + rsum[3])) + ((rsum[4] + rsum[5]) + (rsum[6] + rsum[7])));
+      // s_full(j) tracks every earlier MMA, so PV(j-1) is complete: rescale O now
+      if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t ov[32];
+          tmem_ld32(tO + c * 32, ov);
+          tmem_wait_ld();
+#pragma unroll
+          for (int x = 0; x < 32; ++x) ov[x] = __float_as_uint(__uint_as_float(ov[x]) * alpha);
+          tmem_st32(tO + c * 32, ov);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_full[t]);
+    }
+    if (my_nkv > 0) {
+      mbar_wait(&o_done[t], (my_nkv - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const bool valid = qrow < p.n;
+      __nv_bfloat16* orow = p.o + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(tO + c * 32, ov);
+        tmem_wait_ld();
+        uint32_t pkd[16];
+#pragma unroll
+        for (int x = 0; x < 16; ++x)
+          pkd[x] = pack_bf16(__uint_as_float(ov[2 * x]) * inv, __uint_as_float(ov[2 * x + 1]) * inv);
+        if (valid) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int x = 0; x < 4; ++x) dst[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+        }
+      }
+      if (valid) p.lse[((int64_t)bb * p.hq + h) * p.n + qrow] = (m + log2f(l)) * 0.69314718055994531f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+template <int HD>
+static int launch(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
+                  int64_t hq, int64_t hkv, int causal, float scale, cudaStream_t st) {
+  CUtensorMap mq, mk, mv;
+  UL_TRY(make_tmap_bhsd(&mq, q, n, b * hq, HD, 128));
+  UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, 128));
+  UL_TRY(make_tmap_bhsd(&mv, v, n, b * hkv, HD, 128));
+  Params p;
+  p.n = (int)n;
+  p.b = (int)b;
+  p.hq = (int)hq;
+  p.hkv = (int)hkv;
+  p.causal = causal;
+  p.qtiles = (int)((n + BM - 1) / BM);
+  p.pairs = (p.qtiles + 1) / 2;
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.o = (__nv_bfloat16*)o;
+  p.lse = lse;
+  const int smem = Smem<HD>::kBytes;
+  static bool attr = false;
+  if (!attr) {
+    UL_CUDA(cudaFuncSetAttribute(attn_fwd2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const int64_t grid = (int64_t)p.pairs * b * hq;
+  attn_fwd2_kernel<HD><<<(unsigned)grid, kThreads, smem, st>>>(mq, mk, mv, p);
+  return launched("attn_fwd_sm100");
+}
+
+}  // namespace fwd2
+
+int preload_fwd2() {
+  cudaFuncAttributes a;
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd2::attn_fwd2_kernel<64>));
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd2::attn_fwd2_kernel<128>));
+  return UL_OK;
+}
+
+int sm100_fwd2(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b, int64_t hq,
+               int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st) {
+  switch (hd) {
+    case 64: return fwd2::launch<64>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, st);
+    case 128: return fwd2::launch<128>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, st);
+    default:
+      return fail(UL_ERR_KERNEL, "bf16 attention supports head_dim 64 or 128, got %lld", (long long)hd);
+  }
+}
+
+}  // namespace ul

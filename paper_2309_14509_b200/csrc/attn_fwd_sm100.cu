@@ -194,16 +194,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS[j & 1] + lane_off + c * 32, r + c * 32);
       tmem_wait_ld();
-      int limit = p.n - kv0;
-      if (p.causal) limit = min(limit, qrow - kv0 + 1);
-      float mt = -INFINITY;
-      float t[BN];
+      // mask only the diagonal (causal) and sequence-tail tiles; the branch is
+      // uniform across the CTA
+      if ((p.causal && kv0 + BN - 1 > q0) || kv0 + BN > p.n) {
+        int limit = p.n - kv0;
+        if (p.causal) limit = min(limit, qrow - kv0 + 1);
 #pragma unroll
-      for (int c = 0; c < BN; ++c) {
-        t[c] = __uint_as_float(r[c]) * p.scale_log2;
-        if (c >= limit) t[c] = -INFINITY;
-        mt = fmaxf(mt, t[c]);
+        for (int c = 0; c < BN; ++c)
+          if (c >= limit) r[c] = __float_as_uint(-INFINITY);
       }
+      // row max of the raw scores: 4 independent chains (ILP), then scaled
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < BN; c += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mx[u] = fmaxf(mx[u], __uint_as_float(r[c + u]));
+      }
+      const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
       float alpha = 1.f;
       bool rescale = false;
       if (mt > m + kLazy) {
@@ -212,15 +219,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         m = mt;
       }
       const float mu = (m == -INFINITY) ? 0.f : m;
-      float rs = 0.f;
+      // p = 2^(s*scale*log2e - m): one FFMA + MUFU.EX2 per element; the row
+      // sum runs in 8 independent partial sums
+      float rsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       uint32_t pk[BN / 2];
 #pragma unroll
       for (int c = 0; c < BN; c += 2) {
-        const float e0 = fast_exp2(t[c] - mu);
-        const float e1 = fast_exp2(t[c + 1] - mu);
-        rs += e0 + e1;
+        const float e0 = fast_exp2(fmaf(__uint_as_float(r[c]), p.scale_log2, -mu));
+        const float e1 = fast_exp2(fmaf(__uint_as_float(r[c + 1]), p.scale_log2, -mu));
+        rsum[(c >> 1) & 7] += e0 + e1;
         pk[c / 2] = pack_bf16(e0, e1);
       }
+      const float rs = ((rsum[0] + rsum[1]) + (rsum[2] + rsum[3])) + ((rsum[4] + rsum[5]) + (rsum[6] + rsum[7]));
       l = l * alpha + rs;
       // P_j over the consumed S_j columns [0, BN/2)
 #pragma unroll
