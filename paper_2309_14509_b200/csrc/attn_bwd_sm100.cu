@@ -257,7 +257,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int it = 0; it < total; ++it) {
         const int b = it & 1, s = it % NST;
         const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
-        if (it >= 2) mbar_wait(&buf_free[b], ((it - 2) >> 1) & 1);
+        // buffer b was last read by grads(it-2), issued before this point by
+        // this thread: tcgen05.mma executes in issue order, so no wait
         mbar_wait(&q_full[s], (it / NST) & 1);
         tc_fence_after();
         const uint64_t dQk = dadd(dQk0, s * S::kTileS), dOk = dadd(dOk0, s * S::kTileS);
@@ -466,7 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < nsub; ++j) {
         const int b = j & 1, s = j % NST;
         const uint32_t tS = tbase + b * 64, tdP = tbase + 128 + b * 64;
-        if (j >= 2) mbar_wait(&buf_free[b], ((j - 2) >> 1) & 1);
+        // buffer b was last read by dq(j-2), issued earlier by this thread (in-order)
         mbar_wait(&kv_full[s], (j / NST) & 1);
         tc_fence_after();
         const uint64_t dKk = dadd(dKk0, s * S::kTileS), dVk = dadd(dVk0, s * S::kTileS);

@@ -1,22 +1,25 @@
-// K3: FlashAttention-style forward on sm_100a (tcgen05 + TMEM + TMA).
+// K3: FlashAttention-style forward on sm_100a (tcgen05 + TMEM + TMA), two query tiles per CTA.
 //
 // Replaces the per-head kernel loop of ulysses_attention_forward_with_state
 // (ulysses.py:148-152) over _masked_attention (kernels.py:31-40: scores =
-// q k^T * scale, row_softmax tensor.py:227-249, ctx = probs v) and adds the
-// row LSE the backward needs (the reference recomputes probabilities
-// instead, kernels.py:104).
-//
-// One CTA = one 128-row query tile of one (batch, head); 6 warps:
-//   warp 0  TMA producer: Q once, then K_j / V_j into a 2-stage ring
-//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer:
-//             S_j = Q K_j^T   (SS, both K-major, M=128 N=128, -> TMEM S[j&1])
-//             O  += P_j V_j   (TS: P from TMEM, V MN-major from smem)
-//   warps 2-5 softmax: one query row per thread (TMEM lane == row); online
-//             softmax in the exp2 domain with lazy rescaling (O in TMEM is
-//             only corrected when the running max grows by > 2^8), P written
-//             back to TMEM as packed bf16 over the consumed S columns.
-// Causal tiles beyond the diagonal are skipped; the diagonal and the
-// sequence tail are masked in registers.  CTAs are ordered longest-first.
+// q k^T * scale, row_softmax tensor.py:227-249, ctx = probs v), plus the row
+// LSE the backward needs (the reference recomputes probabilities instead,
+// kernels.py:104); structured so the tensor core never waits on a softmax:
+//   * a CTA owns two 128-row query tiles (A, B) of one (batch, head); every
+//     K_j / V_j tile brought in by TMA serves both (half the smem/L2 traffic
+//     per FLOP of one tile per CTA);
+//   * TMEM = S_A | S_B | O_A | O_B (128 + 128 + hd + hd columns);
+//   * the single MMA thread issues   PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
+//     so softmax A of tile j+1 overlaps PV_B(j)/S_B(j+1) and vice versa.
+//     tcgen05.mma ops of one thread execute in issue order, so S_A(j+1) may
+//     overwrite the TMEM columns PV_A(j) reads P_A(j) from without a wait;
+//     and tcgen05.commit tracks every earlier MMA of the thread, so "S_A(j)
+//     ready" also means "PV_A(j-1) done" -- the (rare, lazy) O rescale needs
+//     no extra barrier;
+//   * warps 2-5 run softmax A, warps 6-9 softmax B (two independent softmax
+//     streams per SMSP); one query row per thread, exp2 domain, masking only
+//     on diagonal/tail tiles, FFMA-fused exponent, ILP'd max/sum chains, P
+//     packed to bf16 and stored 32 columns at a time over consumed S.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -35,25 +38,25 @@ using namespace sm100;
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int NS = 2;               // K/V pipeline stages
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;       // TMA, MMA, 2 x 4 softmax warps
 constexpr float kLazy = 8.0f;       // log2 headroom before O is rescaled
+constexpr int kAtom = 128 * 128;    // SW128 atom column of a 128-row tile
 
 template <int HD>
 struct Smem {
-  static constexpr int kAtom = 128 * 128;          // one SW128 atom column: 128 rows x 128 B
-  static constexpr int kTile = (HD / 64) * kAtom;  // 128 x HD bf16
-  static constexpr int kQ = 0;
-  static constexpr int kK = kQ + kTile;
-  static constexpr int kV = kK + NS * kTile;
+  static constexpr int kTile = (HD / 64) * kAtom;
+  static constexpr int kQ = 0;                    // [2] (tile A, tile B)
+  static constexpr int kK = kQ + 2 * kTile;       // [NS]
+  static constexpr int kV = kK + NS * kTile;      // [NS]
   static constexpr int kBar = kV + NS * kTile;
-  static constexpr int kBytes = kBar + 256 + 1024;  // + barriers + alignment slack
+  static constexpr int kBytes = kBar + 256 + 1024;
 };
 
 struct Params {
   int n, b, hq, hkv;
   int causal;
-  int qtiles;
-  float scale_log2;   // scale * log2(e)
+  int qtiles, pairs;
+  float scale_log2;
   __nv_bfloat16* o;
   float* lse;
 };
@@ -61,7 +64,7 @@ struct Params {
 template <int HD>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const Params p) {
+                     const __grid_constant__ CUtensorMap tmV, const Params p) {
   using S = Smem<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -70,28 +73,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sV = smem + S::kV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;            // [NS]
-  uint64_t* k_empty = bars + 1 + NS;      // [NS]
-  uint64_t* v_full = bars + 1 + 2 * NS;   // [NS]
-  uint64_t* v_empty = bars + 1 + 3 * NS;  // [NS]
-  uint64_t* s_full = bars + 1 + 4 * NS;   // [2]
-  uint64_t* p_full = bars + 3 + 4 * NS;   // [2]
-  uint64_t* o_done = bars + 5 + 4 * NS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 4 * NS);
+  uint64_t* k_full = bars + 1;              // [NS]
+  uint64_t* k_empty = bars + 1 + NS;        // [NS]
+  uint64_t* v_full = bars + 1 + 2 * NS;     // [NS]
+  uint64_t* v_empty = bars + 1 + 3 * NS;    // [NS]
+  uint64_t* s_full = bars + 1 + 4 * NS;     // [2] per tile
+  uint64_t* p_full = bars + 3 + 4 * NS;     // [2] per tile
+  uint64_t* o_done = bars + 5 + 4 * NS;     // [2] per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 4 * NS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // work item: longest (causal) query tiles first
   const int heads = p.b * p.hq;
-  const int qt = p.qtiles - 1 - (int)(blockIdx.x / heads);
+  const int pair = p.pairs - 1 - (int)(blockIdx.x / heads);   // longest (causal) pairs first
   const int bh = (int)(blockIdx.x % heads);
-  const int bb = bh / p.hq;
-  const int h = bh % p.hq;
+  const int bb = bh / p.hq, h = bh % p.hq;
   const int g = h / (p.hq / p.hkv);
-  const int q0 = qt * BM;
   const int nkv_all = (p.n + BN - 1) / BN;
-  const int nkv = p.causal ? min(nkv_all, (q0 + BM - 1) / BN + 1) : nkv_all;
+  int nkvT[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int qt = 2 * pair + t;
+    nkvT[t] = qt >= p.qtiles ? 0 : (p.causal ? min(nkv_all, (qt * BM + BM - 1) / BN + 1) : nkv_all);
+  }
+  const int nkv = max(nkvT[0], nkvT[1]);
+  const int ntiles = nkvT[1] > 0 ? 2 : 1;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -101,11 +108,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 128);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_done[t], 1);
     }
-    mbar_init(o_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -113,8 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const uint32_t tS[2] = {tbase, tbase + 128};
-  const uint32_t tO = tbase + 256;
+  // TMEM columns: S_A 0, S_B 128, O_A 256, O_B 256 + HD
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -122,9 +128,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
-      mbar_expect_tx(q_full, BM * HD * 2);
+      mbar_expect_tx(q_full, ntiles * BM * HD * 2);
+      for (int t = 0; t < ntiles; ++t)
 #pragma unroll
-      for (int a = 0; a < HD / 64; ++a) tma_load_3d(sQ + a * S::kAtom, &tmQ, q_full, a * 64, bb * p.hq + h, q0);
+        for (int a = 0; a < HD / 64; ++a)
+          tma_load_3d(sQ + t * S::kTile + a * kAtom, &tmQ, q_full, a * 64, bb * p.hq + h, (2 * pair + t) * BM);
       for (int j = 0; j < nkv; ++j) {
         const int s = j % NS;
         const uint32_t ph = (j / NS) & 1;
@@ -132,70 +140,83 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(&k_full[s], BN * HD * 2);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a)
-          tma_load_3d(sK + s * S::kTile + a * S::kAtom, &tmK, &k_full[s], a * 64, bb * p.hkv + g, j * BN);
+          tma_load_3d(sK + s * S::kTile + a * kAtom, &tmK, &k_full[s], a * 64, bb * p.hkv + g, j * BN);
         mbar_wait(&v_empty[s], ph ^ 1);
         mbar_expect_tx(&v_full[s], BN * HD * 2);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a)
-          tma_load_3d(sV + s * S::kTile + a * S::kAtom, &tmV, &v_full[s], a * 64, bb * p.hkv + g, j * BN);
+          tma_load_3d(sV + s * S::kTile + a * kAtom, &tmV, &v_full[s], a * 64, bb * p.hkv + g, j * BN);
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    {  // the whole warp runs the issue loop; one elected lane issues
       constexpr uint32_t kIdQK = idesc_bf16(BM, BN, 0, 0);
       constexpr uint32_t kIdPV = idesc_bf16(BM, HD, 0, 1);
-      const uint32_t qaddr = smem_u32(sQ);
-      auto issue_pv = [&](int i) {
-        const int s = i % NS;
-        mbar_wait(&p_full[i & 1], (i >> 1) & 1);
-        mbar_wait(&v_full[s], (i / NS) & 1);
-        tc_fence_after();
-        const uint32_t vaddr = smem_u32(sV + s * S::kTile);
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          const uint64_t bdesc = sdesc(vaddr + kk * 2048, S::kAtom, 1024);
-          mma_ts(tO, tS[i & 1] + kk * 8, bdesc, kIdPV, (i > 0 || kk > 0) ? 1u : 0u);
-        }
-        mma_commit(&v_empty[s]);
-        mma_commit(o_done);
-      };
-      mbar_wait(q_full, 0);
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j % NS;
-        if (j >= 2) mbar_wait(o_done, (j - 2) & 1);  // P_{j-2} consumed -> S buffer free
-        mbar_wait(&k_full[s], (j / NS) & 1);
-        tc_fence_after();
-        const uint32_t kaddr = smem_u32(sK + s * S::kTile);
+      // base descriptors built once; per-MMA cost is a constant add
+      const uint64_t dQ0 = sdesc(smem_u32(sQ), 16, 1024);
+      const uint64_t dK0 = sdesc(smem_u32(sK), 16, 1024);
+      const uint64_t dV0 = sdesc(smem_u32(sV), kAtom, 1024);
+      auto issue_s = [&](int t, int j) {   // S_t = Q_t K_j^T
+        const uint64_t dk = dadd(dK0, (j % NS) * S::kTile);
+        const uint64_t dq = dadd(dQ0, t * S::kTile);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t koff = (kk >> 2) * S::kAtom + (kk & 3) * 32;
-          mma_ss(tS[j & 1], sdesc(qaddr + koff, 16, 1024), sdesc(kaddr + koff, 16, 1024), kIdQK,
-                 kk > 0 ? 1u : 0u);
+          const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
+          mma_ss_w(tbase + t * 128, dadd(dq, off), dadd(dk, off), kIdQK, kk > 0 ? 1u : 0u);
         }
-        mma_commit(&s_full[j & 1]);
-        mma_commit(&k_empty[s]);
-        if (j >= 1) issue_pv(j - 1);
+        mma_commit_w(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j
+        mbar_wait(&p_full[t], j & 1);
+        tc_fence_after();
+        const uint64_t dv = dadd(dV0, (j % NS) * S::kTile);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk)
+          mma_ts_w(tbase + 256 + t * HD, tbase + t * 128 + kk * 8, dadd(dv, kk * 2048), kIdPV,
+                 (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit_w(&o_done[t]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      if (nkvT[0] > 0) issue_s(0, 0);
+      if (nkvT[1] > 0) issue_s(1, 0);
+      mma_commit_w(&k_empty[0]);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % NS;
+        const bool next = j + 1 < nkv;
+        mbar_wait(&v_full[s], (j / NS) & 1);
+        if (next) mbar_wait(&k_full[(j + 1) % NS], ((j + 1) / NS) & 1);
+        tc_fence_after();
+        if (j < nkvT[0]) issue_pv(0, j);
+        if (next && j + 1 < nkvT[0]) issue_s(0, j + 1);
+        if (j < nkvT[1]) issue_pv(1, j);
+        if (next && j + 1 < nkvT[1]) issue_s(1, j + 1);
+        mma_commit_w(&v_empty[s]);
+        if (next) mma_commit_w(&k_empty[(j + 1) % NS]);
       }
-      issue_pv(nkv - 1);
     }
   } else {
-    // ---------------- softmax / correction / epilogue (warps 2..5) ----------------
+    // ---------------- softmax / correction / epilogue ----------------
+    const int t = (warp - 2) >> 2;            // query tile of this warpgroup
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tbase + t * 128 + lane_off;
+    const uint32_t tO = tbase + 256 + t * HD + lane_off;
+    const int q0 = (2 * pair + t) * BM;
     const int qrow = q0 + row;
+    const int my_nkv = nkvT[t];
     float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkv; ++j) {
+    for (int j = 0; j < my_nkv; ++j) {
       const int kv0 = j * BN;
-      mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
       uint32_t r[BN];
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS[j & 1] + lane_off + c * 32, r + c * 32);
+      for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, r + c * 32);
       tmem_wait_ld();
-      // mask only the diagonal (causal) and sequence-tail tiles; the branch is
-      // uniform across the CTA
       if ((p.causal && kv0 + BN - 1 > q0) || kv0 + BN > p.n) {
         int limit = p.n - kv0;
         if (p.causal) limit = min(limit, qrow - kv0 + 1);
@@ -203,7 +224,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < BN; ++c)
           if (c >= limit) r[c] = __float_as_uint(-INFINITY);
       }
-      // row max of the raw scores: 4 independent chains (ILP), then scaled
       float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
       for (int c = 0; c < BN; c += 4) {
@@ -219,64 +239,59 @@ __global__ void __launch_bounds__(kThreads, 1)
         m = mt;
       }
       const float mu = (m == -INFINITY) ? 0.f : m;
-      // p = 2^(s*scale*log2e - m): one FFMA + MUFU.EX2 per element; the row
-      // sum runs in 8 independent partial sums
       float rsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      uint32_t pk[BN / 2];
 #pragma unroll
-      for (int c = 0; c < BN; c += 2) {
-        const float e0 = fast_exp2(fmaf(__uint_as_float(r[c]), p.scale_log2, -mu));
-        const float e1 = fast_exp2(fmaf(__uint_as_float(r[c + 1]), p.scale_log2, -mu));
-        rsum[(c >> 1) & 7] += e0 + e1;
-        pk[c / 2] = pack_bf16(e0, e1);
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int x = 0; x < 32; x += 2) {
+          const float e0 = fast_exp2(fmaf(__uint_as_float(r[c * 32 + x]), p.scale_log2, -mu));
+          const float e1 = fast_exp2(fmaf(__uint_as_float(r[c * 32 + x + 1]), p.scale_log2, -mu));
+          rsum[(x >> 1) & 7] += e0 + e1;
+          pk[x / 2] = pack_bf16(e0, e1);
+        }
+        tmem_st16(tS + c * 16, pk);   // P over S columns already in registers
       }
-      const float rs = ((rsum[0] + rsum[1]) + (rsum[2] + rsum[3])) + ((rsum[4] + rsum[5]) + (rsum[6] + rsum[7]));
-      l = l * alpha + rs;
-      // P_j over the consumed S_j columns [0, BN/2)
-#pragma unroll
-      for (int c = 0; c < BN / 64; ++c) tmem_st32(tS[j & 1] + lane_off + c * 32, pk + c * 32);
-      // tcgen05.ld/st are warp-collective: rescale if any row of the warp
-      // needs it (rows that do not keep alpha == 1)
+      l = l * alpha + (((rsum[0] + rsum[1]) + (rsum[2] + rsum[3])) + ((rsum[4] + rsum[5]) + (rsum[6] + rsum[7])));
+      // s_full(j) tracks every earlier MMA, so PV(j-1) is complete: rescale O now
       if (__any_sync(0xffffffffu, rescale)) {
-        // O must hold the complete sum through PV_{j-1} before it is rescaled
-        mbar_wait(o_done, (j - 1) & 1);
-        tc_fence_after();
 #pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
           uint32_t ov[32];
-          tmem_ld32(tO + lane_off + c * 32, ov);
+          tmem_ld32(tO + c * 32, ov);
           tmem_wait_ld();
 #pragma unroll
           for (int x = 0; x < 32; ++x) ov[x] = __float_as_uint(__uint_as_float(ov[x]) * alpha);
-          tmem_st32(tO + lane_off + c * 32, ov);
+          tmem_st32(tO + c * 32, ov);
         }
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_full[j & 1]);
+      mbar_arrive(&p_full[t]);
     }
-    // epilogue: O / l -> bf16 rows, LSE (natural log)
-    mbar_wait(o_done, (nkv - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    const bool valid = qrow < p.n;
-    __nv_bfloat16* orow = p.o + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD;
+    if (my_nkv > 0) {
+      mbar_wait(&o_done[t], (my_nkv - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const bool valid = qrow < p.n;
+      __nv_bfloat16* orow = p.o + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD;
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      uint32_t ov[32];
-      tmem_ld32(tO + lane_off + c * 32, ov);
-      tmem_wait_ld();
-      uint32_t pkd[16];
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(tO + c * 32, ov);
+        tmem_wait_ld();
+        uint32_t pkd[16];
 #pragma unroll
-      for (int x = 0; x < 16; ++x)
-        pkd[x] = pack_bf16(__uint_as_float(ov[2 * x]) * inv, __uint_as_float(ov[2 * x + 1]) * inv);
-      if (valid) {
-        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+        for (int x = 0; x < 16; ++x)
+          pkd[x] = pack_bf16(__uint_as_float(ov[2 * x]) * inv, __uint_as_float(ov[2 * x + 1]) * inv);
+        if (valid) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
-        for (int x = 0; x < 4; ++x) dst[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+          for (int x = 0; x < 4; ++x) dst[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+        }
       }
+      if (valid) p.lse[((int64_t)bb * p.hq + h) * p.n + qrow] = (m + log2f(l)) * 0.69314718055994531f;
     }
-    if (valid) p.lse[((int64_t)bb * p.hq + h) * p.n + qrow] = (m + log2f(l)) * 0.69314718055994531f;
   }
   tc_fence_before();
   __syncthreads();
@@ -301,6 +316,7 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
   p.hkv = (int)hkv;
   p.causal = causal;
   p.qtiles = (int)((n + BM - 1) / BM);
+  p.pairs = (p.qtiles + 1) / 2;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.o = (__nv_bfloat16*)o;
   p.lse = lse;
@@ -310,7 +326,7 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
     UL_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  const int64_t grid = (int64_t)p.qtiles * b * hq;
+  const int64_t grid = (int64_t)p.pairs * b * hq;
   attn_fwd_kernel<HD><<<(unsigned)grid, kThreads, smem, st>>>(mq, mk, mv, p);
   return launched("attn_fwd_sm100");
 }
@@ -324,11 +340,8 @@ int preload_fwd() {
   return UL_OK;
 }
 
-int sm100_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
-              int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st) {
-  if (n == 0 || b == 0 || hq == 0) return UL_OK;
-  if (n > INT32_MAX / 2 || b * hq > 65535 * 1024)
-    return fail(UL_ERR_SHAPE, "attention: sequence/head extents too large (n=%lld)", (long long)n);
+int sm100_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b, int64_t hq,
+               int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st) {
   switch (hd) {
     case 64: return fwd::launch<64>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, st);
     case 128: return fwd::launch<128>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, st);

@@ -37,10 +37,7 @@ size_t sm100_bwd_workspace(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_
 int preload_a2a();
 int preload_simt();
 int preload_fwd();
-int preload_fwd2();
 int preload_bwd();
-int sm100_fwd2(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b, int64_t hq,
-               int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st);
 
 static int check_attn(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask) {
   if (mask != UL_MASK_NONE && mask != UL_MASK_CAUSAL)
@@ -73,7 +70,7 @@ int ul_preload_kernels(void) {
   UL_TRY(preload_a2a());
   UL_TRY(preload_simt());
   UL_TRY(preload_fwd());
-  UL_TRY(preload_fwd2());
+
   return preload_bwd();
 }
 
@@ -91,11 +88,9 @@ int ul_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse
   if (dtype == UL_DTYPE_F32)
     return simt_fwd((const float*)q, (const float*)k, (const float*)v, (float*)o, lse, n, b, hq, hkv, hd, causal,
                     scale, st);
-  // development A/B switch (to be removed): UL_FWD_V1=1 runs the one-tile kernel
-  static const bool v1 = getenv("UL_FWD_V1") != nullptr;
-  if (v1) return sm100_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, causal, scale, st);
   if (n * b * hq == 0) return UL_OK;
-  return sm100_fwd2(q, k, v, o, lse, n, b, hq, hkv, hd, causal, scale, st);
+  if (n > INT32_MAX / 2) return fail(UL_ERR_SHAPE, "attention: sequence too long (n=%lld)", (long long)n);
+  return sm100_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, causal, scale, st);
 }
 
 size_t ul_attn_bwd_workspace_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype) {
