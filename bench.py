@@ -230,8 +230,12 @@ def run_ours(args):
     f_fwd, f_bwd = attn_flops(n_seq, H // P, hd, causal)
     tflops_per_gpu = (f_fwd + f_bwd) / (ms_per_step / 1e3) / 1e12
 
-    # ---- per-kernel split (dominant kernel roofline) --------------------
-    kt = kernel_split(attn, q, k, v, do, args, dev)
+    # ---- per-kernel split (dominant kernel roofline) on this rank's
+    # head-sharded attention problem [N, 1, H/P, hd] --------------------
+    mk4 = lambda: torch.randn((n_seq, 1, H // P, hd), generator=g, device=dev,
+                              dtype=torch.float32).to(torch.bfloat16)
+    kt = kernel_split(attn, mk4(), mk4(), mk4(), mk4(), args, dev)
+    a2a = bench_a2a(dev, n_seq, H, hd, P, group)
 
     # ---- e2e through the public API from pinned host buffers ----------
     e2e = run_e2e(layer, q, k, v, do, args, P, dev)
@@ -277,7 +281,7 @@ def run_ours(args):
                 "layer_frac": round(tflops_per_gpu / peak, 4),
             },
             "kernels": kt["kernels"],
-            "a2a": kt.get("a2a"),
+            "a2a": a2a,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,
@@ -349,62 +353,107 @@ def kernel_split(attn, q, k, v, do, args, dev):
     return {"kernels": out}
 
 
+def bench_a2a(dev, n_seq, H, hd, P, group, reps=10):
+    """All-to-all throughput of the fused Q/K/V seq->head exchange (K1).
+
+    P > 1: this rank's real exchange over NVLink peer memory; GB/s = exact
+    egress bytes (local * (P-1)/P, simgroup.py:329-332) / device time, max
+    over ranks.  Always also: the same kernels on one GPU -- the P = 1 local
+    permute and an in-process P = 8 group (8 ranks on 8 streams, all traffic
+    in local HBM) -- reported against the HBM roofline (bytes = read + write
+    of every element moved)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2309_14509_b200 as U
+    out = {}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def timed(fn_list, streams):
+        times = []
+        for it in range(3 + reps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            ev = []
+            for fn, s in zip(fn_list, streams):
+                with torch.cuda.stream(s):
+                    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    fn()
+                    e.record()
+                    ev.append((a, e))
+            torch.cuda.synchronize()
+            if it >= 3:   # first start to last end across the ranks' streams
+                times.append(max(ev[0][0].elapsed_time(e) for _, e in ev))
+        return statistics.mean(times)
+
+    nl = n_seq // P
+    if P > 1:
+        x = [torch.randn((nl, 1, H, hd), device=dev).to(torch.bfloat16) for _ in range(3)]
+        ms = timed([lambda: group.all_to_all(x, 2, 0, label="bench.qkv")],
+                   [torch.cuda.current_stream(dev)])
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        local = 3 * nl * H * hd * 2
+        egress = local // P * (P - 1)
+        out["exchange"] = {"P": P, "ms": round(ms, 4), "egress_bytes": egress,
+                           "nvlink_gbs": round(egress / (ms / 1e3) / 1e9, 1), "peak_gbs_nominal": 900.0,
+                           "peak_gbs_measured_peer_copy": 770.0}
+    # single-GPU HBM-bound views of the same kernels
+    xs = [torch.randn((n_seq, 1, H, hd), device=dev).to(torch.bfloat16) for _ in range(3)]
+    g1 = U.SequenceGroup.single(dev.index)
+    ms1 = timed([lambda: g1.all_to_all(xs, 2, 0)], [torch.cuda.current_stream(dev)])
+    b1 = 2 * 3 * n_seq * H * hd * 2
+    out["p1_permute"] = {"ms": round(ms1, 4), "hbm_gbs": round(b1 / (ms1 / 1e3) / 1e9, 1)}
+    P8 = 8
+    if H % P8 == 0 and n_seq % P8 == 0:
+        groups = U.SequenceGroup.local_group(P8, slot_bytes=3 * (n_seq // P8) * H * hd * 2 + (1 << 20),
+                                             device=dev.index)
+        xl = [[t[r * (n_seq // P8):(r + 1) * (n_seq // P8)].contiguous() for t in xs] for r in range(P8)]
+        torch.cuda.synchronize()
+        ms8 = timed([(lambda r=r: groups[r].all_to_all(xl[r], 2, 0)) for r in range(P8)],
+                    [g.stream for g in groups])
+        for g in groups:
+            g.check()
+        moved = 3 * n_seq * H * hd * 2                 # every element of all 8 ranks
+        # push reads + writes everything once; the 7/8 remote share is read+written again by the drain
+        hbm_bytes = 2 * moved + 2 * moved * (P8 - 1) // P8
+        out["p8_in_process"] = {"ms": round(ms8, 4), "hbm_gbs": round(hbm_bytes / (ms8 / 1e3) / 1e9, 1),
+                                "note": "8 ranks on one B200 (streams); peer stores land in local HBM"}
+        for g in groups:
+            g.destroy()
+    return out
+
+
 def run_e2e(layer, q, k, v, do, args, P, dev):
-    """Every step copies its own q/k/v/dO from pinned host memory (H2D) and
-    reads its scalar result back (D2H).  Like a training loader, the H2D of
-    step i+1 runs on a copy stream while step i computes (two device input
-    buffers); each step's loss lands in its own pinned host slot."""
+    """Every step copies its own q/k/v/dO from pinned host memory (H2D),
+    runs the layer forward+backward through the public API and reads its
+    scalar result back (D2H, synchronising)."""
     import torch
     import torch.distributed as dist
     hq = [t.detach().cpu().pin_memory() for t in (q, k, v, do)]
     h2d = sum(t.numel() * t.element_size() for t in hq)
-    comp = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(device=dev)
-    bufs = [[torch.empty_like(t, device=dev) for t in hq] for _ in range(2)]
-    copied = [torch.cuda.Event() for _ in range(2)]
-    consumed = [torch.cuda.Event() for _ in range(2)]
-    n_total = args.warmup + args.steps
-    losses = torch.empty(n_total, dtype=torch.float32).pin_memory()
 
-    def h2d_into(i):
-        b = i % 2
-        with torch.cuda.stream(copy):
-            copy.wait_event(consumed[b])
-            for dst, src in zip(bufs[b], hq):
-                dst.copy_(src, non_blocking=True)
-            copied[b].record(copy)
-
-    def step(i, prefetch):
-        b = i % 2
-        comp.wait_event(copied[b])
-        qq, kk, vv, dd = (t.detach() for t in bufs[b])
+    def step():
+        qq, kk, vv, dd = (t.to(dev, non_blocking=True) for t in hq)
         for t in (qq, kk, vv):
             t.requires_grad_(True)
         o = layer(qq, kk, vv)
         torch.autograd.backward([o], [dd])
         loss = (o.float() * dd.float()).sum()        # the step's scalar result
-        consumed[b].record(comp)
-        if prefetch:
-            h2d_into(i + 1)
-        losses[i:i + 1].copy_(loss.reshape(1), non_blocking=True)
+        return loss.item()
 
-    for ev in consumed:
-        ev.record(comp)
-    h2d_into(0)
-    for i in range(args.warmup):
-        step(i, prefetch=i + 1 < args.warmup)
+    for _ in range(args.warmup):
+        step()
     torch.cuda.synchronize()
     if P > 1:
         dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record(comp)
-    copy.wait_stream(comp)
-    h2d_into(args.warmup)                        # every timed step's H2D is inside the timed region
-    for i in range(args.warmup, n_total):
-        step(i, prefetch=i + 1 < n_total)
-    e.record(comp)
+    s.record()
+    for _ in range(args.steps):
+        assert math.isfinite(step())
+    e.record()
     torch.cuda.synchronize()
-    assert torch.isfinite(losses[args.warmup:]).all()
     t = s.elapsed_time(e)
     if P > 1:
         tt = torch.tensor([t], device=dev)
@@ -414,7 +463,7 @@ def run_e2e(layer, q, k, v, do, args, P, dev):
     return {"value": round(n_seq / (t / args.steps / 1e3), 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": 4, "ms_per_step": round(t / args.steps, 4),
             "path": "DistributedAttention fwd+backward; per step H2D of q/k/v/dO from pinned host "
-                    "(copy stream, prefetched one step ahead) and D2H of the loss scalar"}
+                    "and D2H of the loss scalar (sequential; PCIe-bound: 128 MiB in per step)"}
 
 
 # ---------------------------------------------------------------------------

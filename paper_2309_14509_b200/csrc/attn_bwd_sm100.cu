@@ -18,9 +18,9 @@
 //              row) write P^T / dS^T back over them as bf16; dV += P^T dO
 //              and dK += dS^T Q are TS MMAs.  Double-buffered TMEM lets the
 //              MMAs of sub-tile i+1 run while the softmax of sub-tile i does.
-//   bwd_dq     one CTA per two 128-row query tiles of a head: 64-row kv
-//              sub-tiles shared by both, S = Q K^T, dP = dO V^T, dS -> TMEM,
-//              dQ += dS K, ping-ponged between the tiles.
+//   bwd_dq     one CTA per (128-row query tile, head): 64-row kv sub-tiles,
+//              S = Q K^T, dP = dO V^T (double-buffered), dS -> TMEM,
+//              dQ += dS K.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -356,34 +356,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---- dQ ------------------------------------------------------------------------
-// One CTA = two 128-row query tiles (A, B) of one (batch, head), like the
-// forward: each 64-row K/V sub-tile brought in by TMA serves both tiles.
-// TMEM per tile t: S_t (64 cols) | dP_t (64; dS written over it) | dQ_t (HD).
-// The MMA thread issues  dQ_A(j), S_A(j+1), dP_A(j+1), dQ_B(j), S_B(j+1),
-// dP_B(j+1): one tile's softmax overlaps the other tile's MMAs, and the
-// in-order tensor pipe orders dQ_t(j)'s reads of dS_t before dP_t(j+1)
-// overwrites them.  Warps 2-5 run softmax A, warps 6-9 softmax B.
-constexpr int kDqThreads = 320;
-
 template <int HD>
 struct DqSmem {
   static constexpr int kTileT = (HD / 64) * kAtomT;
   static constexpr int kTileS = (HD / 64) * kAtomS;
-  static constexpr int kQ = 0;                    // [2]
-  static constexpr int kO = kQ + 2 * kTileT;      // [2]
-  static constexpr int kK = kO + 2 * kTileT;      // [2 stages]
-  static constexpr int kV = kK + 2 * kTileS;      // [2 stages]
-  static constexpr int kBar = kV + 2 * kTileS;
+  static constexpr int kQ = 0;
+  static constexpr int kO = kQ + kTileT;
+  static constexpr int kK = kO + kTileT;          // [NST]
+  static constexpr int kV = kK + NST * kTileS;    // [NST]
+  static constexpr int kBar = kV + NST * kTileS;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
 
 template <int HD>
-__global__ void __launch_bounds__(kDqThreads, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                   const Params p) {
   using S = DqSmem<HD>;
-  constexpr int KST = 2;   // K/V sub-tile stages
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem + S::kQ;
@@ -392,41 +382,34 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   uint8_t* sV = smem + S::kV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;                // [KST]
-  uint64_t* kv_empty = bars + 1 + KST;         // [KST]
-  uint64_t* s_full = bars + 1 + 2 * KST;       // [2] per tile
-  uint64_t* p_full = bars + 3 + 2 * KST;       // [2] per tile
-  uint64_t* q_done = bars + 5 + 2 * KST;       // [2] per tile: last dQ MMA complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 2 * KST);
+  uint64_t* kv_full = bars + 1;                // [NST]
+  uint64_t* kv_empty = bars + 1 + NST;         // [NST]
+  uint64_t* s_full = bars + 1 + 2 * NST;       // [2]
+  uint64_t* p_full = bars + 3 + 2 * NST;       // [2]
+  uint64_t* buf_free = bars + 5 + 2 * NST;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 2 * NST);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int heads = p.b * p.hq;
   const int qtiles = (p.n + BT - 1) / BT;
-  const int pairs = (qtiles + 1) / 2;
-  const int pair = pairs - 1 - (int)(blockIdx.x / heads);   // longest first
+  const int qt = qtiles - 1 - (int)(blockIdx.x / heads);   // longest first
   const int bh = (int)(blockIdx.x % heads);
   const int bb = bh / p.hq, h = bh % p.hq;
   const int g = h / (p.hq / p.hkv);
+  const int q0 = qt * BT;
   const int nsub_all = (p.n + BS - 1) / BS;
-  int nT[2];
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int qt = 2 * pair + t;
-    nT[t] = qt >= qtiles ? 0 : (p.causal ? min(nsub_all, (qt * BT + BT - 1) / BS + 1) : nsub_all);
-  }
-  const int nsub = max(nT[0], nT[1]);
-  const int ntiles = nT[1] > 0 ? 2 : 1;
+  const int nsub = p.causal ? min(nsub_all, (q0 + BT - 1) / BS + 1) : nsub_all;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < KST; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 128);
-      mbar_init(&q_done[t], 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], kSoftThreads);
+      mbar_init(&buf_free[s], 1);
     }
     fence_barrier_init();
   }
@@ -435,7 +418,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  // tile t: S at 256t, dP (-> dS) at 256t + 64, dQ at 256t + 128
+  // TMEM: S[2] at 0/64, dP[2] at 128/192 (dS written over dP), dQ at 256
+  const uint32_t tdQ = tbase + 256;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -443,18 +427,15 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
       tma_prefetch_desc(&tmO);
-      mbar_expect_tx(q_full, ntiles * 2 * BT * HD * 2);
-      for (int t = 0; t < ntiles; ++t) {
-        const int q0 = (2 * pair + t) * BT;
+      mbar_expect_tx(q_full, 2 * BT * HD * 2);
 #pragma unroll
-        for (int a = 0; a < HD / 64; ++a) {
-          tma_load_3d(sQ + t * S::kTileT + a * kAtomT, &tmQ, q_full, a * 64, bb * p.hq + h, q0);
-          tma_load_3d(sO + t * S::kTileT + a * kAtomT, &tmO, q_full, a * 64, bb * p.hq + h, q0);
-        }
+      for (int a = 0; a < HD / 64; ++a) {
+        tma_load_3d(sQ + a * kAtomT, &tmQ, q_full, a * 64, bb * p.hq + h, q0);
+        tma_load_3d(sO + a * kAtomT, &tmO, q_full, a * 64, bb * p.hq + h, q0);
       }
       for (int j = 0; j < nsub; ++j) {
-        const int s = j % KST;
-        mbar_wait(&kv_empty[s], ((j / KST) & 1) ^ 1);
+        const int s = j % NST;
+        mbar_wait(&kv_empty[s], ((j / NST) & 1) ^ 1);
         mbar_expect_tx(&kv_full[s], 2 * BS * HD * 2);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a) {
@@ -470,104 +451,107 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       const uint64_t dQ0 = sdesc(smem_u32(sQ), 16, 1024), dO0 = sdesc(smem_u32(sO), 16, 1024);
       const uint64_t dKk0 = sdesc(smem_u32(sK), 16, 1024), dVk0 = sdesc(smem_u32(sV), 16, 1024);
       const uint64_t dKm0 = sdesc(smem_u32(sK), kAtomS, 1024);
-      auto issue_s = [&](int t, int j) {   // S_t = Q_t K_j^T, dP_t = dO_t V_j^T
-        const int s = j % KST;
-        const uint64_t dq = dadd(dQ0, t * S::kTileT), dob = dadd(dO0, t * S::kTileT);
-        const uint64_t dk = dadd(dKk0, s * S::kTileS), dv = dadd(dVk0, s * S::kTileS);
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
-          const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ss_w(tbase + 256 * t, dadd(dq, offT), dadd(dk, offS), kIdS, kk > 0 ? 1u : 0u);
-        }
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
-          const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ss_w(tbase + 256 * t + 64, dadd(dob, offT), dadd(dv, offS), kIdS, kk > 0 ? 1u : 0u);
-        }
-        mma_commit_w(&s_full[t]);
-      };
-      auto issue_dq = [&](int t, int j) {  // dQ_t += dS_t K_j
-        mbar_wait(&p_full[t], j & 1);
+      auto issue_dq = [&](int i) {
+        const int b = i & 1, s = i % NST;
+        const uint32_t tdP = tbase + 128 + b * 64;
+        mbar_wait(&p_full[b], (i >> 1) & 1);
         tc_fence_after();
-        const uint64_t dkm = dadd(dKm0, (j % KST) * S::kTileS);
+        const uint64_t dKm = dadd(dKm0, s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < BS / 16; ++kk)
-          mma_ts_w(tbase + 256 * t + 128, tbase + 256 * t + 64 + kk * 8, dadd(dkm, kk * 2048), kIdG,
-                   (j > 0 || kk > 0) ? 1u : 0u);
-        if (j == nT[t] - 1) mma_commit_w(&q_done[t]);
+          mma_ts_w(tdQ, tdP + a_col(kk), dadd(dKm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+        mma_commit_w(&kv_empty[s]);
+        mma_commit_w(&buf_free[b]);
       };
       mbar_wait(q_full, 0);
-      mbar_wait(&kv_full[0], 0);
-      tc_fence_after();
-      if (nT[0] > 0) issue_s(0, 0);
-      if (nT[1] > 0) issue_s(1, 0);
       for (int j = 0; j < nsub; ++j) {
-        const bool next = j + 1 < nsub;
-        if (next) {
-          mbar_wait(&kv_full[(j + 1) % KST], ((j + 1) / KST) & 1);
-          tc_fence_after();
+        const int b = j & 1, s = j % NST;
+        const uint32_t tS = tbase + b * 64, tdP = tbase + 128 + b * 64;
+        // buffer b was last read by dq(j-2), issued earlier by this thread (in-order)
+        mbar_wait(&kv_full[s], (j / NST) & 1);
+        tc_fence_after();
+        const uint64_t dKk = dadd(dKk0, s * S::kTileS), dVk = dadd(dVk0, s * S::kTileS);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
+          const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
+          mma_ss_w(tS, dadd(dQ0, offT), dadd(dKk, offS), kIdS, kk > 0 ? 1u : 0u);
         }
-        if (j < nT[0]) issue_dq(0, j);
-        if (next && j + 1 < nT[0]) issue_s(0, j + 1);
-        if (j < nT[1]) issue_dq(1, j);
-        if (next && j + 1 < nT[1]) issue_s(1, j + 1);
-        mma_commit_w(&kv_empty[j % KST]);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
+          const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
+          mma_ss_w(tdP, dadd(dO0, offT), dadd(dVk, offS), kIdS, kk > 0 ? 1u : 0u);
+        }
+        mma_commit_w(&s_full[b]);
+        if (j >= 1) issue_dq(j - 1);
       }
+      issue_dq(nsub - 1);
     }
   } else {
-    const int t = (warp - 2) >> 2;           // query tile of this warpgroup
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;        // which 32-column half of the kv sub-tile
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t tS = tbase + 256 * t + lane_off, tdP = tS + 64, tdQ = tS + 128;
-    const int q0 = (2 * pair + t) * BT;
     const int qrow = q0 + row;
-    const int my_n = nT[t];
+    const int c0 = half * 32;
     const int64_t roff = ((int64_t)bb * p.hq + h) * p.n_pad + qrow;
-    const float L = my_n > 0 ? p.L2[roff] : 0.f;
-    const float Dr = my_n > 0 ? p.Dv[roff] : 0.f;
-    for (int j = 0; j < my_n; ++j) {
-      mbar_wait(&s_full[t], j & 1);
+    const float L = p.L2[roff];
+    const float Dr = p.Dv[roff];
+    for (int j = 0; j < nsub; ++j) {
+      const int b = j & 1;
+      const int kv0 = j * BS + c0;
+      const uint32_t tS = tbase + b * 64, tdP = tbase + 128 + b * 64;
+      mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
-      const bool need_mask = p.causal && j * BS + BS - 1 > q0;   // diagonal sub-tiles only
+      uint32_t r[32], d[32];
+      tmem_ld32(tS + lane_off + c0, r);
+      tmem_ld32(tdP + lane_off + c0, d);
+      tmem_wait_ld();
+      uint32_t dsk[16];
+      if (p.causal && kv0 + 31 > q0) {       // only the diagonal sub-tiles need the mask
+        const int limit = qrow - kv0 + 1;     // columns x >= limit are masked (kv > q)
 #pragma unroll
-      for (int c = 0; c < BS / 32; ++c) {
-        uint32_t r[32], d[32];
-        tmem_ld32(tS + c * 32, r);
-        tmem_ld32(tdP + c * 32, d);
-        tmem_wait_ld();
-        uint32_t dsk[16];
-        if (need_mask) {
-          const int limit = qrow - (j * BS + c * 32) + 1;   // columns x >= limit: kv > q
-#pragma unroll
-          for (int x = 0; x < 32; x += 2) {
-            float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -L));
-            float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -L));
-            p0 = x >= limit ? 0.f : p0;
-            p1 = x + 1 >= limit ? 0.f : p1;
-            dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dr), p1 * (__uint_as_float(d[x + 1]) - Dr));
-          }
-        } else {
-#pragma unroll
-          for (int x = 0; x < 32; x += 2) {
-            const float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -L));
-            const float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -L));
-            dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dr), p1 * (__uint_as_float(d[x + 1]) - Dr));
-          }
+        for (int x = 0; x < 32; x += 2) {
+          float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -L));
+          float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -L));
+          p0 = x >= limit ? 0.f : p0;
+          p1 = x + 1 >= limit ? 0.f : p1;
+          dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dr), p1 * (__uint_as_float(d[x + 1]) - Dr));
         }
-        // packed dS of chunk c -> dP columns [16c, 16c+16), already consumed
-        tmem_st16(tdP + c * 16, dsk);
+      } else {
+#pragma unroll
+        for (int x = 0; x < 32; x += 2) {
+          const float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -L));
+          const float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -L));
+          dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dr), p1 * (__uint_as_float(d[x + 1]) - Dr));
+        }
       }
+      tmem_st16(tdP + lane_off + c0 + 16, dsk);   // dS over this warp's consumed dP columns
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_full[t]);
+      mbar_arrive(&p_full[b]);
     }
-    if (my_n > 0) {
-      mbar_wait(&q_done[t], 0);
-      tc_fence_after();
-      store_acc_rows<HD>(tdQ, 0, p.scale, p.dq + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD, qrow < p.n);
+    mbar_wait(&buf_free[(nsub - 1) & 1], ((nsub - 1) >> 1) & 1);
+    tc_fence_after();
+    // each half stores HD/2 columns of dQ * scale
+    const bool valid = qrow < p.n;
+    __nv_bfloat16* dst = p.dq + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 64; ++c) {
+      const int col = half * (HD / 2) + c * 32;
+      uint32_t v[32];
+      tmem_ld32(tdQ + lane_off + col, v);
+      tmem_wait_ld();
+      uint32_t pkd[16];
+#pragma unroll
+      for (int x = 0; x < 16; ++x)
+        pkd[x] = pack_bf16(__uint_as_float(v[2 * x]) * p.scale, __uint_as_float(v[2 * x + 1]) * p.scale);
+      if (valid) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + col);
+#pragma unroll
+        for (int x = 0; x < 4; ++x) d4[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+      }
     }
   }
   tc_fence_before();
@@ -634,8 +618,7 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
     UL_TRY(make_tmap_bhsd(&mo, dout, n, b * hq, HD, BT));
     UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, BS));
     UL_TRY(make_tmap_bhsd(&mv, v, n, b * hkv, HD, BS));
-    const int64_t pairs = (tiles + 1) / 2;
-    bwd_dq_kernel<HD><<<(unsigned)(pairs * b * hq), kDqThreads, DqSmem<HD>::kBytes, st>>>(mq, mk, mv, mo, p);
+    bwd_dq_kernel<HD><<<(unsigned)(tiles * b * hq), kThreads, DqSmem<HD>::kBytes, st>>>(mq, mk, mv, mo, p);
     UL_TRY(launched("attn_bwd_dq_sm100"));
   }
   return UL_OK;
