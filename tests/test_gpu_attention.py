@@ -162,6 +162,39 @@ def test_kernel_errors():
         attn.backward(y, y, y, y, None, y)
 
 
+def test_bwd_bf16_large_gqa_full():
+    # N = 4096, GQA 4q/1kv: every gradient element against the f64 oracle
+    n, hq, hkv, hd = 4096, 4, 1, 128
+    q, k, v, do = inputs(n, 1, hq, hkv, hd, torch.bfloat16, seed=77)
+    dq_r, dk_r, dv_r = O.local_attention_backward(q, k, v, do, "causal", exact=False)
+    attn = U().FlashAttention("causal")
+    tq, tk, tv, tdo = (to_dev(x, torch.bfloat16) for x in (q, k, v, do))
+    o, lse = attn.forward_with_lse(tq, tk, tv)
+    dq, dk, dv = attn.backward(tq, tk, tv, o, lse, tdo)
+    torch.cuda.synchronize()
+    for name, got, ref in (("dq", dq, dq_r), ("dk", dk, dk_r), ("dv", dv, dv_r)):
+        err = rel_max_err(to_np(got), ref)
+        assert err <= BF16_MAXREL, f"{name}: {err:.3e}"
+
+
+def test_p_invariance_of_head_sharded_kernels():
+    # a rank's heads give bitwise the same result as the same heads inside a
+    # larger launch (what Ulysses P-invariance needs from the local kernel)
+    n, hd = 1024, 128
+    q, k, v, do = inputs(n, 1, 8, 8, hd, torch.bfloat16, seed=12)
+    attn = U().FlashAttention("causal")
+    tq, tk, tv, tdo = (to_dev(x, torch.bfloat16) for x in (q, k, v, do))
+    o, lse = attn.forward_with_lse(tq, tk, tv)
+    g = attn.backward(tq, tk, tv, o, lse, tdo)
+    sl = slice(2, 4)
+    parts = [t[:, :, sl].contiguous() for t in (tq, tk, tv, tdo)]
+    o2, lse2 = attn.forward_with_lse(*parts[:3])
+    g2 = attn.backward(*parts[:3], o2, lse2, parts[3])
+    assert torch.equal(o2, o[:, :, sl]) and torch.equal(lse2, lse[:, sl])
+    for a, b in zip(g2, g):
+        assert torch.equal(a, b[:, :, sl])
+
+
 @pytest.mark.parametrize("n", [8192])
 def test_fwd_bf16_large_sampled_rows(n):
     # full-size config-2 shape; oracle on sampled query-row blocks (row_offset)
