@@ -22,27 +22,10 @@
 #include <cstring>
 #include <vector>
 
+#include "comm.cuh"
 #include "common.cuh"
 
 namespace ul {
-
-struct ErrWord {
-  volatile int32_t code;   // 0 or UL_ERR_DESYNC
-  volatile int32_t kind;   // 1 signature mismatch, 2 timeout
-  volatile int32_t peer;
-  volatile int32_t pad;
-  volatile uint64_t epoch;
-  volatile uint64_t expect_sig;
-  volatile uint64_t got;   // peer signature, or bitmask of missing ranks
-};
-
-struct Signals {           // lives at base + 2*slot_bytes on every rank
-  uint64_t flags[2][UL_MAX_RANKS];
-  uint64_t sigs[2][UL_MAX_RANKS];
-  unsigned int counter[2];
-  unsigned int pad[2];
-  ErrWord err;              // device-side error accumulator (local use)
-};
 
 struct Box {               // one (tensor, peer) chunk of a fused all-to-all
   const char* src;
@@ -115,25 +98,68 @@ template <> struct VecT<8>  { using T = int2; };
 template <> struct VecT<4>  { using T = int;  };
 template <> struct VecT<2>  { using T = short; };
 
-// one warp per row, lanes stride over the row's vectors, 4 loads in flight
+// Each warp owns a contiguous range of rows: the row index is decomposed
+// once and then advanced like an odometer (no 64-bit div/mod per row).
+// Short runs (the Ulysses head-group run is (H/P)*hd elements, 512 B-1 KiB)
+// are copied two rows per step so every lane keeps several 16-byte loads in
+// flight.
 template <int V>
 __device__ __forceinline__ void copy_box(const Box& bx, int64_t warp0, int64_t nwarps, int lane) {
   using T = typename VecT<V>::T;
   const int64_t nvec = bx.run / V;
   const int64_t e1 = bx.ext[1], e2 = bx.ext[2];
-  for (int64_t r = warp0; r < bx.rows; r += nwarps) {
-    int64_t c2 = r % e2;
-    int64_t t = r / e2;
-    int64_t c1 = t % e1;
-    int64_t c0 = t / e1;
-    const T* s = reinterpret_cast<const T*>(bx.src + c0 * bx.sst[0] + c1 * bx.sst[1] + c2 * bx.sst[2]);
-    T* d = reinterpret_cast<T*>(bx.dst + c0 * bx.dstr[0] + c1 * bx.dstr[1] + c2 * bx.dstr[2]);
+  const int64_t per = (bx.rows + nwarps - 1) / nwarps;
+  int64_t r = warp0 * per;
+  const int64_t r_end = min(bx.rows, r + per);
+  if (r >= r_end) return;
+  int64_t c2 = r % e2, t = r / e2;
+  int64_t c1 = t % e1, c0 = t / e1;
+  const char* srow = bx.src + c0 * bx.sst[0] + c1 * bx.sst[1] + c2 * bx.sst[2];
+  char* drow = bx.dst + c0 * bx.dstr[0] + c1 * bx.dstr[1] + c2 * bx.dstr[2];
+  auto advance = [&]() {
+    if (++c2 < e2) {
+      srow += bx.sst[2];
+      drow += bx.dstr[2];
+      return;
+    }
+    c2 = 0;
+    if (++c1 < e1) {
+      srow += bx.sst[1] - (e2 - 1) * bx.sst[2];
+      drow += bx.dstr[1] - (e2 - 1) * bx.dstr[2];
+      return;
+    }
+    c1 = 0;
+    ++c0;
+    srow += bx.sst[0] - (e1 - 1) * bx.sst[1] - (e2 - 1) * bx.sst[2];
+    drow += bx.dstr[0] - (e1 - 1) * bx.dstr[1] - (e2 - 1) * bx.dstr[2];
+  };
+  if (nvec <= 64) {
+    // two rows per step, up to 2 x 2 vectors per lane in flight
+    for (; r + 1 < r_end; r += 2) {
+      const T* s0 = reinterpret_cast<const T*>(srow);
+      T* d0 = reinterpret_cast<T*>(drow);
+      advance();
+      const T* s1 = reinterpret_cast<const T*>(srow);
+      T* d1 = reinterpret_cast<T*>(drow);
+      advance();
+      T a0, a1, b0, b1;
+      const bool l0 = lane < nvec, l1 = lane + 32 < nvec;
+      if (l0) { a0 = __ldcs(s0 + lane); b0 = __ldcs(s1 + lane); }
+      if (l1) { a1 = __ldcs(s0 + lane + 32); b1 = __ldcs(s1 + lane + 32); }
+      if (l0) { d0[lane] = a0; d1[lane] = b0; }
+      if (l1) { d0[lane + 32] = a1; d1[lane + 32] = b1; }
+    }
+  }
+  for (; r < r_end; ++r) {
+    const T* s = reinterpret_cast<const T*>(srow);
+    T* d = reinterpret_cast<T*>(drow);
     int64_t i = lane;
     for (; i + 96 < nvec; i += 128) {
       T a0 = __ldcs(s + i), a1 = __ldcs(s + i + 32), a2 = __ldcs(s + i + 64), a3 = __ldcs(s + i + 96);
       d[i] = a0; d[i + 32] = a1; d[i + 64] = a2; d[i + 96] = a3;
     }
     for (; i < nvec; i += 32) d[i] = __ldcs(s + i);
+    advance();
   }
 }
 
@@ -527,9 +553,21 @@ size_t ul_all_to_all_slot_bytes(int n, const int64_t* shapes, int ndim, int dtyp
   return tot;
 }
 
-int ul_all_to_all(ul_comm* c, int n, const void* const* in, void* const* out, const int64_t* shapes,
-                  int ndim, int dtype, int split, int concat, uint64_t label, void* stream) {
-  launch_count() = 0;
+}  // extern "C"
+
+namespace ul {
+
+// One collective call: geometry of every tensor, the receive-slot layout,
+// the cross-rank signature and this call's epoch / slot.
+struct CallPlan {
+  int n = 0, P = 1, me = 0, slot = 0;
+  Geom g[UL_MAX_FUSED];
+  size_t slot_off[UL_MAX_FUSED];
+  uint64_t sig = 0, epoch = 0;
+};
+
+static int plan_call(ul_comm* c, int n, void* const* out, const int64_t* shapes, int ndim, int dtype, int split,
+                     int concat, uint64_t label, CallPlan* pl) {
   if (n < 1 || n > UL_MAX_FUSED)
     return fail(UL_ERR_ARG, "all_to_all: fuses 1..%d tensors, got %d", UL_MAX_FUSED, n);
   if (ndim < 1 || ndim > 4) return fail(UL_ERR_SHAPE, "all_to_all: tensors of rank 1..4, got %d", ndim);
@@ -537,14 +575,11 @@ int ul_all_to_all(ul_comm* c, int n, const void* const* in, void* const* out, co
     return fail(UL_ERR_KERNEL, "all_to_all: unsupported dtype %d", dtype);
   if (split < 0 || split >= ndim || concat < 0 || concat >= ndim)
     return fail(UL_ERR_ARG, "all_to_all: axes (%d, %d) out of range for rank %d", split, concat, ndim);
-  if (!in || !out || !shapes) return fail(UL_ERR_ARG, "all_to_all: NULL argument");
-  const int P = c ? c->world : 1;
-  const int me = c ? c->rank : 0;
+  if (!out || !shapes) return fail(UL_ERR_ARG, "all_to_all: NULL argument");
+  pl->n = n;
+  pl->P = c ? c->world : 1;
+  pl->me = c ? c->rank : 0;
   const int esz = (int)dtype_size(dtype);
-  cudaStream_t st = (cudaStream_t)stream;
-
-  Geom g[UL_MAX_FUSED];
-  size_t slot_off[UL_MAX_FUSED];
   size_t slot_need = 0;
   uint64_t sig = 1469598103934665603ull;
   sig = fnv(sig, (uint64_t)n);
@@ -555,39 +590,133 @@ int ul_all_to_all(ul_comm* c, int n, const void* const* in, void* const* out, co
   sig = fnv(sig, label);
   uint64_t in_total = 0;
   for (int t = 0; t < n; ++t) {
-    UL_TRY(make_geom(ndim, shapes + 4 * t, esz, split, concat, P, &g[t]));
-    if (!in[t] || !out[t]) return fail(UL_ERR_ARG, "all_to_all: NULL tensor %d", t);
+    UL_TRY(make_geom(ndim, shapes + 4 * t, esz, split, concat, pl->P, &pl->g[t]));
+    if (!out[t]) return fail(UL_ERR_ARG, "all_to_all: NULL tensor %d", t);
     for (int k = 0; k < ndim; ++k) sig = fnv(sig, (uint64_t)shapes[4 * t + k]);
-    slot_off[t] = slot_need;
-    slot_need += align_up(g[t].out_bytes, 256);
-    in_total += g[t].in_bytes;
+    pl->slot_off[t] = slot_need;
+    slot_need += align_up(pl->g[t].out_bytes, 256);
+    in_total += pl->g[t].in_bytes;
   }
+  pl->sig = sig;
+  const int P = pl->P;
   if (P > 1 && slot_need > c->slot_bytes)
     return fail(UL_ERR_ARG, "all_to_all: call needs %zu receive-slot bytes, workspace has %zu", slot_need,
                 c->slot_bytes);
   for (int r = 0; P > 1 && r < P; ++r)
     if (!c->peer_base[r])
       return fail(UL_ERR_STATE, "all_to_all: rank %d has no mapping for peer %d (open_peers not called)",
-                  me, r);
-
-  uint64_t epoch = 0;
-  int slot = 0;
+                  pl->me, r);
   if (c) {
-    epoch = ++c->epoch;
-    slot = (int)(epoch & 1);
+    pl->epoch = ++c->epoch;
+    pl->slot = (int)(pl->epoch & 1);
     c->calls += 1;
     c->aggregate += (uint64_t)P * in_total;
     c->egress += in_total / P * (P - 1);
   }
+  return UL_OK;
+}
 
+// receiver side: bounded flag wait + drain of the P-1 remote chunks
+static int wait_and_drain(ul_comm* c, const CallPlan& pl, void* const* out, cudaStream_t st) {
+  Signals* mine = (Signals*)(c->base + 2 * c->slot_bytes);
+  a2a_wait_kernel<<<1, 32, 0, st>>>(mine, pl.me, pl.P, pl.slot, pl.epoch, pl.sig, c->timeout_ns, &mine->err,
+                                      c->err_dev);
+  UL_TRY(launched("a2a_wait"));
+  CopyParams dp;
+  memset(&dp, 0, sizeof(dp));
+  for (int t = 0; t < pl.n; ++t) {
+    for (int j = 0; j < pl.P; ++j) {
+      if (j == pl.me) continue;
+      // the chunk rank j sent sits in my slot exactly where it belongs in out
+      Box b;
+      const char* slot_img = c->base + (size_t)pl.slot * c->slot_bytes + pl.slot_off[t];
+      make_box(pl.g[t], j, pl.me, pl.P, slot_img, (char*)out[t], &b, /*drain=*/true);
+      if (b.rows > 0) dp.box[dp.nbox++] = b;
+    }
+  }
+  return launch_copy(dp, st, "a2a_drain");
+}
+
+int a2a_fused_begin(ul_comm* c, int n, void* const* seq_out, const int64_t* head_shapes, int dtype,
+                    uint64_t label, PeerEpilogue* ep, int* handle_slot, uint64_t* handle_epoch) {
+  // head->seq (split 0, concat 2) of [N, b, h_local, hd] head-layout tensors
+  CallPlan pl;
+  UL_TRY(plan_call(c, n, seq_out, head_shapes, 4, dtype, 0, 2, label, &pl));
+  for (int t = 0; t < n; ++t) {
+    PeerEpilogue& e = ep[t];
+    memset(&e, 0, sizeof(e));
+    e.active = pl.P > 1;
+    e.rank = pl.me;
+    e.world = pl.P;
+    e.slot = pl.slot;
+    e.epoch = pl.epoch;
+    e.sigv = pl.sig;
+    e.rows_per_rank = (int)(pl.g[t].S[0] / pl.P);
+    e.heads_seq = (int)(pl.g[t].S[2] * pl.P);
+    e.head_offset = (int)(pl.me * pl.g[t].S[2]);
+    for (int r = 0; r < pl.P; ++r) {
+      e.dst[r] = (r == pl.me || !c) ? (char*)seq_out[t]
+                                    : c->peer_base[r] + (size_t)pl.slot * c->slot_bytes + pl.slot_off[t];
+      if (c) e.sig[r] = (Signals*)(c->peer_base[r] + 2 * c->slot_bytes);
+    }
+    if (c) e.counter = &((Signals*)(c->base + 2 * c->slot_bytes))->counter[pl.slot];
+  }
+  *handle_slot = pl.slot;
+  *handle_epoch = pl.epoch;
+  return UL_OK;
+}
+
+int a2a_fused_finish(ul_comm* c, int n, void* const* seq_out, const int64_t* head_shapes, int dtype,
+                     uint64_t label, int slot, uint64_t epoch, cudaStream_t st) {
+  if (!c || c->world == 1) return UL_OK;
+  // rebuild the plan without advancing the epoch
+  CallPlan pl;
+  pl.n = n;
+  pl.P = c->world;
+  pl.me = c->rank;
+  const int esz = (int)dtype_size(dtype);
+  size_t off = 0;
+  uint64_t sig = 1469598103934665603ull;
+  sig = fnv(sig, (uint64_t)n);
+  sig = fnv(sig, 4);
+  sig = fnv(sig, (uint64_t)dtype);
+  sig = fnv(sig, 0);
+  sig = fnv(sig, 2);
+  sig = fnv(sig, label);
+  for (int t = 0; t < n; ++t) {
+    UL_TRY(make_geom(4, head_shapes + 4 * t, esz, 0, 2, pl.P, &pl.g[t]));
+    for (int k = 0; k < 4; ++k) sig = fnv(sig, (uint64_t)head_shapes[4 * t + k]);
+    pl.slot_off[t] = off;
+    off += align_up(pl.g[t].out_bytes, 256);
+  }
+  pl.sig = sig;
+  pl.slot = slot;
+  pl.epoch = epoch;
+  return wait_and_drain(c, pl, seq_out, st);
+}
+
+}  // namespace ul
+
+extern "C" {
+
+int ul_all_to_all(ul_comm* c, int n, const void* const* in, void* const* out, const int64_t* shapes,
+                  int ndim, int dtype, int split, int concat, uint64_t label, void* stream) {
+  launch_count() = 0;
+  if (!in) return fail(UL_ERR_ARG, "all_to_all: NULL argument");
+  CallPlan pl;
+  UL_TRY(plan_call(c, n, out, shapes, ndim, dtype, split, concat, label, &pl));
+  for (int t = 0; t < n; ++t)
+    if (!in[t]) return fail(UL_ERR_ARG, "all_to_all: NULL tensor %d", t);
+  const int P = pl.P, me = pl.me, slot = pl.slot;
+  cudaStream_t st = (cudaStream_t)stream;
   // push: local chunk -> out (local HBM), remote chunks -> peer slots (NVLink)
   CopyParams cp;
   memset(&cp, 0, sizeof(cp));
   for (int t = 0; t < n; ++t) {
     for (int k = 0; k < P; ++k) {
       const int i = (me + k) % P;  // rotate destinations to spread switch load
-      char* dst = (i == me) ? (char*)out[t] : c->peer_base[i] + (size_t)slot * c->slot_bytes + slot_off[t];
-      make_box(g[t], me, i, P, (const char*)in[t], dst, &cp.box[cp.nbox]);
+      char* dst = (i == me) ? (char*)out[t] : c->peer_base[i] + (size_t)slot * c->slot_bytes + pl.slot_off[t];
+      make_box(pl.g[t], me, i, P, (const char*)in[t], dst, &cp.box[cp.nbox]);
       if (cp.box[cp.nbox].rows > 0) ++cp.nbox;
     }
   }
@@ -596,38 +725,19 @@ int ul_all_to_all(ul_comm* c, int n, const void* const* in, void* const* out, co
     cp.rank = me;
     cp.world = P;
     cp.slot = slot;
-    cp.epoch = epoch;
-    cp.sig = sig;
+    cp.epoch = pl.epoch;
+    cp.sig = pl.sig;
     for (int r = 0; r < P; ++r) cp.peer_sig[r] = (Signals*)(c->peer_base[r] + 2 * c->slot_bytes);
     cp.counter = &((Signals*)(c->base + 2 * c->slot_bytes))->counter[slot];
     if (cp.nbox == 0) {  // nothing to move (empty tensors) -- still signal
-      make_box(g[0], me, me, P, (const char*)in[0], (char*)out[0], &cp.box[0]);
+      make_box(pl.g[0], me, me, P, (const char*)in[0], (char*)out[0], &cp.box[0]);
       cp.box[0].rows = 0;
       cp.nbox = 1;
     }
   }
   UL_TRY(launch_copy(cp, st, "a2a_push"));
   if (P == 1) return UL_OK;
-
-  Signals* mine = (Signals*)(c->base + 2 * c->slot_bytes);
-  a2a_wait_kernel<<<1, 32, 0, st>>>(mine, me, P, slot, epoch, sig, c->timeout_ns, &mine->err,
-                                      c->err_dev);
-  UL_TRY(launched("a2a_wait"));
-
-  CopyParams dp;
-  memset(&dp, 0, sizeof(dp));
-  for (int t = 0; t < n; ++t) {
-    for (int j = 0; j < P; ++j) {
-      if (j == me) continue;
-      // the chunk rank j sent sits in my slot exactly where it belongs in out
-      Box b;
-      const char* slot_img = c->base + (size_t)slot * c->slot_bytes + slot_off[t];
-      make_box(g[t], j, me, P, slot_img, (char*)out[t], &b, /*drain=*/true);
-      if (b.rows > 0) dp.box[dp.nbox++] = b;
-    }
-  }
-  UL_TRY(launch_copy(dp, st, "a2a_drain"));
-  return UL_OK;
+  return wait_and_drain(c, pl, out, st);
 }
 
 int ul_ulysses_volume(int64_t n, int64_t b, int64_t d, int64_t p, int convention, int64_t* num,

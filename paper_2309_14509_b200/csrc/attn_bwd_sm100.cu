@@ -169,9 +169,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 2 * NST);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int heads = p.b * p.hkv;
-  const int kt = (int)(blockIdx.x / heads);      // ascending kv tile == longest first (causal)
-  const int bg = (int)(blockIdx.x % heads);
+  // head-major: resident CTAs share one kv head's Q/dO stream in L2;
+  // ascending kv tile == longest first (causal)
+  const int ktiles = (p.n + BT - 1) / BT;
+  const int kt = (int)(blockIdx.x % ktiles);
+  const int bg = (int)(blockIdx.x / ktiles);
   const int bb = bg / p.hkv, g = bg % p.hkv;
   const int group = p.hq / p.hkv;
   const int kv0 = kt * BT;
@@ -390,10 +392,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 2 * NST);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int heads = p.b * p.hq;
+  // head-major (L2 reuse of the head's K/V), longest query tiles first
   const int qtiles = (p.n + BT - 1) / BT;
-  const int qt = qtiles - 1 - (int)(blockIdx.x / heads);   // longest first
-  const int bh = (int)(blockIdx.x % heads);
+  const int qt = qtiles - 1 - (int)(blockIdx.x % qtiles);
+  const int bh = (int)(blockIdx.x / qtiles);
   const int bb = bh / p.hq, h = bh % p.hq;
   const int g = h / (p.hq / p.hkv);
   const int q0 = qt * BT;

@@ -85,9 +85,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  const int heads = p.b * p.hq;
-  const int pair = p.pairs - 1 - (int)(blockIdx.x / heads);   // longest (causal) pairs first
-  const int bh = (int)(blockIdx.x % heads);
+  // head-major order: the CTAs resident at any moment work on one or a few
+  // heads and stream the same K/V tiles (L2 reuse even when b*h*N is large);
+  // within a head, the longest (causal) pairs go first
+  const int pair = p.pairs - 1 - (int)(blockIdx.x % p.pairs);
+  const int bh = (int)(blockIdx.x / p.pairs);
   const int bb = bh / p.hq, h = bh % p.hq;
   const int g = h / (p.hq / p.hkv);
   const int nkv_all = (p.n + BN - 1) / BN;
