@@ -47,6 +47,15 @@ def peaks():
         return FALLBACK_PEAKS, "fallback"
 
 
+def gpu_lead(cycles: int = 400_000):
+    """Enqueue a device-side sleep (~0.2 ms) right before a timed region so
+    the GPU queue runs ahead of the host: the start event then fires when the
+    sleep ends, after the host has enqueued the timed launches, and the
+    measured interval is device time, not host launch latency."""
+    import torch
+    torch.cuda._sleep(int(cycles))
+
+
 def attn_flops(n_seq, heads, hd, causal=True):
     """fwd 4*H*N^2*hd*c, bwd 8*H*N^2*hd*c, c = 1/2 causal."""
     c = 0.5 if causal else 1.0
@@ -212,6 +221,7 @@ def run_ours(args):
             dist.barrier()
         for i in range(args.steps):
             flush.zero_()                                  # untimed L2 flush
+            gpu_lead()                                     # keep the GPU queue ahead of the host
             ev[i][0].record()
             step(q.detach(), k.detach(), v.detach(), do)
             ev[i][1].record()
@@ -336,6 +346,7 @@ def kernel_split(attn, q, k, v, do, args, dev):
     for it in range(args.warmup + reps):
         for nm in names:
             flush.zero_()
+            gpu_lead()
             a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             run(nm)
@@ -374,6 +385,10 @@ def bench_a2a(dev, n_seq, H, hd, P, group, reps=10):
             flush.zero_()
             torch.cuda.synchronize()
             ev = []
+            # one device sleep long enough for the host to enqueue every rank
+            gpu_lead(300_000 * len(streams))
+            for s in streams:
+                s.wait_stream(torch.cuda.current_stream(dev))
             for fn, s in zip(fn_list, streams):
                 with torch.cuda.stream(s):
                     a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

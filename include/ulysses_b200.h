@@ -158,6 +158,25 @@ int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* 
                        int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
                        int dtype, int mask, float scale, int stage_mask, void* stream);
 
+/* Local attention with the head->seq exchange (K2) fused into the kernels'
+ * epilogues: every finished output row goes both to the head-layout tensor
+ * (o / dq, dk, dv -- saved for the backward) and straight into its
+ * destination rank's sequence layout (the own seq_out, or the peer's receive
+ * slot over NVLink); the producing kernel's last CTA publishes the call and
+ * the call ends with this rank's flag wait + drain into seq_out.  Equal to
+ * ul_attn_fwd + ul_all_to_all(split 0, concat 2) (which fp32 mode, P = 1
+ * and empty problems run instead).  A collective: every rank calls it with
+ * the same shapes and label.
+ *   seq_out [n/P, b, P*hq, hd];  seq_dq [n/P, b, P*hq, hd], seq_dk/dv [n/P, b, P*hkv, hd] */
+int ul_attn_fwd_exchange(ul_comm* comm, const void* q, const void* k, const void* v, void* o, float* lse,
+                         void* seq_out, int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
+                         int dtype, int mask, float scale, uint64_t label_hash, void* stream);
+int ul_attn_bwd_exchange(ul_comm* comm, const void* q, const void* k, const void* v, const void* o,
+                         const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                         void* workspace, size_t workspace_bytes, void* seq_dq, void* seq_dk,
+                         void* seq_dv, int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
+                         int dtype, int mask, float scale, uint64_t label_hash, void* stream);
+
 /* Number of kernel launches the last ul_* call on this thread issued, and
  * the cumulative count since the library was loaded (all threads). */
 int ul_last_launch_count(void);

@@ -30,7 +30,8 @@ EXPORTS = (
     "ul_comm_open_peers", "ul_comm_validate_handles", "ul_comm_link_local", "ul_comm_destroy", "ul_comm_rank",
     "ul_comm_world", "ul_comm_slot_bytes", "ul_comm_set_timeout_ms", "ul_comm_status",
     "ul_comm_ledger", "ul_all_to_all", "ul_all_to_all_slot_bytes", "ul_attn_fwd",
-    "ul_attn_bwd_workspace_bytes", "ul_attn_bwd", "ul_attn_bwd_stages", "ul_last_launch_count",
+    "ul_attn_bwd_workspace_bytes", "ul_attn_bwd", "ul_attn_bwd_stages", "ul_attn_fwd_exchange",
+    "ul_attn_bwd_exchange", "ul_last_launch_count",
     "ul_total_launch_count", "ul_ulysses_volume",
 )
 
@@ -73,6 +74,13 @@ def _declare(lib):
         "ul_attn_bwd_stages": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                               ctypes.c_size_t, c_i64, c_i64, c_i64, c_i64, c_i64, ctypes.c_int,
                                               ctypes.c_int, ctypes.c_float, ctypes.c_int, c_vp]),
+        "ul_attn_fwd_exchange": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64,
+                                                c_i64, c_i64, ctypes.c_int, ctypes.c_int, ctypes.c_float,
+                                                ctypes.c_uint64, c_vp]),
+        "ul_attn_bwd_exchange": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                                ctypes.c_size_t, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64,
+                                                c_i64, ctypes.c_int, ctypes.c_int, ctypes.c_float, ctypes.c_uint64,
+                                                c_vp]),
         "ul_last_launch_count": (ctypes.c_int, []),
         "ul_total_launch_count": (ctypes.c_uint64, []),
         "ul_ulysses_volume": (ctypes.c_int, [c_i64, c_i64, c_i64, c_i64, ctypes.c_int, P(c_i64), P(c_i64)]),

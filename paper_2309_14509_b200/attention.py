@@ -152,6 +152,51 @@ class FlashAttention:
                                           dt, self.mask_code, self._scale(hd), _stream(q)))
         return dq, dk, dv
 
+    # -- fused head->seq exchange (K2 in the kernels' epilogues) ------------
+    def forward_exchange(self, q, k, v, group: SequenceGroup, label: str = "attn.ctx.head2seq"):
+        """Forward on head-sharded q/k/v [N, b, h, hd] plus the head->seq
+        exchange of O fused into the kernel epilogue.  Returns (o_head, lse,
+        o_seq) with o_seq = seq layout [N/P, b, P*h, hd] of this rank."""
+        from .comm import label_hash
+        n, b, hq, hkv, hd = self._check(q, k, v)
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        p = group.world
+        o = torch.empty_like(q)
+        lse = torch.empty((b, hq, n), dtype=torch.float32, device=q.device)
+        o_seq = torch.empty((n // p, b, hq * p, hd), dtype=q.dtype, device=q.device)
+        _lib.check(_lib.lib().ul_attn_fwd_exchange(group._handle, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                                   o.data_ptr(), lse.data_ptr(), o_seq.data_ptr(), n, b, hq, hkv,
+                                                   hd, _ATTN_DTYPES[q.dtype], self.mask_code, self._scale(hd),
+                                                   label_hash(label), _stream(q)))
+        group._record(label, o.numel())
+        return o, lse, o_seq
+
+    def backward_exchange(self, q, k, v, o, lse, do, group: SequenceGroup, label: str = "bwd.qkv.head2seq"):
+        """Backward with the head->seq exchange of dQ/dK/dV fused into the
+        epilogues.  Returns sequence-layout (dq, dk, dv) of this rank."""
+        from .comm import label_hash
+        if lse is None:
+            raise ForwardStateError("backward needs the state saved by the forward pass")
+        n, b, hq, hkv, hd = self._check(q, k, v)
+        q, k, v, o, do = (x.contiguous() for x in (q, k, v, o, do))
+        p = group.world
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        sq = torch.empty((n // p, b, hq * p, hd), dtype=q.dtype, device=q.device)
+        sk = torch.empty((n // p, b, hkv * p, hd), dtype=q.dtype, device=q.device)
+        sv = torch.empty_like(sk)
+        dt = _ATTN_DTYPES[q.dtype]
+        wsb = int(_lib.lib().ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dt))
+        ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=q.device)
+        _lib.check(_lib.lib().ul_attn_bwd_exchange(group._handle, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                                   o.data_ptr(), do.data_ptr(), lse.data_ptr(), dq.data_ptr(),
+                                                   dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                   sq.data_ptr(), sk.data_ptr(), sv.data_ptr(), n, b, hq, hkv, hd,
+                                                   dt, self.mask_code, self._scale(hd), label_hash(label),
+                                                   _stream(q)))
+        for name, t in (("bwd.q.head2seq", dq), ("bwd.k.head2seq", dk), ("bwd.v.head2seq", dv)):
+            group._record(name, t.numel())
+        return sq, sk, sv
+
     def __call__(self, q, k, v):
         return _LocalAttnFn.apply(self, q, k, v)
 
@@ -196,10 +241,11 @@ class _UlyssesAttnFn(torch.autograd.Function):
                                           labels=["attn.q.seq2head", "attn.k.seq2head", "attn.v.seq2head"])
         else:
             q4, k4, v4 = q.contiguous(), k.contiguous(), v.contiguous()
-        o4, lse = attn.forward_with_lse(q4, k4, v4)
         if group.world > 1:
-            (o,) = group.all_to_all([o4], gather_idx, scatter_idx, label="attn.ctx.head2seq")
+            # head->seq of O fused into the attention epilogue (K2 in K3)
+            o4, lse, o = attn.forward_exchange(q4, k4, v4, group, label="attn.ctx.head2seq")
         else:
+            o4, lse = attn.forward_with_lse(q4, k4, v4)
             o = o4
         ctx.group, ctx.attn, ctx.idx = group, attn, (scatter_idx, gather_idx)
         ctx.save_for_backward(q4, k4, v4, o4, lse)
@@ -215,12 +261,11 @@ class _UlyssesAttnFn(torch.autograd.Function):
             (do4,) = group.all_to_all([do], scatter_idx, gather_idx, label="bwd.ctx.seq2head")
         else:
             do4 = do
-        dq4, dk4, dv4 = attn.backward(q4, k4, v4, o4, lse, do4)
         if group.world > 1:
-            dq, dk, dv = group.all_to_all([dq4, dk4, dv4], gather_idx, scatter_idx, label="bwd.qkv.head2seq",
-                                          labels=["bwd.q.head2seq", "bwd.k.head2seq", "bwd.v.head2seq"])
+            # head->seq of dQ, dK, dV fused into the backward kernels' epilogues
+            dq, dk, dv = attn.backward_exchange(q4, k4, v4, o4, lse, do4, group, label="bwd.qkv.head2seq")
         else:
-            dq, dk, dv = dq4, dk4, dv4
+            dq, dk, dv = attn.backward(q4, k4, v4, o4, lse, do4)
         return None, None, None, None, dq, dk, dv
 
 

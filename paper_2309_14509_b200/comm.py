@@ -198,6 +198,12 @@ class SequenceGroup:
         _lib.check(_lib.lib().ul_comm_ledger(self._handle, ctypes.byref(c), ctypes.byref(e), ctypes.byref(a)))
         return {"calls": c.value, "egress_bytes": e.value, "aggregate_bytes": a.value}
 
+    def _record(self, label: str, local_elements: int):
+        """One logical all_to_all of `local_elements` per rank (simgroup.py:329-332)."""
+        p = self.world
+        self.records.append(CommRecord("all_to_all", label, p * local_elements,
+                                       local_elements // p * (p - 1)))
+
     def total_egress(self) -> int:
         return sum(r.per_rank_egress_elements for r in self.records)
 
@@ -234,8 +240,7 @@ class SequenceGroup:
                 shapes[4 * t + k] = x.shape[k]
         labels = labels or [label] * len(tensors)
         for x, lab in zip(tensors, labels):
-            n = x.numel()
-            self.records.append(CommRecord("all_to_all", lab, p * n, n // p * (p - 1)))
+            self._record(lab, x.numel())
         ins = [x.contiguous() for x in tensors]
         inp = (ctypes.c_void_p * len(ins))(*[x.data_ptr() for x in ins])
         outp = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])

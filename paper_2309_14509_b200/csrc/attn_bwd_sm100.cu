@@ -26,7 +26,9 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstring>
 
+#include "comm.cuh"
 #include "common.cuh"
 #include "sm100.cuh"
 #include "tmap.cuh"
@@ -56,12 +58,17 @@ __device__ __forceinline__ uint32_t a_col(int kk) { return (kk >> 1) * 32 + 16 +
 struct Params {
   int n, n_pad, b, hq, hkv;
   int causal;
+  int head_major;   // CTA order: head-major once a head has a full wave of tiles
   float scale, scale_log2;
   const float* L2;   // [b*hq][n_pad] lse * log2(e), +inf padded
   const float* Dv;   // [b*hq][n_pad] rowsum(dO*O), 0 padded
   __nv_bfloat16* dq;
   __nv_bfloat16* dk;
   __nv_bfloat16* dv;
+  // fused head->seq of dQ / dK / dV (active when P > 1): rows also go to
+  // their destination rank's sequence layout; the dQ kernel (launched last)
+  // publishes the call once all its CTAs and the dK/dV kernel are done
+  PeerEpilogue ep_dq, ep_dk, ep_dv;
 };
 
 // ---- pre-pass ----------------------------------------------------------------
@@ -109,10 +116,12 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
   }
 }
 
-// TMEM epilogue: a 128-lane x HD fp32 accumulator -> bf16 rows (x mul)
+// TMEM epilogue: a 128-lane x HD fp32 accumulator -> bf16 rows (x mul).
+// `peer` (or nullptr) is this row's slot in the destination rank's sequence
+// layout: the fused head->seq exchange stores the same bytes there.
 template <int HD>
 __device__ __forceinline__ void store_acc_rows(uint32_t tacc, uint32_t lane_off, float mul, __nv_bfloat16* dst,
-                                               bool valid) {
+                                               bool valid, char* peer = nullptr) {
 #pragma unroll
   for (int c = 0; c < HD / 32; ++c) {
     uint32_t v[32];
@@ -126,6 +135,11 @@ __device__ __forceinline__ void store_acc_rows(uint32_t tacc, uint32_t lane_off,
       uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
 #pragma unroll
       for (int x = 0; x < 4; ++x) d4[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+      if (peer) {
+        uint4* p4 = reinterpret_cast<uint4*>(peer) + c * 4;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) p4[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+      }
     }
   }
 }
@@ -172,8 +186,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // head-major: resident CTAs share one kv head's Q/dO stream in L2;
   // ascending kv tile == longest first (causal)
   const int ktiles = (p.n + BT - 1) / BT;
-  const int kt = (int)(blockIdx.x % ktiles);
-  const int bg = (int)(blockIdx.x / ktiles);
+  const int kheads = p.b * p.hkv;
+  const int kt = p.head_major ? (int)(blockIdx.x % ktiles) : (int)(blockIdx.x / kheads);
+  const int bg = p.head_major ? (int)(blockIdx.x / ktiles) : (int)(blockIdx.x % kheads);
   const int bb = bg / p.hkv, g = bg % p.hkv;
   const int group = p.hq / p.hkv;
   const int kv0 = kt * BT;
@@ -345,8 +360,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const bool valid = kvrow < p.n;
     const int64_t off = (((int64_t)kvrow * p.b + bb) * p.hkv + g) * HD;
-    if (half == 0) store_acc_rows<HD>(tdV, lane_off, 1.f, p.dv + off, valid);
-    else store_acc_rows<HD>(tdK, lane_off, p.scale, p.dk + off, valid);
+    const PeerEpilogue& ep = half == 0 ? p.ep_dv : p.ep_dk;
+    char* peer = (ep.active && valid) ? peer_row_ptr(ep, kvrow, bb, p.b, g, HD, 2) : nullptr;
+    if (half == 0) store_acc_rows<HD>(tdV, lane_off, 1.f, p.dv + off, valid, peer);
+    else store_acc_rows<HD>(tdK, lane_off, p.scale, p.dk + off, valid, peer);
+    if (ep.active) __threadfence_system();   // dQ kernel signals after this launch completes
   }
   tc_fence_before();
   __syncthreads();
@@ -392,10 +410,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 2 * NST);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // head-major (L2 reuse of the head's K/V), longest query tiles first
+  // longest query tiles first; head-major for long sequences (see the forward)
   const int qtiles = (p.n + BT - 1) / BT;
-  const int qt = qtiles - 1 - (int)(blockIdx.x % qtiles);
-  const int bh = (int)(blockIdx.x / qtiles);
+  const int qheads = p.b * p.hq;
+  const int qt = qtiles - 1 - (int)(p.head_major ? blockIdx.x % qtiles : blockIdx.x / qheads);
+  const int bh = p.head_major ? (int)(blockIdx.x / qtiles) : (int)(blockIdx.x % qheads);
   const int bb = bh / p.hq, h = bh % p.hq;
   const int g = h / (p.hq / p.hkv);
   const int q0 = qt * BT;
@@ -553,11 +572,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint4* d4 = reinterpret_cast<uint4*>(dst + col);
 #pragma unroll
         for (int x = 0; x < 4; ++x) d4[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+        if (p.ep_dq.active) {   // fused head->seq of dQ
+          uint4* p4 = reinterpret_cast<uint4*>(peer_row_ptr(p.ep_dq, qrow, bb, p.b, h, HD, 2) + col * 2);
+#pragma unroll
+          for (int x = 0; x < 4; ++x) p4[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+        }
       }
     }
+    if (p.ep_dq.active) __threadfence_system();
   }
   tc_fence_before();
   __syncthreads();
+  // last CTA publishes the fused dQ/dK/dV exchange (the dK/dV kernel ran before this launch)
+  if (p.ep_dq.active && threadIdx.x == 0) peer_signal_last_cta(p.ep_dq, gridDim.x);
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
@@ -570,7 +597,7 @@ static int64_t pad_n(int64_t n) { return (n + 127) / 128 * 128; }
 template <int HD>
 static int launch(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
                   void* dq, void* dk, void* dv, void* ws, int64_t n, int64_t b, int64_t hq, int64_t hkv, int causal,
-                  float scale, int stages, cudaStream_t st) {
+                  float scale, int stages, const PeerEpilogue* eps, cudaStream_t st) {
   const int64_t npad = pad_n(n);
   float* L2 = reinterpret_cast<float*>(ws);
   float* Dv = L2 + b * hq * npad;
@@ -588,6 +615,7 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
   p.hq = (int)hq;
   p.hkv = (int)hkv;
   p.causal = causal;
+  p.head_major = (n + BT - 1) / BT >= sm_count();
   p.scale = scale;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.L2 = L2;
@@ -595,6 +623,15 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
   p.dq = (__nv_bfloat16*)dq;
   p.dk = (__nv_bfloat16*)dk;
   p.dv = (__nv_bfloat16*)dv;
+  if (eps) {   // [dq, dk, dv]
+    p.ep_dq = eps[0];
+    p.ep_dk = eps[1];
+    p.ep_dv = eps[2];
+  } else {
+    memset(&p.ep_dq, 0, sizeof(PeerEpilogue));
+    memset(&p.ep_dk, 0, sizeof(PeerEpilogue));
+    memset(&p.ep_dv, 0, sizeof(PeerEpilogue));
+  }
   static bool attr = false;
   if (!attr) {
     UL_CUDA(cudaFuncSetAttribute(bwd_dkdv_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -647,13 +684,15 @@ size_t sm100_bwd_workspace(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_
 
 int sm100_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
               void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n, int64_t b, int64_t hq,
-              int64_t hkv, int64_t hd, int causal, float scale, int stages, cudaStream_t st) {
+              int64_t hkv, int64_t hd, int causal, float scale, int stages, cudaStream_t st,
+              const PeerEpilogue* eps) {
   (void)ws_bytes;
   if (n > INT32_MAX / 2) return fail(UL_ERR_SHAPE, "attention: sequence too long (n=%lld)", (long long)n);
   switch (hd) {
-    case 64: return bwd::launch<64>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, st);
+    case 64:
+      return bwd::launch<64>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, eps, st);
     case 128:
-      return bwd::launch<128>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, st);
+      return bwd::launch<128>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, eps, st);
     default:
       return fail(UL_ERR_KERNEL, "bf16 attention supports head_dim 64 or 128, got %lld", (long long)hd);
   }

@@ -25,7 +25,9 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstring>
 
+#include "comm.cuh"
 #include "common.cuh"
 #include "sm100.cuh"
 #include "tmap.cuh"
@@ -56,9 +58,11 @@ struct Params {
   int n, b, hq, hkv;
   int causal;
   int qtiles, pairs;
+  int head_major;
   float scale_log2;
   __nv_bfloat16* o;
   float* lse;
+  PeerEpilogue ep;   // active: also store O rows into the seq layout of their rank (fused head->seq)
 };
 
 template <int HD>
@@ -85,11 +89,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // head-major order: the CTAs resident at any moment work on one or a few
-  // heads and stream the same K/V tiles (L2 reuse even when b*h*N is large);
-  // within a head, the longest (causal) pairs go first
-  const int pair = p.pairs - 1 - (int)(blockIdx.x % p.pairs);
-  const int bh = (int)(blockIdx.x / p.pairs);
+  // CTA order (longest causal pairs first either way):
+  //  head-major when a head has >= one wave of pairs -- resident CTAs then
+  //    stream the same K/V tiles (L2 reuse at long N / many heads);
+  //  pair-major otherwise -- a global longest-first (LPT) order balances
+  //    the waves when every head is short.
+  const int heads = p.b * p.hq;
+  const int pair = p.head_major ? p.pairs - 1 - (int)(blockIdx.x % p.pairs)
+                                : p.pairs - 1 - (int)(blockIdx.x / heads);
+  const int bh = p.head_major ? (int)(blockIdx.x / p.pairs) : (int)(blockIdx.x % heads);
   const int bb = bh / p.hq, h = bh % p.hq;
   const int g = h / (p.hq / p.hkv);
   const int nkv_all = (p.n + BN - 1) / BN;
@@ -290,13 +298,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
           for (int x = 0; x < 4; ++x) dst[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+          if (p.ep.active) {
+            // fused head->seq: the same 64 bytes straight into the destination
+            // rank's sequence layout (own `out`, or its receive slot over NVLink)
+            uint4* pd = reinterpret_cast<uint4*>(peer_row_ptr(p.ep, qrow, bb, p.b, h, HD, 2)) + c * 4;
+#pragma unroll
+            for (int x = 0; x < 4; ++x) pd[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+          }
         }
       }
       if (valid) p.lse[((int64_t)bb * p.hq + h) * p.n + qrow] = (m + log2f(l)) * 0.69314718055994531f;
     }
+    if (p.ep.active) __threadfence_system();
   }
   tc_fence_before();
   __syncthreads();
+  if (p.ep.active && threadIdx.x == 0) peer_signal_last_cta(p.ep, gridDim.x);
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
@@ -306,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int HD>
 static int launch(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
-                  int64_t hq, int64_t hkv, int causal, float scale, cudaStream_t st) {
+                  int64_t hq, int64_t hkv, int causal, float scale, const PeerEpilogue* ep, cudaStream_t st) {
   CUtensorMap mq, mk, mv;
   UL_TRY(make_tmap_bhsd(&mq, q, n, b * hq, HD, 128));
   UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, 128));
@@ -319,9 +336,12 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
   p.causal = causal;
   p.qtiles = (int)((n + BM - 1) / BM);
   p.pairs = (p.qtiles + 1) / 2;
+  p.head_major = p.pairs >= sm_count();
   p.scale_log2 = scale * 1.4426950408889634f;
   p.o = (__nv_bfloat16*)o;
   p.lse = lse;
+  if (ep) p.ep = *ep;
+  else memset(&p.ep, 0, sizeof(p.ep));
   const int smem = Smem<HD>::kBytes;
   static bool attr = false;
   if (!attr) {
@@ -343,10 +363,10 @@ int preload_fwd() {
 }
 
 int sm100_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b, int64_t hq,
-               int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st) {
+               int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st, const PeerEpilogue* ep) {
   switch (hd) {
-    case 64: return fwd::launch<64>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, st);
-    case 128: return fwd::launch<128>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, st);
+    case 64: return fwd::launch<64>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, ep, st);
+    case 128: return fwd::launch<128>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, ep, st);
     default:
       return fail(UL_ERR_KERNEL, "bf16 attention supports head_dim 64 or 128, got %lld", (long long)hd);
   }

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <string>
 
+#include "comm.cuh"
 #include "common.cuh"
 
 namespace ul {
@@ -29,10 +30,12 @@ int simt_bwd(const float* q, const float* k, const float* v, const float* o, con
              const float* lse, float* dq, float* dk, float* dv, float* Dws, int64_t n, int64_t b, int64_t hq,
              int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st);
 int sm100_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
-              int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st);
+              int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st,
+              const PeerEpilogue* ep = nullptr);
 int sm100_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
               void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n, int64_t b, int64_t hq,
-              int64_t hkv, int64_t hd, int causal, float scale, int stages, cudaStream_t st);
+              int64_t hkv, int64_t hd, int causal, float scale, int stages, cudaStream_t st,
+              const PeerEpilogue* eps = nullptr);
 size_t sm100_bwd_workspace(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd);
 int preload_a2a();
 int preload_simt();
@@ -129,6 +132,77 @@ int ul_attn_bwd(const void* q, const void* k, const void* v, const void* o, cons
                 int64_t hkv, int64_t hd, int dtype, int mask, float scale, void* stream) {
   return ul_attn_bwd_stages(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, dtype, mask, scale,
                             7, stream);
+}
+
+// ---- local attention with the head->seq exchange fused into the epilogue ----
+
+int ul_attn_fwd_exchange(ul_comm* comm, const void* q, const void* k, const void* v, void* o, float* lse,
+                         void* seq_out, int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype,
+                         int mask, float scale, uint64_t label, void* stream) {
+  if (!seq_out) return fail(UL_ERR_ARG, "ul_attn_fwd_exchange: NULL seq_out");
+  const int64_t shape[4] = {n, b, hq, hd};
+  // (empty problems take the two-step route: its push kernel still signals)
+  const bool fused = comm && ul_comm_world(comm) > 1 && dtype == UL_DTYPE_BF16 && n * b * hq > 0;
+  if (!fused) {   // same contract, two steps: attention, then the head->seq exchange
+    UL_TRY(ul_attn_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, dtype, mask, scale, stream));
+    const int launches = launch_count();
+    const void* in[1] = {o};
+    void* out[1] = {seq_out};
+    UL_TRY(ul_all_to_all(comm, 1, in, out, shape, 4, dtype, 0, 2, label, stream));
+    launch_count() += launches;
+    return UL_OK;
+  }
+  launch_count() = 0;
+  UL_TRY(check_attn(n, b, hq, hkv, hd, dtype, mask));
+  if (!q || !k || !v || !o || !lse) return fail(UL_ERR_ARG, "ul_attn_fwd_exchange: NULL tensor");
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(UL_ERR_ARG, "scale must be finite and > 0");
+  if (n > INT32_MAX / 2) return fail(UL_ERR_SHAPE, "attention: sequence too long (n=%lld)", (long long)n);
+  cudaStream_t st = (cudaStream_t)stream;
+  PeerEpilogue ep;
+  int slot = 0;
+  uint64_t epoch = 0;
+  void* outs[1] = {seq_out};
+  UL_TRY(a2a_fused_begin(comm, 1, outs, shape, dtype, label, &ep, &slot, &epoch));
+  if (n * b * hq > 0)
+    UL_TRY(sm100_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, mask == UL_MASK_CAUSAL, scale, st, &ep));
+  return a2a_fused_finish(comm, 1, outs, shape, dtype, label, slot, epoch, st);
+}
+
+int ul_attn_bwd_exchange(ul_comm* comm, const void* q, const void* k, const void* v, const void* o,
+                         const void* dout, const float* lse, void* dq, void* dk, void* dv, void* ws,
+                         size_t ws_bytes, void* seq_dq, void* seq_dk, void* seq_dv, int64_t n, int64_t b, int64_t hq,
+                         int64_t hkv, int64_t hd, int dtype, int mask, float scale, uint64_t label, void* stream) {
+  if (!seq_dq || !seq_dk || !seq_dv) return fail(UL_ERR_ARG, "ul_attn_bwd_exchange: NULL sequence output");
+  const int64_t shapes[12] = {n, b, hq, hd, n, b, hkv, hd, n, b, hkv, hd};
+  void* outs[3] = {seq_dq, seq_dk, seq_dv};
+  // (empty problems take the two-step route: its push kernel still signals)
+  const bool fused = comm && ul_comm_world(comm) > 1 && dtype == UL_DTYPE_BF16 && n * b * hq > 0;
+  if (!fused) {
+    UL_TRY(ul_attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, dtype, mask, scale,
+                       stream));
+    const int launches = launch_count();
+    const void* in[3] = {dq, dk, dv};
+    UL_TRY(ul_all_to_all(comm, 3, in, outs, shapes, 4, dtype, 0, 2, label, stream));
+    launch_count() += launches;
+    return UL_OK;
+  }
+  launch_count() = 0;
+  UL_TRY(check_attn(n, b, hq, hkv, hd, dtype, mask));
+  if (!q || !k || !v || !o || !dout || !dq || !dk || !dv) return fail(UL_ERR_ARG, "ul_attn_bwd_exchange: NULL tensor");
+  if (!lse) return fail(UL_ERR_STATE, "backward needs the LSE saved by the forward pass");
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(UL_ERR_ARG, "scale must be finite and > 0");
+  const size_t need = ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dtype);
+  if (!ws || ws_bytes < need)
+    return fail(UL_ERR_ARG, "ul_attn_bwd: workspace of %zu bytes < required %zu", ws_bytes, need);
+  cudaStream_t st = (cudaStream_t)stream;
+  PeerEpilogue eps[3];
+  int slot = 0;
+  uint64_t epoch = 0;
+  UL_TRY(a2a_fused_begin(comm, 3, outs, shapes, dtype, label, eps, &slot, &epoch));
+  if (n * b * hq > 0)
+    UL_TRY(sm100_bwd(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, mask == UL_MASK_CAUSAL,
+                     scale, 7, st, eps));
+  return a2a_fused_finish(comm, 3, outs, shapes, dtype, label, slot, epoch, st);
 }
 
 }  // extern "C"

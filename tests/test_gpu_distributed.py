@@ -116,6 +116,37 @@ def test_bf16_forward_backward_vs_oracle(p, hq, hkv):
     assert groups[0].native_ledger()["calls"] == 4
 
 
+@pytest.mark.parametrize("p,hq,hkv,n", [(2, 4, 4, 640), (4, 8, 4, 1024), (8, 8, 8, 1024)])
+def test_fused_epilogue_exchange_equals_unfused(p, hq, hkv, n):
+    # K2 fused into the attention epilogues must move exactly the bytes the
+    # stand-alone head->seq all-to-all moves (bitwise)
+    hd = 128
+    attn = U().FlashAttention("causal")
+    groups = U().SequenceGroup.local_group(p, slot_bytes=3 * n * hq * hd * 2 // p + (1 << 20))
+    mk = lambda h, s, r: to_dev(O.make_tensor((n, 1, h // p, hd), 60 + r, s, "bfloat16"), torch.bfloat16)
+    ins = run_ranks(groups, lambda r: [mk(hq, 1, r), mk(hkv, 2, r), mk(hkv, 3, r), mk(hq, 4, r)])
+
+    def fused(r):
+        q, k, v, do = ins[r]
+        o, lse, o_seq = attn.forward_exchange(q, k, v, groups[r])
+        return o, lse, o_seq, attn.backward_exchange(q, k, v, o, lse, do, groups[r])
+
+    def unfused(r):
+        q, k, v, do = ins[r]
+        o, lse = attn.forward_with_lse(q, k, v)
+        (o_seq,) = groups[r].all_to_all([o], 0, 2)
+        dq, dk, dv = attn.backward(q, k, v, o, lse, do)
+        return o, lse, o_seq, groups[r].all_to_all([dq, dk, dv], 0, 2)
+
+    a = run_ranks(groups, fused)
+    b = run_ranks(groups, unfused)
+    for r in range(p):
+        assert torch.equal(a[r][0], b[r][0]) and torch.equal(a[r][1], b[r][1])
+        assert torch.equal(a[r][2], b[r][2]), f"rank {r}: fused O exchange differs"
+        for x, y in zip(a[r][3], b[r][3]):
+            assert torch.equal(x, y), f"rank {r}: fused dQ/dK/dV exchange differs"
+
+
 def test_bf16_gqa_forward_p4():
     n, b, hq, hkv, hd = 512, 1, 8, 4, 128
     q, k, v, do = (O.make_tensor((n, b, hh, hd), 41, s, "bfloat16") for s, hh in
