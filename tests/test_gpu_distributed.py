@@ -156,6 +156,35 @@ def test_bf16_gqa_forward_p4():
     assert rel_max_err(o, ref) <= BF16_MAXREL
 
 
+def test_generic_local_attn_plugin_route():
+    # any callable local_attn(q, k, v) on head-sharded tensors plugs in
+    # (kernels.py plugin contract); the exchanges run through seq_all_to_all
+    import torch.nn.functional as F
+
+    def torch_attn(q, k, v):   # [n, b, h, d] -> [n, b, h, d], causal
+        to = lambda x: x.permute(1, 2, 0, 3)
+        return F.scaled_dot_product_attention(to(q), to(k), to(v), is_causal=True).permute(2, 0, 1, 3)
+
+    p, n, h, hd = 4, 256, 8, 64
+    q, k, v, do = (O.make_tensor((n, 1, h, hd), 91, s) for s in (1, 2, 3, 4))
+    groups = U().SequenceGroup.local_group(p, slot_bytes=1 << 20)
+    layers = [U().DistributedAttention(torch_attn, g) for g in groups]
+    nl = n // p
+    ins = run_ranks(groups, lambda r: [to_dev(x[r * nl:(r + 1) * nl]).requires_grad_(True) for x in (q, k, v)])
+    outs = run_ranks(groups, lambda r: layers[r](*ins[r]))
+    ref, _ = O.local_attention(q, k, v, "causal", exact=False)
+    got = np.concatenate([to_np(o) for o in outs], 0)
+    assert rel_max_err(got, ref) <= 1e-4
+    dos = run_ranks(groups, lambda r: to_dev(do[r * nl:(r + 1) * nl]))
+    run_ranks(groups, lambda r: torch.autograd.backward([outs[r]], [dos[r]]))
+    gref = O.local_attention_backward(q, k, v, do, "causal", exact=False)
+    for i in range(3):
+        g = np.concatenate([to_np(ins[r][i].grad) for r in range(p)], 0)
+        assert rel_max_err(g, gref[i]) <= 1e-4
+    # 4 separate seq_all_to_all per direction: 8 logical records, 8 native calls
+    assert len(groups[0].records) == 8 and groups[0].native_ledger()["calls"] == 8
+
+
 def test_divisibility_errors():
     groups = U().SequenceGroup.local_group(4, slot_bytes=1 << 20)
     layer = U().DistributedAttention(U().FlashAttention("causal"), groups[0])
