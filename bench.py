@@ -47,13 +47,17 @@ def peaks():
         return FALLBACK_PEAKS, "fallback"
 
 
-def gpu_lead(cycles: int = 400_000):
-    """Enqueue a device-side sleep (~0.2 ms) right before a timed region so
-    the GPU queue runs ahead of the host: the start event then fires when the
-    sleep ends, after the host has enqueued the timed launches, and the
-    measured interval is device time, not host launch latency."""
+FLUSH_BYTES = 1 << 30
+
+
+def make_flush(dev):
+    """L2 flush buffer: 1 GiB (8x the 126 MB L2).  Writing it takes ~0.2 ms
+    of full-clock HBM work, long enough for the host to enqueue the next timed
+    launches behind it, so the timed interval is device time (an idle GPU
+    before the region would either add host launch latency or -- with a
+    device sleep -- let clocks drop; tools_timing_ab.py measured both)."""
     import torch
-    torch.cuda._sleep(int(cycles))
+    return torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
 
 def attn_flops(n_seq, heads, hd, causal=True):
@@ -197,7 +201,7 @@ def run_ours(args):
         group = U.SequenceGroup.single(local_rank)
     attn = U.FlashAttention("causal")
     layer = U.DistributedAttention(attn, group)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    flush = make_flush(dev)
 
     def step(qq, kk, vv, dd):
         qq.requires_grad_(True)
@@ -221,7 +225,6 @@ def run_ours(args):
             dist.barrier()
         for i in range(args.steps):
             flush.zero_()                                  # untimed L2 flush
-            gpu_lead()                                     # keep the GPU queue ahead of the host
             ev[i][0].record()
             step(q.detach(), k.detach(), v.detach(), do)
             ev[i][1].record()
@@ -276,7 +279,7 @@ def run_ours(args):
                              f"Ulysses DistributedAttention fwd+bwd, P={P}, 16 heads x 128, N={n_seq} "
                              f"(= {SEQ_PER_GPU} x P) bf16 causal"),
                 "seq_len": n_seq, "heads": H, "head_dim": hd, "batch": 1, "parallelism": f"ulysses-sp{P}",
-                "causal": True, "l2": "flushed (256 MB write) before every timed step, flush untimed",
+                "causal": True, "l2": "flushed (1 GiB write) before every timed step, flush untimed",
             },
             "tflops_per_gpu": round(tflops_per_gpu, 1),
             "tflops_per_gpu_fa_convention": round(
@@ -315,7 +318,7 @@ def kernel_split(attn, q, k, v, do, args, dev):
     from paper_2309_14509_b200 import _lib
     n, b, h, hd = q.shape[0], q.shape[1], q.shape[2], q.shape[3]
     lib = _lib.lib()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = make_flush(dev)
     stream = torch.cuda.current_stream(dev).cuda_stream
     o = torch.empty_like(q)
     lse = torch.empty((b, h, n), dtype=torch.float32, device=dev)
@@ -346,7 +349,6 @@ def kernel_split(attn, q, k, v, do, args, dev):
     for it in range(args.warmup + reps):
         for nm in names:
             flush.zero_()
-            gpu_lead()
             a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             run(nm)
@@ -377,7 +379,7 @@ def bench_a2a(dev, n_seq, H, hd, P, group, reps=10):
     import torch.distributed as dist
     import paper_2309_14509_b200 as U
     out = {}
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = make_flush(dev)
 
     def timed(fn_list, streams):
         times = []
@@ -385,8 +387,8 @@ def bench_a2a(dev, n_seq, H, hd, P, group, reps=10):
             flush.zero_()
             torch.cuda.synchronize()
             ev = []
-            # one device sleep long enough for the host to enqueue every rank
-            gpu_lead(300_000 * len(streams))
+            for _ in range(len(streams) - 1):   # keep the GPU busy while the host enqueues every rank
+                flush.zero_()
             for s in streams:
                 s.wait_stream(torch.cuda.current_stream(dev))
             for fn, s in zip(fn_list, streams):

@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tO = tbase + 256 + t * HD + lane_off;
     const int q0 = (2 * pair + t) * BM;
     const int qrow = q0 + row;
-    const int my_nkv = nkvT[t];
+    const int my_nkv = t ? nkvT[1] : nkvT[0];   // (no dynamic index into a local array)
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < my_nkv; ++j) {
       const int kv0 = j * BN;

@@ -167,6 +167,12 @@ def test_generic_local_attn_plugin_route():
 
     p, n, h, hd = 4, 256, 8, 64
     q, k, v, do = (O.make_tensor((n, 1, h, hd), 91, s) for s in (1, 2, 3, 4))
+    # in-process groups: every kernel on the path must be loaded before a
+    # rank's flag wait spins (CUDA lazy loading blocks the issuing thread) --
+    # warm the plugin's own kernels once, forward and backward
+    w = [torch.zeros((n, 1, h // p, hd), device="cuda", requires_grad=True) for _ in range(3)]
+    torch_attn(*w).sum().backward()
+    torch.cuda.synchronize()
     groups = U().SequenceGroup.local_group(p, slot_bytes=1 << 20)
     layers = [U().DistributedAttention(torch_attn, g) for g in groups]
     nl = n // p
