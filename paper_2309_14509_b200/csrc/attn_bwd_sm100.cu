@@ -376,15 +376,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---- dQ ------------------------------------------------------------------------
+constexpr int KNST = 4;   // K/V sub-tile stages of the dQ kernel (dQ lags S/dP by two sub-tiles)
+
 template <int HD>
 struct DqSmem {
   static constexpr int kTileT = (HD / 64) * kAtomT;
   static constexpr int kTileS = (HD / 64) * kAtomS;
   static constexpr int kQ = 0;
   static constexpr int kO = kQ + kTileT;
-  static constexpr int kK = kO + kTileT;          // [NST]
-  static constexpr int kV = kK + NST * kTileS;    // [NST]
-  static constexpr int kBar = kV + NST * kTileS;
+  static constexpr int kK = kO + kTileT;          // [KNST]
+  static constexpr int kV = kK + KNST * kTileS;    // [KNST]
+  static constexpr int kBar = kV + KNST * kTileS;
   static constexpr int kBytes = kBar + 256 + 1024;
 };
 
@@ -401,13 +403,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sK = smem + S::kK;
   uint8_t* sV = smem + S::kV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
+  // TMEM ring of 3 (S, dP) buffers: the MMA thread issues dQ two sub-tiles
+  // behind S/dP, so the softmax of sub-tile j has S(j+1), dP(j+1), dQ(j-1),
+  // S(j+2), dP(j+2) worth of tensor work (~1280 cycles) to hide behind
+  constexpr int NB = 3;
   uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;                // [NST]
-  uint64_t* kv_empty = bars + 1 + NST;         // [NST]
-  uint64_t* s_full = bars + 1 + 2 * NST;       // [2]
-  uint64_t* p_full = bars + 3 + 2 * NST;       // [2]
-  uint64_t* buf_free = bars + 5 + 2 * NST;     // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 + 2 * NST);
+  uint64_t* kv_full = bars + 1;                // [KNST]
+  uint64_t* kv_empty = bars + 1 + KNST;         // [KNST]
+  uint64_t* s_full = bars + 1 + 2 * KNST;       // [NB]
+  uint64_t* p_full = bars + 1 + 2 * KNST + NB;  // [NB]
+  uint64_t* q_done = bars + 1 + 2 * KNST + 2 * NB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 + 2 * KNST + 2 * NB);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // longest query tiles first; head-major for long sequences (see the forward)
@@ -423,15 +429,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
-    for (int s = 0; s < NST; ++s) {
+    for (int s = 0; s < KNST; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NB; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], kSoftThreads);
-      mbar_init(&buf_free[s], 1);
     }
+    mbar_init(q_done, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -439,8 +445,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  // TMEM: S[2] at 0/64, dP[2] at 128/192 (dS written over dP), dQ at 256
-  const uint32_t tdQ = tbase + 256;
+  // TMEM: S[3] at 0/64/128, dP[3] at 192/256/320 (dS written over dP), dQ at 384
+  const uint32_t tdQ = tbase + 384;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -455,8 +461,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_3d(sO + a * kAtomT, &tmO, q_full, a * 64, bb * p.hq + h, q0);
       }
       for (int j = 0; j < nsub; ++j) {
-        const int s = j % NST;
-        mbar_wait(&kv_empty[s], ((j / NST) & 1) ^ 1);
+        const int s = j % KNST;
+        mbar_wait(&kv_empty[s], ((j / KNST) & 1) ^ 1);
         mbar_expect_tx(&kv_full[s], 2 * BS * HD * 2);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a) {
@@ -473,23 +479,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t dKk0 = sdesc(smem_u32(sK), 16, 1024), dVk0 = sdesc(smem_u32(sV), 16, 1024);
       const uint64_t dKm0 = sdesc(smem_u32(sK), kAtomS, 1024);
       auto issue_dq = [&](int i) {
-        const int b = i & 1, s = i % NST;
-        const uint32_t tdP = tbase + 128 + b * 64;
-        mbar_wait(&p_full[b], (i >> 1) & 1);
+        const int b = i % NB, s = i % KNST;
+        const uint32_t tdP = tbase + 192 + b * 64;
+        mbar_wait(&p_full[b], (i / NB) & 1);
         tc_fence_after();
         const uint64_t dKm = dadd(dKm0, s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < BS / 16; ++kk)
           mma_ts_w(tdQ, tdP + a_col(kk), dadd(dKm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
         mma_commit_w(&kv_empty[s]);
-        mma_commit_w(&buf_free[b]);
+        if (i == nsub - 1) mma_commit_w(q_done);
       };
       mbar_wait(q_full, 0);
       for (int j = 0; j < nsub; ++j) {
-        const int b = j & 1, s = j % NST;
-        const uint32_t tS = tbase + b * 64, tdP = tbase + 128 + b * 64;
-        // buffer b was last read by dq(j-2), issued earlier by this thread (in-order)
-        mbar_wait(&kv_full[s], (j / NST) & 1);
+        const int b = j % NB, s = j % KNST;
+        const uint32_t tS = tbase + b * 64, tdP = tbase + 192 + b * 64;
+        // buffer b was last read by dq(j-3), issued earlier by this thread (in-order)
+        mbar_wait(&kv_full[s], (j / KNST) & 1);
         tc_fence_after();
         const uint64_t dKk = dadd(dKk0, s * S::kTileS), dVk = dadd(dVk0, s * S::kTileS);
 #pragma unroll
@@ -505,8 +511,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_ss_w(tdP, dadd(dO0, offT), dadd(dVk, offS), kIdS, kk > 0 ? 1u : 0u);
         }
         mma_commit_w(&s_full[b]);
-        if (j >= 1) issue_dq(j - 1);
+        if (j >= 2) issue_dq(j - 2);   // releases K/V stage (j-2) % KNST = (j+1) % KNST for the TMA
       }
+      if (nsub >= 2) issue_dq(nsub - 2);
       issue_dq(nsub - 1);
     }
   } else {
@@ -520,10 +527,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float L = p.L2[roff];
     const float Dr = p.Dv[roff];
     for (int j = 0; j < nsub; ++j) {
-      const int b = j & 1;
+      const int b = j % NB;
       const int kv0 = j * BS + c0;
-      const uint32_t tS = tbase + b * 64, tdP = tbase + 128 + b * 64;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+      const uint32_t tS = tbase + b * 64, tdP = tbase + 192 + b * 64;
+      mbar_wait(&s_full[b], (j / NB) & 1);
       tc_fence_after();
       uint32_t r[32], d[32];
       tmem_ld32(tS + lane_off + c0, r);
@@ -553,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(&p_full[b]);
     }
-    mbar_wait(&buf_free[(nsub - 1) & 1], ((nsub - 1) >> 1) & 1);
+    mbar_wait(q_done, 0);
     tc_fence_after();
     // each half stores HD/2 columns of dQ * scale
     const bool valid = qrow < p.n;
