@@ -18,9 +18,10 @@
 //              row) write P^T / dS^T back over them as bf16; dV += P^T dO
 //              and dK += dS^T Q are TS MMAs.  Double-buffered TMEM lets the
 //              MMAs of sub-tile i+1 run while the softmax of sub-tile i does.
-//   bwd_dq     one CTA per (128-row query tile, head): 64-row kv sub-tiles,
+//   bwd_dq     one CTA per (128-row query tile, head): Q and dO resident in
+//              TMEM (A operands), 64-row kv sub-tiles streamed by TMA,
 //              S = Q K^T, dP = dO V^T (double-buffered), dS -> TMEM,
-//              dQ += dS K.
+//              dQ += dS K; all MMAs read only B from shared memory.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -376,15 +377,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---- dQ ------------------------------------------------------------------------
-constexpr int KNST = 4;   // K/V sub-tile stages of the dQ kernel (dQ lags S/dP by two sub-tiles)
+// One CTA per (128-row query tile, head).  Q and dO are the A operands of
+// S = Q K^T and dP = dO V^T and stay resident for the CTA's whole kv loop,
+// so they live in TMEM (loaded once by the softmax warps with tcgen05.st):
+// every MMA then reads only its B operand from shared memory.  (As SS MMAs
+// with N = 64 they read (128+64)*32 B of smem per 32 tensor cycles -- more
+// than the smem port delivers -- and ran at ~2/3 rate.)
+// TMEM: Q 0..63 | dO 64..127 | S[2] 128/192 | dP[2] 256/320 (dS over dP) | dQ 384..511.
+constexpr int KNST = 4;   // K/V sub-tile stages
 
 template <int HD>
 struct DqSmem {
-  static constexpr int kTileT = (HD / 64) * kAtomT;
   static constexpr int kTileS = (HD / 64) * kAtomS;
-  static constexpr int kQ = 0;
-  static constexpr int kO = kQ + kTileT;
-  static constexpr int kK = kO + kTileT;          // [KNST]
+  static constexpr int kK = 0;                     // [KNST]
   static constexpr int kV = kK + KNST * kTileS;    // [KNST]
   static constexpr int kBar = kV + KNST * kTileS;
   static constexpr int kBytes = kBar + 256 + 1024;
@@ -392,28 +397,22 @@ struct DqSmem {
 
 template <int HD>
 __global__ void __launch_bounds__(kThreads, 1)
-    bwd_dq_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
-                  const Params p) {
+    bwd_dq_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                  const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ dout, const Params p) {
+  static_assert(HD == 128 || HD == 64, "head dim");
   using S = DqSmem<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem + S::kQ;
-  uint8_t* sO = smem + S::kO;
   uint8_t* sK = smem + S::kK;
   uint8_t* sV = smem + S::kV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
-  // TMEM ring of 3 (S, dP) buffers: the MMA thread issues dQ two sub-tiles
-  // behind S/dP, so the softmax of sub-tile j has S(j+1), dP(j+1), dQ(j-1),
-  // S(j+2), dP(j+2) worth of tensor work (~1280 cycles) to hide behind
-  constexpr int NB = 3;
-  uint64_t* q_full = bars + 0;
+  uint64_t* a_full = bars + 0;                 // Q and dO written to TMEM
   uint64_t* kv_full = bars + 1;                // [KNST]
-  uint64_t* kv_empty = bars + 1 + KNST;         // [KNST]
-  uint64_t* s_full = bars + 1 + 2 * KNST;       // [NB]
-  uint64_t* p_full = bars + 1 + 2 * KNST + NB;  // [NB]
-  uint64_t* q_done = bars + 1 + 2 * KNST + 2 * NB;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 + 2 * KNST + 2 * NB);
+  uint64_t* kv_empty = bars + 1 + KNST;        // [KNST]
+  uint64_t* s_full = bars + 1 + 2 * KNST;      // [2]
+  uint64_t* p_full = bars + 3 + 2 * KNST;      // [2]
+  uint64_t* q_done = bars + 5 + 2 * KNST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * KNST);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // longest query tiles first; head-major for long sequences (see the forward)
@@ -428,12 +427,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nsub = p.causal ? min(nsub_all, (q0 + BT - 1) / BS + 1) : nsub_all;
 
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
+    mbar_init(a_full, kSoftThreads);
     for (int s = 0; s < KNST; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
     }
-    for (int s = 0; s < NB; ++s) {
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], kSoftThreads);
     }
@@ -445,21 +444,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  // TMEM: S[3] at 0/64/128, dP[3] at 192/256/320 (dS written over dP), dQ at 384
-  const uint32_t tdQ = tbase + 384;
+  const uint32_t tQ = tbase, tdO = tbase + 64, tdQ = tbase + 384;
 
   if (warp == 0) {
     if (lane == 0) {
-      tma_prefetch_desc(&tmQ);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
-      tma_prefetch_desc(&tmO);
-      mbar_expect_tx(q_full, 2 * BT * HD * 2);
-#pragma unroll
-      for (int a = 0; a < HD / 64; ++a) {
-        tma_load_3d(sQ + a * kAtomT, &tmQ, q_full, a * 64, bb * p.hq + h, q0);
-        tma_load_3d(sO + a * kAtomT, &tmO, q_full, a * 64, bb * p.hq + h, q0);
-      }
       for (int j = 0; j < nsub; ++j) {
         const int s = j % KNST;
         mbar_wait(&kv_empty[s], ((j / KNST) & 1) ^ 1);
@@ -473,15 +463,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     {  // the whole warp runs the issue loop; one elected lane issues
-      constexpr uint32_t kIdS = idesc_bf16(BT, BS, 0, 0);
-      constexpr uint32_t kIdG = idesc_bf16(BT, HD, 0, 1);
-      const uint64_t dQ0 = sdesc(smem_u32(sQ), 16, 1024), dO0 = sdesc(smem_u32(sO), 16, 1024);
+      constexpr uint32_t kIdS = idesc_bf16(BT, BS, 0, 0);   // A (TMEM) x B K-major
+      constexpr uint32_t kIdG = idesc_bf16(BT, HD, 0, 1);   // dS (TMEM) x K MN-major
       const uint64_t dKk0 = sdesc(smem_u32(sK), 16, 1024), dVk0 = sdesc(smem_u32(sV), 16, 1024);
       const uint64_t dKm0 = sdesc(smem_u32(sK), kAtomS, 1024);
       auto issue_dq = [&](int i) {
-        const int b = i % NB, s = i % KNST;
-        const uint32_t tdP = tbase + 192 + b * 64;
-        mbar_wait(&p_full[b], (i / NB) & 1);
+        const int b = i & 1, s = i % KNST;
+        const uint32_t tdP = tbase + 256 + b * 64;
+        mbar_wait(&p_full[b], (i >> 1) & 1);
         tc_fence_after();
         const uint64_t dKm = dadd(dKm0, s * S::kTileS);
 #pragma unroll
@@ -490,30 +479,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit_w(&kv_empty[s]);
         if (i == nsub - 1) mma_commit_w(q_done);
       };
-      mbar_wait(q_full, 0);
+      mbar_wait(a_full, 0);
       for (int j = 0; j < nsub; ++j) {
-        const int b = j % NB, s = j % KNST;
-        const uint32_t tS = tbase + b * 64, tdP = tbase + 192 + b * 64;
-        // buffer b was last read by dq(j-3), issued earlier by this thread (in-order)
+        const int b = j & 1, s = j % KNST;
+        const uint32_t tS = tbase + 128 + b * 64, tdP = tbase + 256 + b * 64;
+        // buffer b was last read by dq(j-2), issued earlier by this thread (in-order)
         mbar_wait(&kv_full[s], (j / KNST) & 1);
         tc_fence_after();
         const uint64_t dKk = dadd(dKk0, s * S::kTileS), dVk = dadd(dVk0, s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
           const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ss_w(tS, dadd(dQ0, offT), dadd(dKk, offS), kIdS, kk > 0 ? 1u : 0u);
+          mma_ts_w(tS, tQ + kk * 8, dadd(dKk, offS), kIdS, kk > 0 ? 1u : 0u);
         }
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
           const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ss_w(tdP, dadd(dO0, offT), dadd(dVk, offS), kIdS, kk > 0 ? 1u : 0u);
+          mma_ts_w(tdP, tdO + kk * 8, dadd(dVk, offS), kIdS, kk > 0 ? 1u : 0u);
         }
         mma_commit_w(&s_full[b]);
-        if (j >= 2) issue_dq(j - 2);   // releases K/V stage (j-2) % KNST = (j+1) % KNST for the TMA
+        if (j >= 1) issue_dq(j - 1);
       }
-      if (nsub >= 2) issue_dq(nsub - 2);
       issue_dq(nsub - 1);
     }
   } else {
@@ -523,14 +509,38 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int qrow = q0 + row;
     const int c0 = half * 32;
+    const bool valid = qrow < p.n;
+    // prologue: half 0 puts this row of Q, half 1 this row of dO, into TMEM
+    // as packed bf16 pairs (the A-operand layout: lane = row, column c holds
+    // elements 2c, 2c+1)
+    {
+      const __nv_bfloat16* src = (half == 0 ? q : dout) + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD;
+      const uint32_t dst = (half == 0 ? tQ : tdO) + lane_off;
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        uint32_t w[32];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          uint4 v4 = valid ? __ldg(reinterpret_cast<const uint4*>(src + c * 64) + x) : make_uint4(0, 0, 0, 0);
+          w[4 * x] = v4.x;
+          w[4 * x + 1] = v4.y;
+          w[4 * x + 2] = v4.z;
+          w[4 * x + 3] = v4.w;
+        }
+        tmem_st32(dst + c * 32, w);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(a_full);
+    }
     const int64_t roff = ((int64_t)bb * p.hq + h) * p.n_pad + qrow;
     const float L = p.L2[roff];
     const float Dr = p.Dv[roff];
     for (int j = 0; j < nsub; ++j) {
-      const int b = j % NB;
+      const int b = j & 1;
       const int kv0 = j * BS + c0;
-      const uint32_t tS = tbase + b * 64, tdP = tbase + 192 + b * 64;
-      mbar_wait(&s_full[b], (j / NB) & 1);
+      const uint32_t tS = tbase + 128 + b * 64, tdP = tbase + 256 + b * 64;
+      mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
       uint32_t r[32], d[32];
       tmem_ld32(tS + lane_off + c0, r);
@@ -563,7 +573,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_wait(q_done, 0);
     tc_fence_after();
     // each half stores HD/2 columns of dQ * scale
-    const bool valid = qrow < p.n;
     __nv_bfloat16* dst = p.dq + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD;
 #pragma unroll
     for (int c = 0; c < HD / 64; ++c) {
@@ -658,13 +667,12 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
     UL_TRY(launched("attn_bwd_dkdv_sm100"));
   }
   if (stages & 4) {
-    // dq: the query tile is resident, key/value sub-tiles stream
-    CUtensorMap mq, mk, mv, mo;
-    UL_TRY(make_tmap_bhsd(&mq, q, n, b * hq, HD, BT));
-    UL_TRY(make_tmap_bhsd(&mo, dout, n, b * hq, HD, BT));
+    // dq: Q / dO go to TMEM inside the kernel; key/value sub-tiles stream
+    CUtensorMap mk, mv;
     UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, BS));
     UL_TRY(make_tmap_bhsd(&mv, v, n, b * hkv, HD, BS));
-    bwd_dq_kernel<HD><<<(unsigned)(tiles * b * hq), kThreads, DqSmem<HD>::kBytes, st>>>(mq, mk, mv, mo, p);
+    bwd_dq_kernel<HD><<<(unsigned)(tiles * b * hq), kThreads, DqSmem<HD>::kBytes, st>>>(
+        mk, mv, (const __nv_bfloat16*)q, (const __nv_bfloat16*)dout, p);
     UL_TRY(launched("attn_bwd_dq_sm100"));
   }
   return UL_OK;
