@@ -26,3 +26,10 @@ clean:
 	rm -rf build $(LIB)
 
 .PHONY: all clean sass
+
+# profiling build with pipeline timestamps (tools/trace_bwd.py); never shipped
+TRACE_LIB := build/trace/libulysses_b200_trace.so
+trace: $(SRCS) $(HDRS)
+	@mkdir -p build/trace
+	$(NVCC) $(NVFLAGS) -DUL_TRACE -shared -o $(TRACE_LIB) $(SRCS) -lcudart_static -ldl -lrt -lpthread
+.PHONY: trace

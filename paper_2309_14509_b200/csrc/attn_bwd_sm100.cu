@@ -37,11 +37,31 @@
 namespace ul {
 namespace bwd {
 
+// Pipeline trace (profiling builds only, -DUL_TRACE): clock64 stamps of the
+// hand-off points of the first 8 CTAs, [cta][16 events][sub-tile].
+#ifdef UL_TRACE
+__device__ unsigned long long g_trace[8 * 16 * 256];
+// per-CTA life: [cta][0 start, 1 first operands, 2 q_done/epilogue, 3 end, 4 smid] (globaltimer ns)
+__device__ unsigned long long g_cta[8192 * 5];
+#define UL_CTA(k, v) g_cta[blockIdx.x * 5 + (k)] = (v)
+#define UL_EV(ev, j)                                                                      \
+  do {                                                                                    \
+    if (blockIdx.x < 8 && (j) < 256) g_trace[(blockIdx.x * 16 + (ev)) * 256 + (j)] = clock64(); \
+  } while (0)
+#else
+#define UL_EV(ev, j) \
+  do {               \
+  } while (0)
+#define UL_CTA(k, v) \
+  do {               \
+  } while (0)
+#endif
+
 using namespace sm100;
 
 constexpr int BT = 128;           // the tile a CTA owns (kv tile for dkdv, q tile for dq)
 constexpr int BS = 64;            // the sub-tile streamed against it
-constexpr int NST = 3;            // streamed-operand pipeline stages
+constexpr int NST = 4;            // streamed-operand pipeline stages
 // warp 0 TMA, warp 1 MMA, warps 2..9 softmax: two warps per TMEM lane
 // quarter, each owning one 32-column half of the 64-column sub-tile, so
 // every SMSP interleaves two independent softmax streams
@@ -206,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], kSoftThreads);
+      mbar_init(&p_full[s], kSoftWarps);   // one arrive per softmax warp
       mbar_init(&buf_free[s], 1);
     }
     fence_barrier_init();
@@ -215,7 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
+  if (*tmem_slot != 0u) __trap();   // 512 columns = the whole TMEM: base is column 0
+  constexpr uint32_t tbase = 0;
   // TMEM: S^T[2] at 0/64, dP^T[2] at 128/192, dV at 256, dK at 256+HD
   const uint32_t tdV = tbase + 256, tdK = tbase + 256 + HD;
 
@@ -236,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int qi = i0 + it % per_head;
         const int s = it % NST;
         mbar_wait(&q_empty[s], ((it / NST) & 1) ^ 1);
+        UL_EV(8, it);
         mbar_expect_tx(&q_full[s], 2 * BS * HD * 2 + 2 * BS * 4);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a) {
@@ -248,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    {  // the whole warp runs the issue loop; one elected lane issues
+    if (elect_one()) {  // one thread issues every MMA (uniform operands)
       constexpr uint32_t kIdS = idesc_bf16(BT, BS, 0, 0);   // M = kv rows, N = 64 q rows
       constexpr uint32_t kIdG = idesc_bf16(BT, HD, 0, 1);   // M = kv rows, N = hd, B MN-major
       // base descriptors, built once: K/V (K-major A), Q/dO stage 0 as
@@ -260,16 +282,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int b = i & 1, s = i % NST;
         const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
         mbar_wait(&p_full[b], (i >> 1) & 1);
+        UL_EV(1, i);
         tc_fence_after();
         const uint64_t dOm = dadd(dOm0, s * S::kTileS), dQm = dadd(dQm0, s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < BS / 16; ++kk)
-          mma_ts_w(tdV, tSt + a_col(kk), dadd(dOm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tdV, tSt + a_col(kk), dadd(dOm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < BS / 16; ++kk)
-          mma_ts_w(tdK, tdPt + a_col(kk), dadd(dQm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
-        mma_commit_w(&q_empty[s]);
-        mma_commit_w(&buf_free[b]);
+          mma_ts(tdK, tdPt + a_col(kk), dadd(dQm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&q_empty[s]);
+        mma_commit(&buf_free[b]);
+        UL_EV(6, i);
       };
       mbar_wait(kv_full, 0);
       for (int it = 0; it < total; ++it) {
@@ -277,26 +301,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
         // buffer b was last read by grads(it-2), issued before this point by
         // this thread: tcgen05.mma executes in issue order, so no wait
+        UL_EV(10, it);
         mbar_wait(&q_full[s], (it / NST) & 1);
+        UL_EV(0, it);
         tc_fence_after();
         const uint64_t dQk = dadd(dQk0, s * S::kTileS), dOk = dadd(dOk0, s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
           const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ss_w(tSt, dadd(dK0, offT), dadd(dQk, offS), kIdS, kk > 0 ? 1u : 0u);
+          mma_ss(tSt, dadd(dK0, offT), dadd(dQk, offS), kIdS, kk > 0 ? 1u : 0u);
         }
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
           const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ss_w(tdPt, dadd(dV0, offT), dadd(dOk, offS), kIdS, kk > 0 ? 1u : 0u);
+          mma_ss(tdPt, dadd(dV0, offT), dadd(dOk, offS), kIdS, kk > 0 ? 1u : 0u);
         }
-        mma_commit_w(&s_full[b]);
+        mma_commit(&s_full[b]);
+        UL_EV(7, it);
         if (it >= 1) issue_grads(it - 1);
       }
       issue_grads(total - 1);
     }
+    __syncwarp();
   } else {
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;        // which 32-column half of the sub-tile
@@ -310,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
       mbar_wait(&q_full[s], (it / NST) & 1);
       mbar_wait(&s_full[b], (it >> 1) & 1);
+      if (lane == 0 && (warp == 2 || warp == 9)) UL_EV(warp == 2 ? 2 : 4, it);
       tc_fence_after();
       uint32_t r[32], d[32];
       tmem_ld32(tSt + lane_off + c0, r);
@@ -354,7 +383,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_st16(tdPt + lane_off + c0 + 16, dsk);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_full[b]);
+      if (lane == 0 && (warp == 2 || warp == 9)) UL_EV(warp == 2 ? 3 : 5, it);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
     }
     // epilogue: half 0 stores dV, half 1 stores dK * scale (bf16 rows of kv head g)
     mbar_wait(&buf_free[(total - 1) & 1], ((total - 1) >> 1) & 1);
@@ -384,7 +415,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 // with N = 64 they read (128+64)*32 B of smem per 32 tensor cycles -- more
 // than the smem port delivers -- and ran at ~2/3 rate.)
 // TMEM: Q 0..63 | dO 64..127 | S[2] 128/192 | dP[2] 256/320 (dS over dP) | dQ 384..511.
-constexpr int KNST = 4;   // K/V sub-tile stages
+// warp 0 TMA, warp 1 S/dP MMA, warp 2 dQ MMA, warps 3..10 softmax
+constexpr int kDqThreads = 96 + kSoftThreads;
+constexpr int KNST = 6;   // K/V sub-tile stages (a stage is held ~2 sub-tiles: S/dP, then dQ)
 
 template <int HD>
 struct DqSmem {
@@ -396,7 +429,7 @@ struct DqSmem {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kDqThreads, 1)
     bwd_dq_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ dout, const Params p) {
   static_assert(HD == 128 || HD == 64, "head dim");
@@ -409,12 +442,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* a_full = bars + 0;                 // Q and dO written to TMEM
   uint64_t* kv_full = bars + 1;                // [KNST]
   uint64_t* kv_empty = bars + 1 + KNST;        // [KNST]
-  uint64_t* s_full = bars + 1 + 2 * KNST;      // [2]
-  uint64_t* p_full = bars + 3 + 2 * KNST;      // [2]
-  uint64_t* q_done = bars + 5 + 2 * KNST;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * KNST);
+  uint64_t* s_full = bars + 1 + 2 * KNST;      // [2] S(j) and dP(j) in TMEM
+  uint64_t* s_free = bars + 3 + 2 * KNST;      // [2] S(j) read by every softmax warp
+  uint64_t* p_full = bars + 5 + 2 * KNST;      // [2] dS(j) written over dP(j)
+  uint64_t* dq_done = bars + 7 + 2 * KNST;     // [2] dQ(j) has read dS(j)
+  uint64_t* q_done = bars + 9 + 2 * KNST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10 + 2 * KNST);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    UL_CTA(0, globaltimer());
+    UL_CTA(4, smid());
+  }
   // longest query tiles first; head-major for long sequences (see the forward)
   const int qtiles = (p.n + BT - 1) / BT;
   const int qheads = p.b * p.hq;
@@ -434,7 +473,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], kSoftThreads);
+      mbar_init(&s_free[s], kSoftWarps);   // one arrive per softmax warp
+      mbar_init(&p_full[s], kSoftWarps);
+      mbar_init(&dq_done[s], 1);
     }
     mbar_init(q_done, 1);
     fence_barrier_init();
@@ -443,8 +484,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
-  const uint32_t tQ = tbase, tdO = tbase + 64, tdQ = tbase + 384;
+  // a 512-column allocation owns the whole TMEM of the SM: its address is
+  // column 0, lane 0.  Using the constant keeps every TMEM operand of the
+  // MMA issue loop an immediate (no per-MMA register->uniform moves).
+  if (*tmem_slot != 0u) __trap();
+  constexpr uint32_t tbase = 0;
+  constexpr uint32_t tQ = tbase, tdO = tbase + 64, tdQ = tbase + 384;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -453,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < nsub; ++j) {
         const int s = j % KNST;
         mbar_wait(&kv_empty[s], ((j / KNST) & 1) ^ 1);
+        UL_EV(8, j);
         mbar_expect_tx(&kv_full[s], 2 * BS * HD * 2);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a) {
@@ -462,49 +508,74 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    {  // the whole warp runs the issue loop; one elected lane issues
+    // S/dP issuer.  S(j) only needs every softmax warp to have READ S(j-2)
+    // (s_free); dP(j) overwrites dS(j-2), so it waits for dQ(j-2) to have
+    // completed (dq_done, committed by the dQ issuer).  A second issuing
+    // warp keeps this stream from stalling behind dQ's p_full waits: an
+    // issuing thread blocks whenever the tensor queue is full, so one thread
+    // cannot wait on one barrier while MMAs behind another are pending.
+    if (elect_one()) {
       constexpr uint32_t kIdS = idesc_bf16(BT, BS, 0, 0);   // A (TMEM) x B K-major
-      constexpr uint32_t kIdG = idesc_bf16(BT, HD, 0, 1);   // dS (TMEM) x K MN-major
       const uint64_t dKk0 = sdesc(smem_u32(sK), 16, 1024), dVk0 = sdesc(smem_u32(sV), 16, 1024);
-      const uint64_t dKm0 = sdesc(smem_u32(sK), kAtomS, 1024);
-      auto issue_dq = [&](int i) {
-        const int b = i & 1, s = i % KNST;
-        const uint32_t tdP = tbase + 256 + b * 64;
-        mbar_wait(&p_full[b], (i >> 1) & 1);
-        tc_fence_after();
-        const uint64_t dKm = dadd(dKm0, s * S::kTileS);
-#pragma unroll
-        for (int kk = 0; kk < BS / 16; ++kk)
-          mma_ts_w(tdQ, tdP + a_col(kk), dadd(dKm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
-        mma_commit_w(&kv_empty[s]);
-        if (i == nsub - 1) mma_commit_w(q_done);
-      };
       mbar_wait(a_full, 0);
       for (int j = 0; j < nsub; ++j) {
         const int b = j & 1, s = j % KNST;
         const uint32_t tS = tbase + 128 + b * 64, tdP = tbase + 256 + b * 64;
-        // buffer b was last read by dq(j-2), issued earlier by this thread (in-order)
+        UL_EV(10, j);
         mbar_wait(&kv_full[s], (j / KNST) & 1);
+        UL_EV(0, j);
+        if (j == 0) UL_CTA(1, globaltimer());
+        if (j >= 2) mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);
+        UL_EV(9, j);
         tc_fence_after();
         const uint64_t dKk = dadd(dKk0, s * S::kTileS), dVk = dadd(dVk0, s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ts_w(tS, tQ + kk * 8, dadd(dKk, offS), kIdS, kk > 0 ? 1u : 0u);
+          mma_ts(tS, tQ + kk * 8, dadd(dKk, offS), kIdS, kk > 0 ? 1u : 0u);
+        }
+        UL_EV(13, j);
+        if (j >= 2) {
+          mbar_wait(&dq_done[b], ((j - 2) >> 1) & 1);
+          tc_fence_after();
         }
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ts_w(tdP, tdO + kk * 8, dadd(dVk, offS), kIdS, kk > 0 ? 1u : 0u);
+          mma_ts(tdP, tdO + kk * 8, dadd(dVk, offS), kIdS, kk > 0 ? 1u : 0u);
         }
-        mma_commit_w(&s_full[b]);
-        if (j >= 1) issue_dq(j - 1);
+        mma_commit(&s_full[b]);
+        UL_EV(7, j);
       }
-      issue_dq(nsub - 1);
     }
+    __syncwarp();
+  } else if (warp == 2) {
+    // dQ issuer: dQ += dS(i) K(i) as soon as the softmax has written dS(i)
+    if (elect_one()) {
+      constexpr uint32_t kIdG = idesc_bf16(BT, HD, 0, 1);   // dS (TMEM) x K MN-major
+      const uint64_t dKm0 = sdesc(smem_u32(sK), kAtomS, 1024);
+      for (int i = 0; i < nsub; ++i) {
+        const int b = i & 1, s = i % KNST;
+        const uint32_t tdP = tbase + 256 + b * 64;
+        mbar_wait(&p_full[b], (i >> 1) & 1);
+        UL_EV(1, i);
+        tc_fence_after();
+        const uint64_t dKm = dadd(dKm0, s * S::kTileS);
+#pragma unroll
+        for (int kk = 0; kk < BS / 16; ++kk)
+          mma_ts(tdQ, tdP + a_col(kk), dadd(dKm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+        // S(i), dP(i) completed before the softmax produced dS(i): this
+        // commit covers every read of K/V stage s
+        mma_commit(&kv_empty[s]);
+        mma_commit(&dq_done[b]);
+        if (i == nsub - 1) mma_commit(q_done);
+        UL_EV(6, i);
+      }
+    }
+    __syncwarp();
   } else {
     const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;        // which 32-column half of the kv sub-tile
+    const int half = (warp - 3) >> 2;        // which 32-column half of the kv sub-tile
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int qrow = q0 + row;
@@ -541,11 +612,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int kv0 = j * BS + c0;
       const uint32_t tS = tbase + 128 + b * 64, tdP = tbase + 256 + b * 64;
       mbar_wait(&s_full[b], (j >> 1) & 1);
+      if (lane == 0 && (warp == 3 || warp == 10)) UL_EV(warp == 3 ? 2 : 4, j);
       tc_fence_after();
+      // S(j) and dP(j) both land before s_full(j); once this warp has them in
+      // registers the S buffer is released (S(j+2) may overwrite it), while
+      // the dP buffer receives dS(j) in this warp's own columns
       uint32_t r[32], d[32];
       tmem_ld32(tS + lane_off + c0, r);
       tmem_ld32(tdP + lane_off + c0, d);
       tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[b]);
       uint32_t dsk[16];
       if (p.causal && kv0 + 31 > q0) {       // only the diagonal sub-tiles need the mask
         const int limit = qrow - kv0 + 1;     // columns x >= limit are masked (kv > q)
@@ -568,9 +646,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_st16(tdP + lane_off + c0 + 16, dsk);   // dS over this warp's consumed dP columns
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_full[b]);
+      if (lane == 0 && (warp == 3 || warp == 10)) UL_EV(warp == 3 ? 3 : 5, j);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
     }
     mbar_wait(q_done, 0);
+    if (threadIdx.x == 96) UL_CTA(2, globaltimer());
     tc_fence_after();
     // each half stores HD/2 columns of dQ * scale
     __nv_bfloat16* dst = p.dq + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD;
@@ -601,6 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   // last CTA publishes the fused dQ/dK/dV exchange (the dK/dV kernel ran before this launch)
   if (p.ep_dq.active && threadIdx.x == 0) peer_signal_last_cta(p.ep_dq, gridDim.x);
+  if (threadIdx.x == 0) UL_CTA(3, globaltimer());
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
@@ -671,7 +753,7 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
     CUtensorMap mk, mv;
     UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, BS));
     UL_TRY(make_tmap_bhsd(&mv, v, n, b * hkv, HD, BS));
-    bwd_dq_kernel<HD><<<(unsigned)(tiles * b * hq), kThreads, DqSmem<HD>::kBytes, st>>>(
+    bwd_dq_kernel<HD><<<(unsigned)(tiles * b * hq), kDqThreads, DqSmem<HD>::kBytes, st>>>(
         mk, mv, (const __nv_bfloat16*)q, (const __nv_bfloat16*)dout, p);
     UL_TRY(launched("attn_bwd_dq_sm100"));
   }
@@ -679,6 +761,21 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
 }
 
 }  // namespace bwd
+
+#ifdef UL_TRACE
+extern "C" int ul_debug_cta(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, bwd::g_cta, bytes < sizeof(bwd::g_cta) ? bytes : sizeof(bwd::g_cta)) ==
+                 cudaSuccess
+             ? 0
+             : -1;
+}
+extern "C" int ul_debug_trace(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, bwd::g_trace, bytes < sizeof(bwd::g_trace) ? bytes : sizeof(bwd::g_trace)) ==
+                 cudaSuccess
+             ? 0
+             : -1;
+}
+#endif
 
 int preload_bwd() {
   cudaFuncAttributes a;

@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 128);
+      mbar_init(&p_full[t], 4);   // one arrive per softmax warp
       mbar_init(&o_done[t], 1);
     }
     fence_barrier_init();
@@ -129,7 +129,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tbase = *tmem_slot;
+  if (*tmem_slot != 0u) __trap();   // 512 columns = the whole TMEM: base is column 0
+  constexpr uint32_t tbase = 0;
   // TMEM columns: S_A 0, S_B 128, O_A 256, O_B 256 + HD
 
   if (warp == 0) {
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    {  // the whole warp runs the issue loop; one elected lane issues
+    if (elect_one()) {  // one thread issues every MMA (uniform operands)
       constexpr uint32_t kIdQK = idesc_bf16(BM, BN, 0, 0);
       constexpr uint32_t kIdPV = idesc_bf16(BM, HD, 0, 1);
       // base descriptors built once; per-MMA cost is a constant add
@@ -173,9 +174,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
-          mma_ss_w(tbase + t * 128, dadd(dq, off), dadd(dk, off), kIdQK, kk > 0 ? 1u : 0u);
+          mma_ss(tbase + t * 128, dadd(dq, off), dadd(dk, off), kIdQK, kk > 0 ? 1u : 0u);
         }
-        mma_commit_w(&s_full[t]);
+        mma_commit(&s_full[t]);
       };
       auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j
         mbar_wait(&p_full[t], j & 1);
@@ -183,16 +184,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t dv = dadd(dV0, (j % NS) * S::kTile);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)
-          mma_ts_w(tbase + 256 + t * HD, tbase + t * 128 + kk * 8, dadd(dv, kk * 2048), kIdPV,
+          mma_ts(tbase + 256 + t * HD, tbase + t * 128 + kk * 8, dadd(dv, kk * 2048), kIdPV,
                  (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit_w(&o_done[t]);
+        mma_commit(&o_done[t]);
       };
       mbar_wait(q_full, 0);
       mbar_wait(&k_full[0], 0);
       tc_fence_after();
       if (nkvT[0] > 0) issue_s(0, 0);
       if (nkvT[1] > 0) issue_s(1, 0);
-      mma_commit_w(&k_empty[0]);
+      mma_commit(&k_empty[0]);
       for (int j = 0; j < nkv; ++j) {
         const int s = j % NS;
         const bool next = j + 1 < nkv;
@@ -203,10 +204,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (next && j + 1 < nkvT[0]) issue_s(0, j + 1);
         if (j < nkvT[1]) issue_pv(1, j);
         if (next && j + 1 < nkvT[1]) issue_s(1, j + 1);
-        mma_commit_w(&v_empty[s]);
-        if (next) mma_commit_w(&k_empty[(j + 1) % NS]);
+        mma_commit(&v_empty[s]);
+        if (next) mma_commit(&k_empty[(j + 1) % NS]);
       }
     }
+    __syncwarp();
   } else {
     // ---------------- softmax / correction / epilogue ----------------
     const int t = (warp - 2) >> 2;            // query tile of this warpgroup
@@ -277,7 +279,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&p_full[t]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
     }
     if (my_nkv > 0) {
       mbar_wait(&o_done[t], (my_nkv - 1) & 1);
