@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstring>
 
 #include "comm.cuh"
@@ -41,9 +42,10 @@ namespace bwd {
 // hand-off points of the first 8 CTAs, [cta][16 events][sub-tile].
 #ifdef UL_TRACE
 __device__ unsigned long long g_trace[8 * 16 * 256];
-// per-CTA life: [cta][0 start, 1 first operands, 2 q_done/epilogue, 3 end, 4 smid] (globaltimer ns)
-__device__ unsigned long long g_cta[8192 * 5];
-#define UL_CTA(k, v) g_cta[blockIdx.x * 5 + (k)] = (v)
+// per-CTA life: [cta][0 start, 1 first operands, 2 q_done/epilogue, 3 end (globaltimer ns), 4 smid,
+// 5/6 clock64 at start/end]
+__device__ unsigned long long g_cta[8192 * 7];
+#define UL_CTA(k, v) g_cta[blockIdx.x * 7 + (k)] = (v)
 #define UL_EV(ev, j)                                                                      \
   do {                                                                                    \
     if (blockIdx.x < 8 && (j) < 256) g_trace[(blockIdx.x * 16 + (ev)) * 256 + (j)] = clock64(); \
@@ -98,42 +100,42 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
                                                        const __nv_bfloat16* __restrict__ dout,
                                                        const float* __restrict__ lse, float* __restrict__ L2,
                                                        float* __restrict__ Dv, int n, int n_pad, int b, int hq) {
-  const int warp = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  const int64_t rows = (int64_t)b * hq * n_pad;
-  if (warp >= rows) return;
-  const int bh = warp / n_pad;
-  const int i = warp % n_pad;
+  // HD/8 threads per row, rows in memory order ((i*b + bb)*hq + h): every
+  // warp streams contiguous 16-byte chunks of O and dO
+  constexpr int TPR = HD / 8;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = tid / TPR;
+  const int sub = (int)(tid % TPR);
+  const int64_t rows = (int64_t)n * b * hq;
   float s = 0.f;
-  float l = INFINITY;
-  if (i < n) {
-    const int bb = bh / hq, h = bh % hq;
-    const int64_t off = (((int64_t)i * b + bb) * hq + h) * HD;
-    constexpr int PER = HD / 32;  // bf16 per lane
-    if constexpr (PER == 4) {
-      const uint2 a = *reinterpret_cast<const uint2*>(o + off + lane * 4);
-      const uint2 c = *reinterpret_cast<const uint2*>(dout + off + lane * 4);
-      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-      const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c);
+  if (r < rows) {
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(o + r * HD) + sub);
+    const uint4 c = __ldg(reinterpret_cast<const uint4*>(dout + r * HD) + sub);
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c);
 #pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        float2 fa = __bfloat1622float2(a2[x]), fc = __bfloat1622float2(c2[x]);
-        s = fmaf(fa.x, fc.x, s);
-        s = fmaf(fa.y, fc.y, s);
-      }
-    } else {
-      const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(o + off + lane * 2);
-      const __nv_bfloat162 c = *reinterpret_cast<const __nv_bfloat162*>(dout + off + lane * 2);
-      float2 fa = __bfloat1622float2(a), fc = __bfloat1622float2(c);
-      s = fa.x * fc.x + fa.y * fc.y;
+    for (int x = 0; x < 4; ++x) {
+      const float2 fa = __bfloat1622float2(a2[x]), fc = __bfloat1622float2(c2[x]);
+      s = fmaf(fa.x, fc.x, fmaf(fa.y, fc.y, s));
     }
-#pragma unroll
-    for (int m = 16; m; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-    l = lse[(int64_t)bh * n + i] * 1.4426950408889634f;
   }
-  if (lane == 0) {
-    Dv[(int64_t)bh * n_pad + i] = (i < n) ? s : 0.f;
-    L2[(int64_t)bh * n_pad + i] = l;
+#pragma unroll
+  for (int m = TPR / 2; m; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+  if (r < rows && sub == 0) {
+    const int h = (int)(r % hq);
+    const int64_t ib = r / hq;
+    const int bb = (int)(ib % b), i = (int)(ib / b);
+    const int64_t bh = (int64_t)bb * hq + h;
+    Dv[bh * n_pad + i] = s;
+    L2[bh * n_pad + i] = lse[bh * n + i] * 1.4426950408889634f;
+  }
+  // rows n..n_pad of every head: masked-out padding (P = 0, D = 0)
+  const int pad = n_pad - n;
+  if (pad > 0 && tid < (int64_t)b * hq * pad) {
+    const int64_t bh = tid / pad;
+    const int i = n + (int)(tid % pad);
+    Dv[bh * n_pad + i] = 0.f;
+    L2[bh * n_pad + i] = INFINITY;
   }
 }
 
@@ -428,6 +430,58 @@ struct DqSmem {
   static constexpr int kBytes = kBar + 256 + 1024;
 };
 
+// Query tile k of this (persistent) CTA.  Tiles are ranked longest first
+// (causal) -- pair-major, or head-major for long sequences -- and dealt to
+// the CTAs in waves, zig-zagging the order every other wave so the per-CTA
+// sums of tile lengths balance.
+struct DqTile {
+  int bb, h, g, q0, nsub;
+};
+__device__ __forceinline__ bool dq_tile(const Params& p, int k, DqTile& t) {
+  const int qtiles = (p.n + BT - 1) / BT;
+  const int qheads = p.b * p.hq;
+  const int G = (int)gridDim.x;
+  const int idx = k * G + ((k & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
+  if (idx >= qtiles * qheads) return false;
+  const int qt = qtiles - 1 - (p.head_major ? idx % qtiles : idx / qheads);
+  const int bh = p.head_major ? idx / qtiles : idx % qheads;
+  t.bb = bh / p.hq;
+  t.h = bh % p.hq;
+  t.g = t.h / (p.hq / p.hkv);
+  t.q0 = qt * BT;
+  const int nsub_all = (p.n + BS - 1) / BS;
+  t.nsub = p.causal ? min(nsub_all, (t.q0 + BT - 1) / BS + 1) : nsub_all;
+  return true;
+}
+
+// Half 0 of the softmax warps puts its row of Q, half 1 its row of dO, into
+// TMEM as packed bf16 pairs (the A-operand layout: lane = row, column c
+// holds elements 2c, 2c+1), then arrives on a_full.
+template <int HD>
+__device__ __forceinline__ void dq_load_rows(const Params& p, const DqTile& t, const __nv_bfloat16* q,
+                                             const __nv_bfloat16* dout, int half, int row, uint32_t dst,
+                                             uint64_t* a_full) {
+  const int qrow = t.q0 + row;
+  const bool valid = qrow < p.n;
+  const __nv_bfloat16* src = (half == 0 ? q : dout) + (((int64_t)qrow * p.b + t.bb) * p.hq + t.h) * HD;
+#pragma unroll
+  for (int c = 0; c < HD / 64; ++c) {
+    uint32_t w[32];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      uint4 v4 = valid ? __ldg(reinterpret_cast<const uint4*>(src + c * 64) + x) : make_uint4(0, 0, 0, 0);
+      w[4 * x] = v4.x;
+      w[4 * x + 1] = v4.y;
+      w[4 * x + 2] = v4.z;
+      w[4 * x + 3] = v4.w;
+    }
+    tmem_st32(dst + c * 32, w);
+  }
+  tmem_wait_st();
+  tc_fence_before();
+  mbar_arrive(a_full);
+}
+
 template <int HD>
 __global__ void __launch_bounds__(kDqThreads, 1)
     bwd_dq_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
@@ -439,32 +493,23 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   uint8_t* sK = smem + S::kK;
   uint8_t* sV = smem + S::kV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
-  uint64_t* a_full = bars + 0;                 // Q and dO written to TMEM
+  uint64_t* a_full = bars + 0;                 // Q and dO of the tile written to TMEM
   uint64_t* kv_full = bars + 1;                // [KNST]
   uint64_t* kv_empty = bars + 1 + KNST;        // [KNST]
   uint64_t* s_full = bars + 1 + 2 * KNST;      // [2] S(j) and dP(j) in TMEM
   uint64_t* s_free = bars + 3 + 2 * KNST;      // [2] S(j) read by every softmax warp
   uint64_t* p_full = bars + 5 + 2 * KNST;      // [2] dS(j) written over dP(j)
   uint64_t* dq_done = bars + 7 + 2 * KNST;     // [2] dQ(j) has read dS(j)
-  uint64_t* q_done = bars + 9 + 2 * KNST;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10 + 2 * KNST);
+  uint64_t* q_done = bars + 9 + 2 * KNST;      // the tile's dQ accumulation is complete
+  uint64_t* dq_free = bars + 10 + 2 * KNST;    // the epilogue has read dQ out of TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11 + 2 * KNST);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     UL_CTA(0, globaltimer());
     UL_CTA(4, smid());
+    UL_CTA(5, clock64());
   }
-  // longest query tiles first; head-major for long sequences (see the forward)
-  const int qtiles = (p.n + BT - 1) / BT;
-  const int qheads = p.b * p.hq;
-  const int qt = qtiles - 1 - (int)(p.head_major ? blockIdx.x % qtiles : blockIdx.x / qheads);
-  const int bh = p.head_major ? (int)(blockIdx.x / qtiles) : (int)(blockIdx.x % qheads);
-  const int bb = bh / p.hq, h = bh % p.hq;
-  const int g = h / (p.hq / p.hkv);
-  const int q0 = qt * BT;
-  const int nsub_all = (p.n + BS - 1) / BS;
-  const int nsub = p.causal ? min(nsub_all, (q0 + BT - 1) / BS + 1) : nsub_all;
-
   if (threadIdx.x == 0) {
     mbar_init(a_full, kSoftThreads);
     for (int s = 0; s < KNST; ++s) {
@@ -478,6 +523,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       mbar_init(&dq_done[s], 1);
     }
     mbar_init(q_done, 1);
+    mbar_init(dq_free, kSoftWarps);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -491,19 +537,26 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   constexpr uint32_t tbase = 0;
   constexpr uint32_t tQ = tbase, tdO = tbase + 64, tdQ = tbase + 384;
 
+  // Every role walks the same tile sequence; `gj` counts the CTA's sub-tiles
+  // across tiles, so the K/V ring and the S/dP double buffer run on without
+  // draining between tiles.
+  DqTile t;
   if (warp == 0) {
     if (lane == 0) {
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
-      for (int j = 0; j < nsub; ++j) {
-        const int s = j % KNST;
-        mbar_wait(&kv_empty[s], ((j / KNST) & 1) ^ 1);
-        UL_EV(8, j);
-        mbar_expect_tx(&kv_full[s], 2 * BS * HD * 2);
+      int gj = 0;
+      for (int k = 0; dq_tile(p, k, t); ++k) {
+        for (int j = 0; j < t.nsub; ++j, ++gj) {
+          const int s = gj % KNST;
+          mbar_wait(&kv_empty[s], ((gj / KNST) & 1) ^ 1);
+          UL_EV(8, gj);
+          mbar_expect_tx(&kv_full[s], 2 * BS * HD * 2);
 #pragma unroll
-        for (int a = 0; a < HD / 64; ++a) {
-          tma_load_3d(sK + s * S::kTileS + a * kAtomS, &tmK, &kv_full[s], a * 64, bb * p.hkv + g, j * BS);
-          tma_load_3d(sV + s * S::kTileS + a * kAtomS, &tmV, &kv_full[s], a * 64, bb * p.hkv + g, j * BS);
+          for (int a = 0; a < HD / 64; ++a) {
+            tma_load_3d(sK + s * S::kTileS + a * kAtomS, &tmK, &kv_full[s], a * 64, t.bb * p.hkv + t.g, j * BS);
+            tma_load_3d(sV + s * S::kTileS + a * kAtomS, &tmV, &kv_full[s], a * 64, t.bb * p.hkv + t.g, j * BS);
+          }
         }
       }
     }
@@ -517,35 +570,38 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     if (elect_one()) {
       constexpr uint32_t kIdS = idesc_bf16(BT, BS, 0, 0);   // A (TMEM) x B K-major
       const uint64_t dKk0 = sdesc(smem_u32(sK), 16, 1024), dVk0 = sdesc(smem_u32(sV), 16, 1024);
-      mbar_wait(a_full, 0);
-      for (int j = 0; j < nsub; ++j) {
-        const int b = j & 1, s = j % KNST;
-        const uint32_t tS = tbase + 128 + b * 64, tdP = tbase + 256 + b * 64;
-        UL_EV(10, j);
-        mbar_wait(&kv_full[s], (j / KNST) & 1);
-        UL_EV(0, j);
-        if (j == 0) UL_CTA(1, globaltimer());
-        if (j >= 2) mbar_wait(&s_free[b], ((j - 2) >> 1) & 1);
-        UL_EV(9, j);
-        tc_fence_after();
-        const uint64_t dKk = dadd(dKk0, s * S::kTileS), dVk = dadd(dVk0, s * S::kTileS);
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ts(tS, tQ + kk * 8, dadd(dKk, offS), kIdS, kk > 0 ? 1u : 0u);
-        }
-        UL_EV(13, j);
-        if (j >= 2) {
-          mbar_wait(&dq_done[b], ((j - 2) >> 1) & 1);
+      int gj = 0;
+      for (int k = 0; dq_tile(p, k, t); ++k) {
+        mbar_wait(a_full, k & 1);
+        for (int j = 0; j < t.nsub; ++j, ++gj) {
+          const int b = gj & 1, s = gj % KNST;
+          const uint32_t tS = tbase + 128 + b * 64, tdP = tbase + 256 + b * 64;
+          UL_EV(10, gj);
+          mbar_wait(&kv_full[s], (gj / KNST) & 1);
+          UL_EV(0, gj);
+          if (gj == 0) UL_CTA(1, globaltimer());
+          if (gj >= 2) mbar_wait(&s_free[b], ((gj - 2) >> 1) & 1);
+          UL_EV(9, gj);
           tc_fence_after();
-        }
+          const uint64_t dKk = dadd(dKk0, s * S::kTileS), dVk = dadd(dVk0, s * S::kTileS);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
-          mma_ts(tdP, tdO + kk * 8, dadd(dVk, offS), kIdS, kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
+            mma_ts(tS, tQ + kk * 8, dadd(dKk, offS), kIdS, kk > 0 ? 1u : 0u);
+          }
+          UL_EV(13, gj);
+          if (gj >= 2) {
+            mbar_wait(&dq_done[b], ((gj - 2) >> 1) & 1);
+            tc_fence_after();
+          }
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
+            mma_ts(tdP, tdO + kk * 8, dadd(dVk, offS), kIdS, kk > 0 ? 1u : 0u);
+          }
+          mma_commit(&s_full[b]);
+          UL_EV(7, gj);
         }
-        mma_commit(&s_full[b]);
-        UL_EV(7, j);
       }
     }
     __syncwarp();
@@ -554,22 +610,26 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     if (elect_one()) {
       constexpr uint32_t kIdG = idesc_bf16(BT, HD, 0, 1);   // dS (TMEM) x K MN-major
       const uint64_t dKm0 = sdesc(smem_u32(sK), kAtomS, 1024);
-      for (int i = 0; i < nsub; ++i) {
-        const int b = i & 1, s = i % KNST;
-        const uint32_t tdP = tbase + 256 + b * 64;
-        mbar_wait(&p_full[b], (i >> 1) & 1);
-        UL_EV(1, i);
-        tc_fence_after();
-        const uint64_t dKm = dadd(dKm0, s * S::kTileS);
+      int gj = 0;
+      for (int k = 0; dq_tile(p, k, t); ++k) {
+        for (int i = 0; i < t.nsub; ++i, ++gj) {
+          const int b = gj & 1, s = gj % KNST;
+          const uint32_t tdP = tbase + 256 + b * 64;
+          mbar_wait(&p_full[b], (gj >> 1) & 1);
+          UL_EV(1, gj);
+          if (i == 0 && k > 0) mbar_wait(dq_free, (k - 1) & 1);   // previous tile's dQ read out
+          tc_fence_after();
+          const uint64_t dKm = dadd(dKm0, s * S::kTileS);
 #pragma unroll
-        for (int kk = 0; kk < BS / 16; ++kk)
-          mma_ts(tdQ, tdP + a_col(kk), dadd(dKm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
-        // S(i), dP(i) completed before the softmax produced dS(i): this
-        // commit covers every read of K/V stage s
-        mma_commit(&kv_empty[s]);
-        mma_commit(&dq_done[b]);
-        if (i == nsub - 1) mma_commit(q_done);
-        UL_EV(6, i);
+          for (int kk = 0; kk < BS / 16; ++kk)
+            mma_ts(tdQ, tdP + a_col(kk), dadd(dKm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+          // S(i), dP(i) completed before the softmax produced dS(i): this
+          // commit covers every read of K/V stage s
+          mma_commit(&kv_empty[s]);
+          mma_commit(&dq_done[b]);
+          if (i == t.nsub - 1) mma_commit(q_done);
+          UL_EV(6, gj);
+        }
       }
     }
     __syncwarp();
@@ -578,103 +638,102 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     const int half = (warp - 3) >> 2;        // which 32-column half of the kv sub-tile
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const int qrow = q0 + row;
     const int c0 = half * 32;
-    const bool valid = qrow < p.n;
-    // prologue: half 0 puts this row of Q, half 1 this row of dO, into TMEM
-    // as packed bf16 pairs (the A-operand layout: lane = row, column c holds
-    // elements 2c, 2c+1)
-    {
-      const __nv_bfloat16* src = (half == 0 ? q : dout) + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD;
-      const uint32_t dst = (half == 0 ? tQ : tdO) + lane_off;
+    const uint32_t a_dst = (half == 0 ? tQ : tdO) + lane_off;
+    int gj = 0;
+    bool have = dq_tile(p, 0, t);
+    if (have) dq_load_rows<HD>(p, t, q, dout, half, row, a_dst, a_full);
+    for (int k = 0; have; ++k) {
+      const int qrow = t.q0 + row;
+      const bool valid = qrow < p.n;
+      const int64_t roff = ((int64_t)t.bb * p.hq + t.h) * p.n_pad + qrow;
+      const float L = p.L2[roff];
+      const float Dr = p.Dv[roff];
+      for (int j = 0; j < t.nsub; ++j, ++gj) {
+        const int b = gj & 1;
+        const int kv0 = j * BS + c0;
+        const uint32_t tS = tbase + 128 + b * 64, tdP = tbase + 256 + b * 64;
+        mbar_wait(&s_full[b], (gj >> 1) & 1);
+        if (lane == 0 && (warp == 3 || warp == 10)) UL_EV(warp == 3 ? 2 : 4, gj);
+        tc_fence_after();
+        // S(j) and dP(j) both land before s_full(j); once this warp has them in
+        // registers the S buffer is released (S(j+2) may overwrite it), while
+        // the dP buffer receives dS(j) in this warp's own columns
+        uint32_t r[32], d[32];
+        tmem_ld32(tS + lane_off + c0, r);
+        tmem_ld32(tdP + lane_off + c0, d);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[b]);
+        uint32_t dsk[16];
+        if (p.causal && kv0 + 31 > t.q0) {     // only the diagonal sub-tiles need the mask
+          const int limit = qrow - kv0 + 1;     // columns x >= limit are masked (kv > q)
+#pragma unroll
+          for (int x = 0; x < 32; x += 2) {
+            float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -L));
+            float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -L));
+            p0 = x >= limit ? 0.f : p0;
+            p1 = x + 1 >= limit ? 0.f : p1;
+            dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dr), p1 * (__uint_as_float(d[x + 1]) - Dr));
+          }
+        } else {
+#pragma unroll
+          for (int x = 0; x < 32; x += 2) {
+            const float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -L));
+            const float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -L));
+            dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dr), p1 * (__uint_as_float(d[x + 1]) - Dr));
+          }
+        }
+        tmem_st16(tdP + lane_off + c0 + 16, dsk);   // dS over this warp's consumed dP columns
+        tmem_wait_st();
+        tc_fence_before();
+        if (lane == 0 && (warp == 3 || warp == 10)) UL_EV(warp == 3 ? 3 : 5, gj);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[b]);
+      }
+      // every S/dP MMA of this tile has completed (this warp saw the last
+      // s_full): the next tile's Q/dO may replace them in TMEM, so its first
+      // S/dP run under this tile's epilogue
+      DqTile nt;
+      have = dq_tile(p, k + 1, nt);
+      if (have) dq_load_rows<HD>(p, nt, q, dout, half, row, a_dst, a_full);
+      mbar_wait(q_done, k & 1);
+      if (threadIdx.x == 96) UL_CTA(2, globaltimer());
+      tc_fence_after();
+      // each half stores HD/2 columns of dQ * scale
+      __nv_bfloat16* dst = p.dq + (((int64_t)qrow * p.b + t.bb) * p.hq + t.h) * HD;
+      uint32_t pkd[HD / 64][16];
 #pragma unroll
       for (int c = 0; c < HD / 64; ++c) {
-        uint32_t w[32];
+        uint32_t v[32];
+        tmem_ld32(tdQ + lane_off + half * (HD / 2) + c * 32, v);
+        tmem_wait_ld();
 #pragma unroll
-        for (int x = 0; x < 8; ++x) {
-          uint4 v4 = valid ? __ldg(reinterpret_cast<const uint4*>(src + c * 64) + x) : make_uint4(0, 0, 0, 0);
-          w[4 * x] = v4.x;
-          w[4 * x + 1] = v4.y;
-          w[4 * x + 2] = v4.z;
-          w[4 * x + 3] = v4.w;
-        }
-        tmem_st32(dst + c * 32, w);
+        for (int x = 0; x < 16; ++x)
+          pkd[c][x] = pack_bf16(__uint_as_float(v[2 * x]) * p.scale, __uint_as_float(v[2 * x + 1]) * p.scale);
       }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(a_full);
-    }
-    const int64_t roff = ((int64_t)bb * p.hq + h) * p.n_pad + qrow;
-    const float L = p.L2[roff];
-    const float Dr = p.Dv[roff];
-    for (int j = 0; j < nsub; ++j) {
-      const int b = j & 1;
-      const int kv0 = j * BS + c0;
-      const uint32_t tS = tbase + 128 + b * 64, tdP = tbase + 256 + b * 64;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
-      if (lane == 0 && (warp == 3 || warp == 10)) UL_EV(warp == 3 ? 2 : 4, j);
-      tc_fence_after();
-      // S(j) and dP(j) both land before s_full(j); once this warp has them in
-      // registers the S buffer is released (S(j+2) may overwrite it), while
-      // the dP buffer receives dS(j) in this warp's own columns
-      uint32_t r[32], d[32];
-      tmem_ld32(tS + lane_off + c0, r);
-      tmem_ld32(tdP + lane_off + c0, d);
-      tmem_wait_ld();
+      // dQ is in registers: the accumulator may be overwritten by the next tile
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[b]);
-      uint32_t dsk[16];
-      if (p.causal && kv0 + 31 > q0) {       // only the diagonal sub-tiles need the mask
-        const int limit = qrow - kv0 + 1;     // columns x >= limit are masked (kv > q)
-#pragma unroll
-        for (int x = 0; x < 32; x += 2) {
-          float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -L));
-          float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -L));
-          p0 = x >= limit ? 0.f : p0;
-          p1 = x + 1 >= limit ? 0.f : p1;
-          dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dr), p1 * (__uint_as_float(d[x + 1]) - Dr));
-        }
-      } else {
-#pragma unroll
-        for (int x = 0; x < 32; x += 2) {
-          const float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -L));
-          const float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -L));
-          dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dr), p1 * (__uint_as_float(d[x + 1]) - Dr));
-        }
-      }
-      tmem_st16(tdP + lane_off + c0 + 16, dsk);   // dS over this warp's consumed dP columns
-      tmem_wait_st();
-      tc_fence_before();
-      if (lane == 0 && (warp == 3 || warp == 10)) UL_EV(warp == 3 ? 3 : 5, j);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[b]);
-    }
-    mbar_wait(q_done, 0);
-    if (threadIdx.x == 96) UL_CTA(2, globaltimer());
-    tc_fence_after();
-    // each half stores HD/2 columns of dQ * scale
-    __nv_bfloat16* dst = p.dq + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD;
-#pragma unroll
-    for (int c = 0; c < HD / 64; ++c) {
-      const int col = half * (HD / 2) + c * 32;
-      uint32_t v[32];
-      tmem_ld32(tdQ + lane_off + col, v);
-      tmem_wait_ld();
-      uint32_t pkd[16];
-#pragma unroll
-      for (int x = 0; x < 16; ++x)
-        pkd[x] = pack_bf16(__uint_as_float(v[2 * x]) * p.scale, __uint_as_float(v[2 * x + 1]) * p.scale);
+      if (lane == 0) mbar_arrive(dq_free);
       if (valid) {
-        uint4* d4 = reinterpret_cast<uint4*>(dst + col);
 #pragma unroll
-        for (int x = 0; x < 4; ++x) d4[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
-        if (p.ep_dq.active) {   // fused head->seq of dQ
-          uint4* p4 = reinterpret_cast<uint4*>(peer_row_ptr(p.ep_dq, qrow, bb, p.b, h, HD, 2) + col * 2);
+        for (int c = 0; c < HD / 64; ++c) {
+          const int col = half * (HD / 2) + c * 32;
+          uint4* d4 = reinterpret_cast<uint4*>(dst + col);
 #pragma unroll
-          for (int x = 0; x < 4; ++x) p4[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+          for (int x = 0; x < 4; ++x)
+            d4[x] = make_uint4(pkd[c][4 * x], pkd[c][4 * x + 1], pkd[c][4 * x + 2], pkd[c][4 * x + 3]);
+          if (p.ep_dq.active) {   // fused head->seq of dQ
+            uint4* p4 = reinterpret_cast<uint4*>(peer_row_ptr(p.ep_dq, qrow, t.bb, p.b, t.h, HD, 2) + col * 2);
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              p4[x] = make_uint4(pkd[c][4 * x], pkd[c][4 * x + 1], pkd[c][4 * x + 2], pkd[c][4 * x + 3]);
+          }
         }
       }
+      t = nt;
     }
     if (p.ep_dq.active) __threadfence_system();
   }
@@ -682,7 +741,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   __syncthreads();
   // last CTA publishes the fused dQ/dK/dV exchange (the dK/dV kernel ran before this launch)
   if (p.ep_dq.active && threadIdx.x == 0) peer_signal_last_cta(p.ep_dq, gridDim.x);
-  if (threadIdx.x == 0) UL_CTA(3, globaltimer());
+  if (threadIdx.x == 0) {
+    UL_CTA(3, globaltimer());
+    UL_CTA(6, clock64());
+  }
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
@@ -700,8 +762,8 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
   float* L2 = reinterpret_cast<float*>(ws);
   float* Dv = L2 + b * hq * npad;
   if (stages & 1) {
-    const int64_t warps = b * hq * npad;
-    const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
+    const int64_t threads = std::max<int64_t>(n * b * hq * (HD / 8), b * hq * (npad - n));
+    const unsigned blocks = (unsigned)((threads + 255) / 256);
     bwd_prep_kernel<HD><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, lse, L2, Dv,
                                                 (int)n, (int)npad, (int)b, (int)hq);
     UL_TRY(launched("attn_bwd_prep"));
@@ -753,7 +815,8 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
     CUtensorMap mk, mv;
     UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, BS));
     UL_TRY(make_tmap_bhsd(&mv, v, n, b * hkv, HD, BS));
-    bwd_dq_kernel<HD><<<(unsigned)(tiles * b * hq), kDqThreads, DqSmem<HD>::kBytes, st>>>(
+    const unsigned dq_ctas = (unsigned)std::min<int64_t>(tiles * b * hq, sm_count());   // persistent
+    bwd_dq_kernel<HD><<<dq_ctas, kDqThreads, DqSmem<HD>::kBytes, st>>>(
         mk, mv, (const __nv_bfloat16*)q, (const __nv_bfloat16*)dout, p);
     UL_TRY(launched("attn_bwd_dq_sm100"));
   }

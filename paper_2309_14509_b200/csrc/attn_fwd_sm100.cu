@@ -65,6 +65,24 @@ struct Params {
   PeerEpilogue ep;   // active: also store O rows into the seq layout of their rank (fused head->seq)
 };
 
+// P = 2^(S*scale_log2 - mu) for 32 columns, packed to bf16 pairs, row sums
+// accumulated into 8 partials.  kPoly routes one element pair in four to
+// the FMA-pipe exp2 (unmasked tiles only).
+template <bool kPoly>
+__device__ __forceinline__ void exp_chunk(const uint32_t* r, float scale_log2, float mu, uint32_t* pk,
+                                          float* rsum) {
+#pragma unroll
+  for (int x = 0; x < 32; x += 2) {
+    const float a0 = fmaf(__uint_as_float(r[x]), scale_log2, -mu);
+    const float a1 = fmaf(__uint_as_float(r[x + 1]), scale_log2, -mu);
+    const bool poly = kPoly && (x & 6) == 6;
+    const float e0 = poly ? poly_exp2(a0) : fast_exp2(a0);
+    const float e1 = poly ? poly_exp2(a1) : fast_exp2(a1);
+    rsum[(x >> 1) & 7] += e0 + e1;
+    pk[x / 2] = pack_bf16(e0, e1);
+  }
+}
+
 template <int HD>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -252,16 +270,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const float mu = (m == -INFINITY) ? 0.f : m;
       float rsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      // (routing part of the exponentials to the FMA pipe, exp_chunk<true>,
+      // measured slower here: the forward is not MUFU-throughput bound)
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t pk[16];
-#pragma unroll
-        for (int x = 0; x < 32; x += 2) {
-          const float e0 = fast_exp2(fmaf(__uint_as_float(r[c * 32 + x]), p.scale_log2, -mu));
-          const float e1 = fast_exp2(fmaf(__uint_as_float(r[c * 32 + x + 1]), p.scale_log2, -mu));
-          rsum[(x >> 1) & 7] += e0 + e1;
-          pk[x / 2] = pack_bf16(e0, e1);
-        }
+        exp_chunk<false>(r + c * 32, p.scale_log2, mu, pk, rsum);
         tmem_st16(tS + c * 16, pk);   // P over S columns already in registers
       }
       l = l * alpha + (((rsum[0] + rsum[1]) + (rsum[2] + rsum[3])) + ((rsum[4] + rsum[5]) + (rsum[6] + rsum[7])));

@@ -278,5 +278,20 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (Cody-Waite split + cubic, max rel err 2.1e-4 -- far
+// below the bf16 rounding of P).  The MUFU delivers 16 ex2/clk/SM, exactly
+// the rate the forward's tensor pipe consumes them at; routing a quarter of
+// them here keeps the MUFU off the critical path.  Inputs must be finite and
+// > -126 (callers use it only on unmasked tiles, where x <= 0 and moderate).
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.0f;   // 1.5 * 2^23: round(x) lands in the low mantissa bits
+  const float f = x - (t - 12582912.0f);
+  float p = fmaf(f, 0.0531312f, 0.24252087f);
+  p = fmaf(p, f, 0.69378077f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 }  // namespace sm100
 }  // namespace ul

@@ -123,12 +123,13 @@ def cta_report(name):
     first operands), main loop, epilogue, and the per-SM occupancy/tail."""
     lib.ul_debug_cta.restype = ctypes.c_int
     lib.ul_debug_cta.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-    buf = np.zeros(8192 * 5, dtype=np.uint64)
+    buf = np.zeros(8192 * 7, dtype=np.uint64)
     chk(lib.ul_debug_cta(buf.ctypes.data, buf.nbytes))
-    c = buf.reshape(8192, 5).astype(np.int64)
+    c = buf.reshape(8192, 7).astype(np.int64)
     c = c[c[:, 0] > 0]
     t0 = c[:, 0].min()
-    start, first, epi, end, sm = (c[:, i] for i in range(5))
+    start, first, epi, end, sm, ck0, ck1 = (c[:, i] for i in range(7))
+    print(f"   SM clock over CTA lifetimes: median {np.median((ck1 - ck0) / (end - start)):.3f} GHz")
     span = end.max() - t0
     print(f"== CTA life {name}: {len(c)} CTAs, kernel span {span / 1e3:.1f} us")
     print(f"   prologue (start->first operands) median {np.median(first - start) / 1e3:.2f} us,"

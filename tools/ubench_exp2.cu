@@ -1,0 +1,88 @@
+// Micro-benchmark (tool, not product): exp2 throughput per SM on the MUFU
+// (ex2.approx.ftz.f32) vs a Cody-Waite + degree-3 polynomial on the FMA pipe,
+// and the mix, 8 warps x 8 independent chains.
+// nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -I paper_2309_14509_b200/csrc \
+//      tools/ubench_exp2.cu -o build/ubench_exp2
+#include <cstdio>
+
+#include "sm100.cuh"
+
+using namespace ul::sm100;
+
+__device__ __forceinline__ float exp2_poly(float x) {
+  // 2^x = 2^n * 2^f, n = round(x), f in [-0.5, 0.5]; minimax-ish cubic for 2^f
+  const float t = x + 12582912.0f;   // 1.5 * 2^23: rounds x to an integer in the low mantissa bits
+  const float n = t - 12582912.0f;
+  const float f = x - n;
+  float p = fmaf(f, 0.0531312f, 0.24252087f);
+  p = fmaf(p, f, 0.69378077f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+template <int kMode>   // 0 MUFU, 1 poly, 2 one in four poly
+__global__ void __launch_bounds__(256) bench(float* out, int iters) {
+  float v[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) v[c] = -0.001f * (threadIdx.x + c);
+  long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const float x = v[c] * 0.5f - 1.0f;   // stays in [-2, -1]
+      float e;
+      if (kMode == 0 || (kMode == 2 && (c & 3) != 0))
+        e = fast_exp2(x);
+      else
+        e = exp2_poly(x);
+      v[c] = e;
+    }
+  }
+  long long t1 = clock64();
+  float s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += v[c];
+  if (s == 1234.5f) out[0] = s;
+  if (threadIdx.x == 0) out[1 + blockIdx.x] = (float)(t1 - t0);
+}
+
+template <int M>
+static void run(const char* tag) {
+  float* d;
+  cudaMalloc(&d, 4096 * sizeof(float));
+  const int iters = 4096;
+  bench<M><<<148, 256>>>(d, iters);
+  bench<M><<<148, 256>>>(d, iters);
+  cudaDeviceSynchronize();
+  float h[149];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double c = 0;
+  for (int i = 1; i <= 148; ++i) c += h[i];
+  c /= 148;
+  printf("%-22s %.2f exp2/clk/SM\n", tag, 256.0 * 8 * iters / c);
+  cudaFree(d);
+}
+
+__global__ void accuracy(float* out) {
+  float worst = 0;
+  for (int i = 0; i < 100000; ++i) {
+    const float x = -30.0f + 30.0f * i / 100000.0f;
+    const float r = exp2f(x);
+    const float e = exp2_poly(x);
+    worst = fmaxf(worst, fabsf(e - r) / r);
+  }
+  out[0] = worst;
+}
+
+int main() {
+  run<0>("MUFU ex2");
+  run<1>("poly (FMA pipe)");
+  run<2>("1/4 poly + 3/4 MUFU");
+  float* d;
+  cudaMalloc(&d, 4);
+  accuracy<<<1, 1>>>(d);
+  float w;
+  cudaMemcpy(&w, d, 4, cudaMemcpyDeviceToHost);
+  printf("poly max rel err on [-30, 0]: %.3e\n", w);
+  return 0;
+}
