@@ -78,6 +78,17 @@ constexpr int kAtomS = BS * 128;  // ... of a 64-row sub-tile (8 KB)
 // columns [32h + 16, 32h + 32) of the buffer it read them from.
 __device__ __forceinline__ uint32_t a_col(int kk) { return (kk >> 1) * 32 + 16 + (kk & 1) * 8; }
 
+// P = 2^(S*scale_log2 - L) for an element pair, packed f32x2 FMA (sm_100)
+__device__ __forceinline__ float2 pexp2(const uint32_t* r, float2 sc, float2 nl) {
+  const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[0]), __uint_as_float(r[1])), sc, nl);
+  return make_float2(fast_exp2(a.x), fast_exp2(a.y));
+}
+// dS = P * (dP - D) for an element pair, packed to bf16
+__device__ __forceinline__ uint32_t pds(float2 e, const uint32_t* d, float2 nd) {
+  const float2 t = __fmul2_rn(e, __fadd2_rn(make_float2(__uint_as_float(d[0]), __uint_as_float(d[1])), nd));
+  return pack_bf16(t.x, t.y);
+}
+
 struct Params {
   int n, n_pad, b, hq, hkv;
   int causal;
@@ -357,25 +368,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tmem_wait_ld();
       uint32_t pk[16], dsk[16];
+      const float2 sc = make_float2(p.scale_log2, p.scale_log2);
       // only sub-tiles overlapping the kv tile's diagonal need the causal mask
       if (p.causal && q0 + c0 < kv0 + BT) {
         const int first = kvrow - q0 - c0;   // columns x < first are masked (q < kv)
 #pragma unroll
         for (int x = 0; x < 32; x += 2) {
-          float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -Lc[x]));
-          float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -Lc[x + 1]));
-          p0 = x < first ? 0.f : p0;
-          p1 = x + 1 < first ? 0.f : p1;
-          pk[x / 2] = pack_bf16(p0, p1);
-          dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dc[x]), p1 * (__uint_as_float(d[x + 1]) - Dc[x + 1]));
+          float2 e = pexp2(r + x, sc, make_float2(-Lc[x], -Lc[x + 1]));
+          e.x = x < first ? 0.f : e.x;
+          e.y = x + 1 < first ? 0.f : e.y;
+          pk[x / 2] = pack_bf16(e.x, e.y);
+          dsk[x / 2] = pds(e, d + x, make_float2(-Dc[x], -Dc[x + 1]));
         }
       } else {
 #pragma unroll
         for (int x = 0; x < 32; x += 2) {
-          const float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -Lc[x]));
-          const float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -Lc[x + 1]));
-          pk[x / 2] = pack_bf16(p0, p1);
-          dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dc[x]), p1 * (__uint_as_float(d[x + 1]) - Dc[x + 1]));
+          const float2 e = pexp2(r + x, sc, make_float2(-Lc[x], -Lc[x + 1]));
+          pk[x / 2] = pack_bf16(e.x, e.y);
+          dsk[x / 2] = pds(e, d + x, make_float2(-Dc[x], -Dc[x + 1]));
         }
       }
       // packed P^T / dS^T of this half go to the upper 16 of the 32 columns
@@ -649,6 +659,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       const int64_t roff = ((int64_t)t.bb * p.hq + t.h) * p.n_pad + qrow;
       const float L = p.L2[roff];
       const float Dr = p.Dv[roff];
+      const float2 sc = make_float2(p.scale_log2, p.scale_log2), nL = make_float2(-L, -L), nD = make_float2(-Dr, -Dr);
       for (int j = 0; j < t.nsub; ++j, ++gj) {
         const int b = gj & 1;
         const int kv0 = j * BS + c0;
@@ -671,19 +682,14 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           const int limit = qrow - kv0 + 1;     // columns x >= limit are masked (kv > q)
 #pragma unroll
           for (int x = 0; x < 32; x += 2) {
-            float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -L));
-            float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -L));
-            p0 = x >= limit ? 0.f : p0;
-            p1 = x + 1 >= limit ? 0.f : p1;
-            dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dr), p1 * (__uint_as_float(d[x + 1]) - Dr));
+            float2 e = pexp2(r + x, sc, nL);
+            e.x = x >= limit ? 0.f : e.x;
+            e.y = x + 1 >= limit ? 0.f : e.y;
+            dsk[x / 2] = pds(e, d + x, nD);
           }
         } else {
 #pragma unroll
-          for (int x = 0; x < 32; x += 2) {
-            const float p0 = fast_exp2(fmaf(__uint_as_float(r[x]), p.scale_log2, -L));
-            const float p1 = fast_exp2(fmaf(__uint_as_float(r[x + 1]), p.scale_log2, -L));
-            dsk[x / 2] = pack_bf16(p0 * (__uint_as_float(d[x]) - Dr), p1 * (__uint_as_float(d[x + 1]) - Dr));
-          }
+          for (int x = 0; x < 32; x += 2) dsk[x / 2] = pds(pexp2(r + x, sc, nL), d + x, nD);
         }
         tmem_st16(tdP + lane_off + c0 + 16, dsk);   // dS over this warp's consumed dP columns
         tmem_wait_st();

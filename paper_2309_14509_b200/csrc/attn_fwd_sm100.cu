@@ -35,6 +35,25 @@
 namespace ul {
 namespace fwd {
 
+// Pipeline trace (profiling builds only, -DUL_TRACE): clock64 stamps of the
+// first 8 CTAs [cta][16 events][kv tile] and per-CTA life (see tools/trace_bwd.py)
+#ifdef UL_TRACE
+__device__ unsigned long long g_trace[8 * 16 * 256];
+__device__ unsigned long long g_cta[8192 * 7];
+#define UL_EV(ev, j)                                                                             \
+  do {                                                                                           \
+    if (blockIdx.x < 8 && (j) < 256) g_trace[(blockIdx.x * 16 + (ev)) * 256 + (j)] = clock64(); \
+  } while (0)
+#define UL_CTA(k, v) g_cta[blockIdx.x * 7 + (k)] = (v)
+#else
+#define UL_EV(ev, j) \
+  do {               \
+  } while (0)
+#define UL_CTA(k, v) \
+  do {               \
+  } while (0)
+#endif
+
 using namespace sm100;
 
 constexpr int BM = 128;
@@ -70,16 +89,21 @@ struct Params {
 // the FMA-pipe exp2 (unmasked tiles only).
 template <bool kPoly>
 __device__ __forceinline__ void exp_chunk(const uint32_t* r, float scale_log2, float mu, uint32_t* pk,
-                                          float* rsum) {
+                                          float2* rsum) {
+  const float2 sc = make_float2(scale_log2, scale_log2), nm = make_float2(-mu, -mu);
 #pragma unroll
   for (int x = 0; x < 32; x += 2) {
-    const float a0 = fmaf(__uint_as_float(r[x]), scale_log2, -mu);
-    const float a1 = fmaf(__uint_as_float(r[x + 1]), scale_log2, -mu);
-    const bool poly = kPoly && (x & 6) == 6;
-    const float e0 = poly ? poly_exp2(a0) : fast_exp2(a0);
-    const float e1 = poly ? poly_exp2(a1) : fast_exp2(a1);
-    rsum[(x >> 1) & 7] += e0 + e1;
-    pk[x / 2] = pack_bf16(e0, e1);
+    // packed f32x2 FMA / add: half the issue slots of the scalar forms
+    const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[x]), __uint_as_float(r[x + 1])), sc, nm);
+    float2 e;
+    if (kPoly && (x & 6) == 6) {
+      e = poly_exp2x2(a);
+    } else {
+      e.x = fast_exp2(a.x);
+      e.y = fast_exp2(a.y);
+    }
+    rsum[(x >> 1) & 3] = __fadd2_rn(rsum[(x >> 1) & 3], e);
+    pk[x / 2] = pack_bf16(e.x, e.y);
   }
 }
 
@@ -129,6 +153,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int ntiles = nkvT[1] > 0 ? 2 : 1;
 
   if (threadIdx.x == 0) {
+    UL_CTA(0, globaltimer());
+    UL_CTA(4, smid());
+    UL_CTA(5, clock64());
+  }
+  if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&k_full[s], 1);
@@ -166,11 +195,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = j % NS;
         const uint32_t ph = (j / NS) & 1;
         mbar_wait(&k_empty[s], ph ^ 1);
+        UL_EV(8, j);
         mbar_expect_tx(&k_full[s], BN * HD * 2);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a)
           tma_load_3d(sK + s * S::kTile + a * kAtom, &tmK, &k_full[s], a * 64, bb * p.hkv + g, j * BN);
         mbar_wait(&v_empty[s], ph ^ 1);
+        UL_EV(9, j);
         mbar_expect_tx(&v_full[s], BN * HD * 2);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a)
@@ -198,6 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j
         mbar_wait(&p_full[t], j & 1);
+        UL_EV(t == 0 ? 1 : 2, j);
         tc_fence_after();
         const uint64_t dv = dadd(dV0, (j % NS) * S::kTile);
 #pragma unroll
@@ -208,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       mbar_wait(q_full, 0);
       mbar_wait(&k_full[0], 0);
+      UL_CTA(1, globaltimer());
       tc_fence_after();
       if (nkvT[0] > 0) issue_s(0, 0);
       if (nkvT[1] > 0) issue_s(1, 0);
@@ -215,15 +248,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < nkv; ++j) {
         const int s = j % NS;
         const bool next = j + 1 < nkv;
+        UL_EV(10, j);
         mbar_wait(&v_full[s], (j / NS) & 1);
         if (next) mbar_wait(&k_full[(j + 1) % NS], ((j + 1) / NS) & 1);
+        UL_EV(0, j);
         tc_fence_after();
         if (j < nkvT[0]) issue_pv(0, j);
         if (next && j + 1 < nkvT[0]) issue_s(0, j + 1);
+        UL_EV(6, j);
         if (j < nkvT[1]) issue_pv(1, j);
         if (next && j + 1 < nkvT[1]) issue_s(1, j + 1);
         mma_commit(&v_empty[s]);
         if (next) mma_commit(&k_empty[(j + 1) % NS]);
+        UL_EV(7, j);
       }
     }
     __syncwarp();
@@ -242,12 +279,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < my_nkv; ++j) {
       const int kv0 = j * BN;
       mbar_wait(&s_full[t], j & 1);
+      if (lane == 0 && (warp == 2 || warp == 6)) UL_EV(warp == 2 ? 3 : 5, j);
       tc_fence_after();
       uint32_t r[BN];
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, r + c * 32);
       tmem_wait_ld();
-      if ((p.causal && kv0 + BN - 1 > q0) || kv0 + BN > p.n) {
+      const bool masked = (p.causal && kv0 + BN - 1 > q0) || kv0 + BN > p.n;
+      if (masked) {
         int limit = p.n - kv0;
         if (p.causal) limit = min(limit, qrow - kv0 + 1);
 #pragma unroll
@@ -269,16 +308,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         m = mt;
       }
       const float mu = (m == -INFINITY) ? 0.f : m;
-      float rsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      float2 rsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       // (routing part of the exponentials to the FMA pipe, exp_chunk<true>,
       // measured slower here: the forward is not MUFU-throughput bound)
+#ifdef UL_FWD_POLY
+      if (masked) {
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t pk[16];
+          exp_chunk<false>(r + c * 32, p.scale_log2, mu, pk, rsum);
+          tmem_st16(tS + c * 16, pk);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t pk[16];
+          exp_chunk<true>(r + c * 32, p.scale_log2, mu, pk, rsum);
+          tmem_st16(tS + c * 16, pk);
+        }
+      }
+#else
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t pk[16];
         exp_chunk<false>(r + c * 32, p.scale_log2, mu, pk, rsum);
         tmem_st16(tS + c * 16, pk);   // P over S columns already in registers
       }
-      l = l * alpha + (((rsum[0] + rsum[1]) + (rsum[2] + rsum[3])) + ((rsum[4] + rsum[5]) + (rsum[6] + rsum[7])));
+#endif
+      const float2 rs = __fadd2_rn(__fadd2_rn(rsum[0], rsum[1]), __fadd2_rn(rsum[2], rsum[3]));
+      l = l * alpha + (rs.x + rs.y);
       // s_full(j) tracks every earlier MMA, so PV(j-1) is complete: rescale O now
       if (__any_sync(0xffffffffu, rescale)) {
 #pragma unroll
@@ -293,11 +351,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tmem_wait_st();
       tc_fence_before();
+      if (lane == 0 && (warp == 2 || warp == 6)) UL_EV(warp == 2 ? 4 : 11, j);
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
     }
     if (my_nkv > 0) {
       mbar_wait(&o_done[t], (my_nkv - 1) & 1);
+      if (threadIdx.x == 64) UL_CTA(2, globaltimer());
       tc_fence_after();
       const float inv = 1.f / l;
       const bool valid = qrow < p.n;
@@ -331,6 +391,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (p.ep.active && threadIdx.x == 0) peer_signal_last_cta(p.ep, gridDim.x);
+  if (threadIdx.x == 0) {
+    UL_CTA(3, globaltimer());
+    UL_CTA(6, clock64());
+  }
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
@@ -371,6 +435,21 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
 }
 
 }  // namespace fwd
+
+#ifdef UL_TRACE
+extern "C" int ul_debug_trace_fwd(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, fwd::g_trace, bytes < sizeof(fwd::g_trace) ? bytes : sizeof(fwd::g_trace)) ==
+                 cudaSuccess
+             ? 0
+             : -1;
+}
+extern "C" int ul_debug_cta_fwd(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, fwd::g_cta, bytes < sizeof(fwd::g_cta) ? bytes : sizeof(fwd::g_cta)) ==
+                 cudaSuccess
+             ? 0
+             : -1;
+}
+#endif
 
 int preload_fwd() {
   cudaFuncAttributes a;

@@ -292,6 +292,19 @@ __device__ __forceinline__ float poly_exp2(float x) {
   p = fmaf(p, f, 1.0f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+// Same on an element pair with the packed f32x2 FMA pipe ops (sm_100).
+__device__ __forceinline__ float2 poly_exp2x2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 f = __fadd2_rn(x, __fadd2_rn(magic, make_float2(-t.x, -t.y)));
+  float2 p = __ffma2_rn(f, make_float2(0.0531312f, 0.0531312f), make_float2(0.24252087f, 0.24252087f));
+  p = __ffma2_rn(p, f, make_float2(0.69378077f, 0.69378077f));
+  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
 
 }  // namespace sm100
 }  // namespace ul

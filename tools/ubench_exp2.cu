@@ -20,7 +20,7 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
 
-template <int kMode>   // 0 MUFU, 1 poly, 2 one in four poly
+template <int kMode>   // 0 MUFU, 1 poly, 2 one in four poly, 3 bf16x2 pack only, 4 MUFU + pack
 __global__ void __launch_bounds__(256) bench(float* out, int iters) {
   float v[8];
 #pragma unroll
@@ -31,10 +31,18 @@ __global__ void __launch_bounds__(256) bench(float* out, int iters) {
     for (int c = 0; c < 8; ++c) {
       const float x = v[c] * 0.5f - 1.0f;   // stays in [-2, -1]
       float e;
-      if (kMode == 0 || (kMode == 2 && (c & 3) != 0))
+      if (kMode == 3) {
+        const uint32_t pk = pack_bf16(x, v[c]);
+        e = __uint_as_float(pk & 0xffff0000u) - 1.5f;
+      } else if (kMode == 4) {
         e = fast_exp2(x);
-      else
+        const uint32_t pk = pack_bf16(e, x);
+        e = __uint_as_float(pk & 0xffff0000u) * 0.5f;
+      } else if (kMode == 0 || (kMode == 2 && (c & 3) != 0)) {
+        e = fast_exp2(x);
+      } else {
         e = exp2_poly(x);
+      }
       v[c] = e;
     }
   }
@@ -78,6 +86,8 @@ int main() {
   run<0>("MUFU ex2");
   run<1>("poly (FMA pipe)");
   run<2>("1/4 poly + 3/4 MUFU");
+  run<3>("bf16x2 pack (per op)");
+  run<4>("MUFU + pack (per exp)");
   float* d;
   cudaMalloc(&d, 4);
   accuracy<<<1, 1>>>(d);
