@@ -70,6 +70,14 @@ constexpr int NST = 4;            // streamed-operand pipeline stages
 constexpr int kSoftWarps = 8;
 constexpr int kSoftThreads = kSoftWarps * 32;
 constexpr int kThreads = 64 + kSoftThreads;
+// dK/dV kernel: 16 softmax warps, four per TMEM lane quarter, each owning 16
+// of the sub-tile's 64 columns: the softmax is latency-bound, so twice the
+// warps halve its critical path (launch bound 640 keeps the register budget
+// at <= 102/thread, which five resident warps per SMSP require)
+constexpr int kDkSoftWarps = 16;
+constexpr int kDkThreads = 64 + kDkSoftWarps * 32;
+__device__ __forceinline__ uint32_t a_col16(int kk) { return kk * 16 + 8; }
+constexpr bool kDkPoly = true;   // half of the unmasked exponentials on the FMA pipe
 constexpr int kAtomT = BT * 128;  // SW128 atom column of a 128-row tile (16 KB)
 constexpr int kAtomS = BS * 128;  // ... of a 64-row sub-tile (8 KB)
 
@@ -78,9 +86,15 @@ constexpr int kAtomS = BS * 128;  // ... of a 64-row sub-tile (8 KB)
 // columns [32h + 16, 32h + 32) of the buffer it read them from.
 __device__ __forceinline__ uint32_t a_col(int kk) { return (kk >> 1) * 32 + 16 + (kk & 1) * 8; }
 
-// P = 2^(S*scale_log2 - L) for an element pair, packed f32x2 FMA (sm_100)
+// P = 2^(S*scale_log2 - L) for an element pair, packed f32x2 FMA (sm_100).
+// kPoly evaluates the exponentials on the FMA pipe instead of the MUFU: the
+// softmax phases run in bursts (every warp starts on the same s_full) that
+// are MUFU-throughput bound, so a share of FMA-pipe exponentials shortens
+// them.  Only for unmasked elements (poly_exp2 needs finite input).
+template <bool kPoly = false>
 __device__ __forceinline__ float2 pexp2(const uint32_t* r, float2 sc, float2 nl) {
   const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[0]), __uint_as_float(r[1])), sc, nl);
+  if (kPoly) return poly_exp2x2(a);
   return make_float2(fast_exp2(a.x), fast_exp2(a.y));
 }
 // dS = P * (dP - D) for an element pair, packed to bf16
@@ -194,7 +208,7 @@ struct DkdvSmem {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(640, 1)
     bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
                     const Params p) {
@@ -239,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], kSoftWarps);   // one arrive per softmax warp
+      mbar_init(&p_full[s], kDkSoftWarps);   // one arrive per softmax warp
       mbar_init(&buf_free[s], 1);
     }
     fence_barrier_init();
@@ -300,10 +314,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t dOm = dadd(dOm0, s * S::kTileS), dQm = dadd(dQm0, s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < BS / 16; ++kk)
-          mma_ts(tdV, tSt + a_col(kk), dadd(dOm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tdV, tSt + a_col16(kk), dadd(dOm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < BS / 16; ++kk)
-          mma_ts(tdK, tdPt + a_col(kk), dadd(dQm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tdK, tdPt + a_col16(kk), dadd(dQm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&q_empty[s]);
         mma_commit(&buf_free[b]);
         UL_EV(6, i);
@@ -340,74 +354,91 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;        // which 32-column half of the sub-tile
+    const int part = (warp - 2) >> 2;        // which 16-column quarter of the sub-tile
     const int row = quarter * 32 + lane;     // kv row within the tile
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int kvrow = kv0 + row;
-    const int c0 = half * 32;
+    const int c0 = part * 16;
+    const float2 sc = make_float2(p.scale_log2, p.scale_log2);
     for (int it = 0; it < total; ++it) {
       const int b = it & 1, s = it % NST;
       const int q0 = (i0 + it % per_head) * BS;
       const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
       mbar_wait(&q_full[s], (it / NST) & 1);
+      // per-column -LSE / -D of these 16 columns (broadcast 16-byte smem
+      // reads), fetched while S^T/dP^T are still being computed
+      float2 nl[8], nd[8];
+      {
+        const uint32_t la = smem_u32(sL + s * BS + c0), da = smem_u32(sD + s * BS + c0);
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const float4 a = lds_f4(la + 16 * x), e = lds_f4(da + 16 * x);
+          nl[2 * x] = make_float2(-a.x, -a.y);
+          nl[2 * x + 1] = make_float2(-a.z, -a.w);
+          nd[2 * x] = make_float2(-e.x, -e.y);
+          nd[2 * x + 1] = make_float2(-e.z, -e.w);
+        }
+      }
       mbar_wait(&s_full[b], (it >> 1) & 1);
       if (lane == 0 && (warp == 2 || warp == 9)) UL_EV(warp == 2 ? 2 : 4, it);
       tc_fence_after();
-      uint32_t r[32], d[32];
-      tmem_ld32(tSt + lane_off + c0, r);
-      tmem_ld32(tdPt + lane_off + c0, d);
-      // per-column LSE / D of this half: broadcast 16-byte smem reads
-      float Lc[32], Dc[32];
-      const float4* L4 = reinterpret_cast<const float4*>(sL + s * BS + c0);
-      const float4* D4 = reinterpret_cast<const float4*>(sD + s * BS + c0);
-#pragma unroll
-      for (int x = 0; x < 8; ++x) {
-        const float4 a = L4[x], e = D4[x];
-        Lc[4 * x] = a.x; Lc[4 * x + 1] = a.y; Lc[4 * x + 2] = a.z; Lc[4 * x + 3] = a.w;
-        Dc[4 * x] = e.x; Dc[4 * x + 1] = e.y; Dc[4 * x + 2] = e.z; Dc[4 * x + 3] = e.w;
-      }
+      uint32_t r[16], d[16];
+      tmem_ld16(tSt + lane_off + c0, r);
+      tmem_ld16(tdPt + lane_off + c0, d);
       tmem_wait_ld();
-      uint32_t pk[16], dsk[16];
-      const float2 sc = make_float2(p.scale_log2, p.scale_log2);
+#ifdef UL_TRACE
+      {
+        uint32_t dep;   // the stamp must follow the loaded data (LDTM completes by scoreboard)
+        asm volatile("add.u32 %0, %1, %2;" : "=r"(dep) : "r"(r[0]), "r"(d[15]));
+        if (lane == 0 && warp == 2 && dep != 0x7fffffffu) UL_EV(12, it);
+        asm volatile("mov.b32 %0, %1;" : "=r"(dep) : "f"(nl[7].y + nd[7].y));
+        if (lane == 0 && warp == 2 && dep != 0x7fffffffu) UL_EV(15, it);
+      }
+#endif
+      uint32_t pk[8], dsk[8];
       // only sub-tiles overlapping the kv tile's diagonal need the causal mask
       if (p.causal && q0 + c0 < kv0 + BT) {
         const int first = kvrow - q0 - c0;   // columns x < first are masked (q < kv)
 #pragma unroll
-        for (int x = 0; x < 32; x += 2) {
-          float2 e = pexp2(r + x, sc, make_float2(-Lc[x], -Lc[x + 1]));
+        for (int x = 0; x < 16; x += 2) {
+          float2 e = pexp2(r + x, sc, nl[x / 2]);
           e.x = x < first ? 0.f : e.x;
           e.y = x + 1 < first ? 0.f : e.y;
           pk[x / 2] = pack_bf16(e.x, e.y);
-          dsk[x / 2] = pds(e, d + x, make_float2(-Dc[x], -Dc[x + 1]));
+          dsk[x / 2] = pds(e, d + x, nd[x / 2]);
         }
       } else {
 #pragma unroll
-        for (int x = 0; x < 32; x += 2) {
-          const float2 e = pexp2(r + x, sc, make_float2(-Lc[x], -Lc[x + 1]));
+        for (int x = 0; x < 16; x += 2) {
+          const float2 e = (x & 2) ? pexp2<kDkPoly>(r + x, sc, nl[x / 2]) : pexp2(r + x, sc, nl[x / 2]);
           pk[x / 2] = pack_bf16(e.x, e.y);
-          dsk[x / 2] = pds(e, d + x, make_float2(-Dc[x], -Dc[x + 1]));
+          dsk[x / 2] = pds(e, d + x, nd[x / 2]);
         }
       }
-      // packed P^T / dS^T of this half go to the upper 16 of the 32 columns
-      // this warp just consumed (never into the other half's unread columns);
-      // the TS MMAs address K-step kk at a_col(kk)
-      tmem_st16(tSt + lane_off + c0 + 16, pk);
-      tmem_st16(tdPt + lane_off + c0 + 16, dsk);
+      // packed P^T / dS^T of these 16 columns go to the upper 8 of the 16
+      // columns this warp just consumed; the TS MMAs address K-step kk at
+      // a_col16(kk)
+      if (lane == 0 && warp == 2) UL_EV(14, it);
+      tmem_st8(tSt + lane_off + c0 + 8, pk);
+      tmem_st8(tdPt + lane_off + c0 + 8, dsk);
       tmem_wait_st();
       tc_fence_before();
       if (lane == 0 && (warp == 2 || warp == 9)) UL_EV(warp == 2 ? 3 : 5, it);
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
     }
-    // epilogue: half 0 stores dV, half 1 stores dK * scale (bf16 rows of kv head g)
+    // epilogue: parts 0/1 store the two column halves of dV, parts 2/3 of
+    // dK * scale (bf16 rows of kv head g)
     mbar_wait(&buf_free[(total - 1) & 1], ((total - 1) >> 1) & 1);
     tc_fence_after();
     const bool valid = kvrow < p.n;
     const int64_t off = (((int64_t)kvrow * p.b + bb) * p.hkv + g) * HD;
-    const PeerEpilogue& ep = half == 0 ? p.ep_dv : p.ep_dk;
-    char* peer = (ep.active && valid) ? peer_row_ptr(ep, kvrow, bb, p.b, g, HD, 2) : nullptr;
-    if (half == 0) store_acc_rows<HD>(tdV, lane_off, 1.f, p.dv + off, valid, peer);
-    else store_acc_rows<HD>(tdK, lane_off, p.scale, p.dk + off, valid, peer);
+    const bool is_dk = part >= 2;
+    const int col0 = (part & 1) * (HD / 2);
+    const PeerEpilogue& ep = is_dk ? p.ep_dk : p.ep_dv;
+    char* peer = (ep.active && valid) ? peer_row_ptr(ep, kvrow, bb, p.b, g, HD, 2) + col0 * 2 : nullptr;
+    if (!is_dk) store_acc_rows<HD / 2>(tdV + col0, lane_off, 1.f, p.dv + off + col0, valid, peer);
+    else store_acc_rows<HD / 2>(tdK + col0, lane_off, p.scale, p.dk + off + col0, valid, peer);
     if (ep.active) __threadfence_system();   // dQ kernel signals after this launch completes
   }
   tc_fence_before();
@@ -813,7 +844,7 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
     UL_TRY(make_tmap_bhsd(&mo, dout, n, b * hq, HD, BS));
     UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, BT));
     UL_TRY(make_tmap_bhsd(&mv, v, n, b * hkv, HD, BT));
-    bwd_dkdv_kernel<HD><<<(unsigned)(tiles * b * hkv), kThreads, DkdvSmem<HD>::kBytes, st>>>(mq, mk, mv, mo, p);
+    bwd_dkdv_kernel<HD><<<(unsigned)(tiles * b * hkv), kDkThreads, DkdvSmem<HD>::kBytes, st>>>(mq, mk, mv, mo, p);
     UL_TRY(launched("attn_bwd_dkdv_sm100"));
   }
   if (stages & 4) {

@@ -85,6 +85,9 @@ def report(name, tr):
             print(f"        TMA: stage free(j)->data seen(j)={d(0, 8):.0f}  dQ/grads(j-K) issued->stage free(j)="
                   f"{d(8, 6, 0, -4):.0f}/{d(8, 6, 0, -3):.0f}")
         print(f"        MMA: loop top->operands seen={d(0, 10):.0f}")
+        if (ev[14] > 0).sum() > 16:
+            print(f"        w2: tmem ld data={d(12, 2):.0f} L/D data={d(15, 2):.0f} compute={d(14, 15):.0f}"
+                  f" st+wait={d(3, 14):.0f}")
         if (ev[11] > 0).sum() > 16:
             print(f"        w2: phase1={d(12, 2):.0f} wait dP={d(11, 12):.0f} phase2={d(3, 11):.0f}")
 
