@@ -14,6 +14,8 @@ from . import errors
 
 LIB_NAME = "libulysses_b200.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# profiling A/B only (tools/): load a variant build of the same library
+LIB_PATH = os.environ.get("UL_LIB", LIB_PATH)
 
 UL_OK = 0
 DTYPE_F32 = 0

@@ -77,7 +77,16 @@ constexpr int kThreads = 64 + kSoftThreads;
 constexpr int kDkSoftWarps = 16;
 constexpr int kDkThreads = 64 + kDkSoftWarps * 32;
 __device__ __forceinline__ uint32_t a_col16(int kk) { return kk * 16 + 8; }
-constexpr bool kDkPoly = true;   // half of the unmasked exponentials on the FMA pipe
+#ifdef UL_DQ_POLY
+constexpr bool kDqPoly = true;   // a quarter of the unmasked exponentials on the FMA pipe
+#else
+constexpr bool kDqPoly = false;
+#endif
+#ifdef UL_DK_NOPOLY
+constexpr bool kDkPoly = false;
+#else
+constexpr bool kDkPoly = true;
+#endif   // half of the unmasked exponentials on the FMA pipe
 constexpr int kAtomT = BT * 128;  // SW128 atom column of a 128-row tile (16 KB)
 constexpr int kAtomS = BS * 128;  // ... of a 64-row sub-tile (8 KB)
 
@@ -100,7 +109,7 @@ __device__ __forceinline__ float2 pexp2(const uint32_t* r, float2 sc, float2 nl)
 // dS = P * (dP - D) for an element pair, packed to bf16
 __device__ __forceinline__ uint32_t pds(float2 e, const uint32_t* d, float2 nd) {
   const float2 t = __fmul2_rn(e, __fadd2_rn(make_float2(__uint_as_float(d[0]), __uint_as_float(d[1])), nd));
-  return pack_bf16(t.x, t.y);
+  return pack_bf16_op(t.x, t.y);
 }
 
 struct Params {
@@ -404,14 +413,14 @@ __global__ void __launch_bounds__(640, 1)
           float2 e = pexp2(r + x, sc, nl[x / 2]);
           e.x = x < first ? 0.f : e.x;
           e.y = x + 1 < first ? 0.f : e.y;
-          pk[x / 2] = pack_bf16(e.x, e.y);
+          pk[x / 2] = pack_bf16_op(e.x, e.y);
           dsk[x / 2] = pds(e, d + x, nd[x / 2]);
         }
       } else {
 #pragma unroll
         for (int x = 0; x < 16; x += 2) {
           const float2 e = (x & 2) ? pexp2<kDkPoly>(r + x, sc, nl[x / 2]) : pexp2(r + x, sc, nl[x / 2]);
-          pk[x / 2] = pack_bf16(e.x, e.y);
+          pk[x / 2] = pack_bf16_op(e.x, e.y);
           dsk[x / 2] = pds(e, d + x, nd[x / 2]);
         }
       }
@@ -720,7 +729,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           }
         } else {
 #pragma unroll
-          for (int x = 0; x < 32; x += 2) dsk[x / 2] = pds(pexp2(r + x, sc, nL), d + x, nD);
+          for (int x = 0; x < 32; x += 2)
+            dsk[x / 2] = pds((kDqPoly && (x & 6) == 6) ? pexp2<true>(r + x, sc, nL) : pexp2(r + x, sc, nL), d + x, nD);
         }
         tmem_st16(tdP + lane_off + c0 + 16, dsk);   // dS over this warp's consumed dP columns
         tmem_wait_st();

@@ -103,7 +103,7 @@ __device__ __forceinline__ void exp_chunk(const uint32_t* r, float scale_log2, f
       e.y = fast_exp2(a.y);
     }
     rsum[(x >> 1) & 3] = __fadd2_rn(rsum[(x >> 1) & 3], e);
-    pk[x / 2] = pack_bf16(e.x, e.y);
+    pk[x / 2] = pack_bf16_op(e.x, e.y);
   }
 }
 
@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, r + c * 32);
       tmem_wait_ld();
+      if (lane == 0 && warp == 2) UL_EV(12, j);
       const bool masked = (p.causal && kv0 + BN - 1 > q0) || kv0 + BN > p.n;
       if (masked) {
         int limit = p.n - kv0;
@@ -300,6 +301,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int u = 0; u < 4; ++u) mx[u] = fmaxf(mx[u], __uint_as_float(r[c + u]));
       }
       const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
+#ifdef UL_TRACE
+      {
+        uint32_t dep;
+        asm volatile("mov.b32 %0, %1;" : "=r"(dep) : "f"(mt));
+        if (lane == 0 && warp == 2 && dep != 0x7fffffffu) UL_EV(13, j);
+      }
+#endif
       float alpha = 1.f;
       bool rescale = false;
       if (mt > m + kLazy) {
@@ -337,6 +345,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       const float2 rs = __fadd2_rn(__fadd2_rn(rsum[0], rsum[1]), __fadd2_rn(rsum[2], rsum[3]));
       l = l * alpha + (rs.x + rs.y);
+#ifdef UL_TRACE
+      {
+        uint32_t dep;
+        asm volatile("mov.b32 %0, %1;" : "=r"(dep) : "f"(l));
+        if (lane == 0 && warp == 2 && dep != 0x7fffffffu) UL_EV(14, j);
+      }
+#endif
       // s_full(j) tracks every earlier MMA, so PV(j-1) is complete: rescale O now
       if (__any_sync(0xffffffffu, rescale)) {
 #pragma unroll
@@ -352,6 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_st();
       tc_fence_before();
       if (lane == 0 && (warp == 2 || warp == 6)) UL_EV(warp == 2 ? 4 : 11, j);
+      if (lane == 0 && warp == 4) UL_EV(15, j);
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
     }

@@ -285,6 +285,22 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// bf16x2 pack of softmax operands (P, dS).  Default: the hardware convert
+// (cvt.rn.bf16x2.f32 = F2FP).  -DUL_PACK_ALU rounds on the integer pipes
+// instead (integer add + byte permute, round-half-away-from-zero, which
+// differs from RNE only on exact ties); measured r16 (tools/ab_kernels.py):
+// forward unchanged, dK/dV 5% slower -- F2FP does not contend with MUFU.EX2
+// enough to matter (tools/ubench_exp2.cu: 15.9 ex2/clk/SM alone, 15.1 with a
+// pack per exp).
+__device__ __forceinline__ uint32_t pack_bf16_op(float lo, float hi) {
+#ifndef UL_PACK_ALU
+  return pack_bf16(lo, hi);
+#else
+  const uint32_t a = __float_as_uint(lo) + 0x8000u, b = __float_as_uint(hi) + 0x8000u;
+  return __byte_perm(a, b, 0x7632);
+#endif
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -24,7 +24,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2309_14509_b200 import _lib  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-lib = ctypes.CDLL(os.path.join(ROOT, "build/trace/libulysses_b200_trace.so"))
+lib = ctypes.CDLL(os.path.join(ROOT, os.environ.get("TRACE_LIB", "ab_libs/trace/libulysses_b200.so")))
 _lib._declare(lib)
 lib.ul_debug_trace.restype = ctypes.c_int
 lib.ul_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]

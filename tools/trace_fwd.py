@@ -23,7 +23,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2309_14509_b200 import _lib  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-lib = ctypes.CDLL(os.path.join(ROOT, os.environ.get("TRACE_LIB", "build/trace/libulysses_b200_trace.so")))
+lib = ctypes.CDLL(os.path.join(ROOT, os.environ.get("TRACE_LIB", "ab_libs/trace/libulysses_b200.so")))
 _lib._declare(lib)
 for fn in ("ul_debug_trace_fwd", "ul_debug_cta_fwd"):
     getattr(lib, fn).restype = ctypes.c_int
@@ -68,12 +68,15 @@ for cta in range(4):
     print(f"cta {cta}: kv tiles={cnt} period={d(0, 0, 1, 0):.0f}  softmax A={d(4, 3):.0f} B={d(11, 5):.0f}"
           f"  A arrive->MMA sees={d(1, 4):.0f}  B arrive->MMA sees={d(2, 11):.0f}"
           f"  MMA wait V/K={d(0, 10):.0f}  S_A(j+1) issued->s_full seen A={d(3, 6, 1, 0):.0f}")
+    print(f"   A(w2): ld={d(12, 3):.0f} max={d(13, 12):.0f} exp+st={d(14, 13):.0f} wait_st..arrive={d(4, 14):.0f}"
+          f"  w4 arrive - w2 arrive={d(15, 4):.0f}")
 ev = tr[0]
 j0 = 30
 t0 = ev[10][j0]
 names = {10: "MMA top", 0: "MMA V/K landed", 1: "MMA p_full A seen", 6: "MMA PV_A+S_A issued",
          2: "MMA p_full B seen", 7: "MMA all issued", 3: "A s_full seen", 4: "A arrive", 5: "B s_full seen",
-         11: "B arrive", 8: "TMA K stage free", 9: "TMA V stage free"}
+         11: "B arrive", 8: "TMA K stage free", 9: "TMA V stage free", 12: "A ld done", 13: "A max done",
+         14: "A exp done", 15: "A w4 arrive"}
 rows = []
 for jj in range(j0 - 1, j0 + 3):
     for e, nm in names.items():
