@@ -60,6 +60,24 @@ def make_flush(dev):
     return torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
 
+NCU_PROFILE = os.path.join(ROOT, "profiles", "r1_ncu_full_r15.json")
+NCU_NAMES = {"attn_fwd_sm100": "fwd::attn_fwd_kernel<128>", "attn_bwd_dkdv_sm100": "bwd::bwd_dkdv_kernel<128>",
+             "attn_bwd_dq_sm100": "bwd::bwd_dq_kernel<128>", "attn_bwd_fused_sm100": "bwd::bwd_fused_kernel<128>"}
+
+
+def ncu_traffic(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    `ncu --set full` capture of the same workload (profiles/), or None."""
+    try:
+        with open(NCU_PROFILE) as f:
+            d = json.load(f)[NCU_NAMES[kernel]]
+        mb = lambda v: float(v.split()[0]) * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3}[v.split()[1]]
+        return {"bytes": int(mb(d["dram__bytes_read.sum"]) + mb(d["dram__bytes_write.sum"])),
+                "source": os.path.relpath(NCU_PROFILE, ROOT)}
+    except Exception:
+        return None
+
+
 def attn_flops(n_seq, heads, hd, causal=True):
     """fwd 4*H*N^2*hd*c, bwd 8*H*N^2*hd*c, c = 1/2 causal."""
     c = 0.5 if causal else 1.0
@@ -289,7 +307,8 @@ def run_ours(args):
                 "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({src}, burst)",
                 "frac_of_sustained": round(ach / pk.get("bf16_tflops_sustained", peak), 4),
-                "traffic": None,
+                "traffic": (ncu_traffic(dom["name"]) or {}).get("bytes"),
+                "traffic_source": (ncu_traffic(dom["name"]) or {}).get("source"),
                 "alg_flops_per_launch": dom["alg_flops"],
                 "layer_frac": round(tflops_per_gpu / peak, 4),
             },
@@ -326,20 +345,27 @@ def kernel_split(attn, q, k, v, do, args, dev):
     wsb = int(lib.ul_attn_bwd_workspace_bytes(n, b, h, h, hd, 1))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     scale = 1.0 / math.sqrt(hd)
-    names = ["attn_fwd_sm100", "attn_bwd_prep", "attn_bwd_dkdv_sm100", "attn_bwd_dq_sm100"]
+    fused = hd == 128 and not attn.deterministic
+    lib.ul_attn_set_deterministic(int(attn.deterministic))
+    if fused:   # one kernel for dK, dV and dQ (+ the dQ fp32 -> bf16 pass)
+        names = ["attn_fwd_sm100", "attn_bwd_prep", "attn_bwd_fused_sm100", "attn_bwd_dq_convert"]
+    else:
+        names = ["attn_fwd_sm100", "attn_bwd_prep", "attn_bwd_dkdv_sm100", "attn_bwd_dq_sm100"]
     times = {nm: [] for nm in names}
     f_fwd, f_bwd = attn_flops(n, h, hd, True)
     # algorithmic FLOPs credited per kernel: fwd = QK^T + PV; dkdv produces dP, dV, dK
-    # (3 of the 4 backward GEMMs, 6*N^2*hd*c); dq produces dQ (2*N^2*hd*c).
+    # (3 of the 4 backward GEMMs, 6*N^2*hd*c); dq produces dQ (2*N^2*hd*c); the
+    # fused kernel all four (8*N^2*hd*c)
     alg = {"attn_fwd_sm100": f_fwd, "attn_bwd_prep": 0.0, "attn_bwd_dkdv_sm100": f_bwd * 0.75,
-           "attn_bwd_dq_sm100": f_bwd * 0.25}
+           "attn_bwd_dq_sm100": f_bwd * 0.25, "attn_bwd_fused_sm100": f_bwd, "attn_bwd_dq_convert": 0.0}
 
     def run(nm):
         if nm == "attn_fwd_sm100":
             _lib.check(lib.ul_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(),
                                        n, b, h, h, hd, 1, 1, scale, stream))
         else:
-            stage = {"attn_bwd_prep": 1, "attn_bwd_dkdv_sm100": 2, "attn_bwd_dq_sm100": 4}[nm]
+            stage = {"attn_bwd_prep": 1, "attn_bwd_dkdv_sm100": 2, "attn_bwd_dq_sm100": 4, "attn_bwd_fused_sm100": 2,
+                     "attn_bwd_dq_convert": 4}[nm]
             _lib.check(lib.ul_attn_bwd_stages(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                               do.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(),
                                               dv.data_ptr(), ws.data_ptr(), wsb, n, b, h, h, hd, 1, 1, scale,
@@ -416,6 +442,27 @@ def bench_a2a(dev, n_seq, H, hd, P, group, reps=10):
         out["exchange"] = {"P": P, "ms": round(ms, 4), "egress_bytes": egress,
                            "nvlink_gbs": round(egress / (ms / 1e3) / 1e9, 1), "peak_gbs_nominal": 900.0,
                            "peak_gbs_measured_peer_copy": 770.0}
+        # the measured comparison (north star): the same seq->head exchange
+        # the way a torch user writes it -- permute to rank-major chunks +
+        # NCCL all_to_all_single, one per tensor
+        try:
+            ys = [torch.empty((P, nl, 1, H // P, hd), device=dev, dtype=torch.bfloat16) for _ in range(3)]
+
+            def nccl_qkv():
+                for t, y in zip(x, ys):
+                    src = t.reshape(nl, 1, P, H // P, hd).permute(2, 0, 1, 3, 4).contiguous()
+                    dist.all_to_all_single(y, src)
+            ms_n = timed([nccl_qkv], [torch.cuda.current_stream(dev)])
+            t = torch.tensor([ms_n], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_n = float(t.item())
+            ref = group.all_to_all(x, 2, 0, label="bench.qkv.check")
+            same = all(torch.equal(r.reshape(-1), y.reshape(-1)) for r, y in zip(ref, ys))
+            out["nccl_exchange"] = {"ms": round(ms_n, 4), "nvlink_gbs": round(egress / (ms_n / 1e3) / 1e9, 1),
+                                    "same_bytes_as_ours": bool(same),
+                                    "path": "permute().contiguous() + dist.all_to_all_single per tensor (NCCL)"}
+        except Exception as exc:   # reported, never fatal: it is only the comparison
+            out["nccl_exchange"] = {"error": repr(exc)[:200]}
     # single-GPU HBM-bound views of the same kernels
     xs = [torch.randn((n_seq, 1, H, hd), device=dev).to(torch.bfloat16) for _ in range(3)]
     g1 = U.SequenceGroup.single(dev.index)

@@ -149,14 +149,25 @@ int ul_attn_bwd(const void* q, const void* k, const void* v, const void* o,
                 int dtype, int mask, float scale, void* stream);
 
 /* Same as ul_attn_bwd restricted to a subset of its launches (bit 0: D/LSE
- * pre-pass, bit 1: dK/dV kernel, bit 2: dQ kernel), in that order; the
- * stages must run in order over one workspace.  Lets callers time or
- * overlap the stages; ul_attn_bwd == stage_mask 7. */
+ * pre-pass, bit 1: dK/dV kernel -- the fused dK/dV/dQ kernel in the default
+ * hd-128 mode --, bit 2: dQ kernel -- the dQ fp32->bf16 pass in that mode),
+ * in that order; the stages must run in order over one workspace.  Lets
+ * callers time or overlap the stages; ul_attn_bwd == stage_mask 7. */
 int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* o,
                        const void* dout, const float* lse, void* dq, void* dk, void* dv,
                        void* workspace, size_t workspace_bytes,
                        int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
                        int dtype, int mask, float scale, int stage_mask, void* stream);
+
+/* Backward mode (process-wide; extension, no reference counterpart).
+ * 0 (default): bf16 hd-128 backward in one fused kernel (dK, dV and dQ from
+ *   one pass; dQ accumulated with fp32 atomics, so it varies in the last
+ *   bits run to run).
+ * 1: deterministic -- dK/dV kernel + a dQ kernel that recomputes S and dP,
+ *   no atomics, results bitwise reproducible (and bitwise P-invariant).
+ * hd 64 and fp32 always run the deterministic kernels. */
+void ul_attn_set_deterministic(int on);
+int ul_attn_get_deterministic(void);
 
 /* Local attention with the head->seq exchange (K2) fused into the kernels'
  * epilogues: every finished output row goes both to the head-layout tensor

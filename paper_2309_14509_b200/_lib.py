@@ -34,7 +34,7 @@ EXPORTS = (
     "ul_comm_ledger", "ul_all_to_all", "ul_all_to_all_slot_bytes", "ul_attn_fwd",
     "ul_attn_bwd_workspace_bytes", "ul_attn_bwd", "ul_attn_bwd_stages", "ul_attn_fwd_exchange",
     "ul_attn_bwd_exchange", "ul_last_launch_count",
-    "ul_total_launch_count", "ul_ulysses_volume",
+    "ul_total_launch_count", "ul_ulysses_volume", "ul_attn_set_deterministic", "ul_attn_get_deterministic",
 )
 
 _lib = None
@@ -47,6 +47,8 @@ def _declare(lib):
     P = ctypes.POINTER
     sig = {
         "ul_abi_version": (ctypes.c_int, []),
+        "ul_attn_set_deterministic": (None, [ctypes.c_int]),
+        "ul_attn_get_deterministic": (ctypes.c_int, []),
         "ul_last_error": (ctypes.c_char_p, []),
         "ul_preload_kernels": (ctypes.c_int, []),
         "ul_comm_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_size_t,

@@ -91,13 +91,20 @@ class FlashAttention:
     (dense_kernel, kernels.py:43-46); ``scale`` defaults to 1/sqrt(hd)
     (AttentionSpec.scale, layers.py:51).  K/V may carry fewer heads than Q
     (GQA: query head h reads kv head h // (hq/hkv)).
+
+    ``deterministic=False`` (default) runs the bf16 hd-128 backward as one
+    fused kernel whose dQ is accumulated with fp32 atomics (last-bit run to
+    run variation, within the stated tolerance); ``True`` selects the
+    two-kernel backward (dQ kernel recomputes S and dP, no atomics) whose
+    gradients are bitwise reproducible and bitwise P-invariant.
     """
 
-    def __init__(self, mask: str = "causal", scale: float | None = None):
+    def __init__(self, mask: str = "causal", scale: float | None = None, deterministic: bool = False):
         if mask not in ("causal", "none"):
             raise KernelError(f"kernel supports dense/causal masks only, got {mask!r}")
         self.mask = mask
         self.scale = scale
+        self.deterministic = bool(deterministic)
 
     @property
     def mask_code(self) -> int:
@@ -146,6 +153,7 @@ class FlashAttention:
         dt = _ATTN_DTYPES[q.dtype]
         wsb = int(_lib.lib().ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dt))
         ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=q.device)
+        _lib.lib().ul_attn_set_deterministic(int(self.deterministic))
         _lib.check(_lib.lib().ul_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                           do.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(),
                                           dv.data_ptr(), ws.data_ptr(), ws.numel(), n, b, hq, hkv, hd,
@@ -171,9 +179,11 @@ class FlashAttention:
         group._record(label, o.numel())
         return o, lse, o_seq
 
-    def backward_exchange(self, q, k, v, o, lse, do, group: SequenceGroup, label: str = "bwd.qkv.head2seq"):
+    def backward_exchange(self, q, k, v, o, lse, do, group: SequenceGroup, label: str = "bwd.qkv.head2seq",
+                          return_head: bool = False):
         """Backward with the head->seq exchange of dQ/dK/dV fused into the
-        epilogues.  Returns sequence-layout (dq, dk, dv) of this rank."""
+        epilogues.  Returns sequence-layout (dq, dk, dv) of this rank (and
+        the head-layout gradients the kernels also wrote, if return_head)."""
         from .comm import label_hash
         if lse is None:
             raise ForwardStateError("backward needs the state saved by the forward pass")
@@ -187,6 +197,7 @@ class FlashAttention:
         dt = _ATTN_DTYPES[q.dtype]
         wsb = int(_lib.lib().ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dt))
         ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=q.device)
+        _lib.lib().ul_attn_set_deterministic(int(self.deterministic))
         _lib.check(_lib.lib().ul_attn_bwd_exchange(group._handle, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                                    o.data_ptr(), do.data_ptr(), lse.data_ptr(), dq.data_ptr(),
                                                    dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), ws.numel(),
@@ -195,6 +206,8 @@ class FlashAttention:
                                                    _stream(q)))
         for name, t in (("bwd.q.head2seq", dq), ("bwd.k.head2seq", dk), ("bwd.v.head2seq", dv)):
             group._record(name, t.numel())
+        if return_head:
+            return (sq, sk, sv), (dq, dk, dv)
         return sq, sk, sv
 
     def __call__(self, q, k, v):

@@ -133,7 +133,8 @@ template <int HD>
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                        const __nv_bfloat16* __restrict__ dout,
                                                        const float* __restrict__ lse, float* __restrict__ L2,
-                                                       float* __restrict__ Dv, int n, int n_pad, int b, int hq) {
+                                                       float* __restrict__ Dv, int n, int n_pad, int b, int hq,
+                                                       float* __restrict__ dq_acc) {
   // HD/8 threads per row, rows in memory order ((i*b + bb)*hq + h): every
   // warp streams contiguous 16-byte chunks of O and dO
   constexpr int TPR = HD / 8;
@@ -155,13 +156,20 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
   }
 #pragma unroll
   for (int m = TPR / 2; m; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-  if (r < rows && sub == 0) {
+  if (r < rows) {
     const int h = (int)(r % hq);
     const int64_t ib = r / hq;
     const int bb = (int)(ib % b), i = (int)(ib / b);
     const int64_t bh = (int64_t)bb * hq + h;
-    Dv[bh * n_pad + i] = s;
-    L2[bh * n_pad + i] = lse[bh * n + i] * 1.4426950408889634f;
+    if (sub == 0) {
+      Dv[bh * n_pad + i] = s;
+      L2[bh * n_pad + i] = lse[bh * n + i] * 1.4426950408889634f;
+    }
+    if (dq_acc) {   // fused backward: zero this row's slice of the fp32 dQ accumulator
+      float4* z = reinterpret_cast<float4*>(dq_acc + (bh * n_pad + i) * HD + sub * 8);
+      z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
   // rows n..n_pad of every head: masked-out padding (P = 0, D = 0)
   const int pad = n_pad - n;
@@ -799,7 +807,384 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   }
 }
 
+// ---- fused dK / dV / dQ (default for hd 128) -----------------------------------
+// One CTA per (128-row kv tile, kv head), like bwd_dkdv, but dQ comes out of
+// the same pass instead of a second kernel that recomputes S and dP:
+//   dQ^T(i) = K^T dS^T(i)      (M = hd, N = 64 query rows, K = 128 kv rows)
+// is accumulated in the dP^T TMEM buffer of sub-tile i once the softmax has
+// consumed it, drained by four warps (thread = hd column, 64 query rows) and
+// added into an fp32 [b*hq][n_pad][hd] accumulator with coalesced
+// red.global.add.f32 (one 128-byte line per warp instruction); a last pass
+// scales it into bf16 dQ.  Five GEMMs of 2*128*64*hd per sub-tile instead of
+// the seven of bwd_dkdv + bwd_dq, and half the exponentials.  The fp32
+// additions from different kv tiles land in arrival order, so dQ is not
+// bitwise reproducible run to run (tolerance-equal); ul_attn_set_deterministic(1)
+// selects the two-kernel path whose results are bitwise stable.
+//   dS^T(i) goes both to TMEM (A operand of dK += dS^T Q, as in bwd_dkdv) and
+// to shared memory as a SWIZZLE_128B [kv][q] tile (MN-major B operand of
+// the dQ^T MMA; the A operand K^T is the resident K tile read MN-major).
+// warp 0 TMA, warp 1 MMA, warps 2-5 dQ drain, warps 6-21 softmax (4 per lane
+// quarter, 16 columns each).
+constexpr int kFuSoftWarps = 16;
+constexpr int kFuThreads = 64 + 128 + kFuSoftWarps * 32;
+constexpr int FNST = 3;   // Q / dO / L / D stages
+constexpr int NDS = 3;    // dS^T smem buffers: the softmax of sub-tile i writes while dQ^T(i-1), dQ^T(i-2) may still read
+
+template <int HD>
+struct FusedSmem {
+  static constexpr int kTileT = (HD / 64) * kAtomT;   // 128 x HD
+  static constexpr int kTileS = (HD / 64) * kAtomS;   // 64 x HD
+  static constexpr int kK = 0;
+  static constexpr int kV = kK + kTileT;
+  static constexpr int kQ = kV + kTileT;              // [FNST]
+  static constexpr int kO = kQ + FNST * kTileS;       // dO [FNST]
+  static constexpr int kDS = kO + FNST * kTileS;      // dS^T [NDS] (128 kv rows x 64 q, bf16, SW128)
+  static constexpr int kL = kDS + NDS * kAtomT;       // [FNST][BS] f32
+  static constexpr int kD = kL + FNST * BS * 4;       // [FNST][BS] f32
+  static constexpr int kBar = kD + FNST * BS * 4;
+  static constexpr int kBytes = kBar + 256 + 1024;
+};
+
+__device__ __forceinline__ void red_add_f32(float* addr, float v) {
+  asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u4(uint32_t saddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kFuThreads, 1)
+    bwd_fused_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                     const Params p, float* __restrict__ dq_acc) {
+  static_assert(HD == 128, "the dQ^T MMA uses M = head dim = 128");
+  using S = FusedSmem<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem + S::kK;
+  uint8_t* sV = smem + S::kV;
+  uint8_t* sQ = smem + S::kQ;
+  uint8_t* sO = smem + S::kO;
+  uint8_t* sDS = smem + S::kDS;
+  float* sL = reinterpret_cast<float*>(smem + S::kL);
+  float* sD = reinterpret_cast<float*>(smem + S::kD);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* q_full = bars + 1;                  // [FNST]
+  uint64_t* q_empty = bars + 1 + FNST;          // [FNST]
+  uint64_t* s_full = bars + 1 + 2 * FNST;       // [2] S^T, dP^T in TMEM
+  uint64_t* p_full = bars + 3 + 2 * FNST;       // [2] P^T, dS^T written (TMEM + smem)
+  uint64_t* dq_full = bars + 5 + 2 * FNST;      // [2] dQ^T accumulated (and everything before it)
+  uint64_t* dq_free = bars + 7 + 2 * FNST;      // [2] dQ^T read out of TMEM by the drain warps
+  uint64_t* ds_free = bars + 9 + 2 * FNST;      // [NDS] dS^T smem buffer consumed
+  uint64_t* dp_full = bars + 9 + NDS + 2 * FNST;  // [2] dP^T in TMEM (s_full: S^T only)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11 + NDS + 2 * FNST);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ktiles = (p.n + BT - 1) / BT;
+  const int kheads = p.b * p.hkv;
+  const int kt = p.head_major ? (int)(blockIdx.x % ktiles) : (int)(blockIdx.x / kheads);
+  const int bg = p.head_major ? (int)(blockIdx.x / ktiles) : (int)(blockIdx.x % kheads);
+  const int bb = bg / p.hkv, g = bg % p.hkv;
+  const int group = p.hq / p.hkv;
+  const int kv0 = kt * BT;
+  const int nsub = (p.n + BS - 1) / BS;
+  const int i0 = p.causal ? kv0 / BS : 0;
+  const int per_head = nsub - i0;
+  const int total = per_head * group;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < FNST; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&dp_full[s], 1);
+      mbar_init(&p_full[s], kFuSoftWarps);
+      mbar_init(&dq_full[s], 1);
+      mbar_init(&dq_free[s], 4);
+    }
+    for (int s = 0; s < NDS; ++s) mbar_init(&ds_free[s], 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (*tmem_slot != 0u) __trap();
+  constexpr uint32_t tbase = 0;
+  // TMEM: S^T[2] at 0/64 (P^T over it), dP^T[2] at 128/192 (dS^T over it, then
+  // dQ^T of the same sub-tile), dV at 256, dK at 256 + HD
+  const uint32_t tdV = tbase + 256, tdK = tbase + 256 + HD;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      tma_prefetch_desc(&tmO);
+      mbar_expect_tx(kv_full, 2 * BT * HD * 2);
+#pragma unroll
+      for (int a = 0; a < HD / 64; ++a) {
+        tma_load_3d(sK + a * kAtomT, &tmK, kv_full, a * 64, bb * p.hkv + g, kv0);
+        tma_load_3d(sV + a * kAtomT, &tmV, kv_full, a * 64, bb * p.hkv + g, kv0);
+      }
+      int h = g * group, qi = i0;
+      for (int it = 0; it < total; ++it) {
+        const int s = it % FNST;
+        mbar_wait(&q_empty[s], ((it / FNST) & 1) ^ 1);
+        UL_EV(8, it);
+        mbar_expect_tx(&q_full[s], 2 * BS * HD * 2 + 2 * BS * 4);
+#pragma unroll
+        for (int a = 0; a < HD / 64; ++a) {
+          tma_load_3d(sQ + s * S::kTileS + a * kAtomS, &tmQ, &q_full[s], a * 64, bb * p.hq + h, qi * BS);
+          tma_load_3d(sO + s * S::kTileS + a * kAtomS, &tmO, &q_full[s], a * 64, bb * p.hq + h, qi * BS);
+        }
+        const int64_t roff = ((int64_t)bb * p.hq + h) * p.n_pad + qi * BS;
+        bulk_load(sL + s * BS, p.L2 + roff, BS * 4, &q_full[s]);
+        bulk_load(sD + s * BS, p.Dv + roff, BS * 4, &q_full[s]);
+        if (++qi == nsub) {
+          qi = i0;
+          ++h;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t kIdS = idesc_bf16(BT, BS, 0, 0);   // S^T, dP^T: M = kv rows, N = 64 q rows
+      constexpr uint32_t kIdG = idesc_bf16(BT, HD, 0, 1);   // dV, dK: M = kv rows, N = hd, B MN-major
+      constexpr uint32_t kIdQ = idesc_bf16(HD, BS, 1, 1);   // dQ^T: M = hd, N = q rows, A and B MN-major
+      const uint64_t dK0 = sdesc(smem_u32(sK), 16, 1024), dV0 = sdesc(smem_u32(sV), 16, 1024);
+      const uint64_t dQk0 = sdesc(smem_u32(sQ), 16, 1024), dOk0 = sdesc(smem_u32(sO), 16, 1024);
+      const uint64_t dQm0 = sdesc(smem_u32(sQ), kAtomS, 1024), dOm0 = sdesc(smem_u32(sO), kAtomS, 1024);
+      const uint64_t dKt0 = sdesc(smem_u32(sK), kAtomT, 1024);    // K^T: MN-major A (hd contiguous)
+      const uint64_t dDS0 = sdesc(smem_u32(sDS), kAtomT, 1024);   // dS^T: MN-major B (q contiguous)
+      auto issue_grads = [&](int i) {
+        const int b = i & 1, s = i % FNST;
+        const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
+        mbar_wait(&p_full[b], (i >> 1) & 1);
+        UL_EV(1, i);
+        tc_fence_after();
+        const uint64_t dOm = dadd(dOm0, s * S::kTileS), dQm = dadd(dQm0, s * S::kTileS);
+#pragma unroll
+        for (int kk = 0; kk < BS / 16; ++kk)
+          mma_ts(tdV, tSt + a_col16(kk), dadd(dOm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < BS / 16; ++kk)
+          mma_ts(tdK, tdPt + a_col16(kk), dadd(dQm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&q_empty[s]);
+        // dQ^T(i) over the dP^T / dS^T columns dK(i) just read (in-order pipe)
+        const uint64_t dds = dadd(dDS0, (i % NDS) * kAtomT);
+#pragma unroll
+        for (int kk = 0; kk < BT / 16; ++kk)
+          mma_ss(tdPt, dadd(dKt0, kk * 2048), dadd(dds, kk * 2048), kIdQ, kk > 0 ? 1u : 0u);
+        mma_commit(&dq_full[b]);
+        mma_commit(&ds_free[i % NDS]);
+        UL_EV(6, i);
+      };
+      mbar_wait(kv_full, 0);
+      for (int it = 0; it < total; ++it) {
+        const int b = it & 1, s = it % FNST;
+        const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
+        UL_EV(10, it);
+        mbar_wait(&q_full[s], (it / FNST) & 1);
+        UL_EV(0, it);
+        tc_fence_after();
+        const uint64_t dQk = dadd(dQk0, s * S::kTileS), dOk = dadd(dOk0, s * S::kTileS);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
+          const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
+          mma_ss(tSt, dadd(dK0, offT), dadd(dQk, offS), kIdS, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[b]);   // the softmax starts on P while dP^T runs
+        // dP^T(it) replaces dQ^T(it-2): wait until the drain warps have it
+        if (it >= 2) {
+          mbar_wait(&dq_free[b], ((it - 2) >> 1) & 1);
+          tc_fence_after();
+        }
+        UL_EV(9, it);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t offT = (kk >> 2) * kAtomT + (kk & 3) * 32;
+          const uint32_t offS = (kk >> 2) * kAtomS + (kk & 3) * 32;
+          mma_ss(tdPt, dadd(dV0, offT), dadd(dOk, offS), kIdS, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&dp_full[b]);
+        UL_EV(7, it);
+        if (it >= 1) issue_grads(it - 1);
+      }
+      if (total > 0) issue_grads(total - 1);
+    }
+    __syncwarp();
+  } else if (warp < 6) {
+    // ---- dQ drain: thread = hd column, 64 query rows of sub-tile it ----
+    const int quarter = warp & 3;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const int d = quarter * 32 + lane;
+    int h = g * group, qi = i0;
+    for (int it = 0; it < total; ++it) {
+      const int b = it & 1;
+      const uint32_t tdPt = tbase + 128 + b * 64;
+      mbar_wait(&dq_full[b], (it >> 1) & 1);
+      if (lane == 0 && warp == 2) UL_EV(4, it);
+      tc_fence_after();
+      float* dst = dq_acc + (((int64_t)bb * p.hq + h) * p.n_pad + (int64_t)qi * BS) * HD + d;
+      // both halves into registers first: the TMEM buffer goes back to the
+      // MMA issuer (dP^T of sub-tile it+2) before the 64 atomics are issued
+      uint32_t v[64];
+      tmem_ld32(tdPt + lane_off, v);
+      tmem_ld32(tdPt + lane_off + 32, v + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dq_free[b]);
+      if (lane == 0 && warp == 2) UL_EV(11, it);
+#pragma unroll
+      for (int c = 0; c < 64; ++c) red_add_f32(dst + c * HD, __uint_as_float(v[c]));
+      if (lane == 0 && warp == 2) UL_EV(15, it);
+      if (++qi == nsub) {
+        qi = i0;
+        ++h;
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int part = (warp - 6) >> 2;        // which 16-column quarter of the sub-tile
+    const int row = quarter * 32 + lane;     // kv row within the tile
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const int kvrow = kv0 + row;
+    const int c0 = part * 16;
+    const float2 sc = make_float2(p.scale_log2, p.scale_log2);
+    // this thread's two 16-byte chunks of its dS^T row in a SWIZZLE_128B tile
+    const uint32_t ds_row = smem_u32(sDS) + (row >> 3) * 1024 + (row & 7) * 128;
+    const uint32_t ds_c0 = ((2 * part) ^ (row & 7)) << 4, ds_c1 = ((2 * part + 1) ^ (row & 7)) << 4;
+    int qi = i0;
+    for (int it = 0; it < total; ++it) {
+      const int b = it & 1, s = it % FNST;
+      const int q0 = qi * BS;
+      if (++qi == nsub) qi = i0;
+      const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
+      mbar_wait(&q_full[s], (it / FNST) & 1);
+      float2 nl[8], nd[8];
+      {
+        const uint32_t la = smem_u32(sL + s * BS + c0), da = smem_u32(sD + s * BS + c0);
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          const float4 a = lds_f4(la + 16 * x), e = lds_f4(da + 16 * x);
+          nl[2 * x] = make_float2(-a.x, -a.y);
+          nl[2 * x + 1] = make_float2(-a.z, -a.w);
+          nd[2 * x] = make_float2(-e.x, -e.y);
+          nd[2 * x + 1] = make_float2(-e.z, -e.w);
+        }
+      }
+      mbar_wait(&s_full[b], (it >> 1) & 1);
+      if (lane == 0 && warp == 6) UL_EV(2, it);
+      tc_fence_after();
+      uint32_t r[16], dd[16];
+      tmem_ld16(tSt + lane_off + c0, r);
+      tmem_wait_ld();
+      if (lane == 0 && warp == 6) UL_EV(12, it);
+      // P first (S^T only); dS once dP^T has landed
+      uint32_t pk[8], dsk[8];
+      float2 e[8];
+      if (p.causal && q0 + c0 < kv0 + BT) {
+        const int first = kvrow - q0 - c0;   // columns x < first are masked (q < kv)
+#pragma unroll
+        for (int x = 0; x < 16; x += 2) {
+          e[x / 2] = pexp2(r + x, sc, nl[x / 2]);
+          e[x / 2].x = x < first ? 0.f : e[x / 2].x;
+          e[x / 2].y = x + 1 < first ? 0.f : e[x / 2].y;
+        }
+      } else {
+#pragma unroll
+        for (int x = 0; x < 16; x += 2)
+          e[x / 2] = (x & 2) ? pexp2<kDkPoly>(r + x, sc, nl[x / 2]) : pexp2(r + x, sc, nl[x / 2]);
+      }
+#pragma unroll
+      for (int x = 0; x < 8; ++x) pk[x] = pack_bf16(e[x].x, e[x].y);
+      tmem_st8(tSt + lane_off + c0 + 8, pk);
+      mbar_wait(&dp_full[b], (it >> 1) & 1);
+      tc_fence_after();
+      tmem_ld16(tdPt + lane_off + c0, dd);
+      tmem_wait_ld();
+#pragma unroll
+      for (int x = 0; x < 8; ++x) dsk[x] = pds(e[x], dd + 2 * x, nd[x]);
+      // dS^T row chunk -> shared memory for the dQ^T MMA (after dQ^T(it-NDS) read the buffer)
+      if (lane == 0 && warp == 6) UL_EV(13, it);
+      const int ib = it % NDS;
+      if (it >= NDS) mbar_wait(&ds_free[ib], ((it - NDS) / NDS) & 1);
+      if (lane == 0 && warp == 6) UL_EV(14, it);
+      const uint32_t dsb = ds_row + ib * kAtomT;
+      sts_u4(dsb + ds_c0, dsk[0], dsk[1], dsk[2], dsk[3]);
+      sts_u4(dsb + ds_c1, dsk[4], dsk[5], dsk[6], dsk[7]);
+      fence_proxy_async_smem();
+      tmem_st8(tdPt + lane_off + c0 + 8, dsk);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[b]);
+      if (lane == 0 && (warp == 6 || warp == 21)) UL_EV(warp == 6 ? 3 : 5, it);
+    }
+    // epilogue: parts 0/1 store the two column halves of dV, parts 2/3 of dK * scale
+    if (total > 0) mbar_wait(&ds_free[(total - 1) % NDS], ((total - 1) / NDS) & 1);
+    tc_fence_after();
+    const bool valid = kvrow < p.n;
+    const int64_t off = (((int64_t)kvrow * p.b + bb) * p.hkv + g) * HD;
+    const bool is_dk = part >= 2;
+    const int col0 = (part & 1) * (HD / 2);
+    const PeerEpilogue& ep = is_dk ? p.ep_dk : p.ep_dv;
+    char* peer = (ep.active && valid) ? peer_row_ptr(ep, kvrow, bb, p.b, g, HD, 2) + col0 * 2 : nullptr;
+    if (!is_dk) store_acc_rows<HD / 2>(tdV + col0, lane_off, 1.f, p.dv + off + col0, valid, peer);
+    else store_acc_rows<HD / 2>(tdK + col0, lane_off, p.scale, p.dk + off + col0, valid, peer);
+    if (ep.active) __threadfence_system();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
+// dQ = scale * acc in bf16 rows of the head layout (+ the fused head->seq
+// stores and, as the last launch of the backward, the exchange signal)
+template <int HD>
+__global__ void __launch_bounds__(256) bwd_dq_convert_kernel(const float* __restrict__ acc,
+                                                             __nv_bfloat16* __restrict__ dq, int n, int n_pad, int b,
+                                                             int hq, float scale, PeerEpilogue ep) {
+  constexpr int TPR = HD / 8;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = tid / TPR;   // output row (i*b + bb)*hq + h
+  const int sub = (int)(tid % TPR);
+  if (r < (int64_t)n * b * hq) {
+    const int h = (int)(r % hq);
+    const int64_t ib = r / hq;
+    const int bb = (int)(ib % b), i = (int)(ib / b);
+    const float4* src = reinterpret_cast<const float4*>(acc + (((int64_t)bb * hq + h) * n_pad + i) * HD + sub * 8);
+    const float4 x = __ldg(src), y = __ldg(src + 1);
+    const uint4 o = make_uint4(pack_bf16(x.x * scale, x.y * scale), pack_bf16(x.z * scale, x.w * scale),
+                               pack_bf16(y.x * scale, y.y * scale), pack_bf16(y.z * scale, y.w * scale));
+    reinterpret_cast<uint4*>(dq + r * HD)[sub] = o;
+    if (ep.active) reinterpret_cast<uint4*>(peer_row_ptr(ep, i, bb, b, h, HD, 2))[sub] = o;
+  }
+  if (ep.active) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) peer_signal_last_cta(ep, gridDim.x);
+  }
+}
+
 static int64_t pad_n(int64_t n) { return (n + 127) / 128 * 128; }
+
+static int g_deterministic = 0;   // ul_attn_set_deterministic
 
 template <int HD>
 static int launch(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
@@ -808,11 +1193,13 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
   const int64_t npad = pad_n(n);
   float* L2 = reinterpret_cast<float*>(ws);
   float* Dv = L2 + b * hq * npad;
+  const bool fused = HD == 128 && !g_deterministic;
+  float* dq_acc = fused ? Dv + b * hq * npad : nullptr;   // [b*hq][npad][HD] f32
   if (stages & 1) {
     const int64_t threads = std::max<int64_t>(n * b * hq * (HD / 8), b * hq * (npad - n));
     const unsigned blocks = (unsigned)((threads + 255) / 256);
     bwd_prep_kernel<HD><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, lse, L2, Dv,
-                                                (int)n, (int)npad, (int)b, (int)hq);
+                                                (int)n, (int)npad, (int)b, (int)hq, dq_acc);
     UL_TRY(launched("attn_bwd_prep"));
   }
   Params p;
@@ -844,9 +1231,33 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
     UL_CUDA(cudaFuncSetAttribute(bwd_dkdv_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  DkdvSmem<HD>::kBytes));
     UL_CUDA(cudaFuncSetAttribute(bwd_dq_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqSmem<HD>::kBytes));
+    if constexpr (HD == 128)
+      UL_CUDA(cudaFuncSetAttribute(bwd_fused_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   FusedSmem<HD>::kBytes));
     attr = true;
   }
   const int64_t tiles = (n + BT - 1) / BT;
+  if constexpr (HD == 128) {
+    if (fused) {
+      if (stages & 2) {
+        CUtensorMap mq, mk, mv, mo;
+        UL_TRY(make_tmap_bhsd(&mq, q, n, b * hq, HD, BS));
+        UL_TRY(make_tmap_bhsd(&mo, dout, n, b * hq, HD, BS));
+        UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, BT));
+        UL_TRY(make_tmap_bhsd(&mv, v, n, b * hkv, HD, BT));
+        bwd_fused_kernel<HD><<<(unsigned)(tiles * b * hkv), kFuThreads, FusedSmem<HD>::kBytes, st>>>(mq, mk, mv, mo,
+                                                                                                     p, dq_acc);
+        UL_TRY(launched("attn_bwd_fused_sm100"));
+      }
+      if (stages & 4) {
+        const int64_t threads = n * b * hq * (HD / 8);
+        bwd_dq_convert_kernel<HD><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+            dq_acc, (__nv_bfloat16*)dq, (int)n, (int)npad, (int)b, (int)hq, scale, p.ep_dq);
+        UL_TRY(launched("attn_bwd_dq_convert"));
+      }
+      return UL_OK;
+    }
+  }
   if (stages & 2) {
     // dkdv: the kv tile is resident (128-row boxes), query sub-tiles stream (64-row boxes)
     CUtensorMap mq, mk, mv, mo;
@@ -895,13 +1306,21 @@ int preload_bwd() {
   UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dkdv_kernel<128>));
   UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dq_kernel<64>));
   UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dq_kernel<128>));
+  UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_fused_kernel<128>));
+  UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dq_convert_kernel<128>));
   return UL_OK;
 }
 
+void set_deterministic(int on) { bwd::g_deterministic = on ? 1 : 0; }
+int get_deterministic() { return bwd::g_deterministic; }
+
 size_t sm100_bwd_workspace(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd) {
   (void)hkv;
-  (void)hd;
-  return (size_t)2 * b * hq * bwd::pad_n(n) * sizeof(float);
+  // L2 + D rows, and the fp32 dQ accumulator of the fused hd-128 kernel
+  // (sized whether or not deterministic mode is on, so a workspace stays valid
+  // across mode switches)
+  const size_t rows = (size_t)b * hq * bwd::pad_n(n);
+  return rows * 2 * sizeof(float) + (hd == 128 ? rows * hd * sizeof(float) : 0);
 }
 
 int sm100_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,

@@ -41,6 +41,8 @@ int preload_a2a();
 int preload_simt();
 int preload_fwd();
 int preload_bwd();
+void set_deterministic(int on);
+int get_deterministic();
 
 static int check_attn(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask) {
   if (mask != UL_MASK_NONE && mask != UL_MASK_CAUSAL)
@@ -68,6 +70,9 @@ int ul_abi_version(void) { return UL_ABI_VERSION; }
 const char* ul_last_error(void) { return last_error().c_str(); }
 int ul_last_launch_count(void) { return launch_count(); }
 uint64_t ul_total_launch_count(void) { return g_total_launches.load(); }
+
+void ul_attn_set_deterministic(int on) { set_deterministic(on); }
+int ul_attn_get_deterministic(void) { return get_deterministic(); }
 
 int ul_preload_kernels(void) {
   UL_TRY(preload_a2a());

@@ -70,12 +70,13 @@ BWD_CASES = [
 ]
 
 
+@pytest.mark.parametrize("deterministic", [False, True], ids=["fused", "deterministic"])
 @pytest.mark.parametrize("n,b,hq,hkv,hd,mask", BWD_CASES)
-def test_bwd_bf16_vs_oracle(n, b, hq, hkv, hd, mask):
+def test_bwd_bf16_vs_oracle(n, b, hq, hkv, hd, mask, deterministic):
     q, k, v, do = inputs(n, b, hq, hkv, hd, torch.bfloat16, seed=100 + n + hd)
     kind = "causal" if mask == "causal" else "none"
     dq_r, dk_r, dv_r = O.local_attention_backward(q, k, v, do, kind, exact=False)
-    attn = U().FlashAttention(mask)
+    attn = U().FlashAttention(mask, deterministic=deterministic)
     tq, tk, tv, tdo = (to_dev(x, torch.bfloat16) for x in (q, k, v, do))
     o, lse = attn.forward_with_lse(tq, tk, tv)
     dq, dk, dv = attn.backward(tq, tk, tv, o, lse, tdo)
@@ -83,9 +84,14 @@ def test_bwd_bf16_vs_oracle(n, b, hq, hkv, hd, mask):
     for name, got, ref in (("dq", dq, dq_r), ("dk", dk, dk_r), ("dv", dv, dv_r)):
         err = rel_max_err(to_np(got), ref)
         assert err <= BF16_MAXREL, f"{name}: max-abs / max|ref| = {err:.3e}"
-    # deterministic: a second backward is bitwise identical (no atomics)
+    # dK/dV never use atomics: a second backward is bitwise identical; dQ too
+    # in deterministic mode (the fused mode's fp32 atomic order may vary)
     dq2, dk2, dv2 = attn.backward(tq, tk, tv, o, lse, tdo)
-    assert torch.equal(dq, dq2) and torch.equal(dk, dk2) and torch.equal(dv, dv2)
+    assert torch.equal(dk, dk2) and torch.equal(dv, dv2)
+    if deterministic or hd != 128:
+        assert torch.equal(dq, dq2)
+    else:
+        assert rel_max_err(to_np(dq2), to_np(dq)) <= 1e-2
 
 
 @pytest.mark.parametrize("n,b,hq,hkv,hd,mask", [(1, 1, 1, 1, 8, "none"), (7, 2, 4, 2, 3, "causal"),
@@ -182,7 +188,7 @@ def test_p_invariance_of_head_sharded_kernels():
     # larger launch (what Ulysses P-invariance needs from the local kernel)
     n, hd = 1024, 128
     q, k, v, do = inputs(n, 1, 8, 8, hd, torch.bfloat16, seed=12)
-    attn = U().FlashAttention("causal")
+    attn = U().FlashAttention("causal", deterministic=True)
     tq, tk, tv, tdo = (to_dev(x, torch.bfloat16) for x in (q, k, v, do))
     o, lse = attn.forward_with_lse(tq, tk, tv)
     g = attn.backward(tq, tk, tv, o, lse, tdo)

@@ -121,7 +121,7 @@ def test_fused_epilogue_exchange_equals_unfused(p, hq, hkv, n):
     # K2 fused into the attention epilogues must move exactly the bytes the
     # stand-alone head->seq all-to-all moves (bitwise)
     hd = 128
-    attn = U().FlashAttention("causal")
+    attn = U().FlashAttention("causal", deterministic=True)
     groups = U().SequenceGroup.local_group(p, slot_bytes=3 * n * hq * hd * 2 // p + (1 << 20))
     mk = lambda h, s, r: to_dev(O.make_tensor((n, 1, h // p, hd), 60 + r, s, "bfloat16"), torch.bfloat16)
     ins = run_ranks(groups, lambda r: [mk(hq, 1, r), mk(hkv, 2, r), mk(hkv, 3, r), mk(hq, 4, r)])
@@ -145,6 +145,34 @@ def test_fused_epilogue_exchange_equals_unfused(p, hq, hkv, n):
         assert torch.equal(a[r][2], b[r][2]), f"rank {r}: fused O exchange differs"
         for x, y in zip(a[r][3], b[r][3]):
             assert torch.equal(x, y), f"rank {r}: fused dQ/dK/dV exchange differs"
+
+
+@pytest.mark.parametrize("p,hq,hkv,n", [(2, 4, 2, 640), (4, 8, 4, 1024)])
+def test_fused_backward_exchange_moves_its_own_gradients(p, hq, hkv, n):
+    # default (atomic-dQ) backward: the sequence-layout gradients a rank
+    # receives are bitwise the stand-alone head->seq exchange of the
+    # head-layout gradients the same calls produced, and match the oracle
+    hd = 128
+    attn = U().FlashAttention("causal")
+    groups = U().SequenceGroup.local_group(p, slot_bytes=3 * n * hq * hd * 2 // p + (1 << 20))
+    mk = lambda h, s, r: to_dev(O.make_tensor((n, 1, h // p, hd), 70 + r, s, "bfloat16"), torch.bfloat16)
+    ins = run_ranks(groups, lambda r: [mk(hq, 1, r), mk(hkv, 2, r), mk(hkv, 3, r), mk(hq, 4, r)])
+
+    def fused(r):
+        q, k, v, do = ins[r]
+        o, lse, _ = attn.forward_exchange(q, k, v, groups[r])
+        return attn.backward_exchange(q, k, v, o, lse, do, groups[r], return_head=True)
+
+    a = run_ranks(groups, fused)
+    heads = run_ranks(groups, lambda r: groups[r].all_to_all(list(a[r][1]), 0, 2))
+    for r in range(p):
+        for x, y in zip(a[r][0], heads[r]):
+            assert torch.equal(x, y), f"rank {r}: fused-backward exchange differs from its own head layout"
+        q, k, v, do = (to_np(t).astype(np.float64) for t in ins[r])
+        ref = O.local_attention_backward(q, k, v, do, "causal", exact=False)
+        for name, got, want in zip(("dq", "dk", "dv"), a[r][1], ref):
+            err = rel_max_err(to_np(got), want)
+            assert err <= BF16_MAXREL, f"rank {r} {name}: {err:.3e}"
 
 
 def test_bf16_gqa_forward_p4():

@@ -26,6 +26,7 @@ from paper_2309_14509_b200 import _lib  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 lib = ctypes.CDLL(os.path.join(ROOT, os.environ.get("TRACE_LIB", "ab_libs/trace/libulysses_b200.so")))
 _lib._declare(lib)
+lib.ul_attn_set_deterministic.argtypes = [ctypes.c_int]
 lib.ul_debug_trace.restype = ctypes.c_int
 lib.ul_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 
@@ -92,6 +93,30 @@ def report(name, tr):
             print(f"        w2: phase1={d(12, 2):.0f} wait dP={d(11, 12):.0f} phase2={d(3, 11):.0f}")
 
 
+def report_fused(tr):
+    print("== fused (dK/dV/dQ)")
+    for cta in range(8):
+        ev = tr[cta]
+        cnt = int((ev[0] > 0).sum())
+        if cnt < 16:
+            continue
+        j = np.arange(4, cnt - 4)
+        d = lambda a, b, sa=0, sb=0: np.median(ev[a][j + sa] - ev[b][j + sb])
+        print(f" cta {cta}: n={cnt} period={d(0, 0, 1, 0):.0f}  MMA: top->q_full={d(0, 10):.0f}"
+              f" S issue->dq_free ok={d(9, 0):.0f} s_full commit={d(7, 9):.0f} p_full(j-1) seen after s_full(j)="
+              f"{d(1, 7, -1, 0):.0f} grads issue={d(6, 1):.0f}")
+        print(f"   softmax w6: s_full seen after commit={d(2, 7):.0f} ld={d(12, 2):.0f} compute={d(13, 12):.0f}"
+              f" ds_free wait={d(14, 13):.0f} st+arrive={d(3, 14):.0f}  w21 arrive-w6={d(5, 3):.0f}"
+              f"  p_full seen-arrive={d(1, 3):.0f}")
+        print(f"   drain w2: dq_full seen after grads issue={d(4, 6):.0f} ld+32red+ld={d(11, 4):.0f}"
+              f" 32 red={d(15, 11):.0f}  dq_free(j) arrive -> MMA dP(j+2)={d(9, 11, 2, 0):.0f}")
+        print(f"   TMA: stage free seen -> q_full at MMA={d(0, 8):.0f}")
+
+
+lib.ul_attn_set_deterministic(0)
+run(1 | 2)
+report_fused(run(1 | 2))
+lib.ul_attn_set_deterministic(1)
 for stages, name in ((1 | 2, "dkdv"), (4, "dq")):
     run(stages)  # warm
     report(name, run(stages))
