@@ -46,6 +46,12 @@ __device__ unsigned long long g_trace[8 * 16 * 256];
 // 5/6 clock64 at start/end]
 __device__ unsigned long long g_cta[8192 * 7];
 #define UL_CTA(k, v) g_cta[blockIdx.x * 7 + (k)] = (v)
+// per-warp arrival stamps of CTA 0 (fused kernel): [warp][sub-tile]
+__device__ unsigned long long g_warp[32 * 256];
+#define UL_WARP(it)                                                                     \
+  do {                                                                                  \
+    if (blockIdx.x == 0 && (it) < 256 && (threadIdx.x & 31) == 0) g_warp[(threadIdx.x >> 5) * 256 + (it)] = clock64(); \
+  } while (0)
 #define UL_EV(ev, j)                                                                      \
   do {                                                                                    \
     if (blockIdx.x < 8 && (j) < 256) g_trace[(blockIdx.x * 16 + (ev)) * 256 + (j)] = clock64(); \
@@ -56,6 +62,9 @@ __device__ unsigned long long g_cta[8192 * 7];
   } while (0)
 #define UL_CTA(k, v) \
   do {               \
+  } while (0)
+#define UL_WARP(it) \
+  do {              \
   } while (0)
 #endif
 
@@ -325,7 +334,7 @@ __global__ void __launch_bounds__(640, 1)
       auto issue_grads = [&](int i) {
         const int b = i & 1, s = i % NST;
         const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
-        mbar_wait(&p_full[b], (i >> 1) & 1);
+        mbar_wait_mma(&p_full[b], (i >> 1) & 1);
         UL_EV(1, i);
         tc_fence_after();
         const uint64_t dOm = dadd(dOm0, s * S::kTileS), dQm = dadd(dQm0, s * S::kTileS);
@@ -339,14 +348,14 @@ __global__ void __launch_bounds__(640, 1)
         mma_commit(&buf_free[b]);
         UL_EV(6, i);
       };
-      mbar_wait(kv_full, 0);
+      mbar_wait_mma(kv_full, 0);
       for (int it = 0; it < total; ++it) {
         const int b = it & 1, s = it % NST;
         const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
         // buffer b was last read by grads(it-2), issued before this point by
         // this thread: tcgen05.mma executes in issue order, so no wait
         UL_EV(10, it);
-        mbar_wait(&q_full[s], (it / NST) & 1);
+        mbar_wait_mma(&q_full[s], (it / NST) & 1);
         UL_EV(0, it);
         tc_fence_after();
         const uint64_t dQk = dadd(dQk0, s * S::kTileS), dOk = dadd(dOk0, s * S::kTileS);
@@ -630,15 +639,15 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       const uint64_t dKk0 = sdesc(smem_u32(sK), 16, 1024), dVk0 = sdesc(smem_u32(sV), 16, 1024);
       int gj = 0;
       for (int k = 0; dq_tile(p, k, t); ++k) {
-        mbar_wait(a_full, k & 1);
+        mbar_wait_mma(a_full, k & 1);
         for (int j = 0; j < t.nsub; ++j, ++gj) {
           const int b = gj & 1, s = gj % KNST;
           const uint32_t tS = tbase + 128 + b * 64, tdP = tbase + 256 + b * 64;
           UL_EV(10, gj);
-          mbar_wait(&kv_full[s], (gj / KNST) & 1);
+          mbar_wait_mma(&kv_full[s], (gj / KNST) & 1);
           UL_EV(0, gj);
           if (gj == 0) UL_CTA(1, globaltimer());
-          if (gj >= 2) mbar_wait(&s_free[b], ((gj - 2) >> 1) & 1);
+          if (gj >= 2) mbar_wait_mma(&s_free[b], ((gj - 2) >> 1) & 1);
           UL_EV(9, gj);
           tc_fence_after();
           const uint64_t dKk = dadd(dKk0, s * S::kTileS), dVk = dadd(dVk0, s * S::kTileS);
@@ -649,7 +658,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           }
           UL_EV(13, gj);
           if (gj >= 2) {
-            mbar_wait(&dq_done[b], ((gj - 2) >> 1) & 1);
+            mbar_wait_mma(&dq_done[b], ((gj - 2) >> 1) & 1);
             tc_fence_after();
           }
 #pragma unroll
@@ -673,9 +682,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         for (int i = 0; i < t.nsub; ++i, ++gj) {
           const int b = gj & 1, s = gj % KNST;
           const uint32_t tdP = tbase + 256 + b * 64;
-          mbar_wait(&p_full[b], (gj >> 1) & 1);
+          mbar_wait_mma(&p_full[b], (gj >> 1) & 1);
           UL_EV(1, gj);
-          if (i == 0 && k > 0) mbar_wait(dq_free, (k - 1) & 1);   // previous tile's dQ read out
+          if (i == 0 && k > 0) mbar_wait_mma(dq_free, (k - 1) & 1);   // previous tile's dQ read out
           tc_fence_after();
           const uint64_t dKm = dadd(dKm0, s * S::kTileS);
 #pragma unroll
@@ -968,7 +977,7 @@ __global__ void __launch_bounds__(kFuThreads, 1)
       auto issue_grads = [&](int i) {
         const int b = i & 1, s = i % FNST;
         const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
-        mbar_wait(&p_full[b], (i >> 1) & 1);
+        mbar_wait_mma(&p_full[b], (i >> 1) & 1);
         UL_EV(1, i);
         tc_fence_after();
         const uint64_t dOm = dadd(dOm0, s * S::kTileS), dQm = dadd(dQm0, s * S::kTileS);
@@ -988,12 +997,12 @@ __global__ void __launch_bounds__(kFuThreads, 1)
         mma_commit(&ds_free[i % NDS]);
         UL_EV(6, i);
       };
-      mbar_wait(kv_full, 0);
+      mbar_wait_mma(kv_full, 0);
       for (int it = 0; it < total; ++it) {
         const int b = it & 1, s = it % FNST;
         const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
         UL_EV(10, it);
-        mbar_wait(&q_full[s], (it / FNST) & 1);
+        mbar_wait_mma(&q_full[s], (it / FNST) & 1);
         UL_EV(0, it);
         tc_fence_after();
         const uint64_t dQk = dadd(dQk0, s * S::kTileS), dOk = dadd(dOk0, s * S::kTileS);
@@ -1006,7 +1015,7 @@ __global__ void __launch_bounds__(kFuThreads, 1)
         mma_commit(&s_full[b]);   // the softmax starts on P while dP^T runs
         // dP^T(it) replaces dQ^T(it-2): wait until the drain warps have it
         if (it >= 2) {
-          mbar_wait(&dq_free[b], ((it - 2) >> 1) & 1);
+          mbar_wait_mma(&dq_free[b], ((it - 2) >> 1) & 1);
           tc_fence_after();
         }
         UL_EV(9, it);
@@ -1045,6 +1054,7 @@ __global__ void __launch_bounds__(kFuThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&dq_free[b]);
+      UL_WARP(it);
       if (lane == 0 && warp == 2) UL_EV(11, it);
 #pragma unroll
       for (int c = 0; c < 64; ++c) red_add_f32(dst + c * HD, __uint_as_float(v[c]));
@@ -1130,6 +1140,7 @@ __global__ void __launch_bounds__(kFuThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[b]);
+      UL_WARP(it);
       if (lane == 0 && (warp == 6 || warp == 21)) UL_EV(warp == 6 ? 3 : 5, it);
     }
     // epilogue: parts 0/1 store the two column halves of dV, parts 2/3 of dK * scale
@@ -1286,6 +1297,12 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
 #ifdef UL_TRACE
 extern "C" int ul_debug_cta(void* host, size_t bytes) {
   return cudaMemcpyFromSymbol(host, bwd::g_cta, bytes < sizeof(bwd::g_cta) ? bytes : sizeof(bwd::g_cta)) ==
+                 cudaSuccess
+             ? 0
+             : -1;
+}
+extern "C" int ul_debug_warp(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, bwd::g_warp, bytes < sizeof(bwd::g_warp) ? bytes : sizeof(bwd::g_warp)) ==
                  cudaSuccess
              ? 0
              : -1;

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mma_commit(&s_full[t]);
       };
       auto issue_pv = [&](int t, int j) {  // O_t += P_t V_j
-        mbar_wait(&p_full[t], j & 1);
+        mbar_wait_mma(&p_full[t], j & 1);
         UL_EV(t == 0 ? 1 : 2, j);
         tc_fence_after();
         const uint64_t dv = dadd(dV0, (j % NS) * S::kTile);
@@ -238,8 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                  (j > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&o_done[t]);
       };
-      mbar_wait(q_full, 0);
-      mbar_wait(&k_full[0], 0);
+      mbar_wait_mma(q_full, 0);
+      mbar_wait_mma(&k_full[0], 0);
       UL_CTA(1, globaltimer());
       tc_fence_after();
       if (nkvT[0] > 0) issue_s(0, 0);
@@ -249,8 +249,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int s = j % NS;
         const bool next = j + 1 < nkv;
         UL_EV(10, j);
-        mbar_wait(&v_full[s], (j / NS) & 1);
-        if (next) mbar_wait(&k_full[(j + 1) % NS], ((j + 1) / NS) & 1);
+        mbar_wait_mma(&v_full[s], (j / NS) & 1);
+        if (next) mbar_wait_mma(&k_full[(j + 1) % NS], ((j + 1) / NS) & 1);
         UL_EV(0, j);
         tc_fence_after();
         if (j < nkvT[0]) issue_pv(0, j);

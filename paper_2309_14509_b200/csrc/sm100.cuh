@@ -9,6 +9,10 @@
 #include <stdint.h>
 #include <cstdio>
 
+#ifndef UL_MBAR_SUSPEND_NS
+#define UL_MBAR_SUSPEND_NS 200000
+#endif
+
 namespace ul {
 namespace sm100 {
 
@@ -60,23 +64,107 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Bounded wait: a pipeline bug traps (launch error on the host) instead of
+// try_wait with a suspend-time hint (-DUL_MBAR_SUSPEND_NS=ns; off by default:
+// r28 A/B made the fused backward 2% slower): the waiting thread sleeps until the
+// phase completes (or the hint elapses) instead of re-issuing try_wait in a
+// tight loop.  The spinning producer / MMA-issuer threads otherwise take
+// issue slots from the softmax warps of their SMSP (UL_TRACE per-warp
+// arrivals: softmax warps on the TMA and MMA warps' SMSPs finished ~1000
+// cycles later per sub-tile).
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(UL_MBAR_SUSPEND_NS)
+      : "memory");
+  return ok != 0;
+}
+// Up to 4096 try_wait probes in one PTX loop (try_wait + branch + counter per
+// probe); true once the phase with `parity` has completed.
+__device__ __forceinline__ bool mbar_poll(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .u32 i;\n\t"
+      "mov.u32 i, 0;\n\t"
+      "LAB_POLL:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "@p bra.uni LAB_DONE;\n\t"
+      "add.u32 i, i, 1;\n\t"
+      "setp.lt.u32 q, i, 4096;\n\t"
+      "@q bra.uni LAB_POLL;\n\t"
+      "LAB_DONE:\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+static __device__ __noinline__ void mbar_timeout(uint64_t* bar, uint32_t parity) {
+  printf("ulysses_b200: mbarrier wait timeout block %d thread %d bar@%u parity %u\n", (int)blockIdx.x,
+         (int)threadIdx.x, smem_u32(bar), parity);
+  __trap();
+}
+// Bounded waits: a pipeline bug traps (launch error on the host) instead of
 // hanging the GPU; 4 s is orders of magnitude above any legitimate wait.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  if (mbar_try_wait(bar, parity)) return;
-  uint64_t t0;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  uint32_t spins = 0;
-  while (!mbar_try_wait(bar, parity)) {
-    if ((++spins & 255u) != 0) continue;   // try_wait already suspends; read the timer rarely
-    uint64_t t1;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-    if (t1 - t0 > 4000000000ull) {
-      printf("ulysses_b200: mbarrier wait timeout block %d thread %d bar@%u parity %u\n", (int)blockIdx.x,
-             (int)threadIdx.x, smem_u32(bar), parity);
-      __trap();
+// Waiting warps share their SMSP's issue slots with the softmax warps, so
+// how a wait spins matters (r29-r31 A/B, tools/ab_kernels.py):
+//   kind 0: C++ loop around try_wait (ptxas adds YIELD; timer read inline)
+//   kind 1: tight PTX probe loop, timer read once per 4096 probes
+//   kind 2: try_wait with a suspend-time hint (sleep until the phase flips)
+template <int kKind>
+__device__ __forceinline__ void mbar_wait_k(uint64_t* bar, uint32_t parity) {
+  if (kKind == 0) {   // (the exact loop of r15-r28: its compiled shape measured fastest)
+    if (mbar_try_wait(bar, parity)) return;
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    uint32_t spins = 0;
+    while (!mbar_try_wait(bar, parity)) {
+      if ((++spins & 255u) != 0) continue;
+      uint64_t t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      if (t1 - t0 > 4000000000ull) {
+        printf("ulysses_b200: mbarrier wait timeout block %d thread %d bar@%u parity %u\n", (int)blockIdx.x,
+               (int)threadIdx.x, smem_u32(bar), parity);
+        __trap();
+      }
     }
+    return;
   }
+  if (kKind == 2) {
+    if (mbar_try_wait_sleep(bar, parity)) return;
+  } else if (kKind == 1) {
+    if (mbar_poll(bar, parity)) return;
+  } else {
+    if (mbar_try_wait(bar, parity)) return;
+  }
+  const uint64_t t0 = globaltimer();
+  uint32_t spins = 0;
+  while (true) {
+    if (kKind == 2) {
+      if (mbar_try_wait_sleep(bar, parity)) return;
+    } else if (kKind == 1) {
+      if (mbar_poll(bar, parity)) return;
+    } else {
+      if (mbar_try_wait(bar, parity)) return;
+      if ((++spins & 255u) != 0) continue;
+    }
+    if (globaltimer() - t0 > 4000000000ull) mbar_timeout(bar, parity);
+  }
+}
+#ifndef UL_WAIT_KIND
+#define UL_WAIT_KIND 0
+#endif
+#ifndef UL_WAIT_MMA_KIND
+#define UL_WAIT_MMA_KIND 2   // r32 A/B: MMA issuer sleeping on the barrier -0.5% fwd+bwd; others: kind 0
+#endif
+// every role but the MMA issuer
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar_wait_k<UL_WAIT_KIND>(bar, parity); }
+// the single MMA-issuing thread (the tensor pipe idles while it waits)
+__device__ __forceinline__ void mbar_wait_mma(uint64_t* bar, uint32_t parity) {
+  mbar_wait_k<UL_WAIT_MMA_KIND>(bar, parity);
 }
 
 // ---- TMA ----------------------------------------------------------------------

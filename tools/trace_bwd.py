@@ -113,9 +113,39 @@ def report_fused(tr):
         print(f"   TMA: stage free seen -> q_full at MMA={d(0, 8):.0f}")
 
 
+def timeline_fused(tr, j0=60, span=3):
+    ev = tr[0]
+    t0 = ev[10][j0]
+    names = {10: "MMA top", 0: "MMA q_full seen", 9: "MMA dq_free(j-2) ok -> dP^T(j) issue", 7: "MMA dP^T(j) issued",
+             1: "MMA p_full(j) seen", 6: "MMA grads+dQ^T(j) issued", 2: "w6 s_full seen", 12: "w6 S^T loaded",
+             13: "w6 dS computed", 14: "w6 ds_free ok", 3: "w6 p_full arrive", 5: "w21 p_full arrive",
+             4: "drain dq_full seen", 11: "drain dq_free arrive", 15: "drain reds issued", 8: "TMA stage free"}
+    rows = []
+    for j in range(j0 - 2, j0 + span):
+        for e, nm in names.items():
+            if ev[e][j] > 0:
+                rows.append((ev[e][j] - t0, f"{nm} [{j}]"))
+    print("== timeline fused (cta 0)")
+    for t, nm in sorted(rows):
+        if -2500 < t < 5000:
+            print(f"  {t:6d}  {nm}")
+
+
 lib.ul_attn_set_deterministic(0)
 run(1 | 2)
-report_fused(run(1 | 2))
+tr = run(1 | 2)
+report_fused(tr)
+timeline_fused(tr)
+lib.ul_debug_warp.restype = ctypes.c_int
+lib.ul_debug_warp.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+wb = np.zeros(32 * 256, dtype=np.uint64)
+chk(lib.ul_debug_warp(wb.ctypes.data, wb.nbytes))
+w = wb.reshape(32, 256).astype(np.int64)
+for j in (59, 60, 61):
+    ref = tr[0][10][60]
+    print(f"  arrivals [{j}] (rel. MMA top 60): p_full " +
+          " ".join(f"w{x}:{w[x][j] - ref}" for x in range(6, 22)) + "  dq_free " +
+          " ".join(f"w{x}:{w[x][j] - ref}" for x in range(2, 6)))
 lib.ul_attn_set_deterministic(1)
 for stages, name in ((1 | 2, "dkdv"), (4, "dq")):
     run(stages)  # warm
