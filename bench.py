@@ -267,6 +267,7 @@ def run_ours(args):
                               dtype=torch.float32).to(torch.bfloat16)
     kt = kernel_split(attn, mk4(), mk4(), mk4(), mk4(), args, dev)
     a2a = bench_a2a(dev, n_seq, H, hd, P, group)
+    sparse = bench_blocked(kt_inputs=(mk4, n_seq, H // P, hd), args=args, dev=dev)
 
     # ---- e2e through the public API from pinned host buffers ----------
     e2e = run_e2e(layer, q, k, v, do, args, P, dev)
@@ -314,6 +315,7 @@ def run_ours(args):
             },
             "kernels": kt["kernels"],
             "a2a": a2a,
+            "blocked_sparse_fwd": sparse,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,
@@ -390,6 +392,37 @@ def kernel_split(attn, q, k, v, do, args, dev):
             rec["tflops"] = round(alg[nm] / (ms / 1e3) / 1e12, 1)
         out.append(rec)
     return {"kernels": out}
+
+
+def bench_blocked(kt_inputs, args, dev, bs=128, bandwidth=15):
+    """Blocked-sparse forward (blocked_kernel,
+    kernels.py:55-86) on this rank's head-sharded problem with a banded
+    block pattern (tensor.py:200-206): window of bandwidth+1 blocks of 128.
+    FLOPs counted over visible blocks only (4*hd*bs^2 per visible block pair
+    per head)."""
+    import torch
+    import paper_2309_14509_b200 as U
+    mk, n, h, hd = kt_inputs
+    q, k, v = mk(), mk(), mk()
+    nb = n // bs
+    pattern = frozenset((a, b) for a in range(nb) for b in range(max(0, a - bandwidth), a + 1))
+    attn = U.FlashAttention("blocked", block_size=bs, pattern=pattern)
+    flush = make_flush(dev)
+    times = []
+    for it in range(args.warmup + max(3, min(args.steps, 10))):
+        flush.zero_()
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        attn.forward_with_lse(q, k, v)
+        e.record()
+        if it >= args.warmup:
+            times.append((a, e))
+    torch.cuda.synchronize()
+    ms = statistics.mean(a.elapsed_time(e) for a, e in times)
+    flops = 4.0 * hd * len(pattern) * bs * bs * h
+    return {"pattern": f"banded, block {bs}, bandwidth {bandwidth} ({len(pattern)} of {nb * nb} blocks)",
+            "ms": round(ms, 4), "tokens_per_s": round(n / (ms / 1e3), 1),
+            "tflops_visible": round(flops / (ms / 1e3) / 1e12, 1)}
 
 
 def bench_a2a(dev, n_seq, H, hd, P, group, reps=10):

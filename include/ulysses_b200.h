@@ -138,6 +138,20 @@ int ul_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse
                 int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
                 int dtype, int mask, float scale, void* stream);
 
+/* Blocked-sparse forward (blocked_kernel, kernels.py:55-86; Mask.blocked,
+ * tensor.py:147-180): query block qb sees exactly the key blocks kb whose
+ * bit is set in pattern_bits[qb * words_per_row + kb / 32] (DEVICE memory,
+ * n / block_size rows); within a visible block every key is visible (no
+ * causal cut).  The caller validates the pattern against the reference's
+ * rules (no empty query block -> DegenerateRowError, blocks in range);
+ * block_size must divide n (UL_ERR_DIVISIBILITY).  Forward only, like the
+ * reference (masked_attention_backward supports dense/causal only).
+ * bf16: hd in {64, 128}, n <= 1M; fp32: SIMT. */
+int ul_attn_fwd_blocked(const void* q, const void* k, const void* v, void* o, float* lse,
+                        int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype,
+                        int64_t block_size, const uint32_t* pattern_bits, int64_t words_per_row,
+                        float scale, void* stream);
+
 /* dq [n,b,hq,hd], dk/dv [n,b,hkv,hd] (dk/dv summed over each kv head's
  * query group).  workspace >= ul_attn_bwd_workspace_bytes(...). */
 size_t ul_attn_bwd_workspace_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,

@@ -9,6 +9,7 @@ them.  Every vector is produced by the reference's own functions:
   * ``seq_to_head`` / ``head_to_seq``               ulysses.py:104-124
   * ``get_kernel`` (dense/causal)                   kernels.py:43-52,124-128
   * ``masked_attention_backward``                   kernels.py:89-111
+  * ``blocked_kernel`` + ``Mask.blocked`` patterns   kernels.py:55-86, tensor.py:147-206
 
 with the loop structure of ``ulysses_attention_forward_with_state``
 (ulysses.py:144-154) and ``ulysses_attention_backward`` (ulysses.py:
@@ -183,6 +184,67 @@ def gen_config1():
     print("config1.npz", len(out), "arrays")
 
 
+def gen_blocked():
+    """Blocked-sparse forward through the Ulysses core with the reference's
+    ``blocked_kernel`` (kernels.py:55-86) and ``Mask.blocked`` patterns from
+    tensor.py:183-206 (plus one irregular pattern)."""
+    K, L, G, T, U = _ref()
+    out = {}
+    rng = np.random.default_rng([2024, 7])
+    cases = [
+        (2, 64, 1, 4, 16, 8, "causal"),
+        (1, 48, 2, 2, 32, 16, "banded"),
+        (2, 128, 1, 2, 64, 32, "irregular"),
+        (1, 256, 1, 2, 128, 64, "full"),
+    ]
+    for ci, (p, n, b, h, hd, bs, kind) in enumerate(cases):
+        nb = n // bs
+        if kind == "causal":
+            pattern = T.causal_block_pattern(n, bs)
+        elif kind == "banded":
+            pattern = T.banded_block_pattern(n, bs, bandwidth=1)
+        elif kind == "full":
+            pattern = T.full_block_pattern(n, bs)
+        else:   # every query block sees itself plus a random subset
+            pattern = frozenset({(qb, qb) for qb in range(nb)} |
+                                {(qb, kb) for qb in range(nb) for kb in range(nb) if rng.random() < 0.3})
+        seed = 5000 + ci
+        d = h * hd
+        mask = T.Mask.blocked(bs, pattern)
+        spec = L.AttentionSpec(n=n, b=b, d=d, h_heads=h, mask=mask)
+        kernel = K.get_kernel("blocked")
+        q = make_tensor((n, b, h, hd), seed, 1)
+        k = make_tensor((n, b, h, hd), seed, 2)
+        v = make_tensor((n, b, h, hd), seed, 3)
+        nl = n // p
+
+        def shard(x, r):
+            return U.ShardedTensor(rank=r, layout=U.SEQUENCE,
+                                   data=T.Tensor3(x[r * nl:(r + 1) * nl].reshape(nl, b, d)))
+
+        def program(ctx):
+            r = ctx.rank
+            q4 = U.seq_to_head(shard(q, r), spec, ctx, "attn.q.seq2head").data.data
+            k4 = U.seq_to_head(shard(k, r), spec, ctx, "attn.k.seq2head").data.data
+            v4 = U.seq_to_head(shard(v, r), spec, ctx, "attn.v.seq2head").data.data
+            ctx4 = np.empty_like(q4)
+            for hh in range(q4.shape[2]):                              # ulysses.py:149-152
+                ctx4[:, :, hh, :] = kernel(q4[:, :, hh, :], k4[:, :, hh, :], v4[:, :, hh, :],
+                                           spec.mask, spec.scale)
+            return U.head_to_seq(U.ShardedTensor(rank=r, layout=U.HEAD, data=T.Tensor4(ctx4)),
+                                 spec, ctx, "attn.ctx.head2seq").data.data
+
+        results, _ = G.run_group(p, program, mode="concurrent")
+        o = np.concatenate([np.asarray(x).reshape(nl, b, h, hd) for x in results], 0)
+        out[f"case{ci}_meta"] = np.array([p, n, b, h, hd, bs, seed])
+        out[f"case{ci}_pattern"] = np.array(sorted(pattern), dtype=np.int64)
+        for name, arr in (("q", q), ("k", k), ("v", v)):
+            out[f"case{ci}_{name}"] = arr.astype(np.float32)
+        out[f"case{ci}_o"] = o
+    np.savez_compressed(os.path.join(GOLDEN, "blocked.npz"), **out)
+    print("blocked.npz", len(out), "arrays")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--config1", action="store_true")
@@ -190,5 +252,6 @@ if __name__ == "__main__":
     os.makedirs(GOLDEN, exist_ok=True)
     gen_a2a()
     gen_attn_small()
+    gen_blocked()
     if args.config1:
         gen_config1()

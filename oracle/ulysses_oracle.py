@@ -293,6 +293,126 @@ def local_lse(q4, k4, kind, scale=None, exact=False):
 
 
 # ---------------------------------------------------------------------------
+# L2b: blocked-sparse local attention
+# ---------------------------------------------------------------------------
+
+def causal_block_pattern(n: int, block_size: int) -> frozenset:
+    """tensor.py:183-189: (qb, kb) for all kb <= qb."""
+    if n % block_size != 0:
+        raise DivisibilityError(f"block_size {block_size} does not divide n={n}")
+    nb = n // block_size
+    return frozenset((q, k) for q in range(nb) for k in range(q + 1))
+
+
+def full_block_pattern(n: int, block_size: int) -> frozenset:
+    """tensor.py:192-197: every (qb, kb) pair."""
+    if n % block_size != 0:
+        raise DivisibilityError(f"block_size {block_size} does not divide n={n}")
+    nb = n // block_size
+    return frozenset((q, k) for q in range(nb) for k in range(nb))
+
+
+def banded_block_pattern(n: int, block_size: int, bandwidth: int = 1) -> frozenset:
+    """tensor.py:200-206: causal local window, kb in [qb - bandwidth, qb]."""
+    if n % block_size != 0:
+        raise DivisibilityError(f"block_size {block_size} does not divide n={n}")
+    nb = n // block_size
+    return frozenset((q, k) for q in range(nb) for k in range(max(0, q - bandwidth), q + 1))
+
+
+def blocked_visibility(block_size: int, pattern, rows: int, cols: int, row_offset: int = 0) -> np.ndarray:
+    """Mask.visibility for kind 'blocked' (tensor.py:163-180)."""
+    bs = block_size
+    if cols % bs != 0:
+        raise DivisibilityError(f"block_size {bs} does not divide key length {cols}")
+    if rows % bs != 0 or row_offset % bs != 0:
+        raise DivisibilityError(f"block_size {bs} does not align with {rows} rows at offset {row_offset}")
+    nkb = cols // bs
+    bad = sorted(kb for _, kb in pattern if kb >= nkb)
+    if bad:
+        raise ValueError(f"pattern key blocks {bad[:4]} out of range for {nkb} key blocks")
+    qblk = np.arange(row_offset, row_offset + rows) // bs
+    kblk = np.arange(cols) // bs
+    vis = np.zeros((rows, cols), dtype=bool)
+    for qb, kb in pattern:
+        vis |= (qblk[:, None] == qb) & (kblk[None, :] == kb)
+    return vis
+
+
+def check_block_pattern(n: int, block_size: int, pattern) -> dict:
+    """The argument checks of blocked_kernel (kernels.py:63-80), in its
+    order; returns {qb: sorted visible kb}."""
+    if n % block_size != 0:
+        raise DivisibilityError(f"block_size {block_size} does not divide sequence length {n}")
+    nblocks = n // block_size
+    bad = sorted((qb, kb) for qb, kb in pattern if qb >= nblocks or kb >= nblocks)
+    if bad:
+        raise ValueError(f"pattern blocks {bad[:4]} out of range for {nblocks} blocks")
+    visible = {qb: sorted(kb for qb2, kb in pattern if qb2 == qb) for qb in range(nblocks)}
+    for qb in range(nblocks):
+        if not visible[qb]:
+            raise DegenerateRowError(f"query block {qb} has no visible key blocks (invalid sparse pattern)")
+    return visible
+
+
+def blocked_attention_head(q, k, v, block_size: int, pattern, scale: float, exact: bool = True):
+    """blocked_kernel (kernels.py:55-86) on (n, b, hd) views: per query
+    block, scores against the concatenated visible key blocks (ascending
+    kb), unmasked row_softmax, ctx = probs v.  Also returns the row LSE over
+    the same scores (RESTATEMENT, no reference counterpart).
+    Returns (ctx (n, b, hd), lse (b, n))."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    n, b, hd = q.shape
+    bs = block_size
+    visible = check_block_pattern(n, bs, pattern)
+    ctx = np.empty((n, b, hd))
+    lse = np.empty((b, n))
+    for bi in range(b):
+        for qb, kbs in visible.items():
+            rows = slice(qb * bs, (qb + 1) * bs)
+            kcat = np.concatenate([k[kb * bs:(kb + 1) * bs, bi, :] for kb in kbs], axis=0)
+            vcat = np.concatenate([v[kb * bs:(kb + 1) * bs, bi, :] for kb in kbs], axis=0)
+            scores = matmul(q[rows, bi, :], kcat.T, exact) * scale
+            ctx[rows, bi, :] = matmul(row_softmax(scores, "none"), vcat, exact)
+            lse[bi, rows] = row_lse(scores, "none")
+    return ctx, lse
+
+
+def local_attention_blocked(q4, k4, v4, block_size: int, pattern, scale: float | None = None,
+                            exact: bool = True):
+    """Head loop of ulysses.py:148-152 with the blocked kernel (GQA
+    restatement as in local_attention).  Returns (ctx4, lse (b, Hq, n))."""
+    q4 = np.asarray(q4)
+    n, b, hq, hd = q4.shape
+    hkv = np.asarray(k4).shape[2]
+    if scale is None:
+        scale = 1.0 / math.sqrt(hd)
+    ctx4 = np.empty((n, b, hq, hd))
+    lse = np.empty((b, hq, n))
+    for hh in range(hq):
+        g = kv_head_for(hh, hq, hkv)
+        c, l = blocked_attention_head(q4[:, :, hh, :], k4[:, :, g, :], v4[:, :, g, :], block_size, pattern,
+                                      scale, exact)
+        ctx4[:, :, hh, :] = c
+        lse[:, hh, :] = l
+    return ctx4, lse
+
+
+def pattern_bits(n: int, block_size: int, pattern) -> np.ndarray:
+    """Device encoding of a block pattern (include/ulysses_b200.h,
+    ul_attn_fwd_blocked): uint32 rows of ceil(nb/32) words, bit kb % 32 of
+    word kb / 32 in row qb set iff (qb, kb) is in the pattern."""
+    nb = n // block_size
+    words = (nb + 31) // 32
+    bits = np.zeros((nb, words), dtype=np.uint32)
+    for qb, kb in pattern:
+        bits[qb, kb // 32] |= np.uint32(1 << (kb % 32))
+    return bits
+
+
+# ---------------------------------------------------------------------------
 # L3: the DistributedAttention core across P simulated ranks
 # ---------------------------------------------------------------------------
 

@@ -36,7 +36,7 @@ import torch
 
 from . import _lib
 from .comm import SequenceGroup
-from .errors import DivisibilityError, ForwardStateError, KernelError
+from .errors import DegenerateRowError, DivisibilityError, ForwardStateError, KernelError
 
 _ATTN_DTYPES = {torch.float32: _lib.DTYPE_F32, torch.bfloat16: _lib.DTYPE_BF16}
 
@@ -99,16 +99,58 @@ class FlashAttention:
     gradients are bitwise reproducible and bitwise P-invariant.
     """
 
-    def __init__(self, mask: str = "causal", scale: float | None = None, deterministic: bool = False):
-        if mask not in ("causal", "none"):
-            raise KernelError(f"kernel supports dense/causal masks only, got {mask!r}")
+    def __init__(self, mask: str = "causal", scale: float | None = None, deterministic: bool = False,
+                 block_size: int | None = None, pattern=None):
+        if mask not in ("causal", "none", "blocked"):
+            raise KernelError(f"kernel supports dense/causal/blocked masks only, got {mask!r}")
         self.mask = mask
         self.scale = scale
         self.deterministic = bool(deterministic)
+        if mask == "blocked":
+            # Mask.blocked(block_size, pattern) (tensor.py:147-149) + blocked_kernel
+            # (kernels.py:55-86): query block qb sees the key blocks kb with
+            # (qb, kb) in pattern, every key inside a visible block
+            if block_size is None or pattern is None:
+                raise KernelError("blocked kernel needs block_size and pattern")
+            self.block_size = int(block_size)
+            self.pattern = frozenset((int(a), int(b)) for a, b in pattern)
+            self._bits = {}
+        elif block_size is not None or pattern is not None:
+            raise KernelError(f"block_size/pattern apply to the blocked kernel, not {mask!r}")
 
     @property
     def mask_code(self) -> int:
-        return _lib.MASK_CAUSAL if self.mask == "causal" else _lib.MASK_NONE
+        return {"causal": _lib.MASK_CAUSAL, "none": _lib.MASK_NONE, "blocked": _lib.MASK_BLOCKED}[self.mask]
+
+    def _pattern_bits(self, n: int, device) -> torch.Tensor:
+        """Validate the pattern for sequence length n with blocked_kernel's
+        rules and order (kernels.py:63-80) and return its device bitmap
+        (uint32 rows of ceil(nb/32) words, include/ulysses_b200.h)."""
+        key = (n, str(device))
+        if key in self._bits:
+            return self._bits[key]
+        bs = self.block_size
+        if bs < 1 or n % bs != 0:
+            raise DivisibilityError(f"block_size {bs} does not divide sequence length {n}")
+        nb = n // bs
+        bad = sorted((qb, kb) for qb, kb in self.pattern if not (0 <= qb < nb and 0 <= kb < nb))
+        if bad:
+            raise ValueError(f"pattern blocks {bad[:4]} out of range for {nb} blocks")
+        seen = {qb for qb, _ in self.pattern}
+        empty = [qb for qb in range(nb) if qb not in seen]
+        if empty:
+            raise DegenerateRowError(f"query block {empty[0]} has no visible key blocks (invalid sparse pattern)")
+        words = (nb + 31) // 32
+        bits = [0] * (nb * words)
+        for qb, kb in self.pattern:
+            bits[qb * words + kb // 32] |= 1 << (kb % 32)
+        host = torch.tensor(bits, dtype=torch.int64).to(torch.int32).pin_memory()   # (bit 31 wraps: same bits)
+        # stream-ordered, non-blocking: under an in-process group this rank's
+        # stream may still be waiting for its peers' pushes, and a blocking
+        # copy would stall the host thread that has yet to issue them
+        t = host.to(device, non_blocking=True)
+        self._bits[key] = (t, words, host)
+        return self._bits[key]
 
     def _check(self, q, k, v):
         if q.dim() != 4 or k.dim() != 4 or v.dim() != 4:
@@ -134,12 +176,24 @@ class FlashAttention:
         q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
         o = torch.empty_like(q)
         lse = torch.empty((b, hq, n), dtype=torch.float32, device=q.device)
+        if self.mask == "blocked":
+            bits, words, _ = self._pattern_bits(n, q.device)
+            _lib.check(_lib.lib().ul_attn_fwd_blocked(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
+                                                      lse.data_ptr(), n, b, hq, hkv, hd, _ATTN_DTYPES[q.dtype],
+                                                      self.block_size, bits.data_ptr(), words, self._scale(hd),
+                                                      _stream(q)))
+            return o, lse
         _lib.check(_lib.lib().ul_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                           lse.data_ptr(), n, b, hq, hkv, hd, _ATTN_DTYPES[q.dtype],
                                           self.mask_code, self._scale(hd), _stream(q)))
         return o, lse
 
+    def _backward_mask_check(self):
+        if self.mask == "blocked":   # kernels.py:95-96
+            raise KernelError("backward supports dense/causal masks only, got 'blocked'")
+
     def backward(self, q, k, v, o, lse, do):
+        self._backward_mask_check()
         if lse is None:
             raise ForwardStateError("backward needs the state saved by the forward pass")
         n, b, hq, hkv, hd = self._check(q, k, v)
@@ -166,6 +220,10 @@ class FlashAttention:
         exchange of O fused into the kernel epilogue.  Returns (o_head, lse,
         o_seq) with o_seq = seq layout [N/P, b, P*h, hd] of this rank."""
         from .comm import label_hash
+        if self.mask == "blocked":   # (no fused epilogue for the blocked kernel: two steps)
+            o, lse = self.forward_with_lse(q, k, v)
+            (o_seq,) = group.all_to_all([o], 0, 2, label=label)
+            return o, lse, o_seq
         n, b, hq, hkv, hd = self._check(q, k, v)
         q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
         p = group.world
@@ -185,6 +243,7 @@ class FlashAttention:
         epilogues.  Returns sequence-layout (dq, dk, dv) of this rank (and
         the head-layout gradients the kernels also wrote, if return_head)."""
         from .comm import label_hash
+        self._backward_mask_check()
         if lse is None:
             raise ForwardStateError("backward needs the state saved by the forward pass")
         n, b, hq, hkv, hd = self._check(q, k, v)
@@ -229,15 +288,30 @@ class _LocalAttnFn(torch.autograd.Function):
         return None, dq, dk, dv
 
 
-KERNELS = {"dense": FlashAttention("none"), "causal": FlashAttention("causal")}
+def _blocked_kernel(block_size: int, pattern) -> FlashAttention:
+    return FlashAttention("blocked", block_size=block_size, pattern=pattern)
 
 
-def get_kernel(name: str) -> FlashAttention:
+# kernels.py:114-128.  The reference's kernels take the mask per call; here the
+# mask is part of the plugin, so "blocked" maps to a factory taking
+# (block_size, pattern) -- get_kernel("blocked", block_size=..., pattern=...).
+KERNELS = {"dense": FlashAttention("none"), "causal": FlashAttention("causal"), "blocked": _blocked_kernel}
+
+
+def get_kernel(name: str, **mask_args):
     """kernels.py:124-128."""
     try:
-        return KERNELS[name]
+        k = KERNELS[name]
     except KeyError:
         raise KernelError(f"unknown kernel {name!r}, expected one of {sorted(KERNELS)}") from None
+    if name == "blocked":
+        if not mask_args:
+            raise KernelError("the blocked kernel needs block_size and pattern: "
+                              "get_kernel('blocked', block_size=bs, pattern=pairs)")
+        return k(**mask_args)
+    if mask_args:
+        raise KernelError(f"kernel {name!r} takes no mask arguments")
+    return k
 
 
 # ---------------------------------------------------------------------------

@@ -62,6 +62,7 @@ constexpr int NS = 2;               // K/V pipeline stages
 constexpr int kThreads = 320;       // TMA, MMA, 2 x 4 softmax warps
 constexpr float kLazy = 8.0f;       // log2 headroom before O is rescaled
 constexpr int kAtom = 128 * 128;    // SW128 atom column of a 128-row tile
+constexpr int kMaxTiles = 8192;     // kv tiles per head in blocked-sparse mode (n <= 1M)
 
 template <int HD>
 struct Smem {
@@ -70,7 +71,8 @@ struct Smem {
   static constexpr int kK = kQ + 2 * kTile;       // [NS]
   static constexpr int kV = kK + NS * kTile;      // [NS]
   static constexpr int kBar = kV + NS * kTile;
-  static constexpr int kBytes = kBar + 256 + 1024;
+  static constexpr int kList = kBar + 256;               // blocked-sparse: the CTA's kv tile list
+  static constexpr int kBytes = kList + kMaxTiles * 2 + 1024;
 };
 
 struct Params {
@@ -82,7 +84,42 @@ struct Params {
   __nv_bfloat16* o;
   float* lse;
   PeerEpilogue ep;   // active: also store O rows into the seq layout of their rank (fused head->seq)
+  // blocked-sparse mask (Mask.blocked, tensor.py:163-180; blocked_kernel,
+  // kernels.py:55-86): bit (qb, kb) of blk[qb * blk_words + kb / 32] says
+  // whether query block qb sees key block kb (blocks of blk_bs tokens,
+  // blk_nb = n / blk_bs per side).  nullptr: dense / causal.
+  const uint32_t* blk;
+  int blk_bs, blk_words, blk_nb;
 };
+
+__device__ __forceinline__ bool blk_bit(const Params& p, int qb, int kb) {
+  return (__ldg(p.blk + (int64_t)qb * p.blk_words + (kb >> 5)) >> (kb & 31)) & 1u;
+}
+// does any query row in [qlo, qhi] see any key of kv tile kt?
+__device__ __forceinline__ bool blk_tile_needed(const Params& p, int qlo, int qhi, int kt) {
+  const int kb0 = kt * BN / p.blk_bs, kb1 = min(p.blk_nb - 1, (kt * BN + BN - 1) / p.blk_bs);
+  const int qb0 = qlo / p.blk_bs, qb1 = min(p.blk_nb - 1, qhi / p.blk_bs);
+  for (int qb = qb0; qb <= qb1; ++qb)
+    for (int kb = kb0; kb <= kb1; ++kb)
+      if (blk_bit(p, qb, kb)) return true;
+  return false;
+}
+// visible-column bitmask of one query row over kv tile columns [kv0, kv0 + 128)
+__device__ __forceinline__ void blk_row_mask(const Params& p, int qrow, int kv0, uint32_t cm[4]) {
+  cm[0] = cm[1] = cm[2] = cm[3] = 0u;
+  if (qrow >= p.n) return;
+  const int qb = qrow / p.blk_bs;
+  const int kb0 = kv0 / p.blk_bs, kb1 = min(p.blk_nb - 1, (kv0 + BN - 1) / p.blk_bs);
+  for (int kb = kb0; kb <= kb1; ++kb) {
+    if (!blk_bit(p, qb, kb)) continue;
+    const int lo = max(kb * p.blk_bs, kv0) - kv0, hi = min((kb + 1) * p.blk_bs, kv0 + BN) - kv0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int a = max(lo, 32 * w), e = min(hi, 32 * w + 32);
+      if (a < e) cm[w] |= (e - a == 32 ? 0xffffffffu : ((1u << (e - a)) - 1u)) << (a - 32 * w);
+    }
+  }
+}
 
 // P = 2^(S*scale_log2 - mu) for 32 columns, packed to bf16 pairs, row sums
 // accumulated into 8 partials.  kPoly routes one element pair in four to
@@ -143,11 +180,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int bb = bh / p.hq, h = bh % p.hq;
   const int g = h / (p.hq / p.hkv);
   const int nkv_all = (p.n + BN - 1) / BN;
+  uint16_t* tiles = reinterpret_cast<uint16_t*>(smem + S::kList);
+  const bool blocked = p.blk != nullptr;
+  int nblk = 0;   // blocked-sparse: kv tiles any row of this CTA's query tiles sees, ascending
+  if (blocked) {
+    const int qlo = 2 * pair * BM, qhi = min(p.n, (2 * pair + 2) * BM) - 1;
+    if (warp == 0) {
+      for (int base = 0; base < nkv_all; base += 32) {
+        const bool need = base + lane < nkv_all && blk_tile_needed(p, qlo, qhi, base + lane);
+        const uint32_t bal = __ballot_sync(0xffffffffu, need);
+        if (need) tiles[nblk + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)(base + lane);
+        nblk += __popc(bal);
+      }
+    } else {
+      for (int base = 0; base < nkv_all; base += 32)
+        nblk += __popc(__ballot_sync(0xffffffffu, base + lane < nkv_all && blk_tile_needed(p, qlo, qhi, base + lane)));
+    }
+  }
   int nkvT[2];
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
     const int qt = 2 * pair + t;
-    nkvT[t] = qt >= p.qtiles ? 0 : (p.causal ? min(nkv_all, (qt * BM + BM - 1) / BN + 1) : nkv_all);
+    nkvT[t] = qt >= p.qtiles ? 0 : blocked ? nblk : (p.causal ? min(nkv_all, (qt * BM + BM - 1) / BN + 1) : nkv_all);
   }
   const int nkv = max(nkvT[0], nkvT[1]);
   const int ntiles = nkvT[1] > 0 ? 2 : 1;
@@ -199,13 +253,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(&k_full[s], BN * HD * 2);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a)
-          tma_load_3d(sK + s * S::kTile + a * kAtom, &tmK, &k_full[s], a * 64, bb * p.hkv + g, j * BN);
+          tma_load_3d(sK + s * S::kTile + a * kAtom, &tmK, &k_full[s], a * 64, bb * p.hkv + g,
+                      (blocked ? tiles[j] : j) * BN);
         mbar_wait(&v_empty[s], ph ^ 1);
         UL_EV(9, j);
         mbar_expect_tx(&v_full[s], BN * HD * 2);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a)
-          tma_load_3d(sV + s * S::kTile + a * kAtom, &tmV, &v_full[s], a * 64, bb * p.hkv + g, j * BN);
+          tma_load_3d(sV + s * S::kTile + a * kAtom, &tmV, &v_full[s], a * 64, bb * p.hkv + g,
+                      (blocked ? tiles[j] : j) * BN);
       }
     }
   } else if (warp == 1) {
@@ -277,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int my_nkv = t ? nkvT[1] : nkvT[0];   // (no dynamic index into a local array)
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < my_nkv; ++j) {
-      const int kv0 = j * BN;
+      const int kv0 = (blocked ? tiles[j] : j) * BN;
       mbar_wait(&s_full[t], j & 1);
       if (lane == 0 && (warp == 2 || warp == 6)) UL_EV(warp == 2 ? 3 : 5, j);
       tc_fence_after();
@@ -287,7 +343,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_wait_ld();
       if (lane == 0 && warp == 2) UL_EV(12, j);
       const bool masked = (p.causal && kv0 + BN - 1 > q0) || kv0 + BN > p.n;
-      if (masked) {
+      if (blocked) {
+        uint32_t cm[4];
+        blk_row_mask(p, qrow, kv0, cm);
+#pragma unroll
+        for (int c = 0; c < BN; ++c)
+          if (!((cm[c >> 5] >> (c & 31)) & 1u)) r[c] = __float_as_uint(-INFINITY);
+      } else if (masked) {
         int limit = p.n - kv0;
         if (p.causal) limit = min(limit, qrow - kv0 + 1);
 #pragma unroll
@@ -420,7 +482,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int HD>
 static int launch(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
-                  int64_t hq, int64_t hkv, int causal, float scale, const PeerEpilogue* ep, cudaStream_t st) {
+                  int64_t hq, int64_t hkv, int causal, float scale, const PeerEpilogue* ep, cudaStream_t st,
+                  const uint32_t* blk, int64_t blk_bs, int64_t blk_words) {
   CUtensorMap mq, mk, mv;
   UL_TRY(make_tmap_bhsd(&mq, q, n, b * hq, HD, 128));
   UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, 128));
@@ -439,6 +502,11 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
   p.lse = lse;
   if (ep) p.ep = *ep;
   else memset(&p.ep, 0, sizeof(p.ep));
+  p.blk = blk;
+  p.blk_bs = (int)blk_bs;
+  p.blk_words = (int)blk_words;
+  p.blk_nb = blk ? (int)(n / blk_bs) : 0;
+  if (blk) p.causal = 0;
   const int smem = Smem<HD>::kBytes;
   static bool attr = false;
   if (!attr) {
@@ -475,10 +543,15 @@ int preload_fwd() {
 }
 
 int sm100_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b, int64_t hq,
-               int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st, const PeerEpilogue* ep) {
+               int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st, const PeerEpilogue* ep,
+               const uint32_t* blk, int64_t blk_bs, int64_t blk_words) {
+  if (blk && (n + fwd::BN - 1) / fwd::BN > fwd::kMaxTiles)
+    return fail(UL_ERR_SHAPE, "blocked-sparse attention supports n <= %d, got %lld", fwd::kMaxTiles * fwd::BN,
+                (long long)n);
   switch (hd) {
-    case 64: return fwd::launch<64>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, ep, st);
-    case 128: return fwd::launch<128>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, ep, st);
+    case 64: return fwd::launch<64>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, ep, st, blk, blk_bs, blk_words);
+    case 128:
+      return fwd::launch<128>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, ep, st, blk, blk_bs, blk_words);
     default:
       return fail(UL_ERR_KERNEL, "bf16 attention supports head_dim 64 or 128, got %lld", (long long)hd);
   }

@@ -42,6 +42,10 @@ struct Dims {
   int64_t n, b, hq, hkv, hd;
   int causal;
   float scale;
+  // blocked-sparse forward (Mask.blocked, tensor.py:163-180): bit (qb, kb)
+  // of blk[qb * blk_words + kb / 32]; nullptr for dense / causal
+  const uint32_t* blk = nullptr;
+  int64_t blk_bs = 0, blk_words = 0;
 };
 
 // row pointers: x[(row*b + bb)*h + head][hd]
@@ -85,13 +89,19 @@ __global__ void __launch_bounds__(kWarps * 32) fwd_kernel(const float* __restric
   const int64_t kvstride = D.b * D.hkv * hd;
   const float* kbase = k + rowoff(0, bb, g, D.b, D.hkv, hd);
   const float* vbase = v + rowoff(0, bb, g, D.b, D.hkv, hd);
+  const uint32_t* brow = D.blk ? D.blk + (i / D.blk_bs) * D.blk_words : nullptr;
   for (int64_t j0 = 0; j0 < jmax; j0 += 32) {
     const int64_t j = j0 + lane;
+    bool vis = j < jmax;
+    if (vis && brow) {
+      const int64_t kb = j / D.blk_bs;
+      vis = (__ldg(brow + (kb >> 5)) >> (kb & 31)) & 1u;
+    }
     double s = -INFINITY;
-    if (j < jmax) s = dot_row(qs, kbase + j * kvstride, hd) * (double)D.scale;
+    if (vis) s = dot_row(qs, kbase + j * kvstride, hd) * (double)D.scale;
     const double cmax = warp_max(s);
     const double mnew = fmax(m, cmax);
-    const double p = (j < jmax) ? exp(s - mnew) : 0.0;
+    const double p = vis ? exp(s - mnew) : 0.0;
     const double alpha = (m == -INFINITY) ? 0.0 : exp(m - mnew);
     l = l * alpha + warp_sum(p);
     m = mnew;
@@ -279,8 +289,9 @@ static unsigned blocks_for(int64_t warps) { return (unsigned)((warps + kWarps - 
 int preload_simt() { return simt::preload(); }
 
 int simt_fwd(const float* q, const float* k, const float* v, float* o, float* lse, int64_t n, int64_t b,
-             int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st) {
-  simt::Dims D{n, b, hq, hkv, hd, causal, scale};
+             int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st, const uint32_t* blk,
+             int64_t blk_bs, int64_t blk_words) {
+  simt::Dims D{n, b, hq, hkv, hd, blk ? 0 : causal, scale, blk, blk_bs, blk_words};
   const int64_t rows = n * b * hq;
   if (rows == 0) return UL_OK;
   simt::fwd_kernel<<<simt::blocks_for(rows), simt::kWarps * 32, simt::kWarps * hd * sizeof(float), st>>>(

@@ -25,13 +25,15 @@ static std::atomic<uint64_t> g_total_launches{0};
 void count_launch() { g_total_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int simt_fwd(const float* q, const float* k, const float* v, float* o, float* lse, int64_t n, int64_t b,
-             int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st);
+             int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st,
+             const uint32_t* blk = nullptr, int64_t blk_bs = 0, int64_t blk_words = 0);
 int simt_bwd(const float* q, const float* k, const float* v, const float* o, const float* dout,
              const float* lse, float* dq, float* dk, float* dv, float* Dws, int64_t n, int64_t b, int64_t hq,
              int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st);
 int sm100_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
               int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st,
-              const PeerEpilogue* ep = nullptr);
+              const PeerEpilogue* ep = nullptr, const uint32_t* blk = nullptr, int64_t blk_bs = 0,
+              int64_t blk_words = 0);
 int sm100_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
               void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n, int64_t b, int64_t hq,
               int64_t hkv, int64_t hd, int causal, float scale, int stages, cudaStream_t st,
@@ -99,6 +101,31 @@ int ul_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse
   if (n * b * hq == 0) return UL_OK;
   if (n > INT32_MAX / 2) return fail(UL_ERR_SHAPE, "attention: sequence too long (n=%lld)", (long long)n);
   return sm100_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, causal, scale, st);
+}
+
+int ul_attn_fwd_blocked(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
+                        int64_t hq, int64_t hkv, int64_t hd, int dtype, int64_t block_size,
+                        const uint32_t* pattern_bits, int64_t words_per_row, float scale, void* stream) {
+  launch_count() = 0;
+  UL_TRY(check_attn(n, b, hq, hkv, hd, dtype, UL_MASK_NONE));
+  if (block_size < 1) return fail(UL_ERR_ARG, "block_size must be >= 1, got %lld", (long long)block_size);
+  if (n % block_size != 0)   // kernels.py:69-70
+    return fail(UL_ERR_DIVISIBILITY, "block_size %lld does not divide sequence length %lld", (long long)block_size,
+                (long long)n);
+  const int64_t nb = n / block_size;
+  if (words_per_row < (nb + 31) / 32)
+    return fail(UL_ERR_ARG, "pattern rows of %lld words cannot hold %lld key blocks", (long long)words_per_row,
+                (long long)nb);
+  if (n * b * hq == 0) return UL_OK;
+  if (!q || !k || !v || !o || !lse || !pattern_bits) return fail(UL_ERR_ARG, "ul_attn_fwd_blocked: NULL tensor");
+  if (!(scale > 0.f) || !std::isfinite(scale)) return fail(UL_ERR_ARG, "scale must be finite and > 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == UL_DTYPE_F32)
+    return simt_fwd((const float*)q, (const float*)k, (const float*)v, (float*)o, lse, n, b, hq, hkv, hd, 0, scale,
+                    st, pattern_bits, block_size, words_per_row);
+  if (n > INT32_MAX / 2) return fail(UL_ERR_SHAPE, "attention: sequence too long (n=%lld)", (long long)n);
+  return sm100_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, 0, scale, st, nullptr, pattern_bits, block_size,
+                   words_per_row);
 }
 
 size_t ul_attn_bwd_workspace_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype) {
