@@ -245,6 +245,41 @@ def gen_blocked():
     print("blocked.npz", len(out), "arrays")
 
 
+def gen_layer():
+    """The full attention layer with projections (run_ulysses_attention_backward,
+    ulysses.py:281-307) and a 2-block stack (run_ulysses_blocks, ulysses.py:
+    264-278) from the reference, fp64, seeded inputs and weights."""
+    K, L, G, T, U = _ref()
+    out = {}
+    for ci, (p, n, b, d, h, kind, seed) in enumerate([
+        (2, 32, 1, 64, 4, "causal", 11),
+        (1, 24, 2, 48, 3, "none", 12),
+        (4, 32, 1, 64, 4, "causal", 13),
+    ]):
+        mask = T.Mask.causal() if kind == "causal" else T.Mask.none()
+        spec = L.AttentionSpec(n=n, b=b, d=d, h_heads=h, mask=mask)
+        kname = "causal" if kind == "causal" else "dense"
+        w = L.make_weights(d, seed)
+        x = L.make_input(n, b, d, seed)
+        gout = L.make_input(n, b, d, seed + 1000)
+        o, gx, gw, _ = U.run_ulysses_attention_backward(x, gout, w, spec, kname, p)
+        out[f"case{ci}_meta"] = np.array([p, n, b, d, h, 1 if kind == "causal" else 0, seed])
+        out[f"case{ci}_out"] = np.asarray(o.data)
+        out[f"case{ci}_gx"] = np.asarray(gx.data)
+        for key in ("wq", "wk", "wv", "wo"):
+            out[f"case{ci}_g{key}"] = gw[key]
+    # two blocks, P = 2
+    p, n, b, d, h, seed = 2, 32, 1, 64, 4, 21
+    spec = L.AttentionSpec(n=n, b=b, d=d, h_heads=h, mask=T.Mask.causal())
+    ws = [L.make_weights(d, seed, layer=i) for i in range(2)]
+    x = L.make_input(n, b, d, seed)
+    y, _ = U.run_ulysses_blocks(x, ws, spec, "causal", p)
+    out["blocks_meta"] = np.array([p, n, b, d, h, 2, seed])
+    out["blocks_out"] = np.asarray(y.data)
+    np.savez_compressed(os.path.join(GOLDEN, "layer.npz"), **out)
+    print("layer.npz", len(out), "arrays")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--config1", action="store_true")
@@ -253,5 +288,6 @@ if __name__ == "__main__":
     gen_a2a()
     gen_attn_small()
     gen_blocked()
+    gen_layer()
     if args.config1:
         gen_config1()

@@ -465,6 +465,117 @@ def ulysses_backward(dout_loc, state, kind: str, scale: float | None = None,
 
 
 # ---------------------------------------------------------------------------
+# L4: the attention layer with its projections, and the transformer block
+# (ulysses.py:135-157, 172-184, 188-245)
+# ---------------------------------------------------------------------------
+
+LN_EPS = 1e-5           # layers.py:22
+MLP_EXPANSION = 4       # layers.py:23
+
+
+def make_weights(d: int, seed: int, layer: int = 0) -> dict:
+    """layers.py:83-99: one layer's replicated weights from
+    default_rng([seed, 101, layer]) in the reference's draw order."""
+    rng = np.random.default_rng([int(seed), 101, int(layer)])
+    inv = 1.0 / np.sqrt(d)
+    w = {}
+    w["wq"] = rng.standard_normal((d, d)) * inv
+    w["wk"] = rng.standard_normal((d, d)) * inv
+    w["wv"] = rng.standard_normal((d, d)) * inv
+    w["wo"] = rng.standard_normal((d, d)) * inv
+    w["w1"] = rng.standard_normal((d, MLP_EXPANSION * d)) * inv
+    w["w2"] = rng.standard_normal((MLP_EXPANSION * d, d)) / np.sqrt(MLP_EXPANSION * d)
+    w["ln1_gain"] = 1.0 + 0.1 * rng.standard_normal(d)
+    w["ln1_bias"] = 0.1 * rng.standard_normal(d)
+    w["ln2_gain"] = 1.0 + 0.1 * rng.standard_normal(d)
+    w["ln2_bias"] = 0.1 * rng.standard_normal(d)
+    return w
+
+
+def make_input(n: int, b: int, d: int, seed: int) -> np.ndarray:
+    """layers.py:102-105."""
+    return np.random.default_rng([int(seed), 202]).standard_normal((n, b, d))
+
+
+def project(x3, w, exact: bool = True) -> np.ndarray:
+    """layers.py:118-122: (s, b, d_in) @ (d_in, d_out)."""
+    s, b, din = x3.shape
+    return matmul(np.asarray(x3).reshape(s * b, din), w, exact).reshape(s, b, w.shape[1])
+
+
+def layernorm(x, gain, bias) -> np.ndarray:
+    """layers.py:106-110."""
+    mu = x.mean(axis=-1, keepdims=True)
+    var = ((x - mu) ** 2).mean(axis=-1, keepdims=True)
+    return (x - mu) / np.sqrt(var + LN_EPS) * gain + bias
+
+
+def gelu(x) -> np.ndarray:
+    """layers.py:113-115 (exact, erf-based)."""
+    from scipy.special import erf
+    return 0.5 * x * (1.0 + erf(x / np.sqrt(2.0)))
+
+
+def ulysses_attention_layer(x_loc, w: dict, h: int, kind: str, exact: bool = True):
+    """ulysses_attention_forward_with_state (ulysses.py:135-157) on P
+    sequence shards x_loc[r] (n/P, b, d): project, the core, project wo.
+    Returns (out_loc list, state)."""
+    p = len(x_loc)
+    nl, b, d = np.asarray(x_loc[0]).shape
+    hd = d // h
+    four = lambda t: t.reshape(nl, b, h, hd)
+    q = [four(project(x, w["wq"], exact)) for x in x_loc]
+    k = [four(project(x, w["wk"], exact)) for x in x_loc]
+    v = [four(project(x, w["wv"], exact)) for x in x_loc]
+    c_loc, st = ulysses_forward(q, k, v, kind, exact=exact)
+    c_seq = [c.reshape(nl, b, d) for c in c_loc]
+    out = [project(c, w["wo"], exact) for c in c_seq]
+    st = dict(st, x_loc=[np.asarray(x, np.float64) for x in x_loc], c_seq=c_seq, h=h)
+    return out, st
+
+
+def ulysses_attention_layer_backward(grad_loc, state, w: dict, kind: str, exact: bool = True):
+    """ulysses_attention_backward (ulysses.py:188-245): returns (grad_x_loc,
+    grad_w summed over ranks in rank order, like
+    run_ulysses_attention_backward ulysses.py:296-302)."""
+    p = len(grad_loc)
+    nl, b, d = np.asarray(grad_loc[0]).shape
+    h = state["h"]
+    hd = d // h
+    g2 = [np.asarray(g, np.float64).reshape(nl * b, d) for g in grad_loc]
+    c2 = [c.reshape(nl * b, d) for c in state["c_seq"]]
+    dwo = [matmul(c.T, g, exact) for c, g in zip(c2, g2)]
+    dc = [matmul(g, w["wo"].T, exact).reshape(nl, b, h, hd) for g in g2]
+    dq, dk, dv = ulysses_backward(dc, state, kind, exact=exact)
+    x2 = [x.reshape(nl * b, d) for x in state["x_loc"]]
+    flat = lambda t: np.asarray(t).reshape(nl * b, d)
+    gw = {"wq": [matmul(x.T, flat(g), exact) for x, g in zip(x2, dq)],
+          "wk": [matmul(x.T, flat(g), exact) for x, g in zip(x2, dk)],
+          "wv": [matmul(x.T, flat(g), exact) for x, g in zip(x2, dv)],
+          "wo": dwo}
+    grad_w = {}
+    for key, parts in gw.items():
+        tot = parts[0]
+        for t in parts[1:]:
+            tot = tot + t
+        grad_w[key] = tot
+    gx = [(matmul(flat(a), w["wq"].T, exact) + matmul(flat(bq), w["wk"].T, exact)
+           + matmul(flat(c), w["wv"].T, exact)).reshape(nl, b, d) for a, bq, c in zip(dq, dk, dv)]
+    return gx, grad_w
+
+
+def ulysses_block(x_loc, w: dict, h: int, kind: str, exact: bool = True):
+    """ulysses_block_forward (ulysses.py:172-184): pre-LN attention with
+    residual, then pre-LN GELU MLP with residual; only attention talks."""
+    xs = [np.asarray(x, np.float64) for x in x_loc]
+    t1 = [layernorm(x, w["ln1_gain"], w["ln1_bias"]) for x in xs]
+    attn, _ = ulysses_attention_layer(t1, w, h, kind, exact)
+    x1 = [x + a for x, a in zip(xs, attn)]
+    t2 = [layernorm(x, w["ln2_gain"], w["ln2_bias"]) for x in x1]
+    return [x + project(gelu(project(t, w["w1"], exact)), w["w2"], exact) for x, t in zip(x1, t2)]
+
+
+# ---------------------------------------------------------------------------
 # seeded synthetic inputs (SURVEY 8(d))
 # ---------------------------------------------------------------------------
 

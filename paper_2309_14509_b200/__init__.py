@@ -5,7 +5,8 @@ Public API (drop-in for the reference's DistributedAttention path):
     DistributedAttention(local_attn, sequence_process_group, scatter_idx=2, gather_idx=0)
     seq_all_to_all(input, scatter_idx, gather_idx, group)
     SequenceGroup.from_process_group(pg) / SequenceGroup.local_group(P)
-    FlashAttention(mask="causal"|"none"), get_kernel("causal"|"dense")
+    FlashAttention(mask="causal"|"none"|"blocked"), get_kernel("causal"|"dense"|"blocked")
+    UlyssesAttention(d, heads, group) / UlyssesBlock(...)   (layer with projections / block)
 
 All compute runs in libulysses_b200.so (sm_100a); see include/ulysses_b200.h.
 """
@@ -18,6 +19,7 @@ from .attention import (  # noqa: F401
     seq_all_to_all,
 )
 from .comm import CommRecord, SequenceGroup, a2a_out_shape  # noqa: F401
+from .layer import UlyssesAttention, UlyssesBlock, make_weights  # noqa: F401
 from .errors import (  # noqa: F401
     DegenerateRowError,
     DivisibilityError,

@@ -1,0 +1,103 @@
+"""The Ulysses attention layer with its projections, and the transformer
+block around it.
+
+Mirrors the reference's layer (paths relative to /root/reference/pkg/src/seqlab):
+
+  * ``UlyssesAttention`` == ``ulysses_attention_forward_with_state``
+    (ulysses.py:135-157): q/k/v = x @ wq/wk/wv (layers.py:118-122), the
+    DistributedAttention core (3x seq->head, local attention, head->seq),
+    out = c @ wo.  Its backward is ``ulysses_attention_backward``
+    (ulysses.py:188-245): grad_x plus this rank's partial weight gradients
+    (their sum over ranks is the single-rank gradient; reducing them is the
+    data-parallel engine's job, not the attention path's -- ulysses.py:193-197).
+  * ``UlyssesBlock`` == ``ulysses_block_forward`` (ulysses.py:172-184):
+    pre-LN attention + residual, pre-LN GELU MLP (4x, exact erf) + residual;
+    only attention communicates.
+  * ``make_weights`` == layers.py:83-99 (same draws, same order).
+
+The attention core runs on this package's kernels and exchanges; the
+projections are plain GEMMs on cuBLAS (torch.matmul) and the row-wise
+pieces are torch ops -- off the hot path.  Weights are (d_in, d_out) like
+the reference's ``project``.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from .attention import DistributedAttention, FlashAttention
+from .errors import DivisibilityError
+
+LN_EPS = 1e-5          # layers.py:22
+MLP_EXPANSION = 4      # layers.py:23
+
+
+def make_weights(d: int, seed: int, layer: int = 0) -> dict:
+    """layers.py:83-99 (float64 numpy; cast when loading into a module)."""
+    rng = np.random.default_rng([int(seed), 101, int(layer)])
+    inv = 1.0 / np.sqrt(d)
+    w = {}
+    for name in ("wq", "wk", "wv", "wo"):
+        w[name] = rng.standard_normal((d, d)) * inv
+    w["w1"] = rng.standard_normal((d, MLP_EXPANSION * d)) * inv
+    w["w2"] = rng.standard_normal((MLP_EXPANSION * d, d)) / np.sqrt(MLP_EXPANSION * d)
+    w["ln1_gain"] = 1.0 + 0.1 * rng.standard_normal(d)
+    w["ln1_bias"] = 0.1 * rng.standard_normal(d)
+    w["ln2_gain"] = 1.0 + 0.1 * rng.standard_normal(d)
+    w["ln2_bias"] = 0.1 * rng.standard_normal(d)
+    return w
+
+
+def _param(x, dtype, device):
+    return torch.nn.Parameter(torch.as_tensor(np.asarray(x), dtype=torch.float64).to(dtype).to(device))
+
+
+class UlyssesAttention(torch.nn.Module):
+    """``forward(x)``: this rank's sequence shard ``[n/P, b, d]`` -> ``[n/P, b, d]``."""
+
+    def __init__(self, d_model: int, heads: int, sequence_process_group=None, mask: str = "causal",
+                 weights: dict | None = None, dtype=torch.bfloat16, device=None, local_attention=None,
+                 seed: int = 0):
+        super().__init__()
+        if d_model % heads != 0:   # AttentionSpec.__post_init__, layers.py:46-49
+            raise DivisibilityError(f"head count {heads} does not divide hidden size {d_model}")
+        self.d, self.h, self.hd = d_model, heads, d_model // heads
+        device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        w = weights if weights is not None else make_weights(d_model, seed)
+        self.wq, self.wk, self.wv, self.wo = (_param(w[k], dtype, device) for k in ("wq", "wk", "wv", "wo"))
+        attn = local_attention if local_attention is not None else FlashAttention(mask)
+        self.core = DistributedAttention(attn, sequence_process_group, scatter_idx=2, gather_idx=0)
+
+    def forward(self, x):
+        nl, b, d = x.shape
+        x2 = x.reshape(nl * b, d)
+        # one GEMM for q|k|v (ulysses.py:140-142), split into head views
+        qkv = x2 @ torch.cat([self.wq, self.wk, self.wv], dim=1)
+        q, k, v = (t.reshape(nl, b, self.h, self.hd) for t in qkv.split(d, dim=1))
+        c = self.core(q.contiguous(), k.contiguous(), v.contiguous())     # ulysses.py:144-154
+        return (c.reshape(nl * b, d) @ self.wo).reshape(nl, b, d)        # ulysses.py:155
+
+
+class UlyssesBlock(torch.nn.Module):
+    """Pre-LN transformer block on sequence shards (ulysses.py:172-184)."""
+
+    def __init__(self, d_model: int, heads: int, sequence_process_group=None, mask: str = "causal",
+                 weights: dict | None = None, dtype=torch.bfloat16, device=None, seed: int = 0, layer: int = 0):
+        super().__init__()
+        device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        w = weights if weights is not None else make_weights(d_model, seed, layer)
+        self.attn = UlyssesAttention(d_model, heads, sequence_process_group, mask, w, dtype, device)
+        self.w1, self.w2 = _param(w["w1"], dtype, device), _param(w["w2"], dtype, device)
+        self.ln1_gain, self.ln1_bias = _param(w["ln1_gain"], dtype, device), _param(w["ln1_bias"], dtype, device)
+        self.ln2_gain, self.ln2_bias = _param(w["ln2_gain"], dtype, device), _param(w["ln2_bias"], dtype, device)
+
+    def forward(self, x):
+        d = x.shape[-1]
+        t1 = F.layer_norm(x, (d,), self.ln1_gain, self.ln1_bias, eps=LN_EPS)    # layers.py:106-110
+        x1 = x + self.attn(t1)
+        t2 = F.layer_norm(x1, (d,), self.ln2_gain, self.ln2_bias, eps=LN_EPS)
+        return x1 + F.gelu(t2 @ self.w1, approximate="none") @ self.w2           # layers.py:113-127

@@ -30,6 +30,25 @@ def run_ranks(groups, fn):
     return out
 
 
+def warm_streams(groups, dtypes=(torch.float32, torch.bfloat16), mb=256):
+    """Create every rank stream's cuBLAS handle/workspace and reserve
+    allocator memory on it before an in-process group runs library ops:
+    first-use setup can block the host thread while an earlier rank's stream
+    spins in a flag wait that only a later rank (same thread) can satisfy."""
+    torch.cuda.synchronize()
+    for g in groups:
+        s = g.stream if g.stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(s):
+            for dt in dtypes:
+                a = torch.ones((256, 256), dtype=dt, device="cuda")
+                (a @ a).sum().item()
+                t = torch.nn.functional.layer_norm(a, (256,))
+                torch.nn.functional.gelu(t).sum()
+            del a
+            torch.empty(mb << 20, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+
+
 def rel_max_err(a, ref):
     a = np.asarray(a, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
