@@ -268,6 +268,7 @@ def run_ours(args):
     kt = kernel_split(attn, mk4(), mk4(), mk4(), mk4(), args, dev)
     a2a = bench_a2a(dev, n_seq, H, hd, P, group)
     sparse = bench_blocked(kt_inputs=(mk4, n_seq, H // P, hd), args=args, dev=dev)
+    layer_leg = bench_layer(group, nl, H, hd, args, dev)
 
     # ---- e2e through the public API from pinned host buffers ----------
     e2e = run_e2e(layer, q, k, v, do, args, P, dev)
@@ -316,6 +317,7 @@ def run_ours(args):
             "kernels": kt["kernels"],
             "a2a": a2a,
             "blocked_sparse_fwd": sparse,
+            "layer": layer_leg,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,
@@ -392,6 +394,56 @@ def kernel_split(attn, q, k, v, do, args, dev):
             rec["tflops"] = round(alg[nm] / (ms / 1e3) / 1e12, 1)
         out.append(rec)
     return {"kernels": out}
+
+
+def bench_layer(group, nl, H, hd, args, dev):
+    """the whole UlyssesAttention layer (x -> fused
+    QKV GEMM + seq->head exchange -> attention -> O projection, and its
+    backward) on this rank's shard, plus the fused QKV projection kernel
+    alone against cuBLAS (torch.matmul) on the same GEMM."""
+    import torch
+    import paper_2309_14509_b200 as U
+    d = H * hd
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    layer = U.UlyssesAttention(d, H, group, "causal", dtype=torch.bfloat16, device=dev)
+    x = torch.randn((nl, 1, d), generator=g, device=dev).to(torch.bfloat16)
+    gout = torch.randn((nl, 1, d), generator=g, device=dev).to(torch.bfloat16)
+    flush = make_flush(dev)
+
+    def timeit(fn, reps):
+        ts = []
+        for it in range(args.warmup + reps):
+            flush.zero_()
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            e.record()
+            if it >= args.warmup:
+                ts.append((a, e))
+        torch.cuda.synchronize()
+        return statistics.mean(a.elapsed_time(e) for a, e in ts)
+
+    def step():
+        xx = x.detach().requires_grad_(True)
+        torch.autograd.backward([layer(xx)], [gout])
+    reps = max(3, min(args.steps, 10))
+    ms_layer = timeit(step, reps)
+    x2 = x.reshape(nl, d)
+    wqkv = torch.cat([layer.wq, layer.wk, layer.wv], dim=1).detach().contiguous()
+    ms_fused = timeit(lambda: group.qkv_projection(x2, wqkv, 1, H, H), reps)
+    ms_cublas = timeit(lambda: x2 @ wqkv, reps)
+    flops = 2.0 * nl * d * 3 * d
+    P = group.world
+    n_seq = nl * P
+    f_att = sum(attn_flops(n_seq, H // P, hd, True))
+    f_proj = 3 * 2.0 * nl * d * 4 * d     # fwd: x.W_qkv + c.W_o; bwd: 2x each
+    return {"d_model": d, "ms_fwd_bwd": round(ms_layer, 4), "tokens_per_s": round(n_seq / (ms_layer / 1e3), 1),
+            "tflops_per_gpu": round((f_att + f_proj) / (ms_layer / 1e3) / 1e12, 1),
+            "qkv_proj_exchange": {"ms": round(ms_fused, 4), "tflops": round(flops / (ms_fused / 1e3) / 1e12, 1),
+                                  "note": "tcgen05 GEMM x [wq|wk|wv] with the seq->head exchange in its epilogue"},
+            "cublas_qkv_gemm": {"ms": round(ms_cublas, 4), "tflops": round(flops / (ms_cublas / 1e3) / 1e12, 1),
+                                "note": "torch.matmul, same GEMM, no exchange (comparison)"}}
 
 
 def bench_blocked(kt_inputs, args, dev, bs=128, bandwidth=15):

@@ -202,6 +202,19 @@ int ul_attn_bwd_exchange(ul_comm* comm, const void* q, const void* k, const void
                          void* seq_dv, int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
                          int dtype, int mask, float scale, uint64_t label_hash, void* stream);
 
+/* Q/K/V projection fused with the seq->head exchange:
+ * project(x, wq|wk|wv) (layers.py:118-122, ulysses.py:140-142) + _to_head
+ * (ulysses.py:161-164).  x: this rank's sequence shard [nl*b, d] (bf16,
+ * d = hq*hd), w: [d, (hq + 2*hkv)*hd] = [wq | wk | wv] (d_in x d_out,
+ * row-major); q4/k4/v4: this rank's head-layout outputs [nl*P, b, hq/P, hd]
+ * and [nl*P, b, hkv/P, hd].  The GEMM epilogue stores every head block at
+ * its owner (own output or the peer's receive slot over NVLink); a
+ * collective like ul_all_to_all (every rank calls it with the same shapes
+ * and label; comm may be NULL for P = 1).  bf16, hd = 128. */
+int ul_qkv_proj_exchange(ul_comm* comm, const void* x, const void* w, void* q4, void* k4, void* v4,
+                         int64_t nl, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
+                         uint64_t label_hash, void* stream);
+
 /* Number of kernel launches the last ul_* call on this thread issued, and
  * the cumulative count since the library was loaded (all threads). */
 int ul_last_launch_count(void);

@@ -211,6 +211,32 @@ class SequenceGroup:
         return sum(r.aggregate_elements for r in self.records)
 
     # -- the collective ----------------------------------------------------
+    def qkv_projection(self, x2: torch.Tensor, w: torch.Tensor, b: int, hq: int, hkv: int,
+                       labels=("attn.q.seq2head", "attn.k.seq2head", "attn.v.seq2head")):
+        """project(x, wq|wk|wv) (layers.py:118-122) fused with the three
+        seq->head flips (ulysses.py:140-146): x2 = this rank's [nl*b, d]
+        shard, w = [d, (hq + 2 hkv) hd]; returns head-layout q4 [N, b, hq/P,
+        hd], k4 / v4 [N, b, hkv/P, hd].  One GEMM whose epilogue stores every
+        head block at its owner rank (ul_qkv_proj_exchange); a collective."""
+        from .errors import ShardError
+        p = self.world
+        m, d = x2.shape
+        hd = d // hq
+        nl = m // b
+        if hq % p or hkv % p:
+            raise ShardError(f"p={p} does not divide head counts ({hq}, {hkv})")
+        q4 = torch.empty((nl * p, b, hq // p, hd), dtype=x2.dtype, device=x2.device)
+        k4 = torch.empty((nl * p, b, hkv // p, hd), dtype=x2.dtype, device=x2.device)
+        v4 = torch.empty_like(k4)
+        for lab, hh in zip(labels, (hq, hkv, hkv)):
+            self._record(lab, nl * b * hh * hd)
+        stream = torch.cuda.current_stream(x2.device).cuda_stream
+        _lib.check(_lib.lib().ul_qkv_proj_exchange(self._handle, x2.data_ptr(), w.data_ptr(), q4.data_ptr(),
+                                                   k4.data_ptr(), v4.data_ptr(), nl, b, hq, hkv, hd,
+                                                   label_hash("attn.qkv.seq2head"), stream),
+                   exc_override={-1: ShardError})
+        return q4, k4, v4
+
     def all_to_all(self, tensors, split_axis: int, concat_axis: int, label: str = "all_to_all",
                    labels=None):
         """Fused all-to-all of 1..4 contiguous tensors with the same rank,

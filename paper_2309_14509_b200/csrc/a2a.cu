@@ -695,9 +695,58 @@ int a2a_fused_finish(ul_comm* c, int n, void* const* seq_out, const int64_t* hea
   return wait_and_drain(c, pl, seq_out, st);
 }
 
+int sm100_qkv_proj(const void* x, const void* w, int64_t M, int64_t K, int64_t N, const ProjEpilogue& ep,
+                   cudaStream_t st);
+
 }  // namespace ul
 
 extern "C" {
+
+int ul_qkv_proj_exchange(ul_comm* c, const void* x, const void* w, void* q4, void* k4, void* v4, int64_t nl,
+                         int64_t b, int64_t hq, int64_t hkv, int64_t hd, uint64_t label, void* stream) {
+  launch_count() = 0;
+  if (!x || !w || !q4 || !k4 || !v4) return fail(UL_ERR_ARG, "ul_qkv_proj_exchange: NULL tensor");
+  if (nl < 0 || b < 1 || hq < 1 || hkv < 1 || hd < 1)
+    return fail(UL_ERR_SHAPE, "ul_qkv_proj_exchange: bad shape (nl=%lld, b=%lld, hq=%lld, hkv=%lld, hd=%lld)",
+                (long long)nl, (long long)b, (long long)hq, (long long)hkv, (long long)hd);
+  const int64_t d = hq * hd, dkv = hkv * hd;
+  // the fused all-to-all is the seq->head flip of the three projections' sequence shards
+  const int64_t shapes[12] = {nl, b, hq, hd, nl, b, hkv, hd, nl, b, hkv, hd};
+  void* outs[3] = {q4, k4, v4};
+  CallPlan pl;
+  UL_TRY(plan_call(c, 3, outs, shapes, 4, UL_DTYPE_BF16, 2, 0, label, &pl));
+  ProjEpilogue ep;
+  memset(&ep, 0, sizeof(ep));
+  for (int t = 0; t < 3; ++t)
+    for (int r = 0; r < pl.P; ++r)
+      ep.dst[t][r] = (r == pl.me || !c) ? (char*)outs[t]
+                                        : c->peer_base[r] + (size_t)pl.slot * c->slot_bytes + pl.slot_off[t];
+  ep.col0[0] = 0;
+  ep.col0[1] = (int)d;
+  ep.col0[2] = (int)(d + dkv);
+  ep.col0[3] = (int)(d + 2 * dkv);
+  ep.hl[0] = (int)(hq / pl.P);
+  ep.hl[1] = ep.hl[2] = (int)(hkv / pl.P);
+  ep.nl = (int)nl;
+  ep.b = (int)b;
+  ep.hd = (int)hd;
+  ep.me = pl.me;
+  PeerEpilogue& sg = ep.sg;
+  sg.active = pl.P > 1;
+  sg.rank = pl.me;
+  sg.world = pl.P;
+  sg.slot = pl.slot;
+  sg.epoch = pl.epoch;
+  sg.sigv = pl.sig;
+  if (c) {
+    for (int r = 0; r < pl.P; ++r) sg.sig[r] = (Signals*)(c->peer_base[r] + 2 * c->slot_bytes);
+    sg.counter = &((Signals*)(c->base + 2 * c->slot_bytes))->counter[pl.slot];
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  UL_TRY(sm100_qkv_proj(x, w, nl * b, d, d + 2 * dkv, ep, st));
+  if (pl.P > 1) UL_TRY(wait_and_drain(c, pl, outs, st));
+  return UL_OK;
+}
 
 int ul_all_to_all(ul_comm* c, int n, const void* const* in, void* const* out, const int64_t* shapes,
                   int ndim, int dtype, int split, int concat, uint64_t label, void* stream) {

@@ -43,6 +43,7 @@ int preload_a2a();
 int preload_simt();
 int preload_fwd();
 int preload_bwd();
+int preload_proj();
 void set_deterministic(int on);
 int get_deterministic();
 
@@ -80,6 +81,7 @@ int ul_preload_kernels(void) {
   UL_TRY(preload_a2a());
   UL_TRY(preload_simt());
   UL_TRY(preload_fwd());
+  UL_TRY(preload_proj());
 
   return preload_bwd();
 }

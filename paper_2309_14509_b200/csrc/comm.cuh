@@ -46,6 +46,17 @@ struct PeerEpilogue {
   int active;                   // 0: plain kernel (P = 1 or unfused)
 };
 
+// Fused seq->head epilogue of the Q/K/V projection GEMM (csrc/proj_sm100.cu):
+// each 128-column head block of Y = X [wq|wk|wv] goes to the head-layout
+// image of the rank that owns the head.
+struct ProjEpilogue {
+  char* dst[3][UL_MAX_RANKS];   // tensor q/k/v x destination rank: base of its [N, b, hl, hd] image
+  int col0[4];                  // first W column of q, k, v; col0[3] = total columns
+  int hl[3];                    // heads per rank of q, k, v
+  int nl, b, hd, me;
+  PeerEpilogue sg;              // signalling of the exchange (active when P > 1)
+};
+
 __device__ __forceinline__ void st_release_sys_u64(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }

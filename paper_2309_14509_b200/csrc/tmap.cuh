@@ -48,3 +48,23 @@ inline int make_tmap_bhsd(CUtensorMap* m, const void* ptr, int64_t rows, int64_t
 }
 
 }  // namespace ul
+
+namespace ul {
+// 2-D bf16 row-major matrix [rows, cols] (row stride = cols), SWIZZLE_128B
+// boxes of 64 columns x box_rows rows; OOB rows/cols read as zero.
+inline int make_tmap_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int box_rows) {
+  EncodeTiledFn enc;
+  UL_TRY(get_encode_fn(&enc));
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || (cols * 2) % 16 != 0)
+    return fail(UL_ERR_ARG, "GEMM operand not 16-byte aligned");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(cols * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(UL_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return UL_OK;
+}
+}  // namespace ul

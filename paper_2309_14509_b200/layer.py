@@ -15,9 +15,11 @@ Mirrors the reference's layer (paths relative to /root/reference/pkg/src/seqlab)
     only attention communicates.
   * ``make_weights`` == layers.py:83-99 (same draws, same order).
 
-The attention core runs on this package's kernels and exchanges; the
-projections are plain GEMMs on cuBLAS (torch.matmul) and the row-wise
-pieces are torch ops -- off the hot path.  Weights are (d_in, d_out) like
+The attention core runs on this package's kernels and exchanges.  In bf16
+with hd = 128 the Q/K/V projection is this package's tcgen05 GEMM whose
+epilogue performs the seq->head exchange (csrc/proj_sm100.cu), and the layer
+is one autograd node; the O projection and the backward GEMMs are cuBLAS,
+and the row-wise pieces are torch ops -- off the hot path.  Weights are (d_in, d_out) like
 the reference's ``project``.
 """
 
@@ -56,6 +58,48 @@ def _param(x, dtype, device):
     return torch.nn.Parameter(torch.as_tensor(np.asarray(x), dtype=torch.float64).to(dtype).to(device))
 
 
+class _UlyssesLayerFn(torch.autograd.Function):
+    """The whole attention layer as one autograd node (bf16, hd = 128, the
+    library's FlashAttention): fused QKV GEMM + seq->head exchange
+    (ul_qkv_proj_exchange), attention with the O exchange in its epilogue,
+    c @ wo; backward mirrors ulysses_attention_backward (ulysses.py:188-245)
+    with the dQ/dK/dV exchange fused into the backward kernels and the
+    remaining GEMMs on cuBLAS."""
+
+    @staticmethod
+    def forward(ctx, group, attn, h, hkv, x, wqkv, wo):
+        nl, b, d = x.shape
+        x2 = x.reshape(nl * b, d).contiguous()
+        q4, k4, v4 = group.qkv_projection(x2, wqkv.contiguous(), b, h, hkv)
+        if group.world > 1:
+            o4, lse, c = attn.forward_exchange(q4, k4, v4, group, label="attn.ctx.head2seq")
+        else:
+            o4, lse = attn.forward_with_lse(q4, k4, v4)
+            c = o4
+        c2 = c.reshape(nl * b, d)
+        ctx.group, ctx.attn, ctx.shape = group, attn, (nl, b, d, h, hkv)
+        ctx.save_for_backward(x2, wqkv, wo, q4, k4, v4, o4, lse, c2)
+        return (c2 @ wo).reshape(nl, b, d)
+
+    @staticmethod
+    def backward(ctx, gout):
+        group, attn = ctx.group, ctx.attn
+        nl, b, d, h, hkv = ctx.shape
+        x2, wqkv, wo, q4, k4, v4, o4, lse, c2 = ctx.saved_tensors
+        g2 = gout.reshape(nl * b, d)
+        dwo = c2.t() @ g2                                             # ulysses.py:206
+        dc = (g2 @ wo.t()).reshape(nl, b, h, d // h)                  # ulysses.py:207
+        if group.world > 1:
+            (do4,) = group.all_to_all([dc], 2, 0, label="bwd.ctx.seq2head")
+            dq, dk, dv = attn.backward_exchange(q4, k4, v4, o4, lse, do4, group, label="bwd.qkv.head2seq")
+        else:
+            dq, dk, dv = attn.backward(q4, k4, v4, o4, lse, dc)
+        dqkv = torch.cat([t.reshape(nl * b, -1) for t in (dq, dk, dv)], dim=1)
+        dx = (dqkv @ wqkv.t()).reshape(nl, b, d)                      # ulysses.py:240
+        dwqkv = x2.t() @ dqkv                                         # ulysses.py:234-238
+        return None, None, None, None, dx, dwqkv, dwo
+
+
 class UlyssesAttention(torch.nn.Module):
     """``forward(x)``: this rank's sequence shard ``[n/P, b, d]`` -> ``[n/P, b, d]``."""
 
@@ -72,8 +116,16 @@ class UlyssesAttention(torch.nn.Module):
         attn = local_attention if local_attention is not None else FlashAttention(mask)
         self.core = DistributedAttention(attn, sequence_process_group, scatter_idx=2, gather_idx=0)
 
+    def _fused_ok(self, x):
+        a = self.core.local_attn
+        return (isinstance(a, FlashAttention) and a.mask != "blocked" and x.dtype == torch.bfloat16
+                and self.hd == 128 and self.d % 64 == 0)
+
     def forward(self, x):
         nl, b, d = x.shape
+        if self._fused_ok(x):   # one node: fused QKV GEMM + exchange, fused attention exchanges
+            wqkv = torch.cat([self.wq, self.wk, self.wv], dim=1)
+            return _UlyssesLayerFn.apply(self.core.spg, self.core.local_attn, self.h, self.h, x, wqkv, self.wo)
         x2 = x.reshape(nl * b, d)
         # one GEMM for q|k|v (ulysses.py:140-142), split into head views
         qkv = x2 @ torch.cat([self.wq, self.wk, self.wv], dim=1)
