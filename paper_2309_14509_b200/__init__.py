@@ -18,7 +18,7 @@ from .attention import (  # noqa: F401
     get_kernel,
     seq_all_to_all,
 )
-from .comm import CommRecord, SequenceGroup, a2a_out_shape  # noqa: F401
+from .comm import CommLedger, CommRecord, SequenceGroup, a2a_out_shape, check_ledger  # noqa: F401
 from .layer import UlyssesAttention, UlyssesBlock, make_weights  # noqa: F401
 from .errors import (  # noqa: F401
     DegenerateRowError,

@@ -93,6 +93,81 @@ class CommRecord:
     per_rank_egress_elements: int
 
 
+LEDGER_CSV_COLUMNS = ["step_label", "collective", "aggregate_elements", "per_rank_egress_elements"]  # simgroup.py:54-59
+
+
+class CommLedger(list):
+    """Append-only list of CommRecord with the reference ledger's queries and
+    exports (CommLedger, simgroup.py:88-172; CSV/JSON in its schema)."""
+
+    def select(self, collective=None, step_label=None):
+        return tuple(r for r in self if (collective is None or r.collective == collective)
+                     and (step_label is None or r.step_label == step_label))
+
+    def count(self, collective=None, step_label=None) -> int:
+        return len(self.select(collective, step_label))
+
+    def total_egress(self, collective=None, step_label=None) -> int:
+        return sum(r.per_rank_egress_elements for r in self.select(collective, step_label))
+
+    def total_aggregate(self, collective=None, step_label=None) -> int:
+        return sum(r.aggregate_elements for r in self.select(collective, step_label))
+
+    def counts_by_collective(self) -> dict:
+        out = {}
+        for r in self:
+            out[r.collective] = out.get(r.collective, 0) + 1
+        return out
+
+    def egress_by_collective(self) -> dict:
+        out = {}
+        for r in self:
+            out[r.collective] = out.get(r.collective, 0) + r.per_rank_egress_elements
+        return out
+
+    def rows(self) -> list:
+        return [[r.step_label, r.collective, r.aggregate_elements, r.per_rank_egress_elements] for r in self]
+
+    def to_json_obj(self) -> list:
+        return [dict(zip(LEDGER_CSV_COLUMNS, row)) for row in self.rows()]
+
+    def to_csv_text(self) -> str:
+        import csv
+        import io
+        buf = io.StringIO()
+        w = csv.writer(buf, lineterminator="\n")
+        w.writerow(LEDGER_CSV_COLUMNS)
+        w.writerows(self.rows())
+        return buf.getvalue()
+
+    def write_csv(self, path: str) -> str:
+        with open(path, "w") as f:
+            f.write(self.to_csv_text())
+        return path
+
+    def write_json(self, path: str) -> str:
+        import json
+        with open(path, "w") as f:
+            json.dump(self.to_json_obj(), f, indent=2)
+        return path
+
+
+def check_ledger(ledger, n: int, b: int, d: int, p: int, layers: int = 1, backward: bool = False):
+    """verify.check_ledger (verify.py:146-169) for the Ulysses scheme, zero
+    tolerance: total per-rank egress == the exact-convention volume
+    (costmodel.py:82-87) x layers (x2 with the backward's mirrored
+    exchanges), 4 all_to_all per layer per direction (LEDGER_SHAPE,
+    verify.py:43-47), every record of aggregate n*b*d.  Returns
+    (ok, measured, predicted)."""
+    from fractions import Fraction
+    flips = 2 if backward else 1
+    predicted = Fraction(4 * n * b * d) * (p - 1) / (p * p) * layers * flips
+    measured = ledger.total_egress()
+    counts_ok = ledger.counts_by_collective() == ({"all_to_all": 4 * layers * flips} if len(ledger) or layers else {})
+    records_ok = all(r.aggregate_elements == n * b * d for r in ledger)
+    return bool(measured == predicted and counts_ok and records_ok), int(measured), int(predicted)
+
+
 class SequenceGroup:
     """One rank of a P-way Ulysses sequence-parallel group."""
 
@@ -106,7 +181,8 @@ class SequenceGroup:
         self.slot_bytes = slot_bytes
         self.stream = stream
         self._pg = pg
-        self.records: list[CommRecord] = []
+        self.records: CommLedger = CommLedger()   # the logical ledger (elements, reference schema)
+        self.ledger = self.records
 
     # -- construction ------------------------------------------------------
     @staticmethod

@@ -89,3 +89,26 @@ def test_block_stack_fp32_vs_reference():
     for i in range(layers):
         cur = run_ranks(groups, lambda r: blocks[r][i](cur[r]))
     assert_rtol(np.concatenate([to_np(c) for c in cur], 0), g["blocks_out"], rtol=LAYER_RTOL)
+
+
+def test_layer_ledger_law_and_device_bytes():
+    # verify.check_ledger's zero-tolerance law on the fused bf16 layer (P = 2,
+    # fwd + bwd), and the device-side byte ledger agrees with the logical one
+    p, n, b, d, h, seed = 2, 256, 1, 256, 2, 9
+    w = {k: O.bf16_round(v) for k, v in O.make_weights(d, seed).items()}
+    x, go = O.bf16_round(O.make_input(n, b, d, seed)), O.bf16_round(O.make_input(n, b, d, seed + 1))
+    nl = n // p
+    groups = U().SequenceGroup.local_group(p, slot_bytes=16 << 20)
+    warm_streams(groups)
+    run_layer(1, d, h, "causal", x[:nl], go[:nl], w, torch.bfloat16)
+    mods = run_ranks(groups, lambda r: U().UlyssesAttention(d, h, groups[r], "causal", weights=w))
+    xs = run_ranks(groups, lambda r: to_dev(x[r * nl:(r + 1) * nl], torch.bfloat16).requires_grad_(True))
+    gs = run_ranks(groups, lambda r: to_dev(go[r * nl:(r + 1) * nl], torch.bfloat16))
+    outs = run_ranks(groups, lambda r: mods[r](xs[r]))
+    run_ranks(groups, lambda r: torch.autograd.backward([outs[r]], [gs[r]]))
+    for g in groups:
+        ok, measured, predicted = U().check_ledger(g.ledger, n, b, d, p, layers=1, backward=True)
+        assert ok, (measured, predicted, g.ledger.rows())
+        nat = g.native_ledger()
+        assert nat["egress_bytes"] == 2 * g.ledger.total_egress()     # bf16
+        assert nat["aggregate_bytes"] == 2 * g.ledger.total_aggregate()
