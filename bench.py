@@ -55,7 +55,7 @@ def make_flush(dev):
     of full-clock HBM work, long enough for the host to enqueue the next timed
     launches behind it, so the timed interval is device time (an idle GPU
     before the region would either add host launch latency or -- with a
-    device sleep -- let clocks drop; tools_timing_ab.py measured both)."""
+    device sleep -- let clocks drop; tools/timing_ab.py measured both)."""
     import torch
     return torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
@@ -197,10 +197,19 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # UL_BENCH_ONE_GPU=1: every rank on cuda:0 with a gloo rendezvous -- a
+    # functional smoke test of the N > 1 path on a one-GPU box (NCCL refuses
+    # two ranks on one device); timings of such a run mean nothing
+    one_gpu = os.environ.get("UL_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     P = world
     n_seq = args.seq if args.seq else SEQ_PER_GPU * P
     H, hd = args.heads, HEAD_DIM
@@ -309,8 +318,9 @@ def run_ours(args):
                 "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({src}, burst)",
                 "frac_of_sustained": round(ach / pk.get("bf16_tflops_sustained", peak), 4),
-                "traffic": (ncu_traffic(dom["name"]) or {}).get("bytes"),
-                "traffic_source": (ncu_traffic(dom["name"]) or {}).get("source"),
+                # ncu DRAM bytes per launch, captured on the P = 1 (config 2) workload
+                "traffic": (ncu_traffic(dom["name"]) or {}).get("bytes") if P == 1 else None,
+                "traffic_source": (ncu_traffic(dom["name"]) or {}).get("source") if P == 1 else None,
                 "alg_flops_per_launch": dom["alg_flops"],
                 "layer_frac": round(tflops_per_gpu / peak, 4),
             },

@@ -1,7 +1,11 @@
 """Diagnostic: where does the end-to-end (host-buffer) step time go?"""
 import torch
 
-import paper_2309_14509_b200 as U
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2309_14509_b200 as U  # noqa: E402
 
 dev = torch.device("cuda", 0)
 n, H, hd = 8192, 16, 128

@@ -3,13 +3,17 @@ no flushes, e2e or sweeps -- so `ncu --metrics gpu__time_duration.sum` lists
 exactly the kernels of a step.
 
     ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-        --log-file gpurun_out/launches.csv python tools_profile_step.py 1 2
+        --log-file gpurun_out/launches.csv python tools/profile_step.py 1 2
 """
 import sys
 
 import torch
 
-import paper_2309_14509_b200 as U
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2309_14509_b200 as U  # noqa: E402
 
 warm, steps = (int(a) for a in (sys.argv[1:3] if len(sys.argv) > 2 else (1, 2)))
 dev = torch.device("cuda", 0)

@@ -7,7 +7,7 @@ With one GPU available, this tool times (b) at each config's per-rank shape
 in-process group of P ranks on one device (traffic lands in local HBM, so it
 is an HBM-bound lower bound for the NVLink exchange, not an NVLink number).
 
-    python tools_sweep.py [--out profiles/r1_sweep.json] [--quick]
+    python tools/sweep.py [--out profiles/r1_sweep.json] [--quick]
 """
 
 from __future__ import annotations
@@ -19,7 +19,7 @@ import os
 import statistics
 import sys
 
-ROOT = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 # (name, P, N, Hq, Hkv, hd)
