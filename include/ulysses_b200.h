@@ -202,6 +202,14 @@ int ul_attn_bwd_exchange(ul_comm* comm, const void* q, const void* k, const void
                          void* seq_dv, int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
                          int dtype, int mask, float scale, uint64_t label_hash, void* stream);
 
+/* RankContext.ring_shift(local, steps, label) (simgroup.py:374-388, 464-465):
+ * out[t] on rank i = in[t] of rank (i - steps) mod P, n flat tensors of
+ * bytes[t] bytes moved over peer memory; a collective (full barrier) with
+ * the reference's metering (aggregate P*local, egress local*steps).
+ * comm may be NULL for P = 1 (a copy). */
+int ul_ring_shift(ul_comm* comm, int n, const void* const* in, void* const* out, const int64_t* bytes,
+                  int steps, uint64_t label_hash, void* stream);
+
 /* Q/K/V projection fused with the seq->head exchange:
  * project(x, wq|wk|wv) (layers.py:118-122, ulysses.py:140-142) + _to_head
  * (ulysses.py:161-164).  x: this rank's sequence shard [nl*b, d] (bf16,

@@ -276,6 +276,18 @@ def gen_layer():
     y, _ = U.run_ulysses_blocks(x, ws, spec, "causal", p)
     out["blocks_meta"] = np.array([p, n, b, d, h, 2, seed])
     out["blocks_out"] = np.asarray(y.data)
+    # the reference's ring baseline (baselines.py:68-121, run_ring_attention :142-155)
+    import seqlab.baselines as B
+    for ci, (p, n, b, d, h, kind, seed) in enumerate([(2, 32, 1, 64, 4, "causal", 31),
+                                                       (4, 32, 1, 64, 4, "causal", 32),
+                                                       (2, 24, 2, 48, 4, "none", 33)]):
+        mask = T.Mask.causal() if kind == "causal" else T.Mask.none()
+        spec = L.AttentionSpec(n=n, b=b, d=d, h_heads=h, mask=mask)
+        y, led = B.run_ring_attention(L.make_input(n, b, d, seed), [L.make_weights(d, seed)], spec, p)
+        out[f"ring{ci}_meta"] = np.array([p, n, b, d, h, 1 if kind == "causal" else 0, seed])
+        out[f"ring{ci}_out"] = np.asarray(y.data)
+        out[f"ring{ci}_ledger"] = np.array([[r.aggregate_elements, r.per_rank_egress_elements]
+                                            for r in led.records])
     np.savez_compressed(os.path.join(GOLDEN, "layer.npz"), **out)
     print("layer.npz", len(out), "arrays")
 

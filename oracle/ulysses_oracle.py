@@ -575,6 +575,58 @@ def ulysses_block(x_loc, w: dict, h: int, kind: str, exact: bool = True):
     return [x + project(gelu(project(t, w["w1"], exact)), w["w2"], exact) for x, t in zip(x1, t2)]
 
 
+def ring_shift(locals_, steps: int = 1):
+    """RankContext.ring_shift combine (simgroup.py:380-381): rank i gets
+    rank (i - steps) mod P's payload."""
+    p = len(locals_)
+    return [locals_[(i - steps) % p] for i in range(p)]
+
+
+def ring_attention_layer(x_loc, w: dict, h: int, kind: str, exact: bool = True):
+    """ring_attention_forward (baselines.py:68-121): per rank, full score
+    rows assembled from the circulating K chunks (ascending global key
+    order == chunk src), masked row_softmax with row_offset = rank*n/P, the
+    context accumulated over the circulating V chunks in arrival order."""
+    p = len(x_loc)
+    nl, b, d = np.asarray(x_loc[0]).shape
+    hd = d // h
+    n = nl * p
+    scale = 1.0 / np.sqrt(hd)
+    q4 = [project(x, w["wq"], exact).reshape(nl, b, h, hd) for x in x_loc]
+    ks = [project(x, w["wk"], exact) for x in x_loc]
+    vs = [project(x, w["wv"], exact) for x in x_loc]
+    scores = [np.empty((h, b, nl, n)) for _ in range(p)]
+    cur = ks
+    for step in range(p):
+        for r in range(p):
+            src = (r - step) % p
+            k4 = cur[r].reshape(nl, b, h, hd)
+            for hh in range(h):
+                for bi in range(b):
+                    scores[r][hh, bi, :, src * nl:(src + 1) * nl] = matmul(q4[r][:, bi, hh, :],
+                                                                          k4[:, bi, hh, :].T, exact) * scale
+        if step < p - 1:
+            cur = ring_shift(cur, 1)
+    probs = [np.empty_like(s_) for s_ in scores]
+    for r in range(p):
+        for hh in range(h):
+            for bi in range(b):
+                probs[r][hh, bi] = row_softmax(scores[r][hh, bi], kind, row_offset=r * nl)
+    ctx4 = [np.zeros((nl, b, h, hd)) for _ in range(p)]
+    cur = vs
+    for step in range(p):
+        for r in range(p):
+            src = (r - step) % p
+            v4 = cur[r].reshape(nl, b, h, hd)
+            for hh in range(h):
+                for bi in range(b):
+                    ctx4[r][:, bi, hh, :] += matmul(probs[r][hh, bi, :, src * nl:(src + 1) * nl],
+                                                    v4[:, bi, hh, :], exact)
+        if step < p - 1:
+            cur = ring_shift(cur, 1)
+    return [project(c.reshape(nl, b, d), w["wo"], exact) for c in ctx4]
+
+
 # ---------------------------------------------------------------------------
 # seeded synthetic inputs (SURVEY 8(d))
 # ---------------------------------------------------------------------------

@@ -19,7 +19,7 @@ from .attention import (  # noqa: F401
     seq_all_to_all,
 )
 from .comm import CommLedger, CommRecord, SequenceGroup, a2a_out_shape, check_ledger  # noqa: F401
-from .layer import UlyssesAttention, UlyssesBlock, make_weights  # noqa: F401
+from .layer import HybridAttention, RingAttention, UlyssesAttention, UlyssesBlock, make_weights, ring_attention_core  # noqa: F401
 from .errors import (  # noqa: F401
     DegenerateRowError,
     DivisibilityError,

@@ -287,6 +287,26 @@ class SequenceGroup:
         return sum(r.aggregate_elements for r in self.records)
 
     # -- the collective ----------------------------------------------------
+    def ring_shift(self, tensors, steps: int = 1, label: str = "ring_shift", labels=None):
+        """RankContext.ring_shift (simgroup.py:374-388, 464-465) for 1..4
+        tensors at once: rank i receives rank (i - steps) mod P's tensors
+        (fresh outputs).  A collective over peer memory (ul_ring_shift)."""
+        tensors = [t.contiguous() for t in tensors]
+        if not tensors or len(tensors) > _lib.MAX_FUSED:
+            raise ValueError(f"ring_shift moves 1..{_lib.MAX_FUSED} tensors, got {len(tensors)}")
+        if steps < 0:
+            raise ValueError(f"ring_shift steps must be >= 0, got {steps}")
+        outs = [torch.empty_like(t) for t in tensors]
+        for t, lab in zip(tensors, labels or [label] * len(tensors)):
+            self.records.append(CommRecord("ring_shift", lab, self.world * t.numel(), t.numel() * steps))
+        inp = (ctypes.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
+        outp = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        nbytes = (ctypes.c_int64 * len(tensors))(*[t.numel() * t.element_size() for t in tensors])
+        stream = torch.cuda.current_stream(tensors[0].device).cuda_stream
+        _lib.check(_lib.lib().ul_ring_shift(self._handle, len(tensors), inp, outp, nbytes, steps,
+                                            label_hash(label), stream))
+        return outs
+
     def qkv_projection(self, x2: torch.Tensor, w: torch.Tensor, b: int, hq: int, hkv: int,
                        labels=("attn.q.seq2head", "attn.k.seq2head", "attn.v.seq2head")):
         """project(x, wq|wk|wv) (layers.py:118-122) fused with the three

@@ -789,6 +789,98 @@ int ul_all_to_all(ul_comm* c, int n, const void* const* in, void* const* out, co
   return wait_and_drain(c, pl, out, st);
 }
 
+// a flat byte range as rows of `run` bytes (so every warp of the copy gets rows)
+static void flat_box(const char* src, char* dst, int64_t bytes, Box* b) {
+  int64_t run = 4096;
+  while (run > 16 && (bytes % run) != 0) run >>= 1;
+  if (bytes % run != 0) run = bytes;   // (unaligned tail: one row)
+  b->src = src;
+  b->dst = dst;
+  b->run = run;
+  for (int i = 0; i < 3; ++i) b->ext[i] = 1, b->sst[i] = 0, b->dstr[i] = 0;
+  b->ext[2] = run ? bytes / run : 0;
+  b->sst[2] = b->dstr[2] = run;
+  b->rows = bytes > 0 ? b->ext[2] : 0;
+  const uint64_t al = (uint64_t)run | (uint64_t)(uintptr_t)src | (uint64_t)(uintptr_t)dst;
+  b->vec = (al % 16 == 0) ? 16 : (al % 8 == 0) ? 8 : (al % 4 == 0) ? 4 : 2;
+}
+
+int ul_ring_shift(ul_comm* c, int n, const void* const* in, void* const* out, const int64_t* bytes, int steps,
+                  uint64_t label, void* stream) {
+  launch_count() = 0;
+  if (n < 1 || n > UL_MAX_FUSED) return fail(UL_ERR_ARG, "ring_shift: fuses 1..%d tensors, got %d", UL_MAX_FUSED, n);
+  if (!in || !out || !bytes) return fail(UL_ERR_ARG, "ring_shift: NULL argument");
+  if (steps < 0) return fail(UL_ERR_ARG, "ring_shift steps must be >= 0, got %d", steps);
+  const int P = c ? c->world : 1, me = c ? c->rank : 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int k = steps % P;
+  size_t off[UL_MAX_FUSED], need = 0;
+  uint64_t sig = 1469598103934665603ull, total = 0;
+  sig = fnv(sig, 0x72696e67ull);   // "ring"
+  sig = fnv(sig, (uint64_t)n);
+  sig = fnv(sig, (uint64_t)steps);
+  sig = fnv(sig, label);
+  for (int t = 0; t < n; ++t) {
+    if (!in[t] || !out[t] || bytes[t] < 0) return fail(UL_ERR_ARG, "ring_shift: bad tensor %d", t);
+    sig = fnv(sig, (uint64_t)bytes[t]);
+    off[t] = need;
+    need += align_up((size_t)bytes[t], 256);
+    total += (uint64_t)bytes[t];
+  }
+  CopyParams cp;
+  memset(&cp, 0, sizeof(cp));
+  if (P == 1 || k == 0) {   // the payload stays on this rank: a local copy (+ a barrier for P > 1)
+    for (int t = 0; t < n; ++t) {
+      flat_box((const char*)in[t], (char*)out[t], bytes[t], &cp.box[cp.nbox]);
+      if (cp.box[cp.nbox].rows > 0) ++cp.nbox;
+    }
+    if (P == 1) return launch_copy(cp, st, "ring_local");
+  }
+  if (need > c->slot_bytes)
+    return fail(UL_ERR_ARG, "ring_shift: call needs %zu receive-slot bytes, workspace has %zu", need, c->slot_bytes);
+  for (int r = 0; r < P; ++r)
+    if (!c->peer_base[r]) return fail(UL_ERR_STATE, "ring_shift: rank %d has no mapping for peer %d", me, r);
+  const uint64_t epoch = ++c->epoch;
+  const int slot = (int)(epoch & 1);
+  c->calls += 1;
+  c->aggregate += (uint64_t)P * total;
+  c->egress += total * (uint64_t)steps;   // simgroup.py:383-385 metering
+  const int dst = (me + k) % P, src = (me - k + P) % P;
+  if (k != 0) {
+    for (int t = 0; t < n; ++t) {
+      flat_box((const char*)in[t], c->peer_base[dst] + (size_t)slot * c->slot_bytes + off[t], bytes[t],
+               &cp.box[cp.nbox]);
+      if (cp.box[cp.nbox].rows > 0) ++cp.nbox;
+    }
+  }
+  // every rank signals every peer (a full barrier, like the reference's collectives)
+  cp.signal = 1;
+  cp.rank = me;
+  cp.world = P;
+  cp.slot = slot;
+  cp.epoch = epoch;
+  cp.sig = sig;
+  for (int r = 0; r < P; ++r) cp.peer_sig[r] = (Signals*)(c->peer_base[r] + 2 * c->slot_bytes);
+  cp.counter = &((Signals*)(c->base + 2 * c->slot_bytes))->counter[slot];
+  if (cp.nbox == 0) {
+    flat_box((const char*)in[0], (char*)out[0], 0, &cp.box[0]);
+    cp.nbox = 1;
+  }
+  UL_TRY(launch_copy(cp, st, "ring_push"));
+  Signals* mine = (Signals*)(c->base + 2 * c->slot_bytes);
+  a2a_wait_kernel<<<1, 32, 0, st>>>(mine, me, P, slot, epoch, sig, c->timeout_ns, &mine->err, c->err_dev);
+  UL_TRY(launched("a2a_wait"));
+  if (k == 0) return UL_OK;
+  (void)src;
+  CopyParams dp;
+  memset(&dp, 0, sizeof(dp));
+  for (int t = 0; t < n; ++t) {   // the predecessor's payload sits in my slot
+    flat_box(c->base + (size_t)slot * c->slot_bytes + off[t], (char*)out[t], bytes[t], &dp.box[dp.nbox]);
+    if (dp.box[dp.nbox].rows > 0) ++dp.nbox;
+  }
+  return launch_copy(dp, st, "ring_drain");
+}
+
 int ul_ulysses_volume(int64_t n, int64_t b, int64_t d, int64_t p, int convention, int64_t* num,
                       int64_t* den) {
   if (!num || !den || n < 1 || b < 1 || d < 1 || p < 1)

@@ -153,3 +153,106 @@ class UlyssesBlock(torch.nn.Module):
         x1 = x + self.attn(t1)
         t2 = F.layer_norm(x1, (d,), self.ln2_gain, self.ln2_bias, eps=LN_EPS)
         return x1 + F.gelu(t2 @ self.w1, approximate="none") @ self.w2           # layers.py:113-127
+
+
+# ---------------------------------------------------------------------------
+# ring attention (first step: the ring half of a hybrid)
+# ---------------------------------------------------------------------------
+
+def ring_attention_core(q, k, v, group, mask: str = "causal", prefix: str = "attn"):
+    """Ring self-attention on sequence shards [n/P, b, h, hd] (baselines.py:
+    68-121: Q local, K and V circulate P-1 steps; the reference fills full
+    score rows, here every arriving chunk is one local-attention call that
+    also returns its row LSE, and the partial contexts are merged exactly:
+    o = sum_j exp(lse_j - lse) o_j with lse = logsumexp_j lse_j).  With
+    contiguous shards, chunk src of rank r is dense (src < r), causal
+    (src == r) or invisible (src > r) under the causal mask (tensor.py:161).
+    Forward only, like the reference's ring baseline.  Usable when P > H_kv,
+    where Ulysses cannot split the kv heads."""
+    if mask not in ("causal", "none"):
+        from .errors import KernelError
+        raise KernelError(f"ring attention supports dense/causal masks, got {mask!r}")
+    p, r = group.world, group.rank
+    o_acc = lse_acc = None
+    cur_k, cur_v = k, v
+    dense, causal = FlashAttention("none"), FlashAttention("causal")
+    for step in range(p):
+        src = (r - step) % p
+        if mask == "none" or src <= r:
+            attn = causal if (mask == "causal" and src == r) else dense
+            o_s, lse_s = attn.forward_with_lse(q, cur_k, cur_v)        # lse [b, h, n/P]
+            lse_s = lse_s.permute(2, 0, 1).unsqueeze(-1)                  # -> [n/P, b, h, 1]
+            if o_acc is None:
+                o_acc, lse_acc = o_s.float(), lse_s
+            else:
+                lse_new = torch.logaddexp(lse_acc, lse_s)
+                o_acc = o_acc * torch.exp(lse_acc - lse_new) + o_s.float() * torch.exp(lse_s - lse_new)
+                lse_acc = lse_new
+        if step < p - 1:
+            cur_k, cur_v = group.ring_shift([cur_k, cur_v], 1, labels=[f"{prefix}.kring.{step}",
+                                                                      f"{prefix}.vring.{step}"])
+    return o_acc.to(q.dtype)
+
+
+class RingAttention(torch.nn.Module):
+    """``ring_attention_forward`` (baselines.py:68-121): projections, the ring
+    core above, output projection.  ``forward(x)``: [n/P, b, d] -> [n/P, b, d]."""
+
+    def __init__(self, d_model: int, heads: int, sequence_process_group=None, mask: str = "causal",
+                 weights: dict | None = None, dtype=torch.bfloat16, device=None, seed: int = 0):
+        super().__init__()
+        from .attention import _group
+        if d_model % heads != 0:
+            raise DivisibilityError(f"head count {heads} does not divide hidden size {d_model}")
+        self.d, self.h, self.hd, self.mask = d_model, heads, d_model // heads, mask
+        device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        w = weights if weights is not None else make_weights(d_model, seed)
+        self.wq, self.wk, self.wv, self.wo = (_param(w[k], dtype, device) for k in ("wq", "wk", "wv", "wo"))
+        self.group = _group(sequence_process_group)
+
+    @torch.no_grad()
+    def forward(self, x, prefix: str = "L0.attn"):
+        nl, b, d = x.shape
+        x2 = x.reshape(nl * b, d)
+        four = lambda t: t.reshape(nl, b, self.h, self.hd).contiguous()
+        q, k, v = four(x2 @ self.wq), four(x2 @ self.wk), four(x2 @ self.wv)
+        c = ring_attention_core(q, k, v, self.group, self.mask, prefix)
+        return (c.reshape(nl * b, d) @ self.wo).reshape(nl, b, d)
+
+
+class HybridAttention(torch.nn.Module):
+    """Ulysses x ring: P = P_u * P_r ranks, rank index
+    ring-major (rank = i * P_u + j).  Ulysses over the P_u ranks of a ring
+    position (heads split P_u ways, sequence gathered to the n/P_r tokens of
+    ring chunk i -- contiguous global positions), ring attention over the
+    P_r ranks holding the same heads, Ulysses back.  For P beyond the head
+    count (P_u <= H_kv) or across nodes (ring over the slow links).
+    Forward only (the reference's ring is)."""
+
+    def __init__(self, d_model: int, heads: int, ulysses_group, ring_group, mask: str = "causal",
+                 weights: dict | None = None, dtype=torch.bfloat16, device=None, seed: int = 0):
+        super().__init__()
+        from .attention import _group
+        if d_model % heads != 0:
+            raise DivisibilityError(f"head count {heads} does not divide hidden size {d_model}")
+        self.ug, self.rg = _group(ulysses_group), _group(ring_group)
+        if heads % self.ug.world:
+            raise DivisibilityError(f"p_ulysses={self.ug.world} does not divide head count {heads}")
+        self.d, self.h, self.hd, self.mask = d_model, heads, d_model // heads, mask
+        device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        w = weights if weights is not None else make_weights(d_model, seed)
+        self.wq, self.wk, self.wv, self.wo = (_param(w[k], dtype, device) for k in ("wq", "wk", "wv", "wo"))
+
+    @torch.no_grad()
+    def forward(self, x):
+        nl, b, d = x.shape
+        x2 = x.reshape(nl * b, d)
+        four = lambda t: t.reshape(nl, b, self.h, self.hd).contiguous()
+        q, k, v = four(x2 @ self.wq), four(x2 @ self.wk), four(x2 @ self.wv)
+        if self.ug.world > 1:
+            q, k, v = self.ug.all_to_all([q, k, v], 2, 0, label="attn.qkv.seq2head",
+                                         labels=["attn.q.seq2head", "attn.k.seq2head", "attn.v.seq2head"])
+        c = ring_attention_core(q, k, v, self.rg, self.mask, "attn")
+        if self.ug.world > 1:
+            (c,) = self.ug.all_to_all([c], 0, 2, label="attn.ctx.head2seq")
+        return (c.reshape(nl * b, d) @ self.wo).reshape(nl, b, d)

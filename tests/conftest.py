@@ -1,7 +1,13 @@
 import os
 import sys
 
-import pytest
+# In-process sequence groups run P ranks on P streams of one GPU, and a
+# rank's device-side flag wait spins until a peer's push (another stream)
+# lands: streams must not share a hardware work queue, or the push queues
+# behind the spin.  32 connections (read at CUDA context creation).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+import pytest  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:

@@ -44,6 +44,11 @@ def warm_streams(groups, dtypes=(torch.float32, torch.bfloat16), mb=256):
                 (a @ a).sum().item()
                 t = torch.nn.functional.layer_norm(a, (256,))
                 torch.nn.functional.gelu(t).sum()
+                # the ring merge's elementwise kernels (ring_attention_core)
+                f = a.float().reshape(256, 1, 256, 1)
+                m = torch.logaddexp(f, f)
+                ((f * torch.exp(f - m) + f * torch.exp(m - f)).to(dt)).sum()
+                f.permute(2, 0, 1, 3).unsqueeze(-1).contiguous()
             del a
             torch.empty(mb << 20, dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()

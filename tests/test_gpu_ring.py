@@ -1,0 +1,113 @@
+"""Ring attention (the ring half of a hybrid) and the
+ring_shift collective on the B200, against the reference's ring baseline
+(tests/golden/layer.npz: run_ring_attention, baselines.py:68-155) and the
+oracle (simgroup.py:374-388 for ring_shift)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+from helpers import BF16_MAXREL, assert_rtol, rel_max_err, run_ranks, to_dev, to_np, warm_streams
+from oracle import ulysses_oracle as O
+
+pytestmark = pytest.mark.gpu
+LAYER_RTOL = 1e-4
+
+
+def U():
+    import paper_2309_14509_b200 as mod
+    return mod
+
+
+@pytest.mark.parametrize("p,steps", [(2, 1), (3, 1), (3, 2), (4, 0), (4, 5)])
+def test_ring_shift_bitwise(p, steps):
+    groups = U().SequenceGroup.local_group(p, slot_bytes=4 << 20)
+    xs = [O.make_tensor((37, 3, 8), 90 + r, 1) for r in range(p)]
+    ys = [O.make_tensor((129,), 90 + r, 2) for r in range(p)]
+    ins = run_ranks(groups, lambda r: [to_dev(xs[r]), to_dev(ys[r], torch.bfloat16)])
+    outs = run_ranks(groups, lambda r: groups[r].ring_shift(ins[r], steps, label="t"))
+    ex, ey = O.ring_shift(xs, steps), O.ring_shift([O.bf16_round(y) for y in ys], steps)
+    for r in range(p):
+        assert np.array_equal(to_np(outs[r][0]), ex[r]) and np.array_equal(to_np(outs[r][1]), ey[r])
+        rec = groups[r].ledger.select("ring_shift")
+        assert rec[0].aggregate_elements == p * 37 * 3 * 8 and rec[0].per_rank_egress_elements == 37 * 3 * 8 * steps
+
+
+class _LoopbackRing:
+    """world-2 stand-in whose ring_shift returns its input: drives
+    ring_attention_core through the merge path on one stream, so every
+    kernel it launches is loaded before an in-process group runs (lazy
+    module loading can block the host thread that still has to issue the
+    peers' pushes)."""
+    world, rank = 2, 1
+
+    def ring_shift(self, tensors, steps=1, label="", labels=None):
+        return [t.clone() for t in tensors]
+
+
+def warm_ring_merge(n, b, h, hd, dtype):
+    mk = lambda: torch.randn((n, b, h, hd), device="cuda").to(dtype)
+    U().ring_attention_core(mk(), mk(), mk(), _LoopbackRing(), "causal")
+
+
+def run_ring(p, d, h, kind, x, w, dtype):
+    n = x.shape[0]
+    nl = n // p
+    groups = U().SequenceGroup.local_group(p, slot_bytes=16 << 20) if p > 1 else [U().SequenceGroup.single()]
+    warm_streams(groups)
+    t = to_dev(x[:nl], dtype)   # load every library kernel of these shapes first
+    U().RingAttention(d, h, None, kind, weights=w, dtype=dtype)(t)
+    torch.cuda.synchronize()
+    mods = run_ranks(groups, lambda r: U().RingAttention(d, h, groups[r], kind, weights=w, dtype=dtype))
+    xs = run_ranks(groups, lambda r: to_dev(x[r * nl:(r + 1) * nl], dtype))
+    outs = run_ranks(groups, lambda r: mods[r](xs[r]))
+    return np.concatenate([to_np(o) for o in outs], 0), groups
+
+
+@pytest.mark.parametrize("ci", range(3))
+def test_ring_fp32_vs_reference(ci):
+    g = np.load(os.path.join(GOLDEN, "layer.npz"))
+    p, n, b, d, h, causal, seed = (int(x) for x in g[f"ring{ci}_meta"])
+    out, groups = run_ring(p, d, h, "causal" if causal else "none", O.make_input(n, b, d, seed),
+                           O.make_weights(d, seed), torch.float32)
+    assert_rtol(out, g[f"ring{ci}_out"], rtol=LAYER_RTOL)
+    nl = n // p
+    for grp in groups:   # 2 (P-1) ring shifts of n/P*b*d elements, the reference's metering
+        led = grp.ledger.select("ring_shift")
+        assert len(led) == 2 * (p - 1)
+        assert all(r.aggregate_elements == p * nl * b * d and r.per_rank_egress_elements == nl * b * d for r in led)
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_ring_bf16_vs_oracle_and_ulysses(p):
+    # hd 128 on the tcgen05 kernels; ring and Ulysses compute the same layer
+    n, b, d, h, seed = 512, 1, 512, 4, 5
+    w = {k: O.bf16_round(v) for k, v in O.make_weights(d, seed).items()}
+    x = O.bf16_round(O.make_input(n, b, d, seed))
+    out, _ = run_ring(p, d, h, "causal", x, w, torch.bfloat16)
+    nl = n // p
+    ref = np.concatenate(O.ring_attention_layer([x[r * nl:(r + 1) * nl] for r in range(p)], w, h, "causal",
+                                                exact=False))
+    assert rel_max_err(out, ref) <= BF16_MAXREL
+
+
+@pytest.mark.parametrize("pu,pr,dtype", [(2, 2, "float32"), (2, 2, "bfloat16"), (4, 2, "bfloat16")])
+def test_hybrid_ulysses_ring(pu, pr, dtype):
+    # P = pu * pr ranks, ring-major, two sub-groups per rank; same layer as
+    # plain attention.  Runs in a child process with eager CUDA module
+    # loading: the ranks of an in-process group are issued by one host
+    # thread, and a lazily loaded kernel (first launch) can block that
+    # thread while an earlier rank's stream spins in a flag wait
+    import json
+    import subprocess
+    import sys
+    from conftest import ROOT
+    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "hybrid_worker.py"), str(pu), str(pr), dtype],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["ok"], res

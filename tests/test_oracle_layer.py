@@ -44,3 +44,18 @@ def test_package_weights_match_reference_draws():
     from paper_2309_14509_b200.layer import make_weights
     a, b = make_weights(32, 5, 1), O.make_weights(32, 5, 1)
     assert all(np.array_equal(a[k], b[k]) for k in b)
+
+
+@pytest.mark.parametrize("ci", range(3))
+def test_ring_attention_bitwise(ci):
+    # the reference's ring baseline (baselines.py:68-121, run_ring_attention)
+    g = np.load(os.path.join(GOLDEN, "layer.npz"))
+    p, n, b, d, h, causal, seed = (int(x) for x in g[f"ring{ci}_meta"])
+    x, w = O.make_input(n, b, d, seed), O.make_weights(d, seed)
+    nl = n // p
+    out = O.ring_attention_layer([x[r * nl:(r + 1) * nl] for r in range(p)], w, h, "causal" if causal else "none")
+    assert np.array_equal(np.concatenate(out), g[f"ring{ci}_out"])
+    # its ledger: 2 (P-1) ring shifts of the local (n/P, b, d) tensor, metered (P*local, local)
+    led = g[f"ring{ci}_ledger"]
+    assert len(led) == 2 * (p - 1)
+    assert all(int(a) == p * nl * b * d and int(e) == nl * b * d for a, e in led)
