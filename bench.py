@@ -148,27 +148,30 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 def _cpu_sample_worker(args):
-    n_s, hd, seed = args
+    n_s, hd, seed = args[:3]
+    reps = args[3] if len(args) > 3 else 1
     import numpy as np
     from oracle import ulysses_oracle as O
     q, k, v, do = (O.make_tensor((n_s, 1, hd), seed, s) for s in (1, 2, 3, 4))
     t0 = time.perf_counter()
     scale = 1.0 / math.sqrt(hd)
-    O.attention_head(q, k, v, "causal", scale)               # kernels.py:31-52 (fixed-order matmul)
-    O.attention_head_backward(q, k, v, do, "causal", scale)  # kernels.py:89-111
-    return time.perf_counter() - t0
+    for _ in range(reps):                                     # `reps` heads of the same shape
+        O.attention_head(q, k, v, "causal", scale)               # kernels.py:31-52 (fixed-order matmul)
+        O.attention_head_backward(q, k, v, do, "causal", scale)  # kernels.py:89-111
+    return (time.perf_counter() - t0) / reps
 
 
-def cpu_baseline(n_seq, heads, hd, procs=1, n_sample=1024):
+def cpu_baseline(n_seq, heads, hd, procs=1, n_sample=1024, heads_sample=1):
     """Time the reference algorithm (oracle port, fixed-order f64 matmul) on
     `procs` host processes, one head of N=n_sample each, and extrapolate by
     N^2 * hd * heads to the full workload (the reference is O(N^2 hd) per head
     with full n x n scores, kernels.py:37)."""
     import multiprocessing as mp
     if procs <= 1:
-        dt = _cpu_sample_worker((n_sample, hd, 0))
+        reps = heads_sample
+        dt = _cpu_sample_worker((n_sample, hd, 0, reps))
         per_head = dt
-        wall = dt
+        wall = dt * reps
     else:
         ctx = mp.get_context("fork")
         with ctx.Pool(procs) as pool:
@@ -178,8 +181,9 @@ def cpu_baseline(n_seq, heads, hd, procs=1, n_sample=1024):
         per_head = wall / procs            # throughput-equivalent seconds per sampled head
     scale = (n_seq / n_sample) ** 2 * heads
     t_full = per_head * scale
+    nh = procs if procs > 1 else heads_sample
     return {"tokens_per_s": n_seq / t_full, "seconds_full_extrapolated": t_full, "sample_wall_s": wall,
-            "sample": f"{procs} x causal fwd+bwd head of N={n_sample}, hd={hd} (f64, reference fixed-order "
+            "sample": f"{nh} x causal fwd+bwd head of N={n_sample}, hd={hd} (f64, reference fixed-order "
                       f"matmul); extrapolated by N^2*hd*heads to N={n_seq}, {heads} heads"}
 
 
@@ -333,7 +337,8 @@ def run_ours(args):
             "clocks": clocks,
         }
     if args.cpu_baseline and rank == 0:
-        cb = cpu_baseline(n_seq, H, hd, procs=1, n_sample=args.cpu_sample)
+        # ~10-15 s of single-core reference work: two heads of N = 2048
+        cb = cpu_baseline(n_seq, H, hd, procs=1, n_sample=2 * args.cpu_sample, heads_sample=2)
         result["cpu_baseline"] = {"value": round(cb["tokens_per_s"], 4), "unit": "tokens/s", "cores": 1,
                                   "kind": "port", "sample": cb["sample"],
                                   "sample_wall_s": round(cb["sample_wall_s"], 2)}
