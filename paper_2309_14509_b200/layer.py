@@ -159,19 +159,9 @@ class UlyssesBlock(torch.nn.Module):
 # ring attention (first step: the ring half of a hybrid)
 # ---------------------------------------------------------------------------
 
-def ring_attention_core(q, k, v, group, mask: str = "causal", prefix: str = "attn"):
-    """Ring self-attention on sequence shards [n/P, b, h, hd] (baselines.py:
-    68-121: Q local, K and V circulate P-1 steps; the reference fills full
-    score rows, here every arriving chunk is one local-attention call that
-    also returns its row LSE, and the partial contexts are merged exactly:
-    o = sum_j exp(lse_j - lse) o_j with lse = logsumexp_j lse_j).  With
-    contiguous shards, chunk src of rank r is dense (src < r), causal
-    (src == r) or invisible (src > r) under the causal mask (tensor.py:161).
-    Forward only, like the reference's ring baseline.  Usable when P > H_kv,
-    where Ulysses cannot split the kv heads."""
-    if mask not in ("causal", "none"):
-        from .errors import KernelError
-        raise KernelError(f"ring attention supports dense/causal masks, got {mask!r}")
+def _ring_forward(q, k, v, group, mask, prefix):
+    """Forward of the ring core: returns (o, lse [b, h, n/P]) with the
+    partial contexts merged exactly in fp32."""
     p, r = group.world, group.rank
     o_acc = lse_acc = None
     cur_k, cur_v = k, v
@@ -191,7 +181,66 @@ def ring_attention_core(q, k, v, group, mask: str = "causal", prefix: str = "att
         if step < p - 1:
             cur_k, cur_v = group.ring_shift([cur_k, cur_v], 1, labels=[f"{prefix}.kring.{step}",
                                                                       f"{prefix}.vring.{step}"])
-    return o_acc.to(q.dtype)
+    return o_acc.to(q.dtype), lse_acc.squeeze(-1).permute(1, 2, 0).contiguous()
+
+
+class _RingAttnFn(torch.autograd.Function):
+    """Ring attention with its backward: K/V circulate again, each visible
+    chunk runs the local backward kernels with the GLOBAL (merged) O and LSE
+    -- P = exp(S - LSE) and D = rowsum(dO O) are then the full-row values, so
+    the chunk gradients are exact partial sums -- dQ accumulates locally,
+    dK/dV contributions travel with their chunk and a last shift brings
+    them home (fp32 accumulators)."""
+
+    @staticmethod
+    def forward(ctx, group, mask, prefix, q, k, v):
+        o, lse = _ring_forward(q, k, v, group, mask, prefix)
+        ctx.group, ctx.mask, ctx.prefix = group, mask, prefix
+        ctx.save_for_backward(q, k, v, o, lse)
+        return o
+
+    @staticmethod
+    def backward(ctx, do):
+        group, mask, prefix = ctx.group, ctx.mask, ctx.prefix
+        q, k, v, o, lse = ctx.saved_tensors
+        do = do.contiguous()
+        p, r = group.world, group.rank
+        dense, causal = FlashAttention("none"), FlashAttention("causal")
+        dq = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
+        cur = [k, v, torch.zeros(k.shape, dtype=torch.float32, device=k.device),
+               torch.zeros(v.shape, dtype=torch.float32, device=v.device)]
+        for step in range(p):
+            src = (r - step) % p
+            if mask == "none" or src <= r:
+                attn = causal if (mask == "causal" and src == r) else dense
+                dq_c, dk_c, dv_c = attn.backward(q, cur[0], cur[1], o, lse, do)
+                dq += dq_c.float()
+                cur[2] += dk_c.float()
+                cur[3] += dv_c.float()
+            if step < p - 1:
+                cur = group.ring_shift(cur, 1, labels=[f"{prefix}.bwd.kring.{step}", f"{prefix}.bwd.vring.{step}",
+                                                       f"{prefix}.bwd.dkring.{step}", f"{prefix}.bwd.dvring.{step}"])
+        dk, dv = cur[2], cur[3]
+        if p > 1:   # the accumulators of chunk r are one hop away
+            dk, dv = group.ring_shift([dk, dv], 1, labels=[f"{prefix}.bwd.dkring.home", f"{prefix}.bwd.dvring.home"])
+        return None, None, None, dq.to(q.dtype), dk.to(k.dtype), dv.to(v.dtype)
+
+
+def ring_attention_core(q, k, v, group, mask: str = "causal", prefix: str = "attn"):
+    """Ring self-attention on sequence shards [n/P, b, h, hd] (baselines.py:
+    68-121: Q local, K and V circulate P-1 steps; the reference fills full
+    score rows, here every arriving chunk is one local-attention call that
+    also returns its row LSE, and the partial contexts are merged exactly:
+    o = sum_j exp(lse_j - lse) o_j with lse = logsumexp_j lse_j).  With
+    contiguous shards, chunk src of rank r is dense (src < r), causal
+    (src == r) or invisible (src > r) under the causal mask (tensor.py:161).
+    Differentiable (the reference's ring baseline is forward only; the
+    backward here is _RingAttnFn's).  Usable when P > H_kv, where Ulysses
+    cannot split the kv heads."""
+    if mask not in ("causal", "none"):
+        from .errors import KernelError
+        raise KernelError(f"ring attention supports dense/causal masks, got {mask!r}")
+    return _RingAttnFn.apply(group, mask, prefix, q.contiguous(), k.contiguous(), v.contiguous())
 
 
 class RingAttention(torch.nn.Module):
@@ -210,7 +259,6 @@ class RingAttention(torch.nn.Module):
         self.wq, self.wk, self.wv, self.wo = (_param(w[k], dtype, device) for k in ("wq", "wk", "wv", "wo"))
         self.group = _group(sequence_process_group)
 
-    @torch.no_grad()
     def forward(self, x, prefix: str = "L0.attn"):
         nl, b, d = x.shape
         x2 = x.reshape(nl * b, d)
@@ -227,7 +275,7 @@ class HybridAttention(torch.nn.Module):
     ring chunk i -- contiguous global positions), ring attention over the
     P_r ranks holding the same heads, Ulysses back.  For P beyond the head
     count (P_u <= H_kv) or across nodes (ring over the slow links).
-    Forward only (the reference's ring is)."""
+    Differentiable (ring backward: _RingAttnFn)."""
 
     def __init__(self, d_model: int, heads: int, ulysses_group, ring_group, mask: str = "causal",
                  weights: dict | None = None, dtype=torch.bfloat16, device=None, seed: int = 0):
@@ -243,16 +291,15 @@ class HybridAttention(torch.nn.Module):
         w = weights if weights is not None else make_weights(d_model, seed)
         self.wq, self.wk, self.wv, self.wo = (_param(w[k], dtype, device) for k in ("wq", "wk", "wv", "wo"))
 
-    @torch.no_grad()
     def forward(self, x):
+        from .attention import seq_all_to_all
         nl, b, d = x.shape
         x2 = x.reshape(nl * b, d)
         four = lambda t: t.reshape(nl, b, self.h, self.hd).contiguous()
         q, k, v = four(x2 @ self.wq), four(x2 @ self.wk), four(x2 @ self.wv)
-        if self.ug.world > 1:
-            q, k, v = self.ug.all_to_all([q, k, v], 2, 0, label="attn.qkv.seq2head",
-                                         labels=["attn.q.seq2head", "attn.k.seq2head", "attn.v.seq2head"])
+        if self.ug.world > 1:   # differentiable flips (backward swaps the axes)
+            q, k, v = (seq_all_to_all(t, 2, 0, self.ug, f"attn.{n}.seq2head") for t, n in ((q, "q"), (k, "k"), (v, "v")))
         c = ring_attention_core(q, k, v, self.rg, self.mask, "attn")
         if self.ug.world > 1:
-            (c,) = self.ug.all_to_all([c], 0, 2, label="attn.ctx.head2seq")
+            c = seq_all_to_all(c, 0, 2, self.ug, "attn.ctx.head2seq")
         return (c.reshape(nl * b, d) @ self.wo).reshape(nl, b, d)

@@ -49,14 +49,25 @@ def run_all(fn):
 
 # per-stream library setup (cuBLAS handles/workspaces) and a single-rank pass first
 warm_streams(flat)
-U.HybridAttention(d, h, None, None, "causal", weights=w, dtype=dtype)(to_dev(x[:nl], dtype))
+_t = to_dev(x[:nl], dtype).requires_grad_(True)
+_o = U.HybridAttention(d, h, None, None, "causal", weights=w, dtype=dtype)(_t)
+_o.backward(torch.ones_like(_o))
 torch.cuda.synchronize()
 mods = run_all(lambda r: U.HybridAttention(d, h, ug[r // pu][r % pu], rg[r % pu][r // pu], "causal",
                                            weights=w, dtype=dtype))
-xs = run_all(lambda r: to_dev(x[r * nl:(r + 1) * nl], dtype))
+go = O.bf16_round(O.make_input(n, b, d, seed + 1))
+xs = run_all(lambda r: to_dev(x[r * nl:(r + 1) * nl], dtype).requires_grad_(True))
+gs = run_all(lambda r: to_dev(go[r * nl:(r + 1) * nl], dtype))
 outs = run_all(lambda r: mods[r](xs[r]))
+run_all(lambda r: torch.autograd.backward([outs[r]], [gs[r]]))
 out = np.concatenate([to_np(o) for o in outs], 0)
 ref = np.concatenate(O.ring_attention_layer([x], w, h, "causal", exact=False))   # P = 1: plain attention layer
 err = rel_max_err(out, ref)
+# gradients: the same function's, oracle = the attention layer's backward at P = 1
+_, st = O.ulysses_attention_layer([x], w, h, "causal", exact=False)
+rgx, rgw = O.ulysses_attention_layer_backward([go], st, w, "causal", exact=False)
+gx = np.concatenate([to_np(t.grad) for t in xs], 0)
+gerr = max([rel_max_err(gx, rgx[0])] + [rel_max_err(sum(to_np(getattr(m, k).grad) for m in mods), rgw[k])
+                                        for k in ("wq", "wk", "wv", "wo")])
 tol = 1e-4 if dtype == torch.float32 else BF16_MAXREL
-print(json.dumps({"ok": bool(err <= tol), "err": err, "tol": tol}))
+print(json.dumps({"ok": bool(err <= tol and gerr <= tol), "err": err, "grad_err": gerr, "tol": tol}))

@@ -53,6 +53,13 @@ def warm_ring_merge(n, b, h, hd, dtype):
     U().ring_attention_core(mk(), mk(), mk(), _LoopbackRing(), "causal")
 
 
+def warm_ring_backward(n, b, h, hd, dtype):
+    mk = lambda: torch.randn((n, b, h, hd), device="cuda").to(dtype).requires_grad_(True)
+    q, k, v = mk(), mk(), mk()
+    o = U().ring_attention_core(q, k, v, _LoopbackRing(), "causal")
+    o.backward(torch.ones_like(o))
+
+
 def run_ring(p, d, h, kind, x, w, dtype):
     n = x.shape[0]
     nl = n // p
@@ -111,3 +118,41 @@ def test_hybrid_ulysses_ring(pu, pr, dtype):
     assert r.returncode == 0, r.stderr[-3000:]
     res = json.loads(r.stdout.strip().splitlines()[-1])
     assert res["ok"], res
+
+
+@pytest.mark.parametrize("p,dtype", [(2, torch.float32), (3, torch.float32), (2, torch.bfloat16), (4, torch.bfloat16)])
+def test_ring_backward_vs_oracle(p, dtype):
+    # the ring layer's gradients equal the attention layer's (same function):
+    # oracle = ulysses_attention_layer(_backward) at P = 1
+    hd = 128 if dtype == torch.bfloat16 else 16
+    h = 4
+    d, b, seed = h * hd, 1, 8
+    n = 96 * p
+    nl = n // p
+    w = {k: O.bf16_round(v) for k, v in O.make_weights(d, seed).items()}
+    x, go = O.bf16_round(O.make_input(n, b, d, seed)), O.bf16_round(O.make_input(n, b, d, seed + 1))
+    groups = U().SequenceGroup.local_group(p, slot_bytes=16 << 20)
+    warm_streams(groups)
+    t = to_dev(x[:nl], dtype).requires_grad_(True)   # single-rank pass: load every kernel first
+    mod1 = U().RingAttention(d, h, None, "causal", weights=w, dtype=dtype)
+    torch.autograd.backward([mod1(t)], [to_dev(go[:nl], dtype)])
+    warm_ring_merge(nl, b, h, hd, dtype)
+    warm_ring_backward(nl, b, h, hd, dtype)
+    torch.cuda.synchronize()
+    mods = run_ranks(groups, lambda r: U().RingAttention(d, h, groups[r], "causal", weights=w, dtype=dtype))
+    xs = run_ranks(groups, lambda r: to_dev(x[r * nl:(r + 1) * nl], dtype).requires_grad_(True))
+    gs = run_ranks(groups, lambda r: to_dev(go[r * nl:(r + 1) * nl], dtype))
+    outs = run_ranks(groups, lambda r: mods[r](xs[r]))
+    run_ranks(groups, lambda r: torch.autograd.backward([outs[r]], [gs[r]]))
+    gx = np.concatenate([to_np(t.grad) for t in xs], 0)
+    gw = {k: sum(to_np(getattr(m, k).grad) for m in mods) for k in ("wq", "wk", "wv", "wo")}
+    ro, st = O.ulysses_attention_layer([x], w, h, "causal", exact=False)
+    rgx, rgw = O.ulysses_attention_layer_backward([go], st, w, "causal", exact=False)
+    if dtype == torch.float32:
+        assert_rtol(gx, rgx[0], rtol=LAYER_RTOL)
+        for key in gw:
+            assert_rtol(gw[key], rgw[key], rtol=LAYER_RTOL)
+    else:
+        assert rel_max_err(gx, rgx[0]) <= BF16_MAXREL
+        for key in gw:
+            assert rel_max_err(gw[key], rgw[key]) <= BF16_MAXREL, key
