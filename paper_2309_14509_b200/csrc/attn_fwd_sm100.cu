@@ -59,7 +59,11 @@ using namespace sm100;
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int NS = 2;               // K/V pipeline stages
-constexpr int kThreads = 320;       // TMA, MMA, 2 x 4 softmax warps
+// TMA, MMA, 2 x 8 softmax warps: two warps per TMEM lane quarter and query
+// tile, each owning half of a row's 128 columns (row max / sum combined
+// through shared memory + a 64-thread named barrier)
+constexpr int kSoftPerTile = 8;
+constexpr int kThreads = 64 + 2 * kSoftPerTile * 32;
 constexpr float kLazy = 8.0f;       // log2 headroom before O is rescaled
 constexpr int kAtom = 128 * 128;    // SW128 atom column of a 128-row tile
 constexpr int kMaxTiles = 8192;     // kv tiles per head in blocked-sparse mode (n <= 1M)
@@ -72,7 +76,8 @@ struct Smem {
   static constexpr int kV = kK + NS * kTile;      // [NS]
   static constexpr int kBar = kV + NS * kTile;
   static constexpr int kList = kBar + 256;               // blocked-sparse: the CTA's kv tile list
-  static constexpr int kBytes = kList + kMaxTiles * 2 + 1024;
+  static constexpr int kX = kList + kMaxTiles * 2;       // row max / sum exchange [2 parity][2 tiles][128][2]
+  static constexpr int kBytes = kX + 2 * 2 * 128 * 2 * 4 + 1024;
 };
 
 struct Params {
@@ -124,6 +129,13 @@ __device__ __forceinline__ void blk_row_mask(const Params& p, int qrow, int kv0,
 // P = 2^(S*scale_log2 - mu) for 32 columns, packed to bf16 pairs, row sums
 // accumulated into 8 partials.  kPoly routes one element pair in four to
 // the FMA-pipe exp2 (unmasked tiles only).
+// f16x2 exponentials (one MUFU op per element pair) for all pairs
+// (UL_FWD_EXP_H2=1) or every other pair (=2); off by default
+#ifndef UL_FWD_EXP_H2
+#define UL_FWD_EXP_H2 0
+#endif
+constexpr bool kH2 = UL_FWD_EXP_H2 != 0;
+constexpr int kH2Sel = UL_FWD_EXP_H2 == 2 ? 2 : 0;
 template <bool kPoly>
 __device__ __forceinline__ void exp_chunk(const uint32_t* r, float scale_log2, float mu, uint32_t* pk,
                                           float2* rsum) {
@@ -135,6 +147,8 @@ __device__ __forceinline__ void exp_chunk(const uint32_t* r, float scale_log2, f
     float2 e;
     if (kPoly && (x & 6) == 6) {
       e = poly_exp2x2(a);
+    } else if (kH2 && (x & 2) == kH2Sel) {
+      e = exp2_h2(a);
     } else {
       e.x = fast_exp2(a.x);
       e.y = fast_exp2(a.y);
@@ -221,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 4);   // one arrive per softmax warp
+      mbar_init(&p_full[t], kSoftPerTile);   // one arrive per softmax warp
       mbar_init(&o_done[t], 1);
     }
     fence_barrier_init();
@@ -322,8 +336,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ---------------- softmax / correction / epilogue ----------------
-    const int t = (warp - 2) >> 2;            // query tile of this warpgroup
+    const int idx = warp - 2;
+    const int t = idx >> 3;                   // query tile of this warp
     const int quarter = warp & 3;
+    const int half = (idx & 7) >> 2;          // which 64 of the row's 128 columns
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const uint32_t tS = tbase + t * 128 + lane_off;
@@ -331,38 +347,52 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q0 = (2 * pair + t) * BM;
     const int qrow = q0 + row;
     const int my_nkv = t ? nkvT[1] : nkvT[0];   // (no dynamic index into a local array)
-    float m = -INFINITY, l = 0.f;
+    const uint32_t bar_id = 1 + t * 4 + quarter;  // the two warps of this (tile, quarter)
+    float* xch = reinterpret_cast<float*>(smem + S::kX);
+    auto xslot = [&](int par, int hh) { return smem_u32(xch + ((par * 2 + t) * 128 + row) * 2 + hh); };
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
+    float m = -INFINITY, l = 0.f;   // l: this half's partial row sum
     for (int j = 0; j < my_nkv; ++j) {
       const int kv0 = (blocked ? tiles[j] : j) * BN;
       mbar_wait(&s_full[t], j & 1);
-      if (lane == 0 && (warp == 2 || warp == 6)) UL_EV(warp == 2 ? 3 : 5, j);
+      if (lane == 0 && (warp == 2 || warp == 10)) UL_EV(warp == 2 ? 3 : 5, j);
       tc_fence_after();
-      uint32_t r[BN];
-#pragma unroll
-      for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, r + c * 32);
+      uint32_t r[BN / 2];
+      tmem_ld32(tS + half * 64, r);
+      tmem_ld32(tS + half * 64 + 32, r + 32);
       tmem_wait_ld();
       if (lane == 0 && warp == 2) UL_EV(12, j);
       const bool masked = (p.causal && kv0 + BN - 1 > q0) || kv0 + BN > p.n;
       if (blocked) {
         uint32_t cm[4];
         blk_row_mask(p, qrow, kv0, cm);
+        const uint32_t c0w = half ? cm[2] : cm[0], c1w = half ? cm[3] : cm[1];
 #pragma unroll
-        for (int c = 0; c < BN; ++c)
-          if (!((cm[c >> 5] >> (c & 31)) & 1u)) r[c] = __float_as_uint(-INFINITY);
+        for (int c = 0; c < BN / 2; ++c)
+          if (!(((c < 32 ? c0w : c1w) >> (c & 31)) & 1u)) r[c] = __float_as_uint(-INFINITY);
       } else if (masked) {
         int limit = p.n - kv0;
         if (p.causal) limit = min(limit, qrow - kv0 + 1);
+        limit -= half * 64;
 #pragma unroll
-        for (int c = 0; c < BN; ++c)
+        for (int c = 0; c < BN / 2; ++c)
           if (c >= limit) r[c] = __float_as_uint(-INFINITY);
       }
-      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      float mx[8];
 #pragma unroll
-      for (int c = 0; c < BN; c += 4) {
+      for (int u = 0; u < 8; ++u) mx[u] = __uint_as_float(r[u]);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) mx[u] = fmaxf(mx[u], __uint_as_float(r[c + u]));
+      for (int c = 8; c < BN / 2; c += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mx[u] = fmaxf(mx[u], __uint_as_float(r[c + u]));
       }
-      const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * p.scale_log2;
+      float mh = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      // row max across the two halves (double-buffered by tile parity)
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(j & 1, half)), "f"(mh) : "memory");
+      pair_sync();
+      float other;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(xslot(j & 1, half ^ 1)) : "memory");
+      const float mt = fmaxf(mh, other) * p.scale_log2;
 #ifdef UL_TRACE
       {
         uint32_t dep;
@@ -379,32 +409,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const float mu = (m == -INFINITY) ? 0.f : m;
       float2 rsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      // (routing part of the exponentials to the FMA pipe, exp_chunk<true>,
-      // measured slower here: the forward is not MUFU-throughput bound)
-#ifdef UL_FWD_POLY
-      if (masked) {
 #pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t pk[16];
-          exp_chunk<false>(r + c * 32, p.scale_log2, mu, pk, rsum);
-          tmem_st16(tS + c * 16, pk);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t pk[16];
-          exp_chunk<true>(r + c * 32, p.scale_log2, mu, pk, rsum);
-          tmem_st16(tS + c * 16, pk);
-        }
-      }
-#else
-#pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < 2; ++c) {
         uint32_t pk[16];
-        exp_chunk<false>(r + c * 32, p.scale_log2, mu, pk, rsum);
-        tmem_st16(tS + c * 16, pk);   // P over S columns already in registers
-      }
+#ifdef UL_FWD_POLY
+        if (!masked) exp_chunk<true>(r + c * 32, p.scale_log2, mu, pk, rsum);
+        else
 #endif
+        exp_chunk<false>(r + c * 32, p.scale_log2, mu, pk, rsum);
+        tmem_st16(tS + (2 * half + c) * 16, pk);   // P over S columns already in registers
+      }
       const float2 rs = __fadd2_rn(__fadd2_rn(rsum[0], rsum[1]), __fadd2_rn(rsum[2], rsum[3]));
       l = l * alpha + (rs.x + rs.y);
 #ifdef UL_TRACE
@@ -414,36 +428,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && warp == 2 && dep != 0x7fffffffu) UL_EV(14, j);
       }
 #endif
-      // s_full(j) tracks every earlier MMA, so PV(j-1) is complete: rescale O now
+      // s_full(j) tracks every earlier MMA, so PV(j-1) is complete: rescale
+      // this half's 64 O columns now
       if (__any_sync(0xffffffffu, rescale)) {
 #pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
+        for (int c = 0; c < HD / 64; ++c) {
           uint32_t ov[32];
-          tmem_ld32(tO + c * 32, ov);
+          tmem_ld32(tO + half * (HD / 2) + c * 32, ov);
           tmem_wait_ld();
 #pragma unroll
           for (int x = 0; x < 32; ++x) ov[x] = __float_as_uint(__uint_as_float(ov[x]) * alpha);
-          tmem_st32(tO + c * 32, ov);
+          tmem_st32(tO + half * (HD / 2) + c * 32, ov);
         }
       }
       tmem_wait_st();
       tc_fence_before();
-      if (lane == 0 && (warp == 2 || warp == 6)) UL_EV(warp == 2 ? 4 : 11, j);
+      if (lane == 0 && (warp == 2 || warp == 10)) UL_EV(warp == 2 ? 4 : 11, j);
       if (lane == 0 && warp == 4) UL_EV(15, j);
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
     }
     if (my_nkv > 0) {
+      // full row sum from the two halves
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(my_nkv & 1, half)), "f"(l) : "memory");
+      pair_sync();
+      float lo;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lo) : "r"(xslot(my_nkv & 1, half ^ 1)) : "memory");
+      const float lrow = l + lo;
       mbar_wait(&o_done[t], (my_nkv - 1) & 1);
       if (threadIdx.x == 64) UL_CTA(2, globaltimer());
       tc_fence_after();
-      const float inv = 1.f / l;
+      const float inv = 1.f / lrow;
       const bool valid = qrow < p.n;
-      __nv_bfloat16* orow = p.o + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD;
+      __nv_bfloat16* orow = p.o + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD + half * (HD / 2);
 #pragma unroll
-      for (int c = 0; c < HD / 32; ++c) {
+      for (int c = 0; c < HD / 64; ++c) {
         uint32_t ov[32];
-        tmem_ld32(tO + c * 32, ov);
+        tmem_ld32(tO + half * (HD / 2) + c * 32, ov);
         tmem_wait_ld();
         uint32_t pkd[16];
 #pragma unroll
@@ -456,13 +477,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (p.ep.active) {
             // fused head->seq: the same 64 bytes straight into the destination
             // rank's sequence layout (own `out`, or its receive slot over NVLink)
-            uint4* pd = reinterpret_cast<uint4*>(peer_row_ptr(p.ep, qrow, bb, p.b, h, HD, 2)) + c * 4;
+            uint4* pd = reinterpret_cast<uint4*>(peer_row_ptr(p.ep, qrow, bb, p.b, h, HD, 2) + half * HD) + c * 4;
 #pragma unroll
             for (int x = 0; x < 4; ++x) pd[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
           }
         }
       }
-      if (valid) p.lse[((int64_t)bb * p.hq + h) * p.n + qrow] = (m + log2f(l)) * 0.69314718055994531f;
+      if (valid && half == 0) p.lse[((int64_t)bb * p.hq + h) * p.n + qrow] = (m + log2f(lrow)) * 0.69314718055994531f;
     }
     if (p.ep.active) __threadfence_system();
   }

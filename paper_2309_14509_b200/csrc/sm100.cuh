@@ -396,6 +396,20 @@ __device__ __forceinline__ uint32_t pack_bf16_op(float lo, float hi) {
 #endif
 }
 
+// 2^x for an element pair with ONE MUFU op: ex2.approx.f16x2 on the pair
+// rounded to fp16 (softmax exponents are <= 0; fp16 carries them to 2^-24
+// and the result to 11 bits -- finer than the bf16 P that feeds the MMA).
+__device__ __forceinline__ float2 exp2_h2(float2 a) {
+  uint32_t h, e;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(a.y), "f"(a.x));
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(e) : "r"(h));
+  float2 out;
+  asm("{\n\t.reg .f16 lo, hi;\n\tmov.b32 {lo, hi}, %2;\n\tcvt.f32.f16 %0, lo;\n\tcvt.f32.f16 %1, hi;\n\t}"
+      : "=f"(out.x), "=f"(out.y)
+      : "r"(e));
+  return out;
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
