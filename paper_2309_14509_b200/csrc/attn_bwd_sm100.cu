@@ -73,12 +73,11 @@ using namespace sm100;
 constexpr int BT = 128;           // the tile a CTA owns (kv tile for dkdv, q tile for dq)
 constexpr int BS = 64;            // the sub-tile streamed against it
 constexpr int NST = 4;            // streamed-operand pipeline stages
-// warp 0 TMA, warp 1 MMA, warps 2..9 softmax: two warps per TMEM lane
-// quarter, each owning one 32-column half of the 64-column sub-tile, so
-// every SMSP interleaves two independent softmax streams
+// dQ kernel softmax: two warps per TMEM lane quarter, each owning one
+// 32-column half of the 64-column sub-tile, so every SMSP interleaves two
+// independent softmax streams
 constexpr int kSoftWarps = 8;
 constexpr int kSoftThreads = kSoftWarps * 32;
-constexpr int kThreads = 64 + kSoftThreads;
 // dK/dV kernel: 16 softmax warps, four per TMEM lane quarter, each owning 16
 // of the sub-tile's 64 columns: the softmax is latency-bound, so twice the
 // warps halve its critical path (launch bound 640 keeps the register budget
