@@ -213,3 +213,22 @@ def test_fwd_bf16_large_sampled_rows(n):
         ref, ref_lse = O.local_attention(q, k, v, "causal", exact=False, rows=(r0, r0 + 128))
         assert rel_max_err(o[r0:r0 + 128], ref) <= BF16_MAXREL
         assert np.abs(lse[:, :, r0:r0 + 128] - ref_lse).max() <= 2e-2
+
+
+@pytest.mark.parametrize("n,hq,hkv", [(8192, 12, 12), (8192, 24, 12), (4096, 20, 10)])
+def test_fused_bwd_head_groups_match_deterministic(n, hq, hkv):
+    # long sequences with many heads take the head-grouped CTA order (a
+    # partial last group exits early): gradients must equal the
+    # deterministic two-kernel path's within bf16 rounding
+    hd = 128
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n + hq)
+    mk = lambda h: (torch.randn((n, 1, h, hd), generator=g, device="cuda")).to(torch.bfloat16)
+    q, k, v, do = mk(hq), mk(hkv), mk(hkv), mk(hq)
+    fused, det = U().FlashAttention("causal"), U().FlashAttention("causal", deterministic=True)
+    o, lse = fused.forward_with_lse(q, k, v)
+    a = fused.backward(q, k, v, o, lse, do)
+    b = det.backward(q, k, v, o, lse, do)
+    for name, x, y in zip(("dq", "dk", "dv"), a, b):
+        err = float((x.float() - y.float()).abs().max() / y.float().abs().max())
+        assert err <= 1e-2, f"{name}: {err:.3e}"
