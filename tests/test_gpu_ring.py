@@ -157,3 +157,13 @@ def test_ring_backward_vs_oracle(p, dtype):
         assert rel_max_err(gx, rgx[0]) <= BF16_MAXREL
         for key in gw:
             assert rel_max_err(gw[key], rgw[key]) <= BF16_MAXREL, key
+
+
+def test_ring_shift_desync_is_error_not_hang():
+    # mismatched payload sizes across ranks: the signature check fires (simgroup.py:265-276)
+    groups = U().SequenceGroup.local_group(2, slot_bytes=1 << 20)
+    for g in groups:
+        g.set_timeout_ms(3000)
+    ins = run_ranks(groups, lambda r: [torch.zeros(64 + 16 * r, device="cuda")])
+    with pytest.raises(U().GroupDesyncError):
+        run_ranks(groups, lambda r: groups[r].ring_shift(ins[r], 1))
