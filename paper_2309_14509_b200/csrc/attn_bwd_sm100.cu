@@ -834,6 +834,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 // warp 0 TMA, warp 1 MMA, warps 2-5 dQ drain, warps 6-21 softmax (4 per lane
 // quarter, 16 columns each).
 constexpr int kFuSoftWarps = 16;
+// every exponential on the MUFU (r66: FMA-pipe share on the fused kernel's
+// softmax -- which is off its critical path (r42) -- cost 1.4%)
+constexpr bool kFuPoly = false;
 constexpr int kFuThreads = 64 + 128 + kFuSoftWarps * 32;
 constexpr int FNST = 3;   // Q / dO / L / D stages
 constexpr int NDS = 3;    // dS^T smem buffers: the softmax of sub-tile i writes while dQ^T(i-1), dQ^T(i-2) may still read
@@ -1129,7 +1132,7 @@ __global__ void __launch_bounds__(kFuThreads, 1)
       } else {
 #pragma unroll
         for (int x = 0; x < 16; x += 2)
-          e[x / 2] = (x & 2) ? pexp2<kDkPoly>(r + x, sc, nl[x / 2]) : pexp2(r + x, sc, nl[x / 2]);
+          e[x / 2] = (x & 2) ? pexp2<kFuPoly>(r + x, sc, nl[x / 2]) : pexp2(r + x, sc, nl[x / 2]);
       }
 #pragma unroll
       for (int x = 0; x < 8; ++x) pk[x] = pack_bf16(e[x].x, e[x].y);
