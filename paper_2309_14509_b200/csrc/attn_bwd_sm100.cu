@@ -833,7 +833,12 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 // the dQ^T MMA; the A operand K^T is the resident K tile read MN-major).
 // warp 0 TMA, warp 1 MMA, warps 2-5 dQ drain, warps 6-21 softmax (4 per lane
 // quarter, 16 columns each).
-constexpr int kFuSoftWarps = 16;
+#ifndef UL_FU_COLS
+#define UL_FU_COLS 16
+#endif
+constexpr int kFuCols = UL_FU_COLS;            // softmax columns per warp (of the 64-column sub-tile)
+constexpr int kFuSoftWarps = 4 * (64 / kFuCols);
+__device__ __forceinline__ uint32_t fu_acol(int kk) { return kFuCols == 16 ? a_col16(kk) : a_col(kk); }
 // every exponential on the MUFU (r66: FMA-pipe share on the fused kernel's
 // softmax -- which is off its critical path (r42) -- cost 1.4%)
 constexpr bool kFuPoly = false;
@@ -1000,10 +1005,10 @@ __global__ void __launch_bounds__(kFuThreads, 1)
         const uint64_t dOm = dadd(dOm0, s * S::kTileS), dQm = dadd(dQm0, s * S::kTileS);
 #pragma unroll
         for (int kk = 0; kk < BS / 16; ++kk)
-          mma_ts(tdV, tSt + a_col16(kk), dadd(dOm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tdV, tSt + fu_acol(kk), dadd(dOm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < BS / 16; ++kk)
-          mma_ts(tdK, tdPt + a_col16(kk), dadd(dQm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tdK, tdPt + fu_acol(kk), dadd(dQm, kk * 2048), kIdG, (i > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&q_empty[s]);
         // dQ^T(i) over the dP^T / dS^T columns dK(i) just read (in-order pipe)
         const uint64_t dds = dadd(dDS0, (i % NDS) * kAtomT);
@@ -1083,15 +1088,15 @@ __global__ void __launch_bounds__(kFuThreads, 1)
     }
   } else {
     const int quarter = warp & 3;
-    const int part = (warp - 6) >> 2;        // which 16-column quarter of the sub-tile
+    const int part = (warp - 6) >> 2;        // which kFuCols-column part of the sub-tile
     const int row = quarter * 32 + lane;     // kv row within the tile
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int kvrow = kv0 + row;
-    const int c0 = part * 16;
+    const int c0 = part * kFuCols;
     const float2 sc = make_float2(p.scale_log2, p.scale_log2);
     // this thread's two 16-byte chunks of its dS^T row in a SWIZZLE_128B tile
     const uint32_t ds_row = smem_u32(sDS) + (row >> 3) * 1024 + (row & 7) * 128;
-    const uint32_t ds_c0 = ((2 * part) ^ (row & 7)) << 4, ds_c1 = ((2 * part + 1) ^ (row & 7)) << 4;
+    const int chunk0 = part * (kFuCols / 8);   // 16-byte chunks of this row part
     int qi = i0;
     for (int it = 0; it < total; ++it) {
       const int b = it & 1, s = it % FNST;
@@ -1099,11 +1104,11 @@ __global__ void __launch_bounds__(kFuThreads, 1)
       if (++qi == nsub) qi = i0;
       const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
       mbar_wait(&q_full[s], (it / FNST) & 1);
-      float2 nl[8], nd[8];
+      float2 nl[kFuCols / 2], nd[kFuCols / 2];
       {
         const uint32_t la = smem_u32(sL + s * BS + c0), da = smem_u32(sD + s * BS + c0);
 #pragma unroll
-        for (int x = 0; x < 4; ++x) {
+        for (int x = 0; x < kFuCols / 4; ++x) {
           const float4 a = lds_f4(la + 16 * x), e = lds_f4(da + 16 * x);
           nl[2 * x] = make_float2(-a.x, -a.y);
           nl[2 * x + 1] = make_float2(-a.z, -a.w);
@@ -1114,45 +1119,50 @@ __global__ void __launch_bounds__(kFuThreads, 1)
       mbar_wait(&s_full[b], (it >> 1) & 1);
       if (lane == 0 && warp == 6) UL_EV(2, it);
       tc_fence_after();
-      uint32_t r[16], dd[16];
-      tmem_ld16(tSt + lane_off + c0, r);
+      uint32_t r[kFuCols], dd[kFuCols];
+      if constexpr (kFuCols == 16) tmem_ld16(tSt + lane_off + c0, r);
+      else tmem_ld32(tSt + lane_off + c0, r);
       tmem_wait_ld();
       if (lane == 0 && warp == 6) UL_EV(12, it);
       // P first (S^T only); dS once dP^T has landed
-      uint32_t pk[8], dsk[8];
-      float2 e[8];
+      uint32_t pk[kFuCols / 2], dsk[kFuCols / 2];
+      float2 e[kFuCols / 2];
       if (p.causal && q0 + c0 < kv0 + BT) {
         const int first = kvrow - q0 - c0;   // columns x < first are masked (q < kv)
 #pragma unroll
-        for (int x = 0; x < 16; x += 2) {
+        for (int x = 0; x < kFuCols; x += 2) {
           e[x / 2] = pexp2(r + x, sc, nl[x / 2]);
           e[x / 2].x = x < first ? 0.f : e[x / 2].x;
           e[x / 2].y = x + 1 < first ? 0.f : e[x / 2].y;
         }
       } else {
 #pragma unroll
-        for (int x = 0; x < 16; x += 2)
+        for (int x = 0; x < kFuCols; x += 2)
           e[x / 2] = (x & 2) ? pexp2<kFuPoly>(r + x, sc, nl[x / 2]) : pexp2(r + x, sc, nl[x / 2]);
       }
 #pragma unroll
-      for (int x = 0; x < 8; ++x) pk[x] = pack_bf16(e[x].x, e[x].y);
-      tmem_st8(tSt + lane_off + c0 + 8, pk);
+      for (int x = 0; x < kFuCols / 2; ++x) pk[x] = pack_bf16(e[x].x, e[x].y);
+      if constexpr (kFuCols == 16) tmem_st8(tSt + lane_off + c0 + 8, pk);
+      else tmem_st16(tSt + lane_off + c0 + 16, pk);
       mbar_wait(&dp_full[b], (it >> 1) & 1);
       tc_fence_after();
-      tmem_ld16(tdPt + lane_off + c0, dd);
+      if constexpr (kFuCols == 16) tmem_ld16(tdPt + lane_off + c0, dd);
+      else tmem_ld32(tdPt + lane_off + c0, dd);
       tmem_wait_ld();
 #pragma unroll
-      for (int x = 0; x < 8; ++x) dsk[x] = pds(e[x], dd + 2 * x, nd[x]);
+      for (int x = 0; x < kFuCols / 2; ++x) dsk[x] = pds(e[x], dd + 2 * x, nd[x]);
       // dS^T row chunk -> shared memory for the dQ^T MMA (after dQ^T(it-NDS) read the buffer)
       if (lane == 0 && warp == 6) UL_EV(13, it);
       const int ib = it % NDS;
       if (it >= NDS) mbar_wait(&ds_free[ib], ((it - NDS) / NDS) & 1);
       if (lane == 0 && warp == 6) UL_EV(14, it);
       const uint32_t dsb = ds_row + ib * kAtomT;
-      sts_u4(dsb + ds_c0, dsk[0], dsk[1], dsk[2], dsk[3]);
-      sts_u4(dsb + ds_c1, dsk[4], dsk[5], dsk[6], dsk[7]);
+#pragma unroll
+      for (int j = 0; j < kFuCols / 8; ++j)
+        sts_u4(dsb + (((chunk0 + j) ^ (row & 7)) << 4), dsk[4 * j], dsk[4 * j + 1], dsk[4 * j + 2], dsk[4 * j + 3]);
       fence_proxy_async_smem();
-      tmem_st8(tdPt + lane_off + c0 + 8, dsk);
+      if constexpr (kFuCols == 16) tmem_st8(tdPt + lane_off + c0 + 8, dsk);
+      else tmem_st16(tdPt + lane_off + c0 + 16, dsk);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
@@ -1160,17 +1170,20 @@ __global__ void __launch_bounds__(kFuThreads, 1)
       UL_WARP(it);
       if (lane == 0 && (warp == 6 || warp == 21)) UL_EV(warp == 6 ? 3 : 5, it);
     }
-    // epilogue: parts 0/1 store the two column halves of dV, parts 2/3 of dK * scale
+    // epilogue: the first half of the parts stores dV, the second dK * scale
+    // (four parts: two column halves each; two parts: all HD columns)
     if (total > 0) mbar_wait(&ds_free[(total - 1) % NDS], ((total - 1) / NDS) & 1);
     tc_fence_after();
     const bool valid = kvrow < p.n;
     const int64_t off = (((int64_t)kvrow * p.b + bb) * p.hkv + g) * HD;
-    const bool is_dk = part >= 2;
-    const int col0 = (part & 1) * (HD / 2);
+    constexpr int kParts = 64 / kFuCols;
+    constexpr int kEpCols = HD / (kParts / 2);
+    const bool is_dk = part >= kParts / 2;
+    const int col0 = (part % (kParts / 2)) * kEpCols;
     const PeerEpilogue& ep = is_dk ? p.ep_dk : p.ep_dv;
     char* peer = (ep.active && valid) ? peer_row_ptr(ep, kvrow, bb, p.b, g, HD, 2) + col0 * 2 : nullptr;
-    if (!is_dk) store_acc_rows<HD / 2>(tdV + col0, lane_off, 1.f, p.dv + off + col0, valid, peer);
-    else store_acc_rows<HD / 2>(tdK + col0, lane_off, p.scale, p.dk + off + col0, valid, peer);
+    if (!is_dk) store_acc_rows<kEpCols>(tdV + col0, lane_off, 1.f, p.dv + off + col0, valid, peer);
+    else store_acc_rows<kEpCols>(tdK + col0, lane_off, p.scale, p.dk + off + col0, valid, peer);
     if (ep.active) __threadfence_system();
   }
   tc_fence_before();
