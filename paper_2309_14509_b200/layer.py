@@ -166,8 +166,18 @@ def _ring_forward(q, k, v, group, mask, prefix):
     o_acc = lse_acc = None
     cur_k, cur_v = k, v
     dense, causal = FlashAttention("none"), FlashAttention("causal")
+    main = torch.cuda.current_stream(q.device)
+    side = _side_stream(group, q.device) if p > 1 else None
     for step in range(p):
         src = (r - step) % p
+        nxt = None
+        if step < p - 1:
+            # the next chunk travels on a second stream while this one is computed
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                nxt = group.ring_shift([cur_k, cur_v], 1, labels=[f"{prefix}.kring.{step}", f"{prefix}.vring.{step}"])
+            for t in (cur_k, cur_v):
+                t.record_stream(side)
         if mask == "none" or src <= r:
             attn = causal if (mask == "causal" and src == r) else dense
             o_s, lse_s = attn.forward_with_lse(q, cur_k, cur_v)        # lse [b, h, n/P]
@@ -178,10 +188,24 @@ def _ring_forward(q, k, v, group, mask, prefix):
                 lse_new = torch.logaddexp(lse_acc, lse_s)
                 o_acc = o_acc * torch.exp(lse_acc - lse_new) + o_s.float() * torch.exp(lse_s - lse_new)
                 lse_acc = lse_new
-        if step < p - 1:
-            cur_k, cur_v = group.ring_shift([cur_k, cur_v], 1, labels=[f"{prefix}.kring.{step}",
-                                                                      f"{prefix}.vring.{step}"])
+        if nxt is not None:
+            main.wait_stream(side)
+            for t in nxt:
+                t.record_stream(main)
+            cur_k, cur_v = nxt
     return o_acc.to(q.dtype), lse_acc.squeeze(-1).permute(1, 2, 0).contiguous()
+
+
+def _side_stream(group, device):
+    """One extra stream per rank for the ring's transfers (cached on the group)."""
+    s = getattr(group, "_ring_side_stream", None)
+    if s is None:
+        s = torch.cuda.Stream(device=device)
+        try:
+            group._ring_side_stream = s
+        except AttributeError:
+            pass
+    return s
 
 
 class _RingAttnFn(torch.autograd.Function):
@@ -209,17 +233,33 @@ class _RingAttnFn(torch.autograd.Function):
         dq = torch.zeros(q.shape, dtype=torch.float32, device=q.device)
         cur = [k, v, torch.zeros(k.shape, dtype=torch.float32, device=k.device),
                torch.zeros(v.shape, dtype=torch.float32, device=v.device)]
+        main = torch.cuda.current_stream(q.device)
+        side = _side_stream(group, q.device) if p > 1 else None
         for step in range(p):
             src = (r - step) % p
+            nkv = None
+            if step < p - 1:   # the next K/V chunk travels while this one is differentiated
+                side.wait_stream(main)
+                with torch.cuda.stream(side):
+                    nkv = group.ring_shift(cur[:2], 1, labels=[f"{prefix}.bwd.kring.{step}",
+                                                               f"{prefix}.bwd.vring.{step}"])
+                for t in cur[:2]:
+                    t.record_stream(side)
             if mask == "none" or src <= r:
                 attn = causal if (mask == "causal" and src == r) else dense
                 dq_c, dk_c, dv_c = attn.backward(q, cur[0], cur[1], o, lse, do)
                 dq += dq_c.float()
                 cur[2] += dk_c.float()
                 cur[3] += dv_c.float()
-            if step < p - 1:
-                cur = group.ring_shift(cur, 1, labels=[f"{prefix}.bwd.kring.{step}", f"{prefix}.bwd.vring.{step}",
-                                                       f"{prefix}.bwd.dkring.{step}", f"{prefix}.bwd.dvring.{step}"])
+            if nkv is not None:   # the chunk's dK/dV accumulators follow it once updated
+                # (join the side stream first: consecutive calls of one group must
+                # stay stream-ordered -- a rank reuses a receive slot every other call)
+                main.wait_stream(side)
+                for t in nkv:
+                    t.record_stream(main)
+                acc = group.ring_shift(cur[2:], 1, labels=[f"{prefix}.bwd.dkring.{step}",
+                                                           f"{prefix}.bwd.dvring.{step}"])
+                cur = list(nkv) + list(acc)
         dk, dv = cur[2], cur[3]
         if p > 1:   # the accumulators of chunk r are one hop away
             dk, dv = group.ring_shift([dk, dv], 1, labels=[f"{prefix}.bwd.dkring.home", f"{prefix}.bwd.dvring.home"])
