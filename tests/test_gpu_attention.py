@@ -67,6 +67,8 @@ BWD_CASES = [
     (512, 1, 4, 4, 128, "causal"),
     (640, 1, 4, 1, 128, "none"),
     (1000, 1, 2, 2, 128, "causal"),
+    (384, 2, 4, 2, 128, "causal"),      # batch 2 + GQA through the fused kernel
+    (200, 3, 2, 1, 128, "none"),
 ]
 
 
