@@ -210,6 +210,14 @@ int ul_attn_bwd_exchange(ul_comm* comm, const void* q, const void* k, const void
 int ul_ring_shift(ul_comm* comm, int n, const void* const* in, void* const* out, const int64_t* bytes,
                   int steps, uint64_t label_hash, void* stream);
 
+/* Ring attention merge (extension): fold one chunk's normalised context o_s
+ * ([n, b, h, hd], dtype) and row LSE lse_s ([b, h, n], natural log) into the
+ * running fp32 context o_acc and lse_acc: o_acc = o_acc e^(lse_acc - l) +
+ * o_s e^(lse_s - l), lse_acc = l = logaddexp(lse_acc, lse_s) -- the exact
+ * softmax over the union of the chunks' keys.  first != 0 initialises. */
+int ul_lse_merge(void* o_acc, float* lse_acc, const void* o_s, const float* lse_s, int64_t n, int64_t b,
+                 int64_t h, int64_t hd, int dtype, int first, void* stream);
+
 /* Q/K/V projection fused with the seq->head exchange:
  * project(x, wq|wk|wv) (layers.py:118-122, ulysses.py:140-142) + _to_head
  * (ulysses.py:161-164).  x: this rank's sequence shard [nl*b, d] (bf16,

@@ -17,7 +17,10 @@
 // (simgroup.py:265-276); a drain kernel then moves the P-1 remote chunks
 // from the slot into `out`.  Two slots alternate by call parity, which
 // makes one barrier per call sufficient.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include <cmath>
 
 #include <cstring>
 #include <vector>
@@ -908,3 +911,51 @@ int ul_ulysses_volume(int64_t n, int64_t b, int64_t d, int64_t p, int convention
 }
 
 }  // extern "C"
+
+// ---- ring attention: exact merge of a chunk's (O, LSE) into the running one ----
+namespace ul {
+// o_acc[row, :] <- o_acc * e^(lse_acc - l) + o_s * e^(lse_s - l), lse_acc <- l
+// = logaddexp(lse_acc, lse_s); rows (i, bb, hh) of [n, b, h, hd], LSE [b, h, n]
+template <typename T>
+__global__ void __launch_bounds__(256) lse_merge_kernel(float* __restrict__ o_acc, float* __restrict__ lse_acc,
+                                                        const T* __restrict__ o_s, const float* __restrict__ lse_s,
+                                                        int64_t n, int64_t b, int64_t h, int64_t hd, int first) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n * b * h) return;
+  const int64_t hh = warp % h, bb = (warp / h) % b, i = warp / (h * b);
+  const int64_t li = (bb * h + hh) * n + i;
+  const float la = first ? -INFINITY : lse_acc[li], ls = lse_s[li];
+  const float m = fmaxf(la, ls);
+  const float l = (m == -INFINITY) ? -INFINITY : m + logf(expf(la - m) + expf(ls - m));
+  const float wa = (la == -INFINITY) ? 0.f : expf(la - l), ws = (ls == -INFINITY) ? 0.f : expf(ls - l);
+  float* oa = o_acc + warp * hd;
+  const T* os = o_s + warp * hd;
+  for (int64_t d = lane; d < hd; d += 32) {
+    const float prev = first ? 0.f : oa[d];
+    oa[d] = prev * wa + (float)os[d] * ws;
+  }
+  if (lane == 0) lse_acc[li] = l;
+}
+}  // namespace ul
+
+extern "C" int ul_lse_merge(void* o_acc, float* lse_acc, const void* o_s, const float* lse_s, int64_t n, int64_t b,
+                            int64_t h, int64_t hd, int dtype, int first, void* stream) {
+  using namespace ul;
+  launch_count() = 0;
+  if (!o_acc || !lse_acc || !o_s || !lse_s) return fail(UL_ERR_ARG, "ul_lse_merge: NULL tensor");
+  if (n < 0 || b < 0 || h < 0 || hd < 1) return fail(UL_ERR_SHAPE, "ul_lse_merge: bad shape");
+  const int64_t rows = n * b * h;
+  if (rows == 0) return UL_OK;
+  const unsigned blocks = (unsigned)((rows * 32 + 255) / 256);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == UL_DTYPE_BF16)
+    lse_merge_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>((float*)o_acc, lse_acc, (const __nv_bfloat16*)o_s, lse_s,
+                                                            n, b, h, hd, first);
+  else if (dtype == UL_DTYPE_F32)
+    lse_merge_kernel<float><<<blocks, 256, 0, st>>>((float*)o_acc, lse_acc, (const float*)o_s, lse_s, n, b, h, hd,
+                                                    first);
+  else
+    return fail(UL_ERR_KERNEL, "ul_lse_merge: unsupported dtype %d", dtype);
+  return launched("lse_merge");
+}

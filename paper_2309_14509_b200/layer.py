@@ -31,7 +31,8 @@ import numpy as np
 import torch
 import torch.nn.functional as F
 
-from .attention import DistributedAttention, FlashAttention
+from . import _lib
+from .attention import _ATTN_DTYPES, DistributedAttention, FlashAttention
 from .errors import DivisibilityError
 
 LN_EPS = 1e-5          # layers.py:22
@@ -181,19 +182,20 @@ def _ring_forward(q, k, v, group, mask, prefix):
         if mask == "none" or src <= r:
             attn = causal if (mask == "causal" and src == r) else dense
             o_s, lse_s = attn.forward_with_lse(q, cur_k, cur_v)        # lse [b, h, n/P]
-            lse_s = lse_s.permute(2, 0, 1).unsqueeze(-1)                  # -> [n/P, b, h, 1]
-            if o_acc is None:
-                o_acc, lse_acc = o_s.float(), lse_s
-            else:
-                lse_new = torch.logaddexp(lse_acc, lse_s)
-                o_acc = o_acc * torch.exp(lse_acc - lse_new) + o_s.float() * torch.exp(lse_s - lse_new)
-                lse_acc = lse_new
+            first = o_acc is None
+            if first:
+                o_acc = torch.empty(q.shape, dtype=torch.float32, device=q.device)
+                lse_acc = torch.empty_like(lse_s)
+            n_, b_, h_, hd_ = q.shape                                     # exact merge, one kernel
+            _lib.check(_lib.lib().ul_lse_merge(o_acc.data_ptr(), lse_acc.data_ptr(), o_s.data_ptr(),
+                                               lse_s.data_ptr(), n_, b_, h_, hd_, _ATTN_DTYPES[q.dtype],
+                                               int(first), main.cuda_stream))
         if nxt is not None:
             main.wait_stream(side)
             for t in nxt:
                 t.record_stream(main)
             cur_k, cur_v = nxt
-    return o_acc.to(q.dtype), lse_acc.squeeze(-1).permute(1, 2, 0).contiguous()
+    return o_acc.to(q.dtype), lse_acc
 
 
 def _side_stream(group, device):
