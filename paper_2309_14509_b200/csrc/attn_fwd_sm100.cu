@@ -77,7 +77,7 @@ struct Smem {
   static constexpr int kBar = kV + NS * kTile;
   static constexpr int kList = kBar + 256;               // blocked-sparse: the CTA's kv tile list
   static constexpr int kX = kList + kMaxTiles * 2;       // row max / sum exchange [2 parity][2 tiles][128][2]
-  static constexpr int kBytes = kX + 2 * 2 * 128 * 2 * 4 + 1024;
+  static constexpr int kBytes = kX + 3 * 2 * 128 * 2 * 4 + 1024;   // (3 slots: persistent kernel)
 };
 
 struct Params {
@@ -501,6 +501,315 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// Persistent variant (dense / causal): one CTA per SM walks the (query-tile
+// pair, head) items in zig-zag waves; barriers run on across items, the next
+// item's Q is loaded as soon as the last S MMAs of the current one complete,
+// its first S MMAs queue behind the current PVs, and the O accumulator of a
+// tile is handed back by the epilogue warps (o_free) before the next item's
+// first PV overwrites it -- the per-CTA prologue / tail of the one-shot grid
+// overlap with neighbouring items.
+template <int HD>
+__device__ __forceinline__ bool fwd_item(const Params& p, int k, int& pair, int& bh) {
+  const int heads = p.b * p.hq;
+  const int G = (int)gridDim.x;
+  const int idx = k * G + ((k & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
+  if (idx >= p.pairs * heads) return false;
+  pair = p.head_major ? p.pairs - 1 - idx % p.pairs : p.pairs - 1 - idx / heads;
+  bh = p.head_major ? idx / p.pairs : idx % heads;
+  return true;
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_persist_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                            const __grid_constant__ CUtensorMap tmV, const Params p) {
+  using S = Smem<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + S::kQ;
+  uint8_t* sK = smem + S::kK;
+  uint8_t* sV = smem + S::kV;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;              // [NS]
+  uint64_t* k_empty = bars + 1 + NS;        // [NS]
+  uint64_t* v_full = bars + 1 + 2 * NS;     // [NS]
+  uint64_t* v_empty = bars + 1 + 3 * NS;    // [NS]
+  uint64_t* s_full = bars + 1 + 4 * NS;     // [2] per tile
+  uint64_t* p_full = bars + 3 + 4 * NS;     // [2] per tile
+  uint64_t* o_done = bars + 5 + 4 * NS;     // [2] per tile
+  uint64_t* q_empty = bars + 7 + 4 * NS;    // Q smem free (the item's last S MMAs completed)
+  uint64_t* o_free = bars + 8 + 4 * NS;     // [2] per tile: O read out by the epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10 + 4 * NS);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nkv_all = (p.n + BN - 1) / BN;
+  auto item_kv = [&](int pair, int t) {
+    const int qt = 2 * pair + t;
+    return qt >= p.qtiles ? 0 : (p.causal ? min(nkv_all, (qt * BM + BM - 1) / BN + 1) : nkv_all);
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], kSoftPerTile);
+      mbar_init(&o_done[t], 1);
+      mbar_init(&o_free[t], kSoftPerTile);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (*tmem_slot != 0u) __trap();
+  constexpr uint32_t tbase = 0;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      int pair, bh, gk = 0;
+      for (int k = 0; fwd_item<HD>(p, k, pair, bh); ++k) {
+        const int bb = bh / p.hq, h = bh % p.hq, g = h / (p.hq / p.hkv);
+        const int n0 = item_kv(pair, 0), n1 = item_kv(pair, 1);
+        const int nkv = max(n0, n1), ntiles = n1 > 0 ? 2 : 1;
+        if (k > 0) mbar_wait(q_empty, (k - 1) & 1);
+        mbar_expect_tx(q_full, ntiles * BM * HD * 2);
+        for (int t = 0; t < ntiles; ++t)
+#pragma unroll
+          for (int a = 0; a < HD / 64; ++a)
+            tma_load_3d(sQ + t * S::kTile + a * kAtom, &tmQ, q_full, a * 64, bb * p.hq + h, (2 * pair + t) * BM);
+        for (int j = 0; j < nkv; ++j, ++gk) {
+          const int s = gk % NS;
+          const uint32_t ph = (gk / NS) & 1;
+          mbar_wait(&k_empty[s], ph ^ 1);
+          mbar_expect_tx(&k_full[s], BN * HD * 2);
+#pragma unroll
+          for (int a = 0; a < HD / 64; ++a)
+            tma_load_3d(sK + s * S::kTile + a * kAtom, &tmK, &k_full[s], a * 64, bb * p.hkv + g, j * BN);
+          mbar_wait(&v_empty[s], ph ^ 1);
+          mbar_expect_tx(&v_full[s], BN * HD * 2);
+#pragma unroll
+          for (int a = 0; a < HD / 64; ++a)
+            tma_load_3d(sV + s * S::kTile + a * kAtom, &tmV, &v_full[s], a * 64, bb * p.hkv + g, j * BN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t kIdQK = idesc_bf16(BM, BN, 0, 0);
+      constexpr uint32_t kIdPV = idesc_bf16(BM, HD, 0, 1);
+      const uint64_t dQ0 = sdesc(smem_u32(sQ), 16, 1024);
+      const uint64_t dK0 = sdesc(smem_u32(sK), 16, 1024);
+      const uint64_t dV0 = sdesc(smem_u32(sV), kAtom, 1024);
+      int cpv[2] = {0, 0};      // PV MMAs (== p_full waits == o_done commits) per tile so far
+      int items_t[2] = {0, 0};  // items in which the tile existed so far
+      auto issue_s = [&](int t, int stage) {
+        const uint64_t dk = dadd(dK0, stage * S::kTile);
+        const uint64_t dq = dadd(dQ0, t * S::kTile);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
+          mma_ss(tbase + t * 128, dadd(dq, off), dadd(dk, off), kIdQK, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j, int stage) {
+        if (j == 0 && items_t[t] > 0) mbar_wait_mma(&o_free[t], (items_t[t] - 1) & 1);
+        mbar_wait_mma(&p_full[t], cpv[t] & 1);
+        tc_fence_after();
+        const uint64_t dv = dadd(dV0, stage * S::kTile);
+#pragma unroll
+        for (int kk = 0; kk < BN / 16; ++kk)
+          mma_ts(tbase + 256 + t * HD, tbase + t * 128 + kk * 8, dadd(dv, kk * 2048), kIdPV,
+                 (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&o_done[t]);
+        ++cpv[t];
+      };
+      int pair, bh, gk = 0;
+      for (int k = 0; fwd_item<HD>(p, k, pair, bh); ++k) {
+        const int nT0 = item_kv(pair, 0), nT1 = item_kv(pair, 1);
+        const int nkv = max(nT0, nT1);
+        mbar_wait_mma(q_full, k & 1);
+        mbar_wait_mma(&k_full[gk % NS], (gk / NS) & 1);
+        tc_fence_after();
+        if (nT0 > 0) issue_s(0, gk % NS);
+        if (nT1 > 0) issue_s(1, gk % NS);
+        mma_commit(&k_empty[gk % NS]);
+        if (nkv == 1) mma_commit(q_empty);
+        for (int j = 0; j < nkv; ++j) {
+          const int s = (gk + j) % NS, s1 = (gk + j + 1) % NS;
+          const bool next = j + 1 < nkv;
+          mbar_wait_mma(&v_full[s], ((gk + j) / NS) & 1);
+          if (next) mbar_wait_mma(&k_full[s1], ((gk + j + 1) / NS) & 1);
+          tc_fence_after();
+          if (j < nT0) issue_pv(0, j, s);
+          if (next && j + 1 < nT0) issue_s(0, s1);
+          if (j < nT1) issue_pv(1, j, s);
+          if (next && j + 1 < nT1) issue_s(1, s1);
+          mma_commit(&v_empty[s]);
+          if (next) mma_commit(&k_empty[s1]);
+          if (j + 2 == nkv) mma_commit(q_empty);   // the item's last S MMAs are issued: Q may be replaced
+        }
+        if (nT0 > 0) ++items_t[0];
+        if (nT1 > 0) ++items_t[1];
+        gk += nkv;
+      }
+    }
+    __syncwarp();
+  } else {
+    const int idx = warp - 2;
+    const int t = idx >> 3;
+    const int quarter = warp & 3;
+    const int half = (idx & 7) >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tbase + t * 128 + lane_off;
+    const uint32_t tO = tbase + 256 + t * HD + lane_off;
+    const uint32_t bar_id = 1 + t * 4 + quarter;
+    float* xch = reinterpret_cast<float*>(smem + S::kX);
+    // [3 slots: max parity 0/1, row sum][2 tiles][128 rows][2 halves]
+    auto xslot = [&](int sl, int hh) { return smem_u32(xch + ((sl * 2 + t) * 128 + row) * 2 + hh); };
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
+    int cs = 0;   // S tiles of this query tile consumed so far (s_full / o_done phases)
+    int pair, bh;
+    for (int k = 0; fwd_item<HD>(p, k, pair, bh); ++k) {
+      const int my_nkv = item_kv(pair, t);
+      if (my_nkv == 0) continue;
+      const int bb = bh / p.hq, h = bh % p.hq;
+      const int q0 = (2 * pair + t) * BM;
+      const int qrow = q0 + row;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < my_nkv; ++j, ++cs) {
+        const int kv0 = j * BN;
+        mbar_wait(&s_full[t], cs & 1);
+        tc_fence_after();
+        uint32_t r[BN / 2];
+        tmem_ld32(tS + half * 64, r);
+        tmem_ld32(tS + half * 64 + 32, r + 32);
+        tmem_wait_ld();
+        const bool masked = (p.causal && kv0 + BN - 1 > q0) || kv0 + BN > p.n;
+        if (masked) {
+          int limit = p.n - kv0;
+          if (p.causal) limit = min(limit, qrow - kv0 + 1);
+          limit -= half * 64;
+#pragma unroll
+          for (int c = 0; c < BN / 2; ++c)
+            if (c >= limit) r[c] = __float_as_uint(-INFINITY);
+        }
+        float mx[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) mx[u] = __uint_as_float(r[u]);
+#pragma unroll
+        for (int c = 8; c < BN / 2; c += 8) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mx[u] = fmaxf(mx[u], __uint_as_float(r[c + u]));
+        }
+        const float mh =
+            fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(cs & 1, half)), "f"(mh) : "memory");
+        pair_sync();
+        float other;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(xslot(cs & 1, half ^ 1)) : "memory");
+        const float mt = fmaxf(mh, other) * p.scale_log2;
+        float alpha = 1.f;
+        bool rescale = false;
+        if (mt > m + kLazy) {
+          alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - mt);
+          rescale = (j > 0);
+          m = mt;
+        }
+        const float mu = (m == -INFINITY) ? 0.f : m;
+        float2 rsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                          make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t pk[16];
+          exp_chunk<false>(r + c * 32, p.scale_log2, mu, pk, rsum);
+          tmem_st16(tS + (2 * half + c) * 16, pk);
+        }
+        const float2 rs = __fadd2_rn(__fadd2_rn(rsum[0], rsum[1]), __fadd2_rn(rsum[2], rsum[3]));
+        l = l * alpha + (rs.x + rs.y);
+        if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+          for (int c = 0; c < HD / 64; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(tO + half * (HD / 2) + c * 32, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int x = 0; x < 32; ++x) ov[x] = __float_as_uint(__uint_as_float(ov[x]) * alpha);
+            tmem_st32(tO + half * (HD / 2) + c * 32, ov);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+      }
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(2, half)), "f"(l) : "memory");
+      pair_sync();
+      float lo;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lo) : "r"(xslot(2, half ^ 1)) : "memory");
+      pair_sync();   // (the sum slot is rewritten by the next item)
+      const float lrow = l + lo;
+      mbar_wait(&o_done[t], (cs - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / lrow;
+      const bool valid = qrow < p.n;
+      uint32_t pkd[HD / 64][16];
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(tO + half * (HD / 2) + c * 32, ov);
+        tmem_wait_ld();
+#pragma unroll
+        for (int x = 0; x < 16; ++x)
+          pkd[c][x] = pack_bf16(__uint_as_float(ov[2 * x]) * inv, __uint_as_float(ov[2 * x + 1]) * inv);
+      }
+      // O is in registers: the next item's first PV of this tile may overwrite it
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_free[t]);
+      if (valid) {
+        __nv_bfloat16* orow = p.o + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD + half * (HD / 2);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+            dst[x] = make_uint4(pkd[c][4 * x], pkd[c][4 * x + 1], pkd[c][4 * x + 2], pkd[c][4 * x + 3]);
+          if (p.ep.active) {
+            uint4* pd = reinterpret_cast<uint4*>(peer_row_ptr(p.ep, qrow, bb, p.b, h, HD, 2) + half * HD) + c * 4;
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              pd[x] = make_uint4(pkd[c][4 * x], pkd[c][4 * x + 1], pkd[c][4 * x + 2], pkd[c][4 * x + 3]);
+          }
+        }
+        if (half == 0) p.lse[((int64_t)bb * p.hq + h) * p.n + qrow] = (m + log2f(lrow)) * 0.69314718055994531f;
+      }
+    }
+    if (p.ep.active) __threadfence_system();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (p.ep.active && threadIdx.x == 0) peer_signal_last_cta(p.ep, gridDim.x);
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
 template <int HD>
 static int launch(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
                   int64_t hq, int64_t hkv, int causal, float scale, const PeerEpilogue* ep, cudaStream_t st,
@@ -535,6 +844,19 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
     attr = true;
   }
   const int64_t grid = (int64_t)p.pairs * b * hq;
+#ifndef UL_FWD_PERSIST
+#define UL_FWD_PERSIST 1   // r73: -1.5% vs the one-shot grid; blocked-sparse keeps the one-shot kernel
+#endif
+  if (UL_FWD_PERSIST && !blk) {
+    static bool pattr = false;
+    if (!pattr) {
+      UL_CUDA(cudaFuncSetAttribute(attn_fwd_persist_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      pattr = true;
+    }
+    const int64_t pgrid = grid < sm_count() ? grid : sm_count();
+    attn_fwd_persist_kernel<HD><<<(unsigned)pgrid, kThreads, smem, st>>>(mq, mk, mv, p);
+    return launched("attn_fwd_sm100");
+  }
   attn_fwd_kernel<HD><<<(unsigned)grid, kThreads, smem, st>>>(mq, mk, mv, p);
   return launched("attn_fwd_sm100");
 }
