@@ -959,3 +959,12 @@ extern "C" int ul_lse_merge(void* o_acc, float* lse_acc, const void* o_s, const 
     return fail(UL_ERR_KERNEL, "ul_lse_merge: unsupported dtype %d", dtype);
   return launched("lse_merge");
 }
+
+namespace ul {
+int preload_merge() {
+  cudaFuncAttributes a;
+  UL_CUDA(cudaFuncGetAttributes(&a, lse_merge_kernel<float>));
+  UL_CUDA(cudaFuncGetAttributes(&a, lse_merge_kernel<__nv_bfloat16>));
+  return UL_OK;
+}
+}  // namespace ul

@@ -882,6 +882,8 @@ int preload_fwd() {
   cudaFuncAttributes a;
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_kernel<64>));
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_kernel<128>));
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<64>));
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<128>));
   return UL_OK;
 }
 

@@ -44,6 +44,7 @@ int preload_simt();
 int preload_fwd();
 int preload_bwd();
 int preload_proj();
+int preload_merge();
 void set_deterministic(int on);
 int get_deterministic();
 
@@ -82,6 +83,7 @@ int ul_preload_kernels(void) {
   UL_TRY(preload_simt());
   UL_TRY(preload_fwd());
   UL_TRY(preload_proj());
+  UL_TRY(preload_merge());
 
   return preload_bwd();
 }
