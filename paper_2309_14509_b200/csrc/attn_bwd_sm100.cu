@@ -929,6 +929,11 @@ __global__ void __launch_bounds__(kFuThreads, 1)
   const int total = per_head * group;
 
   if (threadIdx.x == 0) {
+    UL_CTA(0, globaltimer());
+    UL_CTA(4, smid());
+    UL_CTA(5, clock64());
+  }
+  if (threadIdx.x == 0) {
     mbar_init(kv_full, 1);
     for (int s = 0; s < FNST; ++s) {
       mbar_init(&q_full[s], 1);
@@ -1020,6 +1025,7 @@ __global__ void __launch_bounds__(kFuThreads, 1)
         UL_EV(6, i);
       };
       mbar_wait_mma(kv_full, 0);
+      UL_CTA(1, globaltimer());
       for (int it = 0; it < total; ++it) {
         const int b = it & 1, s = it % FNST;
         const uint32_t tSt = tbase + b * 64, tdPt = tbase + 128 + b * 64;
@@ -1173,6 +1179,7 @@ __global__ void __launch_bounds__(kFuThreads, 1)
     // epilogue: the first half of the parts stores dV, the second dK * scale
     // (four parts: two column halves each; two parts: all HD columns)
     if (total > 0) mbar_wait(&ds_free[(total - 1) % NDS], ((total - 1) / NDS) & 1);
+    if (threadIdx.x == 192) UL_CTA(2, globaltimer());
     tc_fence_after();
     const bool valid = kvrow < p.n;
     const int64_t off = (((int64_t)kvrow * p.b + bb) * p.hkv + g) * HD;
@@ -1188,6 +1195,10 @@ __global__ void __launch_bounds__(kFuThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) {
+    UL_CTA(3, globaltimer());
+    UL_CTA(6, clock64());
+  }
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();

@@ -213,3 +213,9 @@ def cta_report(name):
 if os.environ.get("CTA"):
     run(4)
     cta_report("dq")
+
+
+if os.environ.get("CTA_FUSED"):
+    lib.ul_attn_set_deterministic(0)
+    run(1 | 2)
+    cta_report("fused")
