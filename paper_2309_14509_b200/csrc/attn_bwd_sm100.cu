@@ -842,6 +842,11 @@ __device__ __forceinline__ uint32_t fu_acol(int kk) { return kFuCols == 16 ? a_c
 // every exponential on the MUFU (r66: FMA-pipe share on the fused kernel's
 // softmax -- which is off its critical path (r42) -- cost 1.4%)
 constexpr bool kFuPoly = false;
+// dK / dV epilogue through shared memory (the K / V tiles, free once every MMA
+// has completed) and per-warp 32-row TMA stores instead of 16-byte row stores
+#ifndef UL_BWD_TMA_EPI
+#define UL_BWD_TMA_EPI 1
+#endif
 constexpr int kFuThreads = 64 + 128 + kFuSoftWarps * 32;
 constexpr int FNST = 3;   // Q / dO / L / D stages
 constexpr int NDS = 3;    // dS^T smem buffers: the softmax of sub-tile i writes while dQ^T(i-1), dQ^T(i-2) may still read
@@ -876,6 +881,7 @@ template <int HD>
 __global__ void __launch_bounds__(kFuThreads, 1)
     bwd_fused_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO,
+                     const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV,
                      const Params p, float* __restrict__ dq_acc) {
   static_assert(HD == 128, "the dQ^T MMA uses M = head dim = 128");
   using S = FusedSmem<HD>;
@@ -1188,10 +1194,40 @@ __global__ void __launch_bounds__(kFuThreads, 1)
     const bool is_dk = part >= kParts / 2;
     const int col0 = (part % (kParts / 2)) * kEpCols;
     const PeerEpilogue& ep = is_dk ? p.ep_dk : p.ep_dv;
-    char* peer = (ep.active && valid) ? peer_row_ptr(ep, kvrow, bb, p.b, g, HD, 2) + col0 * 2 : nullptr;
-    if (!is_dk) store_acc_rows<kEpCols>(tdV + col0, lane_off, 1.f, p.dv + off + col0, valid, peer);
-    else store_acc_rows<kEpCols>(tdK + col0, lane_off, p.scale, p.dk + off + col0, valid, peer);
-    if (ep.active) __threadfence_system();
+    if (UL_BWD_TMA_EPI && kEpCols == 64 && !ep.active) {
+      // this warp's 32 rows x 64 columns -> one SWIZZLE_128B box (4 KB of the
+      // K / V tiles) -> one TMA store; rows >= n are clipped by the tensor map
+      uint8_t* stg = smem + S::kK + (warp - 6) * 4096;
+      const uint32_t srow = smem_u32(stg) + lane * 128;
+      const uint32_t tacc = (is_dk ? tdK : tdV) + col0 + lane_off;
+      const float mul = is_dk ? p.scale : 1.f;
+#pragma unroll
+      for (int c = 0; c < kEpCols / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tacc + c * 32, v);
+        tmem_wait_ld();
+        uint32_t pkd[16];
+#pragma unroll
+        for (int x = 0; x < 16; ++x)
+          pkd[x] = pack_bf16(__uint_as_float(v[2 * x]) * mul, __uint_as_float(v[2 * x + 1]) * mul);
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+          sts_u4(srow + (((c * 4 + x) ^ (lane & 7)) << 4), pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(is_dk ? &tmDK : &tmDV, stg, col0, bb * p.hkv + g, kv0 + quarter * 32);
+        bulk_commit();
+        bulk_wait_read0();
+      }
+      __syncwarp();
+    } else {
+      char* peer = (ep.active && valid) ? peer_row_ptr(ep, kvrow, bb, p.b, g, HD, 2) + col0 * 2 : nullptr;
+      if (!is_dk) store_acc_rows<kEpCols>(tdV + col0, lane_off, 1.f, p.dv + off + col0, valid, peer);
+      else store_acc_rows<kEpCols>(tdK + col0, lane_off, p.scale, p.dk + off + col0, valid, peer);
+      if (ep.active) __threadfence_system();
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1315,7 +1351,10 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
           pf.head_major = (int)G;
           grid = (unsigned)(tiles * ((b * hkv + G - 1) / G) * G);
         }
-        bwd_fused_kernel<HD><<<grid, kFuThreads, FusedSmem<HD>::kBytes, st>>>(mq, mk, mv, mo, pf, dq_acc);
+        CUtensorMap mdk, mdv;   // 32-row store boxes of the dK / dV epilogue
+        UL_TRY(make_tmap_bhsd(&mdk, dk, n, b * hkv, HD, 32));
+        UL_TRY(make_tmap_bhsd(&mdv, dv, n, b * hkv, HD, 32));
+        bwd_fused_kernel<HD><<<grid, kFuThreads, FusedSmem<HD>::kBytes, st>>>(mq, mk, mv, mo, mdk, mdv, pf, dq_acc);
         UL_TRY(launched("attn_bwd_fused_sm100"));
       }
       if (stages & 4) {
