@@ -60,7 +60,7 @@ def make_flush(dev):
     return torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
 
-NCU_PROFILE = os.path.join(ROOT, "profiles", "r1_ncu_full_r75.json")
+NCU_PROFILE = os.path.join(ROOT, "profiles", "r1_ncu_full_r80.json")
 NCU_NAMES = {"attn_fwd_sm100": "fwd::attn_fwd_persist_kernel<128>", "attn_bwd_dkdv_sm100": "bwd::bwd_dkdv_kernel<128>",
              "attn_bwd_dq_sm100": "bwd::bwd_dq_kernel<128>", "attn_bwd_fused_sm100": "bwd::bwd_fused_kernel<128>"}
 
