@@ -847,7 +847,11 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
 #ifndef UL_FWD_PERSIST
 #define UL_FWD_PERSIST 1   // r73: -1.5% vs the one-shot grid; blocked-sparse keeps the one-shot kernel
 #endif
-  if (UL_FWD_PERSIST && !blk) {
+  // head-major orders (a head's pairs fill a wave: long sequences) keep the
+  // one-shot grid: the static zig-zag waves of the persistent kernel balance
+  // the tile-major length ramp but not the per-head sawtooth (r83: N = 64K,
+  // 4 heads 3.7 -> 5.1 ms)
+  if (UL_FWD_PERSIST && !blk && !p.head_major) {
     static bool pattr = false;
     if (!pattr) {
       UL_CUDA(cudaFuncSetAttribute(attn_fwd_persist_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
