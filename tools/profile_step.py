@@ -17,7 +17,7 @@ import paper_2309_14509_b200 as U  # noqa: E402
 
 warm, steps = (int(a) for a in (sys.argv[1:3] if len(sys.argv) > 2 else (1, 2)))
 dev = torch.device("cuda", 0)
-n, H, hd = 8192, 16, 128
+n, H, hd = int(os.environ.get("PS_N", 8192)), int(os.environ.get("PS_H", 16)), 128   # shape override for long-N captures
 g = torch.Generator(device=dev)
 g.manual_seed(2024)
 mk = lambda: torch.randn((n, 1, H, hd), generator=g, device=dev).to(torch.bfloat16)
