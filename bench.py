@@ -352,14 +352,7 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic N(0,1) q/k/v/dO, seed 2024 (no dataset)",
-            "config": {
-                "workload": ("config2: single-GPU local attention fwd+bwd, GPT-1.3B layer 16 heads x 128, "
-                             f"N={n_seq} bf16 causal" if P == 1 else
-                             f"Ulysses DistributedAttention fwd+bwd, P={P}, 16 heads x 128, N={n_seq} "
-                             f"(= {SEQ_PER_GPU} x P) bf16 causal"),
-                "seq_len": n_seq, "heads": H, "head_dim": hd, "batch": 1, "parallelism": f"ulysses-sp{P}",
-                "causal": True, "l2": "flushed (1 GiB write) before every timed step, flush untimed",
-            },
+            "config": workload_config(P, n_seq, H, hd),
             "tflops_per_gpu": round(tflops_per_gpu, 1),
             "tflops_per_gpu_fa_convention": round(
                 (f_fwd * 3.5) / (ms_per_step / 1e3) / 1e12, 1),
@@ -707,6 +700,18 @@ def run_e2e(layer, q, k, v, do, args, P, dev):
 # reference arm: the reference algorithm on the host cores
 # ---------------------------------------------------------------------------
 
+def workload_config(P, n_seq, H, hd):
+    """The `config` both arms report (the reference arm on the same workload)."""
+    return {
+        "workload": ("config2: single-GPU local attention fwd+bwd, GPT-1.3B layer 16 heads x 128, "
+                     f"N={n_seq} bf16 causal" if P == 1 else
+                     f"Ulysses DistributedAttention fwd+bwd, P={P}, 16 heads x 128, N={n_seq} "
+                     f"(= {SEQ_PER_GPU} x P) bf16 causal"),
+        "seq_len": n_seq, "heads": H, "head_dim": hd, "batch": 1, "parallelism": f"ulysses-sp{P}",
+        "causal": True, "l2": "flushed (1 GiB write) before every timed step, flush untimed",
+    }
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -731,8 +736,9 @@ def run_reference(args):
         "value": round(tok, 4), "unit": "tokens/s", "n_gpus": P, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic N(0,1), seed-derived",
-        "config": {"workload": f"reference algorithm (seqlab kernels.py fixed-order f64) for N={n_seq}, "
-                               f"{args.heads} heads x {HEAD_DIM}, causal fwd+bwd", "seq_len": n_seq},
+        "config": workload_config(P, n_seq, args.heads, HEAD_DIM),
+        "reference_impl": (f"reference algorithm (seqlab kernels.py fixed-order f64, oracle port) for N={n_seq}, "
+                           f"{args.heads} heads x {HEAD_DIM}, causal fwd+bwd on {procs} host cores"),
         "cpu_baseline": {"value": round(tok, 4), "unit": "tokens/s", "cores": procs, "kind": "port",
                          "sample": vals[0]["sample"]},
         "e2e": {"value": round(tok, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -826,7 +826,11 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
   p.causal = causal;
   p.qtiles = (int)((n + BM - 1) / BM);
   p.pairs = (p.qtiles + 1) / 2;
+#ifdef UL_FWD_HEAD_MAJOR
+  p.head_major = UL_FWD_HEAD_MAJOR;
+#else
   p.head_major = p.pairs >= sm_count();
+#endif
   p.scale_log2 = scale * 1.4426950408889634f;
   p.o = (__nv_bfloat16*)o;
   p.lse = lse;
