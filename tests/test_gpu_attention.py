@@ -203,24 +203,27 @@ def test_p_invariance_of_head_sharded_kernels():
         assert torch.equal(a, b[:, :, sl])
 
 
-@pytest.mark.parametrize("n", [8192])
-def test_fwd_bf16_large_sampled_rows(n):
-    # full-size config-2 shape; oracle on sampled query-row blocks (row_offset)
-    hq, hd = 4, 128
+@pytest.mark.parametrize("n,hq", [(8192, 4), (40960, 2)])
+def test_fwd_bf16_large_sampled_rows(n, hq):
+    # full-size config-2 shape (persistent grid, pair-major order) and a
+    # sequence with >= 148 query-tile pairs per head (one-shot grid,
+    # head-major order); oracle on sampled query-row blocks (row_offset)
+    hd = 128
     q, k, v, _ = inputs(n, 1, hq, hq, hd, torch.bfloat16, seed=9)
     o, lse = U().FlashAttention("causal").forward_with_lse(*(to_dev(x, torch.bfloat16) for x in (q, k, v)))
     o = to_np(o)
     lse = to_np(lse)
-    for r0 in (0, 4000, n - 128):
+    for r0 in (0, 4000, n // 2 + 64, n - 128):
         ref, ref_lse = O.local_attention(q, k, v, "causal", exact=False, rows=(r0, r0 + 128))
         assert rel_max_err(o[r0:r0 + 128], ref) <= BF16_MAXREL
         assert np.abs(lse[:, :, r0:r0 + 128] - ref_lse).max() <= 2e-2
 
 
-@pytest.mark.parametrize("n,hq,hkv", [(8192, 12, 12), (8192, 24, 12), (4096, 20, 10)])
+@pytest.mark.parametrize("n,hq,hkv", [(8192, 12, 12), (8192, 24, 12), (4096, 20, 10), (20480, 2, 2)])
 def test_fused_bwd_head_groups_match_deterministic(n, hq, hkv):
     # long sequences with many heads take the head-grouped CTA order (a
-    # partial last group exits early): gradients must equal the
+    # partial last group exits early), >= 148 kv tiles per head the
+    # head-major order: gradients must equal the
     # deterministic two-kernel path's within bf16 rounding
     hd = 128
     g = torch.Generator(device="cuda")
