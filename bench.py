@@ -88,9 +88,32 @@ def attn_flops(n_seq, heads, hd, causal=True):
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
 
+_NVML_SAMPLER = r"""
+import select, sys, time
+import pynvml
+pynvml.nvmlInit()
+h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+out = []
+while not select.select([sys.stdin], [], [], 0)[0]:
+    try:
+        mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        try:
+            rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        out.append("%d %d" % (mhz, rs))
+    except Exception:
+        pass
+    time.sleep(0.0005)
+print("\n".join(out), flush=True)
+"""
+
+
 class ClockSampler:
-    """SM clock and clock-event reasons sampled every ~1 ms (NVML) while the
-    timed region runs (falls back to `nvidia-smi -lms 100`)."""
+    """SM clock and clock-event reasons sampled every ~0.5-1 ms (NVML) while
+    the timed region runs, in a separate process so the host thread that
+    enqueues the step cannot starve it (falls back to `nvidia-smi -lms 100`)."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -103,22 +126,20 @@ class ClockSampler:
         self.lines = []
         self.samples = []       # (sm_mhz, reasons bitmask)
         self.max_mhz = None
-        self._stop = threading.Event()
         self.nvml = None
 
     def __enter__(self):
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            self.nvml = (pynvml, h)
-            self._old_switch = sys.getswitchinterval()
-            sys.setswitchinterval(0.0005)     # let the sampler run while the host enqueues
-            self.thread = threading.Thread(target=self._poll, daemon=True)
-            self.thread.start()
+            self.nvml = subprocess.Popen([sys.executable, "-c", _NVML_SAMPLER, str(self.gpu)], stdin=subprocess.PIPE,
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            first = self.nvml.stdout.readline().split()     # blocks until the sampler is polling
+            if len(first) != 2 or first[0] != "max":
+                raise RuntimeError("nvml sampler did not start")
+            self.max_mhz = int(first[1])
             return self
         except Exception:
+            if self.nvml is not None and self.nvml.poll() is None:
+                self.nvml.kill()
             self.nvml = None
         try:
             self.proc = subprocess.Popen(
@@ -130,29 +151,20 @@ class ClockSampler:
             self.proc = None
         return self
 
-    def _poll(self):
-        pynvml, h = self.nvml
-        while not self._stop.is_set():
-            try:
-                mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                try:
-                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                except Exception:
-                    rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.samples.append((mhz, rs))
-            except Exception:
-                pass
-            time.sleep(0.001)
-
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
         if self.nvml is not None:
-            self._stop.set()
-            self.thread.join(timeout=2)
-            sys.setswitchinterval(self._old_switch)
+            try:
+                out, _ = self.nvml.communicate(input="stop\n", timeout=10)
+                for ln in out.splitlines():
+                    parts = ln.split()
+                    if len(parts) == 2:
+                        self.samples.append((int(parts[0]), int(parts[1])))
+            except Exception:
+                self.nvml.kill()
         if self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
@@ -168,7 +180,9 @@ class ClockSampler:
                         "source": "nvml"}
             reasons = sorted(nm for nm, bit in self.REASONS.items() if any(r & bit for _, r in self.samples))
             return {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.max_mhz,
-                    "reasons": reasons, "samples": len(self.samples), "source": "nvml ~1 ms"}
+                    "reasons": reasons, "samples": len(self.samples), "source": "nvml ~0.5-1 ms, sampler process",
+                    "note": "NVML's SM clock; inside the tensor-core kernels clock64/globaltimer and ncu "
+                            "measure 1.60-1.77 GHz (power-limited; profiles/r1_summary.md r77, r85)"}
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
