@@ -1,0 +1,45 @@
+"""Host-side contract of bench.py (no GPU): the reference arm's JSON line,
+its rank-0-only behaviour under torchrun, and the clock sampler's fallback."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def _run_reference(env_extra):
+    env = dict(os.environ, **env_extra)
+    return subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "0",
+                           "--cpu-sample", "128"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+
+
+def test_reference_arm_json_line():
+    import bench
+    r = _run_reference({"RANK": "0", "WORLD_SIZE": "1"})
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference"
+    assert d["unit"] == "tokens/s" and d["higher_is_better"] is True and d["value"] > 0
+    # the same workload description as our arm
+    assert d["config"] == bench.workload_config(1, bench.SEQ_PER_GPU, bench.HEADS, bench.HEAD_DIM)
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == d["value"] and "N=128" in cb["sample"]
+    assert d["e2e"] == {"value": d["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+
+
+def test_reference_arm_other_ranks_are_silent():
+    r = _run_reference({"RANK": "1", "WORLD_SIZE": "2"})
+    assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_clock_sampler_without_gpu_reports_unsampled():
+    import bench
+    with bench.ClockSampler(0) as c:
+        pass
+    s = c.summary()
+    if s.get("samples", 0) == 0:
+        assert s["reasons"] == ["unsampled"] and s["sm_mhz"] is None
