@@ -569,6 +569,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) {   // CTA life (trace builds): start
+    UL_CTA(0, globaltimer());
+    UL_CTA(1, globaltimer());
+    UL_CTA(4, smid());
+    UL_CTA(5, clock64());
+  }
   tc_fence_after();
   if (*tmem_slot != 0u) __trap();
   constexpr uint32_t tbase = 0;
@@ -802,6 +808,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) {   // CTA life (trace builds): end
+    UL_CTA(2, globaltimer());
+    UL_CTA(3, globaltimer());
+    UL_CTA(6, clock64());
+  }
   if (p.ep.active && threadIdx.x == 0) peer_signal_last_cta(p.ep, gridDim.x);
   if (warp == 1) {
     __syncwarp();

@@ -95,3 +95,9 @@ start, first, epi, end, sm, ck0, ck1 = (c[:, i] for i in range(7))
 print(f"== CTA life: {len(c)} CTAs, span {(end.max() - start.min()) / 1e3:.1f} us,"
       f" clock {np.median((ck1 - ck0) / (end - start)):.3f} GHz, prologue {np.median(first - start) / 1e3:.2f} us,"
       f" epilogue {np.median(end - epi) / 1e3:.2f} us, main {np.median(epi - first) / 1e3:.2f} us")
+if os.environ.get("CTA_PERSIST"):
+    # persistent grid: one CTA per SM; the spread of their end times is the
+    # static schedule's imbalance
+    print(f"== persistent CTAs: end spread {(end.max() - end.min()) / 1e3:.1f} us "
+          f"(p10 {np.percentile(end - start.min(), 10) / 1e3:.1f}, median {np.median(end - start.min()) / 1e3:.1f}, "
+          f"max {(end.max() - start.min()) / 1e3:.1f} us)")
