@@ -20,6 +20,8 @@
 //     streams per SMSP); one query row per thread, exp2 domain, masking only
 //     on diagonal/tail tiles, FFMA-fused exponent, ILP'd max/sum chains, P
 //     packed to bf16 and stored 32 columns at a time over consumed S.
+#include <mutex>
+#include <unordered_map>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -95,6 +97,9 @@ struct Params {
   // blk_nb = n / blk_bs per side).  nullptr: dense / causal.
   const uint32_t* blk;
   int blk_bs, blk_words, blk_nb;
+  // persistent kernel: [next item, CTAs done] counters (per stream, zero at
+  // rest: the last CTA resets them), or nullptr for the static zig-zag waves
+  int* ctr;
 };
 
 __device__ __forceinline__ bool blk_bit(const Params& p, int qb, int kb) {
@@ -519,6 +524,33 @@ __device__ __forceinline__ bool fwd_item(const Params& p, int k, int& pair, int&
   return true;
 }
 
+// dynamic items: the TMA thread (role 0) takes the next item index from the
+// launch's counter and publishes it in a 4-slot shared ring; the MMA thread
+// (role 1) and every softmax warp (role 2, all lanes) read it in the same
+// order -- greedy longest-first over the length-sorted list
+template <int HD>
+__device__ __forceinline__ bool fwd_item_dyn(const Params& p, int k, int& pair, int& bh, int role,
+                                             uint64_t* it_full, uint64_t* it_empty, volatile int* sitem) {
+  const int slot = k & 3;
+  int idx;
+  if (role == 0) {
+    if (k >= 4) mbar_wait(&it_empty[slot], ((k >> 2) - 1) & 1);
+    idx = atomicAdd(p.ctr, 1);
+    sitem[slot] = idx;
+    mbar_arrive(&it_full[slot]);
+  } else {
+    mbar_wait(&it_full[slot], (k >> 2) & 1);
+    idx = sitem[slot];
+    if (role == 2) __syncwarp();
+    if (role == 1 || (threadIdx.x & 31) == 0) mbar_arrive(&it_empty[slot]);
+  }
+  const int heads = p.b * p.hq;
+  if (idx >= p.pairs * heads) return false;
+  pair = p.head_major ? p.pairs - 1 - idx % p.pairs : p.pairs - 1 - idx / heads;
+  bh = p.head_major ? idx / p.pairs : idx % heads;
+  return true;
+}
+
 template <int HD>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_persist_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -541,6 +573,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* q_empty = bars + 7 + 4 * NS;    // Q smem free (the item's last S MMAs completed)
   uint64_t* o_free = bars + 8 + 4 * NS;     // [2] per tile: O read out by the epilogue
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10 + 4 * NS);
+  uint64_t* it_full = bars + 11 + 4 * NS;   // [4] dynamic item ring
+  uint64_t* it_empty = bars + 15 + 4 * NS;  // [4]
+  volatile int* sitem = reinterpret_cast<volatile int*>(bars + 19 + 4 * NS);
+  static_assert((21 + 4 * NS) * 8 <= 256, "barrier area");
+  auto item = [&](int k, int& pair, int& bh, int role) {
+    return p.ctr ? fwd_item_dyn<HD>(p, k, pair, bh, role, it_full, it_empty, sitem) : fwd_item<HD>(p, k, pair, bh);
+  };
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nkv_all = (p.n + BN - 1) / BN;
@@ -564,6 +603,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&o_done[t], 1);
       mbar_init(&o_free[t], kSoftPerTile);
     }
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&it_full[s], 1);
+      mbar_init(&it_empty[s], 1 + 2 * kSoftPerTile);
+    }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -585,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
       int pair, bh, gk = 0;
-      for (int k = 0; fwd_item<HD>(p, k, pair, bh); ++k) {
+      for (int k = 0; item(k, pair, bh, 0); ++k) {
         const int bb = bh / p.hq, h = bh % p.hq, g = h / (p.hq / p.hkv);
         const int n0 = item_kv(pair, 0), n1 = item_kv(pair, 1);
         const int nkv = max(n0, n1), ntiles = n1 > 0 ? 2 : 1;
@@ -643,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++cpv[t];
       };
       int pair, bh, gk = 0;
-      for (int k = 0; fwd_item<HD>(p, k, pair, bh); ++k) {
+      for (int k = 0; item(k, pair, bh, 1); ++k) {
         const int nT0 = item_kv(pair, 0), nT1 = item_kv(pair, 1);
         const int nkv = max(nT0, nT1);
         mbar_wait_mma(q_full, k & 1);
@@ -689,7 +732,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
     int cs = 0;   // S tiles of this query tile consumed so far (s_full / o_done phases)
     int pair, bh;
-    for (int k = 0; fwd_item<HD>(p, k, pair, bh); ++k) {
+    for (int k = 0; item(k, pair, bh, 2); ++k) {
       const int my_nkv = item_kv(pair, t);
       if (my_nkv == 0) continue;
       const int bb = bh / p.hq, h = bh % p.hq;
@@ -813,12 +856,54 @@ __global__ void __launch_bounds__(kThreads, 1)
     UL_CTA(3, globaltimer());
     UL_CTA(6, clock64());
   }
+  if (p.ctr && threadIdx.x == 0) {   // every CTA has taken its last index: the last one resets
+    __threadfence();
+    if (atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1) {
+      atomicExch(p.ctr, 0);
+      atomicExch(p.ctr + 1, 0);
+    }
+  }
   if (p.ep.active && threadIdx.x == 0) peer_signal_last_cta(p.ep, gridDim.x);
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
     tmem_dealloc<512>(tbase);
   }
+}
+
+// [next item, CTAs done] counters of the persistent forward, one pair per
+// stream (launches on one stream are ordered; the kernel leaves them zero).
+// nullptr (static zig-zag schedule) while a stream is being captured or if
+// the allocation fails.
+#ifndef UL_FWD_DYNAMIC
+#define UL_FWD_DYNAMIC 1
+#endif
+static int* stream_counters(cudaStream_t st) {
+  if (!UL_FWD_DYNAMIC) return nullptr;
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, int*> ctrs;   // key: (device, stream); never freed (8 bytes per stream)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  const uint64_t key = reinterpret_cast<uint64_t>(st) * 64 + (uint64_t)dev;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = ctrs.find(key);
+  if (it != ctrs.end()) return it->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  int* c = nullptr;
+  if (cudaMalloc(&c, 2 * sizeof(int)) != cudaSuccess || cudaMemsetAsync(c, 0, 2 * sizeof(int), st) != cudaSuccess) {
+    cudaGetLastError();
+    if (c) cudaFree(c);
+    return nullptr;
+  }
+  ctrs[key] = c;
+  return c;
 }
 
 template <int HD>
@@ -851,6 +936,7 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
   p.blk_bs = (int)blk_bs;
   p.blk_words = (int)blk_words;
   p.blk_nb = blk ? (int)(n / blk_bs) : 0;
+  p.ctr = nullptr;
   if (blk) p.causal = 0;
   const int smem = Smem<HD>::kBytes;
   static bool attr = false;
@@ -862,19 +948,25 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
 #ifndef UL_FWD_PERSIST
 #define UL_FWD_PERSIST 1   // r73: -1.5% vs the one-shot grid; blocked-sparse keeps the one-shot kernel
 #endif
-  // head-major orders (a head's pairs fill a wave: long sequences) keep the
-  // one-shot grid: the static zig-zag waves of the persistent kernel balance
-  // the tile-major length ramp but not the per-head sawtooth (r83: N = 64K,
-  // 4 heads 3.7 -> 5.1 ms)
-  if (UL_FWD_PERSIST && !blk && !p.head_major) {
-    static bool pattr = false;
-    if (!pattr) {
-      UL_CUDA(cudaFuncSetAttribute(attn_fwd_persist_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      pattr = true;
+  // Items are fetched dynamically from a per-stream counter (greedy
+  // longest-first).  Without one (stream capture) the static zig-zag waves
+  // are used, which balance the pair-major length ramp but not the per-head
+  // sawtooth of head-major orders (r83: N = 64K, 4 heads 3.7 -> 5.1 ms): those
+  // keep the one-shot grid then.  (r89: dynamic vs static at config 2 equal;
+  // head-major persistent vs one-shot within noise, config 5 -2%.)
+  if (UL_FWD_PERSIST && !blk) {
+    p.ctr = stream_counters(st);
+    if (p.ctr || !p.head_major) {
+      static bool pattr = false;
+      if (!pattr) {
+        UL_CUDA(cudaFuncSetAttribute(attn_fwd_persist_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        pattr = true;
+      }
+      const int64_t pgrid = grid < sm_count() ? grid : sm_count();
+      attn_fwd_persist_kernel<HD><<<(unsigned)pgrid, kThreads, smem, st>>>(mq, mk, mv, p);
+      return launched("attn_fwd_sm100");
     }
-    const int64_t pgrid = grid < sm_count() ? grid : sm_count();
-    attn_fwd_persist_kernel<HD><<<(unsigned)pgrid, kThreads, smem, st>>>(mq, mk, mv, p);
-    return launched("attn_fwd_sm100");
+    p.ctr = nullptr;
   }
   attn_fwd_kernel<HD><<<(unsigned)grid, kThreads, smem, st>>>(mq, mk, mv, p);
   return launched("attn_fwd_sm100");
