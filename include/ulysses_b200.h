@@ -133,6 +133,10 @@ size_t ul_all_to_all_slot_bytes(int n_tensors, const int64_t* shapes, int ndim, 
  *   o  [n, b, hq,  hd]      lse  [b, hq, n] float32, natural log
  * mask UL_MASK_NONE / UL_MASK_CAUSAL on global indices (kv <= q).
  * bf16: hd in {64, 128}; fp32: hd <= 256.
+ * The bf16 dense/causal forward (persistent grid) fetches its work items
+ * from an 8-byte device counter pair the library allocates once per
+ * (device, stream) on the first call outside stream capture; the kernel
+ * leaves it zeroed.  Nothing else is allocated.
  * ==================================================================== */
 int ul_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
                 int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
