@@ -89,23 +89,49 @@ def attn_flops(n_seq, heads, hd, causal=True):
 # ---------------------------------------------------------------------------
 
 _NVML_SAMPLER = r"""
-import select, sys, time
+import os, select, sys, time
+try:   # stay off the launching thread's core, at low priority
+    cpus = sorted(os.sched_getaffinity(0))
+    if len(cpus) > 1:
+        os.sched_setaffinity(0, {cpus[-1]})
+    os.nice(10)
+except Exception:
+    pass
 import pynvml
 pynvml.nvmlInit()
 h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
 print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
 out = []
-while not select.select([sys.stdin], [], [], 0)[0]:
+period = float(sys.argv[2])
+idle = os.environ.get("UL_BENCH_CLOCK_IDLE") == "1"   # diagnostics: NVML initialised, no queries
+clocks = False
+last_clk, n_clk = -1e9, 0
+while True:
+    if select.select([sys.stdin], [], [], 0)[0]:
+        cmd = sys.stdin.readline().strip()
+        if cmd == "clocks":      # the host has enqueued the timed steps: the GPU is busy with them
+            clocks = True
+        else:
+            break
     try:
-        mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        # every NVML query perturbs the GPU work (~10-20 us of step time,
+        # r90): clock-event reasons every period over the whole region, the
+        # SM clock at most twice, once the host has enqueued every timed step
+        if idle:
+            time.sleep(period)
+            continue
         try:
             rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
         except Exception:
             rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        mhz = -1
+        if clocks and n_clk < 2:
+            mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)   # each query stalls the GPU ~20 us (r90)
+            last_clk, n_clk = time.perf_counter(), n_clk + 1
         out.append("%d %d" % (mhz, rs))
     except Exception:
         pass
-    time.sleep(0.0005)
+    time.sleep(period)
 print("\n".join(out), flush=True)
 """
 
@@ -119,6 +145,17 @@ class ClockSampler:
               "clocks_event_reasons.sw_power_cap")
     # nvmlClocksEventReason* bits
     REASONS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
+    PERIOD_MS = 3.0      # each NVML query perturbs the timed GPU work (~10-20 us, r90)
+
+    def enqueued(self):
+        """All timed steps are enqueued (the GPU is still running them): start
+        sampling the SM clock too."""
+        if self.nvml is not None:
+            try:
+                self.nvml.stdin.write("clocks\n")
+                self.nvml.stdin.flush()
+            except Exception:
+                pass
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
@@ -129,8 +166,12 @@ class ClockSampler:
         self.nvml = None
 
     def __enter__(self):
+        if os.environ.get("UL_BENCH_CLOCKS") == "off":     # diagnostics only: A/B of the sampler's cost
+            return self
         try:
-            self.nvml = subprocess.Popen([sys.executable, "-c", _NVML_SAMPLER, str(self.gpu)], stdin=subprocess.PIPE,
+            period = float(os.environ.get("UL_BENCH_CLOCK_MS", self.PERIOD_MS)) / 1e3
+            self.nvml = subprocess.Popen([sys.executable, "-c", _NVML_SAMPLER, str(self.gpu), str(period)],
+                                         stdin=subprocess.PIPE,
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             first = self.nvml.stdout.readline().split()     # blocks until the sampler is polling
             if len(first) != 2 or first[0] != "max":
@@ -179,8 +220,13 @@ class ClockSampler:
                 return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0,
                         "source": "nvml"}
             reasons = sorted(nm for nm, bit in self.REASONS.items() if any(r & bit for _, r in self.samples))
-            return {"sm_mhz": statistics.median(m for m, _ in self.samples), "sm_max_mhz": self.max_mhz,
-                    "reasons": reasons, "samples": len(self.samples), "source": "nvml ~0.5-1 ms, sampler process",
+            mhz = [m for m, _ in self.samples if m >= 0]
+            return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons if mhz else reasons + ["sm clock unsampled"], "samples": len(self.samples),
+                    "sm_clock_samples": len(mhz),
+                    "source": f"nvml sampler process every {self.PERIOD_MS} ms: clock-event reasons over "
+                              "the whole timed region; SM clock <= 2 samples while the GPU runs the enqueued "
+                              "timed steps (each NVML query perturbs the step, r90)",
                     "note": "NVML's SM clock; inside the tensor-core kernels clock64/globaltimer and ncu "
                             "measure 1.60-1.77 GHz (power-limited; profiles/r1_summary.md r77, r85)"}
         sm, mx, reasons = [], [], set()
@@ -319,6 +365,7 @@ def run_ours(args):
             ev[i][0].record()
             step(q.detach(), k.detach(), v.detach(), do)
             ev[i][1].record()
+        clk.enqueued()
         torch.cuda.synchronize()
         if P > 1:
             dist.barrier()
