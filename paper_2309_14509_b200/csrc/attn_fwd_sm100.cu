@@ -887,15 +887,16 @@ static int* stream_counters(cudaStream_t st) {
     cudaGetLastError();
     return nullptr;
   }
-  const uint64_t key = reinterpret_cast<uint64_t>(st) * 64 + (uint64_t)dev;
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = ctrs.find(key);
-  if (it != ctrs.end()) return it->second;
+  // never inside a capture: a graph may be replayed on several streams at once
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
     cudaGetLastError();
     return nullptr;
   }
+  const uint64_t key = reinterpret_cast<uint64_t>(st) * 64 + (uint64_t)dev;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = ctrs.find(key);
+  if (it != ctrs.end()) return it->second;
   int* c = nullptr;
   if (cudaMalloc(&c, 2 * sizeof(int)) != cudaSuccess || cudaMemsetAsync(c, 0, 2 * sizeof(int), st) != cudaSuccess) {
     cudaGetLastError();
