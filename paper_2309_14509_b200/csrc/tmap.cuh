@@ -40,8 +40,11 @@ inline int make_tmap_bhsd(CUtensorMap* m, const void* ptr, int64_t rows, int64_t
   cuuint64_t strides[2] = {(cuuint64_t)(hd * 2), (cuuint64_t)(heads * hd * 2)};
   cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
   cuuint32_t es[3] = {1, 1, 1};
+#ifndef UL_TMAP_L2_PROMOTION
+#define UL_TMAP_L2_PROMOTION CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, UL_TMAP_L2_PROMOTION,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(UL_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return UL_OK;
