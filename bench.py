@@ -463,9 +463,9 @@ def kernel_split(attn, q, k, v, do, args, dev):
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     wsb = int(lib.ul_attn_bwd_workspace_bytes(n, b, h, h, hd, 1))
     ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    sched = torch.zeros(2, dtype=torch.int32, device=dev)   # persistent-forward work counter (UL_ATTN_SCHED_BYTES)
     scale = 1.0 / math.sqrt(hd)
     fused = hd == 128 and not attn.deterministic
-    lib.ul_attn_set_deterministic(int(attn.deterministic))
     if fused:   # one kernel for dK, dV and dQ (+ the dQ fp32 -> bf16 pass)
         names = ["attn_fwd_sm100", "attn_bwd_prep", "attn_bwd_fused_sm100", "attn_bwd_dq_convert"]
     else:
@@ -481,14 +481,14 @@ def kernel_split(attn, q, k, v, do, args, dev):
     def run(nm):
         if nm == "attn_fwd_sm100":
             _lib.check(lib.ul_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(),
-                                       n, b, h, h, hd, 1, 1, scale, stream))
+                                       n, b, h, h, hd, 1, 1, scale, sched.data_ptr(), stream))
         else:
             stage = {"attn_bwd_prep": 1, "attn_bwd_dkdv_sm100": 2, "attn_bwd_dq_sm100": 4, "attn_bwd_fused_sm100": 2,
                      "attn_bwd_dq_convert": 4}[nm]
             _lib.check(lib.ul_attn_bwd_stages(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                               do.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(),
                                               dv.data_ptr(), ws.data_ptr(), wsb, n, b, h, h, hd, 1, 1, scale,
-                                              stage, stream))
+                                              stage, attn.flags, stream))
 
     reps = max(3, min(args.steps, 10))
     for it in range(args.warmup + reps):

@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define UL_ABI_VERSION 1
+#define UL_ABI_VERSION 2
 
 /* ---- status codes: one per reference exception type ------------------ */
 #define UL_OK                 0
@@ -133,14 +133,17 @@ size_t ul_all_to_all_slot_bytes(int n_tensors, const int64_t* shapes, int ndim, 
  *   o  [n, b, hq,  hd]      lse  [b, hq, n] float32, natural log
  * mask UL_MASK_NONE / UL_MASK_CAUSAL on global indices (kv <= q).
  * bf16: hd in {64, 128}; fp32: hd <= 256.
- * The bf16 dense/causal forward (persistent grid) fetches its work items
- * from an 8-byte device counter pair the library allocates once per
- * (device, stream) on the first call outside stream capture; the kernel
- * leaves it zeroed.  Nothing else is allocated.
+ * `sched` (may be NULL): caller-owned DEVICE memory of UL_ATTN_SCHED_BYTES,
+ * zeroed once before first use, from which the bf16 dense/causal forward's
+ * persistent grid fetches its work items (greedy longest-first); the kernel
+ * leaves it zeroed again.  Launches sharing one `sched` must be
+ * stream-ordered (one per stream).  NULL, or a stream under capture, selects
+ * a static schedule.  The library allocates nothing.
  * ==================================================================== */
+#define UL_ATTN_SCHED_BYTES 8
 int ul_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse,
                 int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
-                int dtype, int mask, float scale, void* stream);
+                int dtype, int mask, float scale, void* sched, void* stream);
 
 /* Blocked-sparse forward (blocked_kernel, kernels.py:55-86; Mask.blocked,
  * tensor.py:147-180): query block qb sees exactly the key blocks kb whose
@@ -157,14 +160,22 @@ int ul_attn_fwd_blocked(const void* q, const void* k, const void* v, void* o, fl
                         float scale, void* stream);
 
 /* dq [n,b,hq,hd], dk/dv [n,b,hkv,hd] (dk/dv summed over each kv head's
- * query group).  workspace >= ul_attn_bwd_workspace_bytes(...). */
+ * query group).  workspace >= ul_attn_bwd_workspace_bytes(...).
+ * flags (per call; extension, no reference counterpart):
+ *   0: bf16 hd-128 backward in one fused kernel (dK, dV and dQ from one
+ *      pass; dQ accumulated with fp32 atomics, so it varies in the last
+ *      bits run to run);
+ *   UL_ATTN_DETERMINISTIC: dK/dV kernel + a dQ kernel that recomputes S and
+ *      dP, no atomics: bitwise reproducible (and bitwise P-invariant).
+ * hd 64 and fp32 always run the deterministic kernels. */
+#define UL_ATTN_DETERMINISTIC 1
 size_t ul_attn_bwd_workspace_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
                                    int dtype);
 int ul_attn_bwd(const void* q, const void* k, const void* v, const void* o,
                 const void* dout, const float* lse, void* dq, void* dk, void* dv,
                 void* workspace, size_t workspace_bytes,
                 int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
-                int dtype, int mask, float scale, void* stream);
+                int dtype, int mask, float scale, int flags, void* stream);
 
 /* Same as ul_attn_bwd restricted to a subset of its launches (bit 0: D/LSE
  * pre-pass, bit 1: dK/dV kernel -- the fused dK/dV/dQ kernel in the default
@@ -175,17 +186,7 @@ int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* 
                        const void* dout, const float* lse, void* dq, void* dk, void* dv,
                        void* workspace, size_t workspace_bytes,
                        int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
-                       int dtype, int mask, float scale, int stage_mask, void* stream);
-
-/* Backward mode (process-wide; extension, no reference counterpart).
- * 0 (default): bf16 hd-128 backward in one fused kernel (dK, dV and dQ from
- *   one pass; dQ accumulated with fp32 atomics, so it varies in the last
- *   bits run to run).
- * 1: deterministic -- dK/dV kernel + a dQ kernel that recomputes S and dP,
- *   no atomics, results bitwise reproducible (and bitwise P-invariant).
- * hd 64 and fp32 always run the deterministic kernels. */
-void ul_attn_set_deterministic(int on);
-int ul_attn_get_deterministic(void);
+                       int dtype, int mask, float scale, int stage_mask, int flags, void* stream);
 
 /* Local attention with the head->seq exchange (K2) fused into the kernels'
  * epilogues: every finished output row goes both to the head-layout tensor
@@ -199,12 +200,12 @@ int ul_attn_get_deterministic(void);
  *   seq_out [n/P, b, P*hq, hd];  seq_dq [n/P, b, P*hq, hd], seq_dk/dv [n/P, b, P*hkv, hd] */
 int ul_attn_fwd_exchange(ul_comm* comm, const void* q, const void* k, const void* v, void* o, float* lse,
                          void* seq_out, int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
-                         int dtype, int mask, float scale, uint64_t label_hash, void* stream);
+                         int dtype, int mask, float scale, uint64_t label_hash, void* sched, void* stream);
 int ul_attn_bwd_exchange(ul_comm* comm, const void* q, const void* k, const void* v, const void* o,
                          const void* dout, const float* lse, void* dq, void* dk, void* dv,
                          void* workspace, size_t workspace_bytes, void* seq_dq, void* seq_dk,
                          void* seq_dv, int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
-                         int dtype, int mask, float scale, uint64_t label_hash, void* stream);
+                         int dtype, int mask, float scale, uint64_t label_hash, int flags, void* stream);
 
 /* RankContext.ring_shift(local, steps, label) (simgroup.py:374-388, 464-465):
  * out[t] on rank i = in[t] of rank (i - steps) mod P, n flat tensors of

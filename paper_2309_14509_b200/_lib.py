@@ -26,6 +26,9 @@ MASK_BLOCKED = 2   # Python-side tag; the blocked forward has its own entry poin
 MAX_RANKS = 16
 MAX_FUSED = 4
 IPC_HANDLE_BYTES = 128
+ABI_VERSION = 2
+ATTN_SCHED_BYTES = 8
+ATTN_DETERMINISTIC = 1
 
 # every symbol include/ulysses_b200.h declares (tests check the exports)
 EXPORTS = (
@@ -35,7 +38,7 @@ EXPORTS = (
     "ul_comm_ledger", "ul_all_to_all", "ul_all_to_all_slot_bytes", "ul_attn_fwd", "ul_attn_fwd_blocked", "ul_qkv_proj_exchange", "ul_ring_shift", "ul_lse_merge",
     "ul_attn_bwd_workspace_bytes", "ul_attn_bwd", "ul_attn_bwd_stages", "ul_attn_fwd_exchange",
     "ul_attn_bwd_exchange", "ul_last_launch_count",
-    "ul_total_launch_count", "ul_ulysses_volume", "ul_attn_set_deterministic", "ul_attn_get_deterministic",
+    "ul_total_launch_count", "ul_ulysses_volume",
 )
 
 _lib = None
@@ -48,8 +51,6 @@ def _declare(lib):
     P = ctypes.POINTER
     sig = {
         "ul_abi_version": (ctypes.c_int, []),
-        "ul_attn_set_deterministic": (None, [ctypes.c_int]),
-        "ul_attn_get_deterministic": (ctypes.c_int, []),
         "ul_last_error": (ctypes.c_char_p, []),
         "ul_preload_kernels": (ctypes.c_int, []),
         "ul_comm_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_size_t,
@@ -79,21 +80,21 @@ def _declare(lib):
         "ul_attn_fwd_blocked": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64,
                                                 ctypes.c_int, c_i64, c_vp, c_i64, ctypes.c_float, c_vp]),
         "ul_attn_fwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64,
-                                       ctypes.c_int, ctypes.c_int, ctypes.c_float, c_vp]),
+                                       ctypes.c_int, ctypes.c_int, ctypes.c_float, c_vp, c_vp]),
         "ul_attn_bwd_workspace_bytes": (ctypes.c_size_t, [c_i64, c_i64, c_i64, c_i64, c_i64, ctypes.c_int]),
         "ul_attn_bwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        ctypes.c_size_t, c_i64, c_i64, c_i64, c_i64, c_i64, ctypes.c_int,
-                                       ctypes.c_int, ctypes.c_float, c_vp]),
+                                       ctypes.c_int, ctypes.c_float, ctypes.c_int, c_vp]),
         "ul_attn_bwd_stages": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                               ctypes.c_size_t, c_i64, c_i64, c_i64, c_i64, c_i64, ctypes.c_int,
-                                              ctypes.c_int, ctypes.c_float, ctypes.c_int, c_vp]),
+                                              ctypes.c_int, ctypes.c_float, ctypes.c_int, ctypes.c_int, c_vp]),
         "ul_attn_fwd_exchange": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64,
                                                 c_i64, c_i64, ctypes.c_int, ctypes.c_int, ctypes.c_float,
-                                                ctypes.c_uint64, c_vp]),
+                                                ctypes.c_uint64, c_vp, c_vp]),
         "ul_attn_bwd_exchange": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                                 ctypes.c_size_t, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64,
                                                 c_i64, ctypes.c_int, ctypes.c_int, ctypes.c_float, ctypes.c_uint64,
-                                                c_vp]),
+                                                ctypes.c_int, c_vp]),
         "ul_last_launch_count": (ctypes.c_int, []),
         "ul_total_launch_count": (ctypes.c_uint64, []),
         "ul_ulysses_volume": (ctypes.c_int, [c_i64, c_i64, c_i64, c_i64, ctypes.c_int, P(c_i64), P(c_i64)]),
@@ -114,7 +115,7 @@ def lib():
                 "There is no fallback path.")
         _lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
         _declare(_lib)
-        if _lib.ul_abi_version() != 1:
+        if _lib.ul_abi_version() != ABI_VERSION:
             raise RuntimeError("libulysses_b200 ABI version mismatch")
     return _lib
 

@@ -35,7 +35,7 @@ import math
 import torch
 
 from . import _lib
-from .comm import SequenceGroup
+from .comm import SequenceGroup, slot_need
 from .errors import DegenerateRowError, DivisibilityError, ForwardStateError, KernelError
 
 _ATTN_DTYPES = {torch.float32: _lib.DTYPE_F32, torch.bfloat16: _lib.DTYPE_BF16}
@@ -45,13 +45,45 @@ def _stream(t: torch.Tensor) -> int:
     return torch.cuda.current_stream(t.device).cuda_stream
 
 
+_SCHED = {}
+
+
+def _sched_counter(t: torch.Tensor):
+    """Work counter of the persistent forward (UL_ATTN_SCHED_BYTES of zeroed
+    device memory, one per (device, stream): launches sharing it must be
+    stream-ordered).  None -- the static schedule -- under stream capture."""
+    if torch.cuda.is_current_stream_capturing():
+        return None
+    s = torch.cuda.current_stream(t.device)
+    key = (t.device.index, s.stream_id)
+    c = _SCHED.get(key)
+    if c is None:
+        c = torch.zeros(_lib.ATTN_SCHED_BYTES // 4, dtype=torch.int32, device=t.device)
+        _SCHED[key] = c
+    return c.data_ptr()
+
+
+_PG_GROUPS = {}
+
+
 def _group(group) -> SequenceGroup:
+    """sequence_process_group: a SequenceGroup, a torch.distributed
+    ProcessGroup (wrapped once -- a collective over its ranks -- and cached),
+    or None (P = 1)."""
     if group is None:
         return SequenceGroup.single()
-    if not isinstance(group, SequenceGroup):
-        raise TypeError("sequence_process_group must be a SequenceGroup "
-                        "(SequenceGroup.from_process_group(torch.distributed group))")
-    return group
+    if isinstance(group, SequenceGroup):
+        return group
+    import torch.distributed as dist
+    if isinstance(group, dist.ProcessGroup):
+        key = id(group)
+        hit = _PG_GROUPS.get(key)
+        if hit is None or hit[0] is not group:
+            hit = (group, SequenceGroup.from_process_group(group))
+            _PG_GROUPS[key] = hit
+        return hit[1]
+    raise TypeError("sequence_process_group must be a SequenceGroup or a torch.distributed ProcessGroup, "
+                    f"got {type(group).__name__}")
 
 
 # ---------------------------------------------------------------------------
@@ -119,14 +151,21 @@ class FlashAttention:
             raise KernelError(f"block_size/pattern apply to the blocked kernel, not {mask!r}")
 
     @property
+    def flags(self) -> int:
+        """Per-call backward flags of the C-ABI (UL_ATTN_DETERMINISTIC)."""
+        return _lib.ATTN_DETERMINISTIC if self.deterministic else 0
+
+    @property
     def mask_code(self) -> int:
         return {"causal": _lib.MASK_CAUSAL, "none": _lib.MASK_NONE, "blocked": _lib.MASK_BLOCKED}[self.mask]
 
     def _pattern_bits(self, n: int, device) -> torch.Tensor:
         """Validate the pattern for sequence length n with blocked_kernel's
         rules and order (kernels.py:63-80) and return its device bitmap
-        (uint32 rows of ceil(nb/32) words, include/ulysses_b200.h)."""
-        key = (n, str(device))
+        (uint32 rows of ceil(nb/32) words, include/ulysses_b200.h).  One
+        device copy per (n, device, stream): the copy is stream-ordered on the
+        stream that reads it, so no other stream can see it unfinished."""
+        key = (n, str(device), torch.cuda.current_stream(device).stream_id)
         if key in self._bits:
             return self._bits[key]
         bs = self.block_size
@@ -185,7 +224,7 @@ class FlashAttention:
             return o, lse
         _lib.check(_lib.lib().ul_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                           lse.data_ptr(), n, b, hq, hkv, hd, _ATTN_DTYPES[q.dtype],
-                                          self.mask_code, self._scale(hd), _stream(q)))
+                                          self.mask_code, self._scale(hd), _sched_counter(q), _stream(q)))
         return o, lse
 
     def _backward_mask_check(self):
@@ -207,11 +246,10 @@ class FlashAttention:
         dt = _ATTN_DTYPES[q.dtype]
         wsb = int(_lib.lib().ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dt))
         ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=q.device)
-        _lib.lib().ul_attn_set_deterministic(int(self.deterministic))
         _lib.check(_lib.lib().ul_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                           do.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(),
                                           dv.data_ptr(), ws.data_ptr(), ws.numel(), n, b, hq, hkv, hd,
-                                          dt, self.mask_code, self._scale(hd), _stream(q)))
+                                          dt, self.mask_code, self._scale(hd), self.flags, _stream(q)))
         return dq, dk, dv
 
     # -- fused head->seq exchange (K2 in the kernels' epilogues) ------------
@@ -230,10 +268,11 @@ class FlashAttention:
         o = torch.empty_like(q)
         lse = torch.empty((b, hq, n), dtype=torch.float32, device=q.device)
         o_seq = torch.empty((n // p, b, hq * p, hd), dtype=q.dtype, device=q.device)
+        group.ensure_slot(slot_need([o_seq.numel() * o_seq.element_size()]))
         _lib.check(_lib.lib().ul_attn_fwd_exchange(group._handle, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                                    o.data_ptr(), lse.data_ptr(), o_seq.data_ptr(), n, b, hq, hkv,
                                                    hd, _ATTN_DTYPES[q.dtype], self.mask_code, self._scale(hd),
-                                                   label_hash(label), _stream(q)))
+                                                   label_hash(label), _sched_counter(q), _stream(q)))
         group._record(label, o.numel())
         return o, lse, o_seq
 
@@ -256,13 +295,13 @@ class FlashAttention:
         dt = _ATTN_DTYPES[q.dtype]
         wsb = int(_lib.lib().ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dt))
         ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=q.device)
-        _lib.lib().ul_attn_set_deterministic(int(self.deterministic))
+        group.ensure_slot(slot_need(t.numel() * t.element_size() for t in (sq, sk, sv)))
         _lib.check(_lib.lib().ul_attn_bwd_exchange(group._handle, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                                    o.data_ptr(), do.data_ptr(), lse.data_ptr(), dq.data_ptr(),
                                                    dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), ws.numel(),
                                                    sq.data_ptr(), sk.data_ptr(), sv.data_ptr(), n, b, hq, hkv, hd,
                                                    dt, self.mask_code, self._scale(hd), label_hash(label),
-                                                   _stream(q)))
+                                                   self.flags, _stream(q)))
         for name, t in (("bwd.q.head2seq", dq), ("bwd.k.head2seq", dk), ("bwd.v.head2seq", dv)):
             group._record(name, t.numel())
         if return_head:
@@ -386,11 +425,13 @@ class DistributedAttention(torch.nn.Module):
         if hkv % p != 0:
             raise DivisibilityError(f"p={p} does not divide kv head count {hkv}")
 
-    def forward(self, query, key, value):
+    def forward(self, query, key, value, *args, **kwargs):
+        """``*args`` / ``**kwargs`` pass through to ``local_attn`` (the
+        DeepSpeed signature); with extra arguments the generic route runs."""
         self._check(query, key, value)
         fused_layout = (self.scatter_idx, self.gather_idx) == (2, 0) or \
             ((self.scatter_idx, self.gather_idx) == (2, 1) and query.shape[0] == 1)
-        if isinstance(self.local_attn, FlashAttention) and fused_layout:
+        if isinstance(self.local_attn, FlashAttention) and fused_layout and not args and not kwargs:
             if (self.scatter_idx, self.gather_idx) == (2, 1):      # [1, s, h, d] == [s, 1, h, d]
                 q, k, v = (x.reshape(x.shape[1], 1, x.shape[2], x.shape[3]) for x in (query, key, value))
                 o = _UlyssesAttnFn.apply(self.spg, self.local_attn, 2, 0, q, k, v)
@@ -401,5 +442,5 @@ class DistributedAttention(torch.nn.Module):
         q4 = seq_all_to_all(query, self.scatter_idx, self.gather_idx, self.spg, "attn.q.seq2head")
         k4 = seq_all_to_all(key, self.scatter_idx, self.gather_idx, self.spg, "attn.k.seq2head")
         v4 = seq_all_to_all(value, self.scatter_idx, self.gather_idx, self.spg, "attn.v.seq2head")
-        ctx = self.local_attn(q4, k4, v4)
+        ctx = self.local_attn(q4, k4, v4, *args, **kwargs)
         return seq_all_to_all(ctx, self.gather_idx, self.scatter_idx, self.spg, "attn.ctx.head2seq")

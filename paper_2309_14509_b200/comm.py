@@ -26,6 +26,13 @@ from .errors import GroupDesyncError, ShardError
 _DTYPES = {torch.float32: _lib.DTYPE_F32, torch.bfloat16: _lib.DTYPE_BF16}
 
 DEFAULT_SLOT_BYTES = 64 << 20
+SLOT_GRANULE = 16 << 20      # receive slots grow in multiples of this
+
+
+def slot_need(byte_counts) -> int:
+    """Receive-slot bytes a call with these per-tensor output sizes needs
+    (each tensor image 256-byte aligned, csrc/a2a.cu plan_call)."""
+    return sum((int(n) + 255) // 256 * 256 for n in byte_counts)
 
 # layout of one rank's handle blob (csrc/a2a.cu HandleBlob): IPC handle,
 # magic, slot bytes, rank, world -- padded to UL_IPC_HANDLE_BYTES
@@ -172,7 +179,7 @@ class SequenceGroup:
     """One rank of a P-way Ulysses sequence-parallel group."""
 
     def __init__(self, rank: int, world: int, device: int, handle, slot_bytes: int,
-                 stream: torch.cuda.Stream | None = None, pg=None):
+                 stream: torch.cuda.Stream | None = None, pg=None, local=None):
         self.rank = rank
         self.world = world
         self.p = world                      # reference spelling (RankContext.p)
@@ -181,6 +188,8 @@ class SequenceGroup:
         self.slot_bytes = slot_bytes
         self.stream = stream
         self._pg = pg
+        self._local = local                 # in-process group: every rank's SequenceGroup
+        self._timeout_ms = None
         self.records: CommLedger = CommLedger()   # the logical ledger (elements, reference schema)
         self.ledger = self.records
 
@@ -210,17 +219,22 @@ class SequenceGroup:
             device = torch.cuda.current_device()
         if world == 1:
             return cls.single(device)
+        h = cls._open_ipc(rank, world, device, slot_bytes, pg)
+        g = cls(rank, world, device, h, int(_lib.lib().ul_comm_slot_bytes(h)), pg=pg)
+        if timeout_ms:
+            g.set_timeout_ms(timeout_ms)
+        dist.barrier(group=pg)
+        return g
+
+    @classmethod
+    def _open_ipc(cls, rank, world, device, slot_bytes, pg):
         h = cls._create(rank, world, device, slot_bytes)
         blob = ctypes.create_string_buffer(_lib.IPC_HANDLE_BYTES)
         _lib.check(_lib.lib().ul_comm_export_handle(h, blob))
         all_blobs = gather_handles(blob.raw, pg)
         allb = ctypes.create_string_buffer(all_blobs, world * _lib.IPC_HANDLE_BYTES)
         _lib.check(_lib.lib().ul_comm_open_peers(h, allb))
-        g = cls(rank, world, device, h, int(_lib.lib().ul_comm_slot_bytes(h)), pg=pg)
-        if timeout_ms:
-            g.set_timeout_ms(timeout_ms)
-        dist.barrier(group=pg)
-        return g
+        return h
 
     @classmethod
     def local_group(cls, world: int, slot_bytes: int = DEFAULT_SLOT_BYTES,
@@ -233,16 +247,62 @@ class SequenceGroup:
             device = torch.cuda.current_device()
         if world == 1:
             return [cls.single(device)]
+        handles = cls._link_local(world, device, slot_bytes)
+        sb = int(_lib.lib().ul_comm_slot_bytes(handles[0]))
+        local = []
+        local.extend(cls(r, world, device, handles[r], sb, stream=torch.cuda.Stream(device=device), local=local)
+                     for r in range(world))
+        return local
+
+    @classmethod
+    def _link_local(cls, world, device, slot_bytes):
         handles = [cls._create(r, world, device, slot_bytes) for r in range(world)]
         arr = (ctypes.c_void_p * world)(*[h.value for h in handles])
         _lib.check(_lib.lib().ul_comm_link_local(arr, world))
-        sb = int(_lib.lib().ul_comm_slot_bytes(handles[0]))
-        return [cls(r, world, device, handles[r], sb, stream=torch.cuda.Stream(device=device))
-                for r in range(world)]
+        return handles
 
     def set_timeout_ms(self, ms: int):
         if self._handle is not None:
             _lib.check(_lib.lib().ul_comm_set_timeout_ms(self._handle, int(ms)))
+            self._timeout_ms = int(ms)
+
+    # -- receive-slot sizing -------------------------------------------------
+    def ensure_slot(self, need: int):
+        """Grow the receive slots to at least `need` bytes before a call.
+
+        Every rank issues the same calls with the same shapes, so every rank
+        reaches the same decision at the same call; the regrowth is then a
+        collective re-registration: all previous calls complete (a device
+        sync -- their flag waits mean every peer finished writing into the
+        old slots), the old workspace is released, a larger one is created
+        and mapped by every peer (IPC handles over the process group, or
+        direct pointers for an in-process group), and epochs restart at 0 on
+        every rank."""
+        if self._handle is None or need <= self.slot_bytes:
+            return
+        new = (int(need) + SLOT_GRANULE - 1) // SLOT_GRANULE * SLOT_GRANULE
+        if self._local is not None:
+            # in-process: this rank is the first of the group to reach the
+            # call; the others have issued every earlier call already
+            torch.cuda.synchronize(self.device)
+            for g in self._local:
+                g.destroy()
+            handles = self._link_local(self.world, self.device, new)
+            sb = int(_lib.lib().ul_comm_slot_bytes(handles[0]))
+            for g, h in zip(self._local, handles):
+                g._handle, g.slot_bytes = h, sb
+                if g._timeout_ms:
+                    g.set_timeout_ms(g._timeout_ms)
+            return
+        import torch.distributed as dist
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self._pg)           # every peer is done with the old slots
+        self.destroy()
+        self._handle = self._open_ipc(self.rank, self.world, self.device, new, self._pg)
+        self.slot_bytes = int(_lib.lib().ul_comm_slot_bytes(self._handle))
+        if self._timeout_ms:
+            self.set_timeout_ms(self._timeout_ms)
+        dist.barrier(group=self._pg)
 
     def destroy(self):
         if self._handle is not None:
@@ -297,6 +357,8 @@ class SequenceGroup:
         if steps < 0:
             raise ValueError(f"ring_shift steps must be >= 0, got {steps}")
         outs = [torch.empty_like(t) for t in tensors]
+        if self.world > 1:
+            self.ensure_slot(slot_need(t.numel() * t.element_size() for t in tensors))
         for t, lab in zip(tensors, labels or [label] * len(tensors)):
             self.records.append(CommRecord("ring_shift", lab, self.world * t.numel(), t.numel() * steps))
         inp = (ctypes.c_void_p * len(tensors))(*[t.data_ptr() for t in tensors])
@@ -324,6 +386,8 @@ class SequenceGroup:
         q4 = torch.empty((nl * p, b, hq // p, hd), dtype=x2.dtype, device=x2.device)
         k4 = torch.empty((nl * p, b, hkv // p, hd), dtype=x2.dtype, device=x2.device)
         v4 = torch.empty_like(k4)
+        if p > 1:
+            self.ensure_slot(slot_need(t.numel() * t.element_size() for t in (q4, k4, v4)))
         for lab, hh in zip(labels, (hq, hkv, hkv)):
             self._record(lab, nl * b * hh * hd)
         stream = torch.cuda.current_stream(x2.device).cuda_stream
@@ -361,6 +425,8 @@ class SequenceGroup:
             for k in range(ndim):
                 shapes[4 * t + k] = x.shape[k]
         labels = labels or [label] * len(tensors)
+        if p > 1:
+            self.ensure_slot(slot_need(o.numel() * o.element_size() for o in outs))
         for x, lab in zip(tensors, labels):
             self._record(lab, x.numel())
         ins = [x.contiguous() for x in tensors]

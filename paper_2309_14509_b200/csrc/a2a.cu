@@ -37,7 +37,7 @@ struct Box {               // one (tensor, peer) chunk of a fused all-to-all
   int64_t run;             // contiguous bytes per row (both sides)
   int64_t ext[3];          // outer extents (slowest first); unused dims = 1
   int64_t sst[3], dstr[3]; // byte strides of the outer dims
-  int32_t vec;             // access width: 16, 8, 4 or 2 bytes
+  int32_t vec;             // access width: 16, 8, 4, 2 or 1 bytes
   int32_t pad;
 };
 
@@ -100,6 +100,7 @@ template <> struct VecT<16> { using T = int4; };
 template <> struct VecT<8>  { using T = int2; };
 template <> struct VecT<4>  { using T = int;  };
 template <> struct VecT<2>  { using T = short; };
+template <> struct VecT<1>  { using T = char; };
 
 // Each warp owns a contiguous range of rows: the row index is decomposed
 // once and then advanced like an odometer (no 64-bit div/mod per row).
@@ -176,7 +177,8 @@ __global__ void __launch_bounds__(256) a2a_copy_kernel(const __grid_constant__ C
     case 16: copy_box<16>(bx, w0, nwarps, lane); break;
     case 8:  copy_box<8>(bx, w0, nwarps, lane); break;
     case 4:  copy_box<4>(bx, w0, nwarps, lane); break;
-    default: copy_box<2>(bx, w0, nwarps, lane); break;
+    case 2:  copy_box<2>(bx, w0, nwarps, lane); break;
+    default: copy_box<1>(bx, w0, nwarps, lane); break;
   }
   if (!p.signal) return;
   // make this CTA's peer stores visible system-wide, then count CTAs
@@ -335,7 +337,7 @@ static void make_box(const Geom& g, int src_rank, int dst_rank, int P, const cha
   if (run == 0) b->rows = 0;
   uint64_t al = (uint64_t)run | (uint64_t)(uintptr_t)b->src | (uint64_t)(uintptr_t)b->dst;
   for (int i = 0; i < 3; ++i) al |= (uint64_t)b->sst[i] | (uint64_t)b->dstr[i];
-  b->vec = (al % 16 == 0) ? 16 : (al % 8 == 0) ? 8 : (al % 4 == 0) ? 4 : 2;
+  b->vec = (al % 16 == 0) ? 16 : (al % 8 == 0) ? 8 : (al % 4 == 0) ? 4 : (al % 2 == 0) ? 2 : 1;
 }
 
 static int launch_copy(CopyParams& p, cudaStream_t st, const char* name) {
@@ -640,6 +642,24 @@ static int wait_and_drain(ul_comm* c, const CallPlan& pl, void* const* out, cuda
   return launch_copy(dp, st, "a2a_drain");
 }
 
+// a push with nothing to move that still publishes this rank's flag + signature
+static int signal_only(ul_comm* c, const CallPlan& pl, cudaStream_t st) {
+  CopyParams cp;
+  memset(&cp, 0, sizeof(cp));
+  cp.signal = 1;
+  cp.rank = pl.me;
+  cp.world = pl.P;
+  cp.slot = pl.slot;
+  cp.epoch = pl.epoch;
+  cp.sig = pl.sig;
+  for (int r = 0; r < pl.P; ++r) cp.peer_sig[r] = (Signals*)(c->peer_base[r] + 2 * c->slot_bytes);
+  cp.counter = &((Signals*)(c->base + 2 * c->slot_bytes))->counter[pl.slot];
+  cp.box[0].rows = 0;
+  cp.box[0].vec = 16;
+  cp.nbox = 1;
+  return launch_copy(cp, st, "a2a_signal");
+}
+
 int a2a_fused_begin(ul_comm* c, int n, void* const* seq_out, const int64_t* head_shapes, int dtype,
                     uint64_t label, PeerEpilogue* ep, int* handle_slot, uint64_t* handle_epoch) {
   // head->seq (split 0, concat 2) of [N, b, h_local, hd] head-layout tensors
@@ -746,7 +766,13 @@ int ul_qkv_proj_exchange(ul_comm* c, const void* x, const void* w, void* q4, voi
     sg.counter = &((Signals*)(c->base + 2 * c->slot_bytes))->counter[pl.slot];
   }
   cudaStream_t st = (cudaStream_t)stream;
-  UL_TRY(sm100_qkv_proj(x, w, nl * b, d, d + 2 * dkv, ep, st));
+  if (nl * b == 0) {
+    // empty sequence shard: no GEMM tile runs, so no CTA would publish the
+    // call -- peers still expect this rank's flag (a signal-only push)
+    if (pl.P > 1) UL_TRY(signal_only(c, pl, st));
+  } else {
+    UL_TRY(sm100_qkv_proj(x, w, nl * b, d, d + 2 * dkv, ep, st));
+  }
   if (pl.P > 1) UL_TRY(wait_and_drain(c, pl, outs, st));
   return UL_OK;
 }
@@ -805,7 +831,7 @@ static void flat_box(const char* src, char* dst, int64_t bytes, Box* b) {
   b->sst[2] = b->dstr[2] = run;
   b->rows = bytes > 0 ? b->ext[2] : 0;
   const uint64_t al = (uint64_t)run | (uint64_t)(uintptr_t)src | (uint64_t)(uintptr_t)dst;
-  b->vec = (al % 16 == 0) ? 16 : (al % 8 == 0) ? 8 : (al % 4 == 0) ? 4 : 2;
+  b->vec = (al % 16 == 0) ? 16 : (al % 8 == 0) ? 8 : (al % 4 == 0) ? 4 : (al % 2 == 0) ? 2 : 1;   // odd byte counts: 1
 }
 
 int ul_ring_shift(ul_comm* c, int n, const void* const* in, void* const* out, const int64_t* bytes, int steps,

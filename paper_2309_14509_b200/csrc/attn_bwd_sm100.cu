@@ -826,7 +826,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 // scales it into bf16 dQ.  Five GEMMs of 2*128*64*hd per sub-tile instead of
 // the seven of bwd_dkdv + bwd_dq, and half the exponentials.  The fp32
 // additions from different kv tiles land in arrival order, so dQ is not
-// bitwise reproducible run to run (tolerance-equal); ul_attn_set_deterministic(1)
+// bitwise reproducible run to run (tolerance-equal); UL_ATTN_DETERMINISTIC
 // selects the two-kernel path whose results are bitwise stable.
 //   dS^T(i) goes both to TMEM (A operand of dK += dS^T Q, as in bwd_dkdv) and
 // to shared memory as a SWIZZLE_128B [kv][q] tile (MN-major B operand of
@@ -1272,16 +1272,14 @@ __global__ void __launch_bounds__(256) bwd_dq_convert_kernel(const float* __rest
 
 static int64_t pad_n(int64_t n) { return (n + 127) / 128 * 128; }
 
-static int g_deterministic = 0;   // ul_attn_set_deterministic
-
 template <int HD>
 static int launch(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
                   void* dq, void* dk, void* dv, void* ws, int64_t n, int64_t b, int64_t hq, int64_t hkv, int causal,
-                  float scale, int stages, const PeerEpilogue* eps, cudaStream_t st) {
+                  float scale, int stages, int deterministic, const PeerEpilogue* eps, cudaStream_t st) {
   const int64_t npad = pad_n(n);
   float* L2 = reinterpret_cast<float*>(ws);
   float* Dv = L2 + b * hq * npad;
-  const bool fused = HD == 128 && !g_deterministic;
+  const bool fused = HD == 128 && !deterministic;
   float* dq_acc = fused ? Dv + b * hq * npad : nullptr;   // [b*hq][npad][HD] f32
   if (stages & 1) {
     const int64_t threads = std::max<int64_t>(n * b * hq * (HD / 8), b * hq * (npad - n));
@@ -1318,16 +1316,10 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
     memset(&p.ep_dk, 0, sizeof(PeerEpilogue));
     memset(&p.ep_dv, 0, sizeof(PeerEpilogue));
   }
-  static bool attr = false;
-  if (!attr) {
-    UL_CUDA(cudaFuncSetAttribute(bwd_dkdv_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 DkdvSmem<HD>::kBytes));
-    UL_CUDA(cudaFuncSetAttribute(bwd_dq_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, DqSmem<HD>::kBytes));
-    if constexpr (HD == 128)
-      UL_CUDA(cudaFuncSetAttribute(bwd_fused_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   FusedSmem<HD>::kBytes));
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_dkdv{0}, attr_dq{0}, attr_fused{0};
+  UL_TRY(smem_opt_in((const void*)bwd_dkdv_kernel<HD>, DkdvSmem<HD>::kBytes, attr_dkdv));
+  UL_TRY(smem_opt_in((const void*)bwd_dq_kernel<HD>, DqSmem<HD>::kBytes, attr_dq));
+  if constexpr (HD == 128) UL_TRY(smem_opt_in((const void*)bwd_fused_kernel<HD>, FusedSmem<HD>::kBytes, attr_fused));
   const int64_t tiles = (n + BT - 1) / BT;
   if constexpr (HD == 128) {
     if (fused) {
@@ -1425,8 +1417,6 @@ int preload_bwd() {
   return UL_OK;
 }
 
-void set_deterministic(int on) { bwd::g_deterministic = on ? 1 : 0; }
-int get_deterministic() { return bwd::g_deterministic; }
 
 size_t sm100_bwd_workspace(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd) {
   (void)hkv;
@@ -1439,15 +1429,17 @@ size_t sm100_bwd_workspace(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_
 
 int sm100_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
               void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n, int64_t b, int64_t hq,
-              int64_t hkv, int64_t hd, int causal, float scale, int stages, cudaStream_t st,
+              int64_t hkv, int64_t hd, int causal, float scale, int stages, int deterministic, cudaStream_t st,
               const PeerEpilogue* eps) {
   (void)ws_bytes;
   if (n > INT32_MAX / 2) return fail(UL_ERR_SHAPE, "attention: sequence too long (n=%lld)", (long long)n);
   switch (hd) {
     case 64:
-      return bwd::launch<64>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, eps, st);
+      return bwd::launch<64>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, deterministic,
+                             eps, st);
     case 128:
-      return bwd::launch<128>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, eps, st);
+      return bwd::launch<128>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, deterministic,
+                              eps, st);
     default:
       return fail(UL_ERR_KERNEL, "bf16 attention supports head_dim 64 or 128, got %lld", (long long)hd);
   }

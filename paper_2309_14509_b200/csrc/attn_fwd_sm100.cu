@@ -20,8 +20,6 @@
 //     streams per SMSP); one query row per thread, exp2 domain, masking only
 //     on diagonal/tail tiles, FFMA-fused exponent, ILP'd max/sum chains, P
 //     packed to bf16 and stored 32 columns at a time over consumed S.
-#include <mutex>
-#include <unordered_map>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -871,46 +869,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// [next item, CTAs done] counters of the persistent forward, one pair per
-// stream (launches on one stream are ordered; the kernel leaves them zero).
-// nullptr (static zig-zag schedule) while a stream is being captured or if
-// the allocation fails.
+// The persistent forward's [next item, CTAs done] counter pair is caller
+// memory (`sched`, UL_ATTN_SCHED_BYTES, zeroed once; the kernel leaves it
+// zero): launches sharing one pair must be stream-ordered.  No counter, or a
+// stream under capture (a graph may be replayed on several streams at once),
+// selects the static zig-zag schedule.
 #ifndef UL_FWD_DYNAMIC
 #define UL_FWD_DYNAMIC 1
 #endif
-static int* stream_counters(cudaStream_t st) {
-  if (!UL_FWD_DYNAMIC) return nullptr;
-  static std::mutex mu;
-  static std::unordered_map<uint64_t, int*> ctrs;   // key: (device, stream); never freed (8 bytes per stream)
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  // never inside a capture: a graph may be replayed on several streams at once
+static int* schedule_counter(void* sched, cudaStream_t st) {
+  if (!UL_FWD_DYNAMIC || !sched) return nullptr;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
     cudaGetLastError();
     return nullptr;
   }
-  const uint64_t key = reinterpret_cast<uint64_t>(st) * 64 + (uint64_t)dev;
-  std::lock_guard<std::mutex> lock(mu);
-  auto it = ctrs.find(key);
-  if (it != ctrs.end()) return it->second;
-  int* c = nullptr;
-  if (cudaMalloc(&c, 2 * sizeof(int)) != cudaSuccess || cudaMemsetAsync(c, 0, 2 * sizeof(int), st) != cudaSuccess) {
-    cudaGetLastError();
-    if (c) cudaFree(c);
-    return nullptr;
-  }
-  ctrs[key] = c;
-  return c;
+  return reinterpret_cast<int*>(sched);
 }
 
 template <int HD>
 static int launch(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
                   int64_t hq, int64_t hkv, int causal, float scale, const PeerEpilogue* ep, cudaStream_t st,
-                  const uint32_t* blk, int64_t blk_bs, int64_t blk_words) {
+                  const uint32_t* blk, int64_t blk_bs, int64_t blk_words, void* sched) {
   CUtensorMap mq, mk, mv;
   UL_TRY(make_tmap_bhsd(&mq, q, n, b * hq, HD, 128));
   UL_TRY(make_tmap_bhsd(&mk, k, n, b * hkv, HD, 128));
@@ -940,11 +920,8 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
   p.ctr = nullptr;
   if (blk) p.causal = 0;
   const int smem = Smem<HD>::kBytes;
-  static bool attr = false;
-  if (!attr) {
-    UL_CUDA(cudaFuncSetAttribute(attn_fwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0}, pattr{0};
+  UL_TRY(smem_opt_in((const void*)attn_fwd_kernel<HD>, smem, attr));
   const int64_t grid = (int64_t)p.pairs * b * hq;
 #ifndef UL_FWD_PERSIST
 #define UL_FWD_PERSIST 1   // r73: -1.5% vs the one-shot grid; blocked-sparse keeps the one-shot kernel
@@ -956,13 +933,9 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
   // keep the one-shot grid then.  (r89: dynamic vs static at config 2 equal;
   // head-major persistent vs one-shot within noise, config 5 -2%.)
   if (UL_FWD_PERSIST && !blk) {
-    p.ctr = stream_counters(st);
+    p.ctr = schedule_counter(sched, st);
     if (p.ctr || !p.head_major) {
-      static bool pattr = false;
-      if (!pattr) {
-        UL_CUDA(cudaFuncSetAttribute(attn_fwd_persist_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        pattr = true;
-      }
+      UL_TRY(smem_opt_in((const void*)attn_fwd_persist_kernel<HD>, smem, pattr));
       const int64_t pgrid = grid < sm_count() ? grid : sm_count();
       attn_fwd_persist_kernel<HD><<<(unsigned)pgrid, kThreads, smem, st>>>(mq, mk, mv, p);
       return launched("attn_fwd_sm100");
@@ -1001,14 +974,15 @@ int preload_fwd() {
 
 int sm100_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b, int64_t hq,
                int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st, const PeerEpilogue* ep,
-               const uint32_t* blk, int64_t blk_bs, int64_t blk_words) {
+               const uint32_t* blk, int64_t blk_bs, int64_t blk_words, void* sched) {
   if (blk && (n + fwd::BN - 1) / fwd::BN > fwd::kMaxTiles)
     return fail(UL_ERR_SHAPE, "blocked-sparse attention supports n <= %d, got %lld", fwd::kMaxTiles * fwd::BN,
                 (long long)n);
   switch (hd) {
-    case 64: return fwd::launch<64>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, ep, st, blk, blk_bs, blk_words);
+    case 64: return fwd::launch<64>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, ep, st, blk, blk_bs, blk_words, sched);
     case 128:
-      return fwd::launch<128>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, ep, st, blk, blk_bs, blk_words);
+      return fwd::launch<128>(q, k, v, o, lse, n, b, hq, hkv, causal, scale, ep, st, blk, blk_bs, blk_words,
+                              sched);
     default:
       return fail(UL_ERR_KERNEL, "bf16 attention supports head_dim 64 or 128, got %lld", (long long)hd);
   }

@@ -33,10 +33,10 @@ int simt_bwd(const float* q, const float* k, const float* v, const float* o, con
 int sm100_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
               int64_t hq, int64_t hkv, int64_t hd, int causal, float scale, cudaStream_t st,
               const PeerEpilogue* ep = nullptr, const uint32_t* blk = nullptr, int64_t blk_bs = 0,
-              int64_t blk_words = 0);
+              int64_t blk_words = 0, void* sched = nullptr);
 int sm100_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
               void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n, int64_t b, int64_t hq,
-              int64_t hkv, int64_t hd, int causal, float scale, int stages, cudaStream_t st,
+              int64_t hkv, int64_t hd, int causal, float scale, int stages, int deterministic, cudaStream_t st,
               const PeerEpilogue* eps = nullptr);
 size_t sm100_bwd_workspace(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd);
 int preload_a2a();
@@ -45,8 +45,6 @@ int preload_fwd();
 int preload_bwd();
 int preload_proj();
 int preload_merge();
-void set_deterministic(int on);
-int get_deterministic();
 
 static int check_attn(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask) {
   if (mask != UL_MASK_NONE && mask != UL_MASK_CAUSAL)
@@ -75,8 +73,6 @@ const char* ul_last_error(void) { return last_error().c_str(); }
 int ul_last_launch_count(void) { return launch_count(); }
 uint64_t ul_total_launch_count(void) { return g_total_launches.load(); }
 
-void ul_attn_set_deterministic(int on) { set_deterministic(on); }
-int ul_attn_get_deterministic(void) { return get_deterministic(); }
 
 int ul_preload_kernels(void) {
   UL_TRY(preload_a2a());
@@ -89,7 +85,7 @@ int ul_preload_kernels(void) {
 }
 
 int ul_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
-                int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask, float scale, void* stream) {
+                int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask, float scale, void* sched, void* stream) {
   launch_count() = 0;
   UL_TRY(check_attn(n, b, hq, hkv, hd, dtype, mask));
   if (!q || !k || !v || !o || !lse) {
@@ -104,7 +100,7 @@ int ul_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse
                     scale, st);
   if (n * b * hq == 0) return UL_OK;
   if (n > INT32_MAX / 2) return fail(UL_ERR_SHAPE, "attention: sequence too long (n=%lld)", (long long)n);
-  return sm100_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, causal, scale, st);
+  return sm100_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, causal, scale, st, nullptr, nullptr, 0, 0, sched);
 }
 
 int ul_attn_fwd_blocked(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,
@@ -141,7 +137,7 @@ size_t ul_attn_bwd_workspace_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv
 int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* o, const void* dout,
                        const float* lse, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n,
                        int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask, float scale,
-                       int stages, void* stream) {
+                       int stages, int flags, void* stream) {
   launch_count() = 0;
   UL_TRY(check_attn(n, b, hq, hkv, hd, dtype, mask));
   if (n * b * hq == 0) return UL_OK;
@@ -150,6 +146,7 @@ int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* 
   if (!lse) return fail(UL_ERR_STATE, "backward needs the LSE saved by the forward pass");
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(UL_ERR_ARG, "scale must be finite and > 0");
   if (stages < 1 || stages > 7) return fail(UL_ERR_ARG, "stage mask must be in [1, 7], got %d", stages);
+  if (flags & ~UL_ATTN_DETERMINISTIC) return fail(UL_ERR_ARG, "unknown backward flags 0x%x", flags);
   const size_t need = ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dtype);
   if (!ws || ws_bytes < need)
     return fail(UL_ERR_ARG, "ul_attn_bwd: workspace of %zu bytes < required %zu", ws_bytes, need);
@@ -160,27 +157,28 @@ int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* 
     return simt_bwd((const float*)q, (const float*)k, (const float*)v, (const float*)o, (const float*)dout, lse,
                     (float*)dq, (float*)dk, (float*)dv, (float*)ws, n, b, hq, hkv, hd, causal, scale, st);
   }
-  return sm100_bwd(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, causal, scale, stages, st);
+  return sm100_bwd(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, causal, scale, stages,
+                   flags & UL_ATTN_DETERMINISTIC, st);
 }
 
 int ul_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
                 void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n, int64_t b, int64_t hq,
-                int64_t hkv, int64_t hd, int dtype, int mask, float scale, void* stream) {
+                int64_t hkv, int64_t hd, int dtype, int mask, float scale, int flags, void* stream) {
   return ul_attn_bwd_stages(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, dtype, mask, scale,
-                            7, stream);
+                            7, flags, stream);
 }
 
 // ---- local attention with the head->seq exchange fused into the epilogue ----
 
 int ul_attn_fwd_exchange(ul_comm* comm, const void* q, const void* k, const void* v, void* o, float* lse,
                          void* seq_out, int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype,
-                         int mask, float scale, uint64_t label, void* stream) {
+                         int mask, float scale, uint64_t label, void* sched, void* stream) {
   if (!seq_out) return fail(UL_ERR_ARG, "ul_attn_fwd_exchange: NULL seq_out");
   const int64_t shape[4] = {n, b, hq, hd};
   // (empty problems take the two-step route: its push kernel still signals)
   const bool fused = comm && ul_comm_world(comm) > 1 && dtype == UL_DTYPE_BF16 && n * b * hq > 0;
   if (!fused) {   // same contract, two steps: attention, then the head->seq exchange
-    UL_TRY(ul_attn_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, dtype, mask, scale, stream));
+    UL_TRY(ul_attn_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, dtype, mask, scale, sched, stream));
     const int launches = launch_count();
     const void* in[1] = {o};
     void* out[1] = {seq_out};
@@ -200,21 +198,23 @@ int ul_attn_fwd_exchange(ul_comm* comm, const void* q, const void* k, const void
   void* outs[1] = {seq_out};
   UL_TRY(a2a_fused_begin(comm, 1, outs, shape, dtype, label, &ep, &slot, &epoch));
   if (n * b * hq > 0)
-    UL_TRY(sm100_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, mask == UL_MASK_CAUSAL, scale, st, &ep));
+    UL_TRY(sm100_fwd(q, k, v, o, lse, n, b, hq, hkv, hd, mask == UL_MASK_CAUSAL, scale, st, &ep, nullptr, 0, 0,
+                     sched));
   return a2a_fused_finish(comm, 1, outs, shape, dtype, label, slot, epoch, st);
 }
 
 int ul_attn_bwd_exchange(ul_comm* comm, const void* q, const void* k, const void* v, const void* o,
                          const void* dout, const float* lse, void* dq, void* dk, void* dv, void* ws,
                          size_t ws_bytes, void* seq_dq, void* seq_dk, void* seq_dv, int64_t n, int64_t b, int64_t hq,
-                         int64_t hkv, int64_t hd, int dtype, int mask, float scale, uint64_t label, void* stream) {
+                         int64_t hkv, int64_t hd, int dtype, int mask, float scale, uint64_t label, int flags,
+                         void* stream) {
   if (!seq_dq || !seq_dk || !seq_dv) return fail(UL_ERR_ARG, "ul_attn_bwd_exchange: NULL sequence output");
   const int64_t shapes[12] = {n, b, hq, hd, n, b, hkv, hd, n, b, hkv, hd};
   void* outs[3] = {seq_dq, seq_dk, seq_dv};
   // (empty problems take the two-step route: its push kernel still signals)
   const bool fused = comm && ul_comm_world(comm) > 1 && dtype == UL_DTYPE_BF16 && n * b * hq > 0;
   if (!fused) {
-    UL_TRY(ul_attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, dtype, mask, scale,
+    UL_TRY(ul_attn_bwd(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, dtype, mask, scale, flags,
                        stream));
     const int launches = launch_count();
     const void* in[3] = {dq, dk, dv};
@@ -227,6 +227,7 @@ int ul_attn_bwd_exchange(ul_comm* comm, const void* q, const void* k, const void
   if (!q || !k || !v || !o || !dout || !dq || !dk || !dv) return fail(UL_ERR_ARG, "ul_attn_bwd_exchange: NULL tensor");
   if (!lse) return fail(UL_ERR_STATE, "backward needs the LSE saved by the forward pass");
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(UL_ERR_ARG, "scale must be finite and > 0");
+  if (flags & ~UL_ATTN_DETERMINISTIC) return fail(UL_ERR_ARG, "unknown backward flags 0x%x", flags);
   const size_t need = ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dtype);
   if (!ws || ws_bytes < need)
     return fail(UL_ERR_ARG, "ul_attn_bwd: workspace of %zu bytes < required %zu", ws_bytes, need);
@@ -237,7 +238,7 @@ int ul_attn_bwd_exchange(ul_comm* comm, const void* q, const void* k, const void
   UL_TRY(a2a_fused_begin(comm, 3, outs, shapes, dtype, label, eps, &slot, &epoch));
   if (n * b * hq > 0)
     UL_TRY(sm100_bwd(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, mask == UL_MASK_CAUSAL,
-                     scale, 7, st, eps));
+                     scale, 7, flags & UL_ATTN_DETERMINISTIC, st, eps));
   return a2a_fused_finish(comm, 3, outs, shapes, dtype, label, slot, epoch, st);
 }
 

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
@@ -51,15 +52,38 @@ inline int launched(const char* name) {
 
 inline size_t dtype_size(int dtype) { return dtype == UL_DTYPE_F32 ? 4 : 2; }
 
+// SM count of the CURRENT device (cached per device: a process may drive
+// several GPUs)
 inline int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    dev = 0;
+  }
+  dev &= 63;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;
+    }
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
+}
+
+// Dynamic shared-memory opt-in of `fn` on the CURRENT device.  The attribute
+// is per device context, so it is tracked per device (`done` is one bit per
+// device, owned by the call site).
+inline int smem_opt_in(const void* fn, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  UL_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return UL_OK;
+  UL_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.fetch_or(bit, std::memory_order_release);
+  return UL_OK;
 }
 
 }  // namespace ul

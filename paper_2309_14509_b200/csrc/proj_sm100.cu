@@ -212,12 +212,8 @@ int sm100_qkv_proj(const void* x, const void* w, int64_t M, int64_t K, int64_t N
   p.mtiles = (int)((M + proj::BM - 1) / proj::BM);
   p.ntiles = (int)((N + proj::BN - 1) / proj::BN);
   p.ep = ep;
-  static bool attr = false;
-  if (!attr) {
-    UL_CUDA(cudaFuncSetAttribute(proj::qkv_proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 proj::Smem::kBytes));
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  UL_TRY(smem_opt_in((const void*)proj::qkv_proj_kernel, proj::Smem::kBytes, attr));
   const int tiles = p.mtiles * p.ntiles;
   const int grid = tiles < sm_count() ? tiles : sm_count();
   proj::qkv_proj_kernel<<<grid, proj::kThreads, proj::Smem::kBytes, st>>>(mx, mw, p);

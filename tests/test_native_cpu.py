@@ -29,7 +29,7 @@ def header_symbols():
 
 def test_library_loads_and_abi():
     L = lib().lib()
-    assert L.ul_abi_version() == 1
+    assert L.ul_abi_version() == lib().ABI_VERSION == 2
 
 
 def test_every_header_symbol_is_exported():
@@ -55,16 +55,19 @@ def test_attention_argument_errors_before_any_launch():
     from paper_2309_14509_b200 import errors
     L = lib().lib()
     # GQA divisibility
-    st = L.ul_attn_fwd(None, None, None, None, None, 4, 1, 4, 3, 64, 1, 0, 0.1, None)
+    st = L.ul_attn_fwd(None, None, None, None, None, 4, 1, 4, 3, 64, 1, 0, 0.1, None, None)
     assert errors.STATUS[st] is errors.DivisibilityError
     assert b"does not divide" in L.ul_last_error()
     # unsupported mask kind -> KernelError (kernels.py:43-52)
-    st = L.ul_attn_fwd(None, None, None, None, None, 4, 1, 4, 4, 64, 1, 7, 0.1, None)
+    st = L.ul_attn_fwd(None, None, None, None, None, 4, 1, 4, 4, 64, 1, 7, 0.1, None, None)
     assert errors.STATUS[st] is errors.KernelError
     # backward without LSE -> ForwardStateError (ulysses.py:198-207)
     p = ctypes.c_void_p(16)
-    st = L.ul_attn_bwd(p, p, p, p, p, None, p, p, p, p, 1 << 20, 4, 1, 4, 4, 64, 1, 1, 0.1, None)
+    st = L.ul_attn_bwd(p, p, p, p, p, None, p, p, p, p, 1 << 20, 4, 1, 4, 4, 64, 1, 1, 0.1, 0, None)
     assert errors.STATUS[st] is errors.ForwardStateError
+    # unknown per-call backward flags -> ValueError (UL_ERR_ARG), before any launch
+    st = L.ul_attn_bwd(p, p, p, p, p, p, p, p, p, p, 1 << 20, 4, 1, 4, 4, 64, 1, 1, 0.1, 2, None)
+    assert st == -8 and b"flags" in L.ul_last_error()
 
 
 def test_all_to_all_argument_errors_before_any_launch():
