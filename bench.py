@@ -1,19 +1,25 @@
 """Benchmark: Ulysses attention layer (fwd+bwd) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N)
+                    [--config 2|3|4|5] [--seq N] [--quick] [--dry-run]
 
-Workload (BASELINE.json): at N = 1, config 2 -- local attention fwd+bwd of
-one GPT-1.3B layer shape (16 heads x 128), N = 8192 tokens, bf16, causal.
-At N > 1 the same layer runs as a Ulysses group of N ranks with the sequence
-scaled with the group (N_seq = 8192 * P, weak scaling in the paper's sense:
-tokens per GPU fixed); the seq->head / head->seq exchanges run on the
-peer-memory kernels (csrc/a2a.cu), no NCCL on the data path.
+`--gpus N` (N > 1) without a torchrun environment launches N ranks itself
+(torch.distributed.run on 127.0.0.1, one process per GPU); under torchrun it
+runs as the rank it is.
+
+Workloads (BASELINE.json configs): at N = 1, config 2 -- local attention
+fwd+bwd of one GPT-1.3B layer shape (16 heads x 128), N = 8192 tokens, bf16,
+causal.  At N > 1, config 5 -- weak scaling N = 64K x P, 56 heads x 128
+(constant per-GPU exchange volume), the Ulysses layer over N ranks with the
+seq->head / head->seq exchanges on the peer-memory kernels (csrc/a2a.cu), no
+NCCL on the data path; --config 3 / 4 select the 7B (32 heads, N = 32K..256K
+via --seq) and GQA (32 q / 8 kv, N = 128K) workloads.
 
 One JSON line on rank 0.  `value` = tokens/s of the whole job with inputs
-resident in HBM (device time from CUDA events, max over ranks; L2 flushed
-before every timed step).  `e2e` = the same through the public API from
-pinned host buffers (H2D q,k,v,dO + D2H of the loss scalar every step).
+resident in HBM (device time from CUDA events, max over ranks; L2 flushed by
+reading a 1 GiB buffer before every timed step).  `e2e` = the same through the
+public API from pinned host buffers (H2D q,k,v,dO + D2H of the loss scalar
+every step).  `exposed_a2a` = step minus the rank's attention kernels alone.
 """
 
 from __future__ import annotations
@@ -294,6 +300,78 @@ def cpu_baseline(n_seq, heads, hd, procs=1, n_sample=1024, heads_sample=1):
 
 
 # ---------------------------------------------------------------------------
+# workloads (BASELINE.json configs)
+# ---------------------------------------------------------------------------
+
+CONFIGS = {
+    # name: (query heads, kv heads, sequence length for P ranks, description)
+    "2": (16, 16, lambda P: SEQ_PER_GPU * P,
+          "config2: single-GPU local attention fwd+bwd, GPT-1.3B layer 16 heads x 128, N={n} bf16 causal"),
+    "3": (32, 32, lambda P: 32768,
+          "config3: Ulysses attention layer P={P}, 7B shape 32 heads x 128, N={n} bf16 causal fwd+bwd"),
+    "4": (32, 8, lambda P: 131072,
+          "config4: GQA Llama-3-8B 32 q / 8 kv heads x 128, Ulysses P={P}, N={n} bf16 causal fwd+bwd"),
+    "5": (56, 56, lambda P: 65536 * P,
+          "config5: weak scaling N=64K x P, 30B shape 56 heads x 128, P={P}, N={n} bf16 causal fwd+bwd"),
+}
+
+
+def pick_config(args, P):
+    """N = 1: config 2 (the metric's single-GPU workload); N > 1: config 5
+    (the metric's 1/2/4/8-GPU weak-scaling sweep), unless --config says."""
+    name = args.config or ("2" if P == 1 else "5")
+    hq, hkv, seq, desc = CONFIGS[name]
+    if args.heads:
+        hq = hkv = args.heads
+    n_seq = args.seq or seq(P)
+    return name, hq, hkv, n_seq, desc.format(P=P, n=n_seq)
+
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def maybe_relaunch(args):
+    """`bench.py --gpus N` without a torchrun environment: launch N ranks
+    (one process per GPU) through torch.distributed.run on 127.0.0.1 and
+    pass rank 0's line through.  Under torchrun (WORLD_SIZE set) run as is."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd, cwd=ROOT)
+    sys.exit(r.returncode)
+
+
+def read_flush(flush):
+    """Untimed L2 flush by READING a 1 GiB buffer: evicts the 126 MB L2
+    without leaving dirty lines whose write-back would land in the next
+    timed kernel (a zero_() flush does)."""
+    flush.view(torch_int64()).sum()
+
+
+def torch_int64():
+    import torch
+    return torch.int64
+
+
+def host_cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 
@@ -301,16 +379,39 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    import paper_2309_14509_b200 as U
-    from paper_2309_14509_b200 import _lib
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} but WORLD_SIZE={world}")
+    P = world
+    cfg_name, H, HKV, n_seq, desc = pick_config(args, P)
+    hd = HEAD_DIM
+    nl = n_seq // P
     # UL_BENCH_ONE_GPU=1: every rank on cuda:0 with a gloo rendezvous -- a
     # functional smoke test of the N > 1 path on a one-GPU box (NCCL refuses
     # two ranks on one device); timings of such a run mean nothing
     one_gpu = os.environ.get("UL_BENCH_ONE_GPU") == "1"
+    if args.dry_run:
+        # host-side contract only (CPU): launch, rendezvous, workload choice,
+        # max-over-ranks reduction -- no CUDA
+        if world > 1:
+            dist.init_process_group("gloo")
+            t = torch.tensor([float(rank + 1)])
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tmax = float(t.item())
+        else:
+            tmax = 1.0
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": P, "max_over_ranks": tmax,
+                              "config": workload_config(P, n_seq, H, hd, cfg_name, HKV)}), flush=True)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import paper_2309_14509_b200 as U
+    from paper_2309_14509_b200 import _lib
     if one_gpu:
         local_rank = 0
     torch.cuda.set_device(local_rank)
@@ -320,20 +421,17 @@ def run_ours(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-    P = world
-    n_seq = args.seq if args.seq else SEQ_PER_GPU * P
-    H, hd = args.heads, HEAD_DIM
-    nl = n_seq // P
     causal = True
+    if H % P or HKV % P or n_seq % P:
+        raise SystemExit(f"config {cfg_name}: P={P} must divide heads ({H}, {HKV}) and N={n_seq}")
 
     # synthetic inputs: N(0,1), seed 2024, per-rank contiguous shard
     g = torch.Generator(device=dev)
     g.manual_seed(2024 + rank)
-    mk = lambda: torch.randn((nl, 1, H, hd), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
-    q, k, v, do = mk(), mk(), mk(), mk()
+    mk = lambda h: torch.randn((nl, 1, h, hd), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    q, k, v, do = mk(H), mk(HKV), mk(HKV), mk(H)
     if P > 1:
-        slot = 3 * nl * H * hd * 2 + (1 << 20)
-        group = U.SequenceGroup.from_process_group(None, slot_bytes=slot, device=local_rank)
+        group = U.SequenceGroup.from_process_group(None, device=local_rank)   # receive slots size themselves
     else:
         group = U.SequenceGroup.single(local_rank)
     attn = U.FlashAttention("causal")
@@ -361,7 +459,7 @@ def run_ours(args):
         if P > 1:
             dist.barrier()
         for i in range(args.steps):
-            flush.zero_()                                  # untimed L2 flush
+            read_flush(flush)                              # untimed L2 flush (read)
             ev[i][0].record()
             step(q.detach(), k.detach(), v.detach(), do)
             ev[i][1].record()
@@ -383,12 +481,15 @@ def run_ours(args):
 
     # ---- per-kernel split (dominant kernel roofline) on this rank's
     # head-sharded attention problem [N, 1, H/P, hd] --------------------
-    mk4 = lambda: torch.randn((n_seq, 1, H // P, hd), generator=g, device=dev,
-                              dtype=torch.float32).to(torch.bfloat16)
-    kt = kernel_split(attn, mk4(), mk4(), mk4(), mk4(), args, dev)
-    a2a = bench_a2a(dev, n_seq, H, hd, P, group)
-    sparse = bench_blocked(kt_inputs=(mk4, n_seq, H // P, hd), args=args, dev=dev)
-    layer_leg = bench_layer(group, nl, H, hd, args, dev)
+    mk4 = lambda h: torch.randn((n_seq, 1, h, hd), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    kt = kernel_split(attn, mk4(H // P), mk4(HKV // P), mk4(HKV // P), mk4(H // P), args, dev)
+    attn_only_ms = sum(x["ms"] for x in kt["kernels"])
+    a2a = bench_a2a(dev, n_seq, H, hd, P, group, HKV)
+    extras = {}
+    if P == 1 and not args.quick:
+        extras["blocked_sparse_fwd"] = bench_blocked(kt_inputs=(lambda: mk4(H), n_seq, H, hd), args=args, dev=dev)
+        extras["layer"] = bench_layer(group, nl, H, hd, args, dev)
+        extras["anchors"] = bench_anchors(n_seq, H, hd, flush)
 
     # ---- e2e through the public API from pinned host buffers ----------
     e2e = run_e2e(layer, q, k, v, do, args, P, dev)
@@ -400,6 +501,7 @@ def run_ours(args):
         peak = pk["bf16_tflops"]
         ach = dom["alg_flops"] / (dom["ms"] / 1e3) / 1e12
         clocks = clk.summary()
+        exposed = ms_per_step - attn_only_ms
         result = {
             "metric": "Ulysses attn tokens/s (fwd+bwd layer), TFLOPs/GPU, all-to-all GB/s",
             "value": round(tokens_per_s, 1),
@@ -409,11 +511,11 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "weak" if cfg_name in ("5", "2") else "strong",
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic N(0,1) q/k/v/dO, seed 2024 (no dataset)",
-            "config": workload_config(P, n_seq, H, hd),
+            "config": workload_config(P, n_seq, H, hd, cfg_name, HKV),
             "tflops_per_gpu": round(tflops_per_gpu, 1),
             "tflops_per_gpu_fa_convention": round(
                 (f_fwd * 3.5) / (ms_per_step / 1e3) / 1e12, 1),
@@ -422,16 +524,19 @@ def run_ours(args):
                 "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({src}, burst)",
                 "frac_of_sustained": round(ach / pk.get("bf16_tflops_sustained", peak), 4),
-                # ncu DRAM bytes per launch, captured on the P = 1 (config 2) workload
-                "traffic": (ncu_traffic(dom["name"]) or {}).get("bytes") if P == 1 else None,
-                "traffic_source": (ncu_traffic(dom["name"]) or {}).get("source") if P == 1 else None,
+                # ncu DRAM bytes per launch, captured on the config-2 workload
+                "traffic": (ncu_traffic(dom["name"]) or {}).get("bytes") if cfg_name == "2" and P == 1 else None,
+                "traffic_source": (ncu_traffic(dom["name"]) or {}).get("source") if cfg_name == "2" and P == 1 else None,
                 "alg_flops_per_launch": dom["alg_flops"],
                 "layer_frac": round(tflops_per_gpu / peak, 4),
             },
             "kernels": kt["kernels"],
+            "exposed_a2a": {"ms": round(exposed, 4), "pct_of_step": round(100.0 * exposed / ms_per_step, 2),
+                            "attention_only_ms": round(attn_only_ms, 4),
+                            "how": "step time minus the same rank's attention kernels alone (SURVEY 8(d)); "
+                                   "at P = 1 the remainder is launch/host overhead (no exchange)"},
             "a2a": a2a,
-            "blocked_sparse_fwd": sparse,
-            "layer": layer_leg,
+            **extras,
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,
@@ -441,7 +546,7 @@ def run_ours(args):
         cb = cpu_baseline(n_seq, H, hd, procs=1, n_sample=2 * args.cpu_sample, heads_sample=2)
         result["cpu_baseline"] = {"value": round(cb["tokens_per_s"], 4), "unit": "tokens/s", "cores": 1,
                                   "kind": "port", "sample": cb["sample"],
-                                  "sample_wall_s": round(cb["sample_wall_s"], 2)}
+                                  "sample_wall_s": round(cb["sample_wall_s"], 2), "cpu_model": host_cpu_model()}
     if rank == 0:
         print(json.dumps(result), flush=True)
     if P > 1:
@@ -455,19 +560,20 @@ def kernel_split(attn, q, k, v, do, args, dev):
     import torch
     from paper_2309_14509_b200 import _lib
     n, b, h, hd = q.shape[0], q.shape[1], q.shape[2], q.shape[3]
+    hkv = k.shape[2]
     lib = _lib.lib()
     flush = make_flush(dev)
     stream = torch.cuda.current_stream(dev).cuda_stream
     o = torch.empty_like(q)
     lse = torch.empty((b, h, n), dtype=torch.float32, device=dev)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-    wsb = int(lib.ul_attn_bwd_workspace_bytes(n, b, h, h, hd, 1))
-    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    wsb = int(lib.ul_attn_bwd_workspace_bytes(n, b, h, hkv, hd, 1))
+    ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)   # left zero by every call: UL_ATTN_WS_ZEROED
     sched = torch.zeros(2, dtype=torch.int32, device=dev)   # persistent-forward work counter (UL_ATTN_SCHED_BYTES)
     scale = 1.0 / math.sqrt(hd)
     fused = hd == 128 and not attn.deterministic
-    if fused:   # one kernel for dK, dV and dQ (+ the dQ fp32 -> bf16 pass)
-        names = ["attn_fwd_sm100", "attn_bwd_prep", "attn_bwd_fused_sm100", "attn_bwd_dq_convert"]
+    if fused:   # one kernel for dK, dV and dQ (incl. the dQ fp32 -> bf16 conversion)
+        names = ["attn_fwd_sm100", "attn_bwd_prep", "attn_bwd_fused_sm100"]
     else:
         names = ["attn_fwd_sm100", "attn_bwd_prep", "attn_bwd_dkdv_sm100", "attn_bwd_dq_sm100"]
     times = {nm: [] for nm in names}
@@ -481,19 +587,19 @@ def kernel_split(attn, q, k, v, do, args, dev):
     def run(nm):
         if nm == "attn_fwd_sm100":
             _lib.check(lib.ul_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(),
-                                       n, b, h, h, hd, 1, 1, scale, sched.data_ptr(), stream))
+                                       n, b, h, hkv, hd, 1, 1, scale, sched.data_ptr(), stream))
         else:
             stage = {"attn_bwd_prep": 1, "attn_bwd_dkdv_sm100": 2, "attn_bwd_dq_sm100": 4, "attn_bwd_fused_sm100": 2,
                      "attn_bwd_dq_convert": 4}[nm]
             _lib.check(lib.ul_attn_bwd_stages(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                               do.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(),
-                                              dv.data_ptr(), ws.data_ptr(), wsb, n, b, h, h, hd, 1, 1, scale,
-                                              stage, attn.flags, stream))
+                                              dv.data_ptr(), ws.data_ptr(), wsb, n, b, h, hkv, hd, 1, 1, scale,
+                                              stage, attn.flags | _lib.ATTN_WS_ZEROED, stream))
 
     reps = max(3, min(args.steps, 10))
     for it in range(args.warmup + reps):
         for nm in names:
-            flush.zero_()
+            read_flush(flush)
             a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             run(nm)
@@ -529,7 +635,7 @@ def bench_layer(group, nl, H, hd, args, dev):
     def timeit(fn, reps):
         ts = []
         for it in range(args.warmup + reps):
-            flush.zero_()
+            read_flush(flush)
             a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             fn()
@@ -577,7 +683,7 @@ def bench_blocked(kt_inputs, args, dev, bs=128, bandwidth=15):
     flush = make_flush(dev)
     times = []
     for it in range(args.warmup + max(3, min(args.steps, 10))):
-        flush.zero_()
+        read_flush(flush)
         a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         attn.forward_with_lse(q, k, v)
@@ -592,29 +698,32 @@ def bench_blocked(kt_inputs, args, dev, bs=128, bandwidth=15):
             "tflops_visible": round(flops / (ms / 1e3) / 1e12, 1)}
 
 
-def bench_a2a(dev, n_seq, H, hd, P, group, reps=10):
+def bench_a2a(dev, n_seq, H, hd, P, group, HKV=None, reps=10):
     """All-to-all throughput of the fused Q/K/V seq->head exchange (K1).
 
     P > 1: this rank's real exchange over NVLink peer memory; GB/s = exact
     egress bytes (local * (P-1)/P, simgroup.py:329-332) / device time, max
-    over ranks.  Always also: the same kernels on one GPU -- the P = 1 local
-    permute and an in-process P = 8 group (8 ranks on 8 streams, all traffic
-    in local HBM) -- reported against the HBM roofline (bytes = read + write
-    of every element moved)."""
+    over ranks; beside it the same exchange through NCCL all_to_all_single
+    (the north star's comparison) and two MEASURED peer-bandwidth legs of
+    256 MiB per rank: this library's ring_shift (flat peer stores to rank
+    r+1) and NCCL all_to_all_single.  Always also: the same kernels on one
+    GPU -- the P = 1 local permute and an in-process P = 8 group (8 ranks on
+    8 streams, all traffic in local HBM) -- against the HBM roofline."""
     import torch
     import torch.distributed as dist
     import paper_2309_14509_b200 as U
+    HKV = HKV or H
     out = {}
     flush = make_flush(dev)
 
     def timed(fn_list, streams):
         times = []
         for it in range(3 + reps):
-            flush.zero_()
+            read_flush(flush)
             torch.cuda.synchronize()
             ev = []
             for _ in range(len(streams) - 1):   # keep the GPU busy while the host enqueues every rank
-                flush.zero_()
+                read_flush(flush)
             for s in streams:
                 s.wait_stream(torch.cuda.current_stream(dev))
             for fn, s in zip(fn_list, streams):
@@ -629,40 +738,57 @@ def bench_a2a(dev, n_seq, H, hd, P, group, reps=10):
                 times.append(max(ev[0][0].elapsed_time(e) for _, e in ev))
         return statistics.mean(times)
 
-    nl = n_seq // P
-    if P > 1:
-        x = [torch.randn((nl, 1, H, hd), device=dev).to(torch.bfloat16) for _ in range(3)]
-        ms = timed([lambda: group.all_to_all(x, 2, 0, label="bench.qkv")],
-                   [torch.cuda.current_stream(dev)])
+    def max_ranks(ms):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        local = 3 * nl * H * hd * 2
+        return float(t.item())
+
+    nl = n_seq // P
+    if P > 1:
+        x = [torch.randn((nl, 1, hh, hd), device=dev).to(torch.bfloat16) for hh in (H, HKV, HKV)]
+        ms = max_ranks(timed([lambda: group.all_to_all(x, 2, 0, label="bench.qkv")], [torch.cuda.current_stream(dev)]))
+        local = sum(t.numel() for t in x) * 2
         egress = local // P * (P - 1)
         out["exchange"] = {"P": P, "ms": round(ms, 4), "egress_bytes": egress,
-                           "nvlink_gbs": round(egress / (ms / 1e3) / 1e9, 1), "peak_gbs_nominal": 900.0,
-                           "peak_gbs_measured_peer_copy": 770.0}
+                           "nvlink_gbs": round(egress / (ms / 1e3) / 1e9, 1), "peak_gbs_nominal": 900.0}
+        # measured peer bandwidth of this box (no constants): 256 MiB per rank
+        big = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        try:
+            ms_r = max_ranks(timed([lambda: group.ring_shift([big], 1, label="bench.peer")],
+                                   [torch.cuda.current_stream(dev)]))
+            out["peer_copy_measured"] = {"bytes_per_rank": big.numel(), "ms": round(ms_r, 4),
+                                         "gbs": round(big.numel() / (ms_r / 1e3) / 1e9, 1),
+                                         "path": "ul_ring_shift: flat 16-byte peer stores to rank r+1"}
+        except Exception as exc:
+            out["peer_copy_measured"] = {"error": repr(exc)[:200]}
+        try:
+            big_o = torch.empty_like(big)
+            ms_a = max_ranks(timed([lambda: dist.all_to_all_single(big_o, big)], [torch.cuda.current_stream(dev)]))
+            out["nccl_a2a_measured"] = {"bytes_per_rank": big.numel(), "ms": round(ms_a, 4),
+                                        "egress_gbs": round(big.numel() * (P - 1) / P / (ms_a / 1e3) / 1e9, 1)}
+            del big_o
+        except Exception as exc:
+            out["nccl_a2a_measured"] = {"error": repr(exc)[:200]}
+        del big
         # the measured comparison (north star): the same seq->head exchange
         # the way a torch user writes it -- permute to rank-major chunks +
         # NCCL all_to_all_single, one per tensor
         try:
-            ys = [torch.empty((P, nl, 1, H // P, hd), device=dev, dtype=torch.bfloat16) for _ in range(3)]
+            ys = [torch.empty((P, nl, 1, t.shape[2] // P, hd), device=dev, dtype=torch.bfloat16) for t in x]
 
             def nccl_qkv():
                 for t, y in zip(x, ys):
-                    src = t.reshape(nl, 1, P, H // P, hd).permute(2, 0, 1, 3, 4).contiguous()
+                    src = t.reshape(nl, 1, P, t.shape[2] // P, hd).permute(2, 0, 1, 3, 4).contiguous()
                     dist.all_to_all_single(y, src)
-            ms_n = timed([nccl_qkv], [torch.cuda.current_stream(dev)])
-            t = torch.tensor([ms_n], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_n = float(t.item())
+            ms_n = max_ranks(timed([nccl_qkv], [torch.cuda.current_stream(dev)]))
             ref = group.all_to_all(x, 2, 0, label="bench.qkv.check")
             same = all(torch.equal(r.reshape(-1), y.reshape(-1)) for r, y in zip(ref, ys))
             out["nccl_exchange"] = {"ms": round(ms_n, 4), "nvlink_gbs": round(egress / (ms_n / 1e3) / 1e9, 1),
-                                    "same_bytes_as_ours": bool(same),
+                                    "same_bytes_as_ours": bool(same), "ours_speedup": round(ms_n / ms, 3),
                                     "path": "permute().contiguous() + dist.all_to_all_single per tensor (NCCL)"}
         except Exception as exc:   # reported, never fatal: it is only the comparison
             out["nccl_exchange"] = {"error": repr(exc)[:200]}
+        return out
     # single-GPU HBM-bound views of the same kernels
     xs = [torch.randn((n_seq, 1, H, hd), device=dev).to(torch.bfloat16) for _ in range(3)]
     g1 = U.SequenceGroup.single(dev.index)
@@ -671,10 +797,11 @@ def bench_a2a(dev, n_seq, H, hd, P, group, reps=10):
     out["p1_permute"] = {"ms": round(ms1, 4), "hbm_gbs": round(b1 / (ms1 / 1e3) / 1e9, 1)}
     P8 = 8
     if H % P8 == 0 and n_seq % P8 == 0:
-        groups = U.SequenceGroup.local_group(P8, slot_bytes=3 * (n_seq // P8) * H * hd * 2 + (1 << 20),
-                                             device=dev.index)
+        groups = U.SequenceGroup.local_group(P8, device=dev.index)
         xl = [[t[r * (n_seq // P8):(r + 1) * (n_seq // P8)].contiguous() for t in xs] for r in range(P8)]
         torch.cuda.synchronize()
+        for r in range(P8):   # size every rank's slots before the timed runs (collective regrowth)
+            groups[r].ensure_slot(sum(t.numel() * 2 for t in xl[r]) + 4096)
         ms8 = timed([(lambda r=r: groups[r].all_to_all(xl[r], 2, 0)) for r in range(P8)],
                     [g.stream for g in groups])
         for g in groups:
@@ -687,6 +814,18 @@ def bench_a2a(dev, n_seq, H, hd, P, group, reps=10):
         for g in groups:
             g.destroy()
     return out
+
+
+def bench_anchors(n_seq, H, hd, flush):
+    """Same-box library anchors for the config-2 attention (never on the
+    product path): cuDNN SDPA forward and forward+backward (torch), torch's
+    built-in flash SDPA and flashinfer's prefill forward (tools/anchor.py)."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from anchor import library_anchors
+        return library_anchors(n=n_seq, h=H, hd=hd, flush=flush.view(torch_int64()))
+    except Exception as exc:
+        return {"error": repr(exc)[:300]}
 
 
 def run_e2e(layer, q, k, v, do, args, P, dev):
@@ -761,15 +900,71 @@ def run_e2e(layer, q, k, v, do, args, P, dev):
 # reference arm: the reference algorithm on the host cores
 # ---------------------------------------------------------------------------
 
-def workload_config(P, n_seq, H, hd):
+def workload_config(P, n_seq, H, hd, cfg_name="2", HKV=None):
     """The `config` both arms report (the reference arm on the same workload)."""
+    HKV = HKV or H
+    desc = CONFIGS[cfg_name][3].format(P=P, n=n_seq)
     return {
-        "workload": ("config2: single-GPU local attention fwd+bwd, GPT-1.3B layer 16 heads x 128, "
-                     f"N={n_seq} bf16 causal" if P == 1 else
-                     f"Ulysses DistributedAttention fwd+bwd, P={P}, 16 heads x 128, N={n_seq} "
-                     f"(= {SEQ_PER_GPU} x P) bf16 causal"),
-        "seq_len": n_seq, "heads": H, "head_dim": hd, "batch": 1, "parallelism": f"ulysses-sp{P}",
-        "causal": True, "l2": "flushed (1 GiB write) before every timed step, flush untimed",
+        "workload": desc, "baseline_config": int(cfg_name),
+        "seq_len": n_seq, "heads": H, "kv_heads": HKV, "head_dim": hd, "batch": 1,
+        "parallelism": f"ulysses-sp{P}", "causal": True,
+        "l2": "flushed before every timed step by reading a 1 GiB buffer (untimed)",
+    }
+
+
+def reference_plan_items():
+    """BASELINE.md section 3's CPU timings of the reference algorithm (oracle
+    port: fixed-order f64 matmul, reference all_to_all), measured in full,
+    no extrapolation:
+      * config 1 -- Ulysses DistributedAttention P = 2 simulated ranks,
+        N = 1024, 8 heads x 64, causal: forward (best of 2) and forward +
+        backward, ranks in lockstep (one core) and concurrent (one thread per
+        rank, numpy releases the GIL in its array ops);
+      * the reference all_to_all (np.split / np.concatenate,
+        simgroup.py:322-327) at config 3's full per-rank size (P = 8,
+        N = 32K, 32 heads x 128, f64): GB/s per rank."""
+    import threading as th
+    import numpy as np
+    from oracle import ulysses_oracle as O
+    P, n, H, hd = 2, 1024, 8, 64
+    nl = n // P
+    mk = lambda s: [O.make_tensor((nl, 1, H, hd), 2024, s * 10 + r) for r in range(P)]
+    q, k, v, do = mk(1), mk(2), mk(3), mk(4)
+    fwd = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        out, st = O.ulysses_forward(q, k, v, "causal")
+        fwd.append(time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    out, st = O.ulysses_forward(q, k, v, "causal")
+    O.ulysses_backward(do, st, "causal")
+    fb = time.perf_counter() - t0
+    # concurrent: the per-rank attention of the forward core on P threads
+    q4, k4, v4 = O.all_to_all(q, 2, 0), O.all_to_all(k, 2, 0), O.all_to_all(v, 2, 0)
+    t0 = time.perf_counter()
+    ths = [th.Thread(target=O.local_attention, args=(q4[r], k4[r], v4[r], "causal")) for r in range(P)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    conc = time.perf_counter() - t0   # the per-rank attention of the forward only
+    xs = [np.random.default_rng(r).standard_normal((4096, 1, 32, 128)) for r in range(8)]
+    t0 = time.perf_counter()
+    O.all_to_all(xs, 2, 0)
+    ta = time.perf_counter() - t0
+    local = xs[0].nbytes
+    return {
+        "config1_full": {"P": P, "n": n, "heads": H, "head_dim": hd, "mask": "causal",
+                         "fwd_s_best_of_2_lockstep": round(min(fwd), 3),
+                         "fwd_bwd_s_lockstep": round(fb, 3),
+                         "fwd_attention_s_concurrent_threads": round(conc, 3),
+                         "tokens_per_s_fwd_bwd": round(n / fb, 2),
+                         "impl": "oracle port of run_ulysses_attention's core (ulysses.py:144-154, 213-226), "
+                                 "exact fixed-order matmul (tensor.py:209-224)"},
+        "a2a_config3_full": {"P": 8, "per_rank_shape": [4096, 1, 32, 128], "dtype": "f64",
+                             "seconds_all_ranks": round(ta, 3),
+                             "gbs_per_rank": round(local / (ta / 8) / 1e9, 3),
+                             "impl": "np.split + np.concatenate per rank (simgroup.py:322-327), ranks in lockstep"},
     }
 
 
@@ -779,15 +974,15 @@ def run_reference(args):
     if rank != 0:
         return
     P = world
-    n_seq = args.seq if args.seq else SEQ_PER_GPU * P
+    cfg_name, H, HKV, n_seq, _ = pick_config(args, P)
     cores = os.cpu_count() or 1
     procs = max(1, min(cores, 16))
     for _ in range(args.warmup):
-        cpu_baseline(n_seq, args.heads, HEAD_DIM, procs=procs, n_sample=args.cpu_sample // 2)
+        cpu_baseline(n_seq, H, HEAD_DIM, procs=procs, n_sample=args.cpu_sample // 2)
     vals = []
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(cpu_baseline(n_seq, args.heads, HEAD_DIM, procs=procs, n_sample=args.cpu_sample))
+        vals.append(cpu_baseline(n_seq, H, HEAD_DIM, procs=procs, n_sample=args.cpu_sample))
     wall = time.perf_counter() - t0
     tok = statistics.mean(v["tokens_per_s"] for v in vals)
     ms_per_step = n_seq / tok * 1e3
@@ -797,14 +992,16 @@ def run_reference(args):
         "value": round(tok, 4), "unit": "tokens/s", "n_gpus": P, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic N(0,1), seed-derived",
-        "config": workload_config(P, n_seq, args.heads, HEAD_DIM),
+        "config": workload_config(P, n_seq, H, HEAD_DIM, cfg_name, HKV),
         "reference_impl": (f"reference algorithm (seqlab kernels.py fixed-order f64, oracle port) for N={n_seq}, "
-                           f"{args.heads} heads x {HEAD_DIM}, causal fwd+bwd on {procs} host cores"),
+                           f"{H} heads x {HEAD_DIM}, causal fwd+bwd on {procs} host cores"),
         "cpu_baseline": {"value": round(tok, 4), "unit": "tokens/s", "cores": procs, "kind": "port",
-                         "sample": vals[0]["sample"]},
+                         "sample": vals[0]["sample"], "cpu_model": host_cpu_model()},
         "e2e": {"value": round(tok, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": round(wall, 1),
     }
+    if P == 1 and not args.quick:
+        res["plan_items"] = reference_plan_items()
     print(json.dumps(res), flush=True)
 
 
@@ -814,11 +1011,16 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="", choices=["", "2", "3", "4", "5"],
+                    help="BASELINE.json config (default: 2 at N=1, 5 at N>1)")
     ap.add_argument("--seq", type=int, default=0, help="override total sequence length")
-    ap.add_argument("--heads", type=int, default=HEADS)
+    ap.add_argument("--heads", type=int, default=0, help="override head count (q = kv)")
     ap.add_argument("--cpu-sample", type=int, default=1024)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--quick", action="store_true", help="skip the side legs (anchors, layer, sparse, plan items)")
+    ap.add_argument("--dry-run", action="store_true", help="host-side contract only (no CUDA)")
     args = ap.parse_args()
+    maybe_relaunch(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -167,10 +167,20 @@ int ul_attn_fwd_blocked(const void* q, const void* k, const void* v, void* o, fl
  *      bits run to run);
  *   UL_ATTN_DETERMINISTIC: dK/dV kernel + a dQ kernel that recomputes S and
  *      dP, no atomics: bitwise reproducible (and bitwise P-invariant).
+ *   UL_ATTN_WS_ZEROED: the first ul_attn_bwd_workspace_zero_bytes() bytes of
+ *      `workspace` are zero (as every bf16 call leaves them: the fused
+ *      kernel's dQ accumulator and sub-tile counters are cleared by the
+ *      kernel itself), so the pre-pass does not clear them again -- for
+ *      callers that keep one workspace per stream across calls.
  * hd 64 and fp32 always run the deterministic kernels. */
 #define UL_ATTN_DETERMINISTIC 1
+#define UL_ATTN_WS_ZEROED     2
 size_t ul_attn_bwd_workspace_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
                                    int dtype);
+/* Leading bytes of the workspace that must be zero on entry with
+ * UL_ATTN_WS_ZEROED (and that every call leaves zero). */
+size_t ul_attn_bwd_workspace_zero_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
+                                        int dtype);
 int ul_attn_bwd(const void* q, const void* k, const void* v, const void* o,
                 const void* dout, const float* lse, void* dq, void* dk, void* dv,
                 void* workspace, size_t workspace_bytes,
@@ -179,7 +189,8 @@ int ul_attn_bwd(const void* q, const void* k, const void* v, const void* o,
 
 /* Same as ul_attn_bwd restricted to a subset of its launches (bit 0: D/LSE
  * pre-pass, bit 1: dK/dV kernel -- the fused dK/dV/dQ kernel in the default
- * hd-128 mode --, bit 2: dQ kernel -- the dQ fp32->bf16 pass in that mode),
+ * hd-128 mode, which also converts dQ --, bit 2: dQ kernel -- nothing in
+ * that mode),
  * in that order; the stages must run in order over one workspace.  Lets
  * callers time or overlap the stages; ul_attn_bwd == stage_mask 7. */
 int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* o,

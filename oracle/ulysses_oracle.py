@@ -225,6 +225,73 @@ def attention_head_backward(q, k, v, dctx, kind: str, scale: float, exact: bool 
     return dq, dk, dv
 
 
+def attention_head_backward_rows(q, k, v, dctx, kind: str, scale: float, rows: tuple[int, int]):
+    """dq of query rows [r0, r1) only: kernels.py:89-111 restricted to those
+    rows with the reference's row_offset convention (tensor.py:151-156,
+    227-249) -- each row's probabilities, dprobs, dot and dscores depend on
+    that row alone, so the block equals the same rows of the full result.
+    q, k, v, dctx: (n, hd) of ONE batch entry.  BLAS float64."""
+    _check_kind(kind)
+    r0, r1 = rows
+    q = np.asarray(q[r0:r1], dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    d2 = np.asarray(dctx[r0:r1], dtype=np.float64)
+    probs = row_softmax((q @ k.T) * scale, kind, row_offset=r0)
+    dprobs = d2 @ v.T
+    dot = (dprobs * probs).sum(axis=1, keepdims=True)
+    dscores = probs * (dprobs - dot) * scale
+    return dscores @ k
+
+
+def attention_head_backward_cols(q, k, v, dctx, kind: str, scale: float, cols: tuple[int, int],
+                                 lse=None, dot=None, chunk: int = 2048):
+    """dk, dv of key rows [c0, c1) only (kernels.py:89-111: dk = dscores^T q,
+    dv = probs^T dctx, restricted to those columns of probs / dscores).
+
+    Every query row that sees a key in the block contributes (causal: rows
+    i >= c0).  A row's probabilities need its full-row normaliser and its
+    dot = rowsum(dprobs * probs); both are computed here from the row's full
+    scores (exact, costs O(rows * n * hd)) unless given as ``lse`` /
+    ``dot`` arrays over all n rows (natural-log LSE; dot == rowsum(dctx *
+    ctx)), in which case only the block's columns are evaluated.  Query rows
+    are processed in chunks.  q, k, v, dctx: (n, hd) of ONE batch entry."""
+    _check_kind(kind)
+    c0, c1 = cols
+    n = q.shape[0]
+    k = np.asarray(k, dtype=np.float64)
+    v = np.asarray(v, dtype=np.float64)
+    kb, vb = k[c0:c1], v[c0:c1]
+    dk = np.zeros((c1 - c0, q.shape[1]))
+    dv = np.zeros((c1 - c0, v.shape[1]))
+    start = c0 if kind == "causal" else 0
+    for i0 in range(start, n, chunk):
+        i1 = min(n, i0 + chunk)
+        qi = np.asarray(q[i0:i1], dtype=np.float64)
+        di = np.asarray(dctx[i0:i1], dtype=np.float64)
+        if lse is None or dot is None:
+            s_full = (qi @ k.T) * scale
+            vis = visibility(kind, i1 - i0, n, row_offset=i0)
+            shifted = np.where(vis, s_full, -np.inf)
+            mx = shifted.max(axis=1, keepdims=True)
+            e = np.where(vis, np.exp(np.where(vis, s_full - mx, 0.0)), 0.0)
+            probs_full = e / e.sum(axis=1, keepdims=True)
+            dprobs_full = di @ v.T
+            row_dot = (dprobs_full * probs_full).sum(axis=1, keepdims=True)
+            pb = probs_full[:, c0:c1]
+            dpb = dprobs_full[:, c0:c1]
+        else:
+            sb = (qi @ kb.T) * scale
+            vis = visibility(kind, i1 - i0, n, row_offset=i0)[:, c0:c1]
+            pb = np.where(vis, np.exp(np.where(vis, sb - np.asarray(lse[i0:i1])[:, None], 0.0)), 0.0)
+            dpb = di @ vb.T
+            row_dot = np.asarray(dot[i0:i1])[:, None]
+        dsb = pb * (dpb - row_dot) * scale
+        dk += dsb.T @ qi
+        dv += pb.T @ di
+    return dk, dv
+
+
 def kv_head_for(h: int, hq: int, hkv: int) -> int:
     """GQA RESTATEMENT: query head h reads kv head h // (hq/hkv)."""
     if hq % hkv != 0:

@@ -29,6 +29,7 @@ IPC_HANDLE_BYTES = 128
 ABI_VERSION = 2
 ATTN_SCHED_BYTES = 8
 ATTN_DETERMINISTIC = 1
+ATTN_WS_ZEROED = 2
 
 # every symbol include/ulysses_b200.h declares (tests check the exports)
 EXPORTS = (
@@ -36,7 +37,7 @@ EXPORTS = (
     "ul_comm_open_peers", "ul_comm_validate_handles", "ul_comm_link_local", "ul_comm_destroy", "ul_comm_rank",
     "ul_comm_world", "ul_comm_slot_bytes", "ul_comm_set_timeout_ms", "ul_comm_status",
     "ul_comm_ledger", "ul_all_to_all", "ul_all_to_all_slot_bytes", "ul_attn_fwd", "ul_attn_fwd_blocked", "ul_qkv_proj_exchange", "ul_ring_shift", "ul_lse_merge",
-    "ul_attn_bwd_workspace_bytes", "ul_attn_bwd", "ul_attn_bwd_stages", "ul_attn_fwd_exchange",
+    "ul_attn_bwd_workspace_bytes", "ul_attn_bwd_workspace_zero_bytes", "ul_attn_bwd", "ul_attn_bwd_stages", "ul_attn_fwd_exchange",
     "ul_attn_bwd_exchange", "ul_last_launch_count",
     "ul_total_launch_count", "ul_ulysses_volume",
 )
@@ -82,6 +83,7 @@ def _declare(lib):
         "ul_attn_fwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64,
                                        ctypes.c_int, ctypes.c_int, ctypes.c_float, c_vp, c_vp]),
         "ul_attn_bwd_workspace_bytes": (ctypes.c_size_t, [c_i64, c_i64, c_i64, c_i64, c_i64, ctypes.c_int]),
+        "ul_attn_bwd_workspace_zero_bytes": (ctypes.c_size_t, [c_i64, c_i64, c_i64, c_i64, c_i64, ctypes.c_int]),
         "ul_attn_bwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        ctypes.c_size_t, c_i64, c_i64, c_i64, c_i64, c_i64, ctypes.c_int,
                                        ctypes.c_int, ctypes.c_float, ctypes.c_int, c_vp]),

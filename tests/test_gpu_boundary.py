@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 import torch
 
-from helpers import run_ranks, to_dev, to_np, rel_max_err, BF16_MAXREL
+from helpers import run_ranks, rel_max_err, BF16_MAXREL
 from oracle import ulysses_oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -39,28 +39,18 @@ def test_receive_slot_grows_on_demand_in_process():
         assert torch.equal(back[r][0], xs[r][0])
 
 
-def test_distributed_attention_default_slot_fused_layer_grows():
+def test_distributed_attention_small_slot_fused_layer_grows():
     # DistributedAttention over a group created with a slot far below what
     # the fused Q/K/V exchange needs: no slot arithmetic by the caller
+    from test_gpu_distributed import run_layer
     p, n, h, hd = 2, 2048, 4, 128
     q, k, v, do = (O.make_tensor((n, 1, h, hd), 2024, s, "bfloat16") for s in (1, 2, 3, 4))
-    groups = U().SequenceGroup.local_group(p, slot_bytes=256 << 10)
-    layers = [U().DistributedAttention(U().FlashAttention("causal"), g) for g in groups]
-    nl = n // p
-    shard = lambda x, r: to_dev(x[r * nl:(r + 1) * nl], torch.bfloat16).requires_grad_(True)
-    ins = [[shard(x, r) for x in (q, k, v)] for r in range(p)]
-
-    def fwd_bwd(r):
-        o = layers[r](*ins[r])
-        o.backward(to_dev(do[r * nl:(r + 1) * nl], torch.bfloat16))
-        return o
-    outs = run_ranks(groups, fwd_bwd)
+    o, (dq, dk, dv), groups = run_layer(p, q, k, v, do, "causal", torch.bfloat16, slot_bytes=256 << 10)
+    assert all(g.slot_bytes >= 3 * (n // p) * h * hd * 2 for g in groups)
     ref, _ = O.local_attention(q, k, v, "causal", exact=False)
-    got = np.concatenate([to_np(o) for o in outs])
-    assert rel_max_err(got, ref) <= BF16_MAXREL
-    dq_r, _, _ = O.local_attention_backward(q, k, v, do, "causal", exact=False)
-    dq = np.concatenate([to_np(ins[r][0].grad) for r in range(p)])
-    assert rel_max_err(dq, dq_r) <= BF16_MAXREL
+    assert rel_max_err(o, ref) <= BF16_MAXREL
+    for got, exp in zip((dq, dk, dv), O.local_attention_backward(q, k, v, do, "causal", exact=False)):
+        assert rel_max_err(got, exp) <= BF16_MAXREL
 
 
 def test_args_pass_through_to_local_attention():

@@ -66,7 +66,7 @@ def test_attention_argument_errors_before_any_launch():
     st = L.ul_attn_bwd(p, p, p, p, p, None, p, p, p, p, 1 << 20, 4, 1, 4, 4, 64, 1, 1, 0.1, 0, None)
     assert errors.STATUS[st] is errors.ForwardStateError
     # unknown per-call backward flags -> ValueError (UL_ERR_ARG), before any launch
-    st = L.ul_attn_bwd(p, p, p, p, p, p, p, p, p, p, 1 << 20, 4, 1, 4, 4, 64, 1, 1, 0.1, 2, None)
+    st = L.ul_attn_bwd(p, p, p, p, p, p, p, p, p, p, 1 << 20, 4, 1, 4, 4, 64, 1, 1, 0.1, 4, None)
     assert st == -8 and b"flags" in L.ul_last_error()
 
 
