@@ -596,7 +596,7 @@ static int plan_call(ul_comm* c, int n, void* const* out, const int64_t* shapes,
   uint64_t in_total = 0;
   for (int t = 0; t < n; ++t) {
     UL_TRY(make_geom(ndim, shapes + 4 * t, esz, split, concat, pl->P, &pl->g[t]));
-    if (!out[t]) return fail(UL_ERR_ARG, "all_to_all: NULL tensor %d", t);
+    if (!out[t] && pl->g[t].out_bytes > 0) return fail(UL_ERR_ARG, "all_to_all: NULL tensor %d", t);
     for (int k = 0; k < ndim; ++k) sig = fnv(sig, (uint64_t)shapes[4 * t + k]);
     pl->slot_off[t] = slot_need;
     slot_need += align_up(pl->g[t].out_bytes, 256);
@@ -728,7 +728,8 @@ extern "C" {
 int ul_qkv_proj_exchange(ul_comm* c, const void* x, const void* w, void* q4, void* k4, void* v4, int64_t nl,
                          int64_t b, int64_t hq, int64_t hkv, int64_t hd, uint64_t label, void* stream) {
   launch_count() = 0;
-  if (!x || !w || !q4 || !k4 || !v4) return fail(UL_ERR_ARG, "ul_qkv_proj_exchange: NULL tensor");
+  if ((!x || !q4 || !k4 || !v4) && nl * b > 0) return fail(UL_ERR_ARG, "ul_qkv_proj_exchange: NULL tensor");
+  if (!w) return fail(UL_ERR_ARG, "ul_qkv_proj_exchange: NULL weight");
   if (nl < 0 || b < 1 || hq < 1 || hkv < 1 || hd < 1)
     return fail(UL_ERR_SHAPE, "ul_qkv_proj_exchange: bad shape (nl=%lld, b=%lld, hq=%lld, hkv=%lld, hd=%lld)",
                 (long long)nl, (long long)b, (long long)hq, (long long)hkv, (long long)hd);
@@ -784,7 +785,7 @@ int ul_all_to_all(ul_comm* c, int n, const void* const* in, void* const* out, co
   CallPlan pl;
   UL_TRY(plan_call(c, n, out, shapes, ndim, dtype, split, concat, label, &pl));
   for (int t = 0; t < n; ++t)
-    if (!in[t]) return fail(UL_ERR_ARG, "all_to_all: NULL tensor %d", t);
+    if (!in[t] && pl.g[t].in_bytes > 0) return fail(UL_ERR_ARG, "all_to_all: NULL tensor %d", t);
   const int P = pl.P, me = pl.me, slot = pl.slot;
   cudaStream_t st = (cudaStream_t)stream;
   // push: local chunk -> out (local HBM), remote chunks -> peer slots (NVLink)

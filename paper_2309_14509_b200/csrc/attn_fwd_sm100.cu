@@ -25,7 +25,6 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
-#include <cstdlib>
 #include <cstring>
 
 #include "comm.cuh"
@@ -266,14 +265,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < nkv; ++j) {
         const int s = j % NS;
         const uint32_t ph = (j / NS) & 1;
-        mbar_wait(&k_empty[s], ph ^ 1);
+        mbar_wait_prod(&k_empty[s], ph ^ 1);
         UL_EV(8, j);
         mbar_expect_tx(&k_full[s], BN * HD * 2);
 #pragma unroll
         for (int a = 0; a < HD / 64; ++a)
           tma_load_3d(sK + s * S::kTile + a * kAtom, &tmK, &k_full[s], a * 64, bb * p.hkv + g,
                       (blocked ? tiles[j] : j) * BN);
-        mbar_wait(&v_empty[s], ph ^ 1);
+        mbar_wait_prod(&v_empty[s], ph ^ 1);
         UL_EV(9, j);
         mbar_expect_tx(&v_full[s], BN * HD * 2);
 #pragma unroll
@@ -640,12 +639,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < nkv; ++j, ++gk) {
           const int s = gk % NS;
           const uint32_t ph = (gk / NS) & 1;
-          mbar_wait(&k_empty[s], ph ^ 1);
+          mbar_wait_prod(&k_empty[s], ph ^ 1);
           mbar_expect_tx(&k_full[s], BN * HD * 2);
 #pragma unroll
           for (int a = 0; a < HD / 64; ++a)
             tma_load_3d(sK + s * S::kTile + a * kAtom, &tmK, &k_full[s], a * 64, bb * p.hkv + g, j * BN);
-          mbar_wait(&v_empty[s], ph ^ 1);
+          mbar_wait_prod(&v_empty[s], ph ^ 1);
           mbar_expect_tx(&v_full[s], BN * HD * 2);
 #pragma unroll
           for (int a = 0; a < HD / 64; ++a)
@@ -870,400 +869,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// ---- one query tile per CTA, S double-buffered (default for dense / causal, hd 128) ----
-//
-// The two-tile kernels above chain each tile's softmax -> PV -> next S
-// (S(j+1) overwrites the TMEM columns PV(j) reads P(j) from), so a tile's
-// period is softmax + 2 GEMMs and the tensor pipe idles whenever a softmax
-// runs long.  Here a CTA owns ONE 128-row query tile and TMEM holds
-//   S[0] | S[1] | Q | O        (128 + 128 + 64 + 128 columns)
-// -- Q resident as the A operand of S = Q K^T (TS MMA: only K is read from
-// shared memory, 64 B/clk instead of 128), and S double-buffered so S(j+1)
-// runs while the softmax of tile j does: the MMA thread issues
-//   S(j+1), PV(j)   (PV(j) waits for P(j))
-// and the period becomes max(softmax, S + PV) instead of their sum.
-// Persistent: one CTA per SM walks (query tile, head) items longest first
-// (dynamic counter or static zig-zag waves, like attn_fwd_persist_kernel);
-// the next item's Q rows are fetched into registers during the current
-// item's last softmax and stored into TMEM as soon as its last S completed,
-// so its first S MMAs queue behind the current PV while the epilogue drains O.
-// kParts softmax warps share each TMEM lane quarter (128 / kParts columns each).
-constexpr int NS1 = 3;   // K/V stages
-template <int kParts>
-struct Q1 {
-  static constexpr int kSoftWarps = 4 * kParts;
-  static constexpr int kThreads = 64 + kSoftWarps * 32;
-  static constexpr int kCols = BN / kParts;           // S columns per softmax warp
-  static constexpr int kTile = 2 * kAtom;              // 128 x 128 bf16 (two SW128 atoms)
-  static constexpr int kK = 0;                         // [NS1]
-  static constexpr int kV = kK + NS1 * kTile;          // [NS1]
-  static constexpr int kBar = kV + NS1 * kTile;
-  static constexpr int kX = kBar + 512;                // [3 slots][128 rows][kParts] f32
-  static constexpr int kBytes = kX + 3 * 128 * kParts * 4 + 1024;
-};
-
-// item k of this CTA: (query tile, batch*head), longest first
-__device__ __forceinline__ bool q1_item_static(const Params& p, int k, int& qt, int& bh) {
-  const int heads = p.b * p.hq;
-  const int G = (int)gridDim.x;
-  const int idx = k * G + ((k & 1) ? G - 1 - (int)blockIdx.x : (int)blockIdx.x);
-  if (idx >= p.qtiles * heads) return false;
-  qt = p.head_major ? p.qtiles - 1 - idx % p.qtiles : p.qtiles - 1 - idx / heads;
-  bh = p.head_major ? idx / p.qtiles : idx % heads;
-  return true;
-}
-__device__ __forceinline__ bool q1_item_dyn(const Params& p, int k, int& qt, int& bh, int role, uint64_t* it_full,
-                                            uint64_t* it_empty, volatile int* sitem) {
-  const int slot = k & 3;
-  int idx;
-  if (role == 0) {
-    if (k >= 4) mbar_wait(&it_empty[slot], ((k >> 2) - 1) & 1);
-    idx = atomicAdd(p.ctr, 1);
-    sitem[slot] = idx;
-    mbar_arrive(&it_full[slot]);
-  } else {
-    mbar_wait(&it_full[slot], (k >> 2) & 1);
-    idx = sitem[slot];
-    if (role == 2) __syncwarp();
-    if (role == 1 || (threadIdx.x & 31) == 0) mbar_arrive(&it_empty[slot]);
-  }
-  const int heads = p.b * p.hq;
-  if (idx >= p.qtiles * heads) return false;
-  qt = p.head_major ? p.qtiles - 1 - idx % p.qtiles : p.qtiles - 1 - idx / heads;
-  bh = p.head_major ? idx / p.qtiles : idx % heads;
-  return true;
-}
-
-template <int kParts, bool kPoly>
-__global__ void __launch_bounds__(Q1<kParts>::kThreads, 1)
-    attn_fwd_q1_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                       const __nv_bfloat16* __restrict__ qptr, const Params p) {
-  constexpr int HD = 128;
-  using C = Q1<kParts>;
-  constexpr int kCols = C::kCols;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sK = smem + C::kK;
-  uint8_t* sV = smem + C::kV;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBar);
-  uint64_t* k_full = bars + 0;                 // [NS1]
-  uint64_t* k_empty = bars + NS1;              // [NS1]
-  uint64_t* v_full = bars + 2 * NS1;           // [NS1]
-  uint64_t* v_empty = bars + 3 * NS1;          // [NS1]
-  uint64_t* s_full = bars + 4 * NS1;           // [2] S(g) in buffer g & 1
-  uint64_t* p_full = bars + 4 * NS1 + 2;       // [2] P(g) written over it
-  uint64_t* o_done = bars + 4 * NS1 + 4;       // [2] PV(g) complete (by buffer)
-  uint64_t* o_last = bars + 4 * NS1 + 6;       // an item's last PV complete
-  uint64_t* o_free = bars + 4 * NS1 + 7;       // O read out by the epilogue
-  uint64_t* q_full = bars + 4 * NS1 + 8;       // an item's Q rows in TMEM
-  uint64_t* it_full = bars + 4 * NS1 + 9;      // [4] dynamic item ring
-  uint64_t* it_empty = bars + 4 * NS1 + 13;    // [4]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * NS1 + 17);
-  volatile int* sitem = reinterpret_cast<volatile int*>(bars + 4 * NS1 + 18);
-  static_assert((4 * NS1 + 20) * 8 <= 512, "barrier area");
-  auto item = [&](int k, int& qt, int& bh, int role) {
-    return p.ctr ? q1_item_dyn(p, k, qt, bh, role, it_full, it_empty, sitem) : q1_item_static(p, k, qt, bh);
-  };
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int nkv_all = (p.n + BN - 1) / BN;
-  auto item_kv = [&](int qt) { return p.causal ? min(nkv_all, (qt * BM + BM - 1) / BN + 1) : nkv_all; };
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NS1; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
-      mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], C::kSoftWarps);
-      mbar_init(&o_done[b], 1);
-    }
-    mbar_init(o_last, 1);
-    mbar_init(o_free, C::kSoftWarps);
-    mbar_init(q_full, C::kSoftWarps);
-    for (int s = 0; s < 4; ++s) {
-      mbar_init(&it_full[s], 1);
-      mbar_init(&it_empty[s], 1 + C::kSoftWarps);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (*tmem_slot != 0u) __trap();
-  constexpr uint32_t tbase = 0, tQ = 256, tO = 384;   // S[b] at b * 128
-
-  if (warp == 0) {
-    // ---------------- TMA producer: K / V tiles of every item ----------------
-    if (lane == 0) {
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
-      int qt, bh, g = 0;
-      for (int k = 0; item(k, qt, bh, 0); ++k) {
-        const int bb = bh / p.hq, kvh = bb * p.hkv + (bh % p.hq) / (p.hq / p.hkv);
-        const int nkv = item_kv(qt);
-        for (int j = 0; j < nkv; ++j, ++g) {
-          const int s = g % NS1;
-          const uint32_t ph = (g / NS1) & 1;
-          mbar_wait(&k_empty[s], ph ^ 1);
-          mbar_expect_tx(&k_full[s], BN * HD * 2);
-#pragma unroll
-          for (int a = 0; a < HD / 64; ++a)
-            tma_load_3d(sK + s * C::kTile + a * kAtom, &tmK, &k_full[s], a * 64, kvh, j * BN);
-          mbar_wait(&v_empty[s], ph ^ 1);
-          mbar_expect_tx(&v_full[s], BN * HD * 2);
-#pragma unroll
-          for (int a = 0; a < HD / 64; ++a)
-            tma_load_3d(sV + s * C::kTile + a * kAtom, &tmV, &v_full[s], a * 64, kvh, j * BN);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (elect_one()) {
-      constexpr uint32_t kIdQK = idesc_bf16(BM, BN, 0, 0);   // A = Q (TMEM), B = K K-major
-      constexpr uint32_t kIdPV = idesc_bf16(BM, HD, 0, 1);   // A = P (TMEM), B = V MN-major
-      const uint64_t dK0 = sdesc(smem_u32(sK), 16, 1024);
-      const uint64_t dV0 = sdesc(smem_u32(sV), kAtom, 1024);
-      auto issue_s = [&](int gg) {   // S(gg) = Q K(gg)^T into buffer gg & 1
-        const int s = gg % NS1;
-        mbar_wait_mma(&k_full[s], (gg / NS1) & 1);
-        tc_fence_after();
-        const uint64_t dk = dadd(dK0, s * C::kTile);
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          mma_ts(tbase + (gg & 1) * 128, tQ + kk * 8, dadd(dk, (kk >> 2) * kAtom + (kk & 3) * 32), kIdQK,
-                 kk > 0 ? 1u : 0u);
-        mma_commit(&s_full[gg & 1]);
-        mma_commit(&k_empty[s]);
-      };
-      int qt, bh, g = 0;
-      bool have = item(0, qt, bh, 1);
-      if (have) {
-        mbar_wait_mma(q_full, 0);
-        issue_s(0);
-      }
-      for (int k = 0; have; ++k) {
-        const int nkv = item_kv(qt);
-        for (int j = 0; j < nkv; ++j, ++g) {
-          if (j + 1 < nkv) issue_s(g + 1);           // S(g+1) overlaps the softmax of g
-          if (j == 0 && k > 0) mbar_wait_mma(o_free, (k - 1) & 1);   // previous item's O read out
-          const int s = g % NS1;
-          mbar_wait_mma(&v_full[s], (g / NS1) & 1);
-          mbar_wait_mma(&p_full[g & 1], (g >> 1) & 1);
-          tc_fence_after();
-          const uint64_t dv = dadd(dV0, s * C::kTile);
-#pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk)
-            mma_ts(tO, tbase + (g & 1) * 128 + kk * 8, dadd(dv, kk * 2048), kIdPV, (j > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&o_done[g & 1]);
-          mma_commit(&v_empty[s]);
-          if (j + 1 == nkv) {
-            mma_commit(o_last);
-            have = item(k + 1, qt, bh, 1);
-            if (have) {   // the next item's first S: Q(k+1) is stored once S(g) completed
-              mbar_wait_mma(q_full, (k + 1) & 1);
-              issue_s(g + 1);
-            }
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else {
-    // ---------------- softmax / correction / epilogue ----------------
-    const int quarter = warp & 3;                 // TMEM lane quarter this warp may access
-    const int part = (warp - 2) >> 2;             // which kCols columns of the row
-    const int row = quarter * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t bar_id = 1 + quarter;
-    float* xch = reinterpret_cast<float*>(smem + C::kX);
-    auto xslot = [&](int sl, int pp) { return smem_u32(xch + (sl * 128 + row) * kParts + pp); };
-    auto quarter_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(kParts * 32) : "memory"); };
-    // this thread's Q elements: row `row`, columns [part * HD / kParts, ...)
-    constexpr int kQv = HD / kParts / 8;          // uint4 per thread
-    uint4 qreg[kQv];
-    auto q_fetch = [&](int qt, int bh) {
-      const int qrow = qt * BM + row;
-      const __nv_bfloat16* src = qptr + (((int64_t)qrow * p.b + bh / p.hq) * p.hq + bh % p.hq) * HD + part * (HD / kParts);
-#pragma unroll
-      for (int x = 0; x < kQv; ++x)
-        qreg[x] = qrow < p.n ? __ldg(reinterpret_cast<const uint4*>(src) + x) : make_uint4(0, 0, 0, 0);
-    };
-    auto q_store = [&]() {
-      uint32_t w[kQv * 4];
-#pragma unroll
-      for (int x = 0; x < kQv; ++x) {
-        w[4 * x] = qreg[x].x;
-        w[4 * x + 1] = qreg[x].y;
-        w[4 * x + 2] = qreg[x].z;
-        w[4 * x + 3] = qreg[x].w;
-      }
-      if constexpr (kQv * 4 == 32) tmem_st32(tQ + lane_off + part * 32, w);
-      else tmem_st16(tQ + lane_off + part * 16, w);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(q_full);
-    };
-    int qt, bh, g = 0;
-    bool have = item(0, qt, bh, 2);
-    if (have) {
-      q_fetch(qt, bh);
-      q_store();
-    }
-    for (int k = 0; have; ++k) {
-      const int nkv = item_kv(qt);
-      const int bb = bh / p.hq, h = bh % p.hq;
-      const int q0 = qt * BM, qrow = q0 + row;
-      int nqt = 0, nbh = 0;
-      bool next = false;
-      float m = -INFINITY, l = 0.f;
-      for (int j = 0; j < nkv; ++j, ++g) {
-        const int kv0 = j * BN;
-        const uint32_t tS = tbase + (g & 1) * 128 + lane_off;
-        mbar_wait(&s_full[g & 1], (g >> 1) & 1);
-        tc_fence_after();
-        if (j + 1 == nkv) {   // the item's last S: prefetch the next item's Q rows (stored after this softmax)
-          next = item(k + 1, nqt, nbh, 2);
-          if (next) q_fetch(nqt, nbh);
-        }
-        uint32_t r[kCols];
-#pragma unroll
-        for (int c = 0; c < kCols / 32; ++c) tmem_ld32(tS + part * kCols + c * 32, r + c * 32);
-        tmem_wait_ld();
-        const bool masked = (p.causal && kv0 + BN - 1 > q0) || kv0 + BN > p.n;
-        if (masked) {
-          int limit = p.n - kv0;
-          if (p.causal) limit = min(limit, qrow - kv0 + 1);
-          limit -= part * kCols;
-#pragma unroll
-          for (int c = 0; c < kCols; ++c)
-            if (c >= limit) r[c] = __float_as_uint(-INFINITY);
-        }
-        float mx[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) mx[u] = __uint_as_float(r[u]);
-#pragma unroll
-        for (int c = 8; c < kCols; c += 8) {
-#pragma unroll
-          for (int u = 0; u < 8; ++u) mx[u] = fmaxf(mx[u], __uint_as_float(r[c + u]));
-        }
-        float mh = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(g & 1, part)), "f"(mh) : "memory");
-        quarter_sync();
-#pragma unroll
-        for (int pp = 0; pp < kParts; ++pp) {
-          float o_;
-          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o_) : "r"(xslot(g & 1, pp)) : "memory");
-          mh = fmaxf(mh, o_);
-        }
-        const float mt = mh * p.scale_log2;
-        float alpha = 1.f;
-        bool rescale = false;
-        if (mt > m + kLazy) {
-          alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - mt);
-          rescale = (j > 0);
-          m = mt;
-        }
-        const float mu = (m == -INFINITY) ? 0.f : m;
-        float2 rsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int c = 0; c < kCols / 32; ++c) {
-          uint32_t pk[16];
-          if (kPoly && !masked) exp_chunk<true>(r + c * 32, p.scale_log2, mu, pk, rsum);
-          else exp_chunk<false>(r + c * 32, p.scale_log2, mu, pk, rsum);
-          tmem_st16(tS + part * (kCols / 2) + c * 16, pk);   // P over S columns already read
-        }
-        const float2 rs = __fadd2_rn(__fadd2_rn(rsum[0], rsum[1]), __fadd2_rn(rsum[2], rsum[3]));
-        l = l * alpha + (rs.x + rs.y);
-        if (__any_sync(0xffffffffu, rescale)) {
-          // PV(g-1) must have landed before O is scaled (S(g) was issued
-          // before it); the rows of this warp scale their HD/kParts columns
-          mbar_wait(&o_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int c = 0; c < HD / kParts / 32; ++c) {
-            uint32_t ov[32];
-            tmem_ld32(tO + lane_off + part * (HD / kParts) + c * 32, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int x = 0; x < 32; ++x) ov[x] = __float_as_uint(__uint_as_float(ov[x]) * alpha);
-            tmem_st32(tO + lane_off + part * (HD / kParts) + c * 32, ov);
-          }
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[g & 1]);
-        if (j + 1 == nkv && next) q_store();   // every S MMA of this item has completed: Q may be replaced
-      }
-      // full row sum over the kParts warps of the row
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(2, part)), "f"(l) : "memory");
-      quarter_sync();
-      float lrow = 0.f;
-#pragma unroll
-      for (int pp = 0; pp < kParts; ++pp) {
-        float o_;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o_) : "r"(xslot(2, pp)) : "memory");
-        lrow += o_;
-      }
-      quarter_sync();   // (slot 2 is rewritten by the next item)
-      mbar_wait(o_last, k & 1);
-      tc_fence_after();
-      const float inv = 1.f / lrow;
-      constexpr int kOc = HD / kParts;             // O columns of this thread
-      uint32_t pkd[kOc / 2];
-#pragma unroll
-      for (int c = 0; c < kOc / 32; ++c) {
-        uint32_t ov[32];
-        tmem_ld32(tO + lane_off + part * kOc + c * 32, ov);
-        tmem_wait_ld();
-#pragma unroll
-        for (int x = 0; x < 16; ++x)
-          pkd[c * 16 + x] = pack_bf16(__uint_as_float(ov[2 * x]) * inv, __uint_as_float(ov[2 * x + 1]) * inv);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(o_free);          // the next item's first PV may overwrite O
-      if (qrow < p.n) {
-        uint4* dst = reinterpret_cast<uint4*>(p.o + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD + part * kOc);
-#pragma unroll
-        for (int x = 0; x < kOc / 8; ++x) dst[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
-        if (p.ep.active) {   // fused head->seq: the same bytes into the destination rank's sequence layout
-          uint4* pd = reinterpret_cast<uint4*>(peer_row_ptr(p.ep, qrow, bb, p.b, h, HD, 2) + part * kOc * 2);
-#pragma unroll
-          for (int x = 0; x < kOc / 8; ++x) pd[x] = make_uint4(pkd[4 * x], pkd[4 * x + 1], pkd[4 * x + 2], pkd[4 * x + 3]);
-        }
-        if (part == 0) p.lse[((int64_t)bb * p.hq + h) * p.n + qrow] = (m + log2f(lrow)) * 0.69314718055994531f;
-      }
-      qt = nqt;
-      bh = nbh;
-      have = next;
-    }
-    if (p.ep.active) __threadfence_system();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (p.ctr && threadIdx.x == 0) {   // every CTA has taken its last index: the last one resets
-    __threadfence();
-    if (atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1) {
-      atomicExch(p.ctr, 0);
-      atomicExch(p.ctr + 1, 0);
-    }
-  }
-  if (p.ep.active && threadIdx.x == 0) peer_signal_last_cta(p.ep, gridDim.x);
-  if (warp == 1) {
-    __syncwarp();
-    tc_fence_after();
-    tmem_dealloc<512>(tbase);
-  }
-}
-
 // The persistent forward's [next item, CTAs done] counter pair is caller
 // memory (`sched`, UL_ATTN_SCHED_BYTES, zeroed once; the kernel leaves it
 // zero): launches sharing one pair must be stream-ordered.  No counter, or a
@@ -1318,40 +923,6 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
   static std::atomic<uint64_t> attr{0}, pattr{0};
   UL_TRY(smem_opt_in((const void*)attn_fwd_kernel<HD>, smem, attr));
   const int64_t grid = (int64_t)p.pairs * b * hq;
-  if (HD == 128 && !blk) {
-    // one query tile per CTA, S double-buffered (default; UL_FWD_VARIANT
-    // selects an instantiation for A/B runs: 0 = the two-tile kernels)
-    static const int variant = [] {
-      const char* e = getenv("UL_FWD_VARIANT");
-      return e ? atoi(e) : 1;
-    }();
-    if (variant >= 1 && variant <= 4) {
-      p.head_major = p.qtiles >= sm_count();
-      p.ctr = schedule_counter(sched, st);
-      const int64_t items = (int64_t)p.qtiles * b * hq;
-      const unsigned qgrid = (unsigned)(items < sm_count() ? items : sm_count());
-      static std::atomic<uint64_t> a1{0}, a2{0}, a3{0}, a4{0};
-      switch (variant) {
-        case 1:
-          UL_TRY(smem_opt_in((const void*)attn_fwd_q1_kernel<2, false>, Q1<2>::kBytes, a1));
-          attn_fwd_q1_kernel<2, false><<<qgrid, Q1<2>::kThreads, Q1<2>::kBytes, st>>>(mk, mv, (const __nv_bfloat16*)q, p);
-          break;
-        case 2:
-          UL_TRY(smem_opt_in((const void*)attn_fwd_q1_kernel<2, true>, Q1<2>::kBytes, a2));
-          attn_fwd_q1_kernel<2, true><<<qgrid, Q1<2>::kThreads, Q1<2>::kBytes, st>>>(mk, mv, (const __nv_bfloat16*)q, p);
-          break;
-        case 3:
-          UL_TRY(smem_opt_in((const void*)attn_fwd_q1_kernel<4, false>, Q1<4>::kBytes, a3));
-          attn_fwd_q1_kernel<4, false><<<qgrid, Q1<4>::kThreads, Q1<4>::kBytes, st>>>(mk, mv, (const __nv_bfloat16*)q, p);
-          break;
-        default:
-          UL_TRY(smem_opt_in((const void*)attn_fwd_q1_kernel<4, true>, Q1<4>::kBytes, a4));
-          attn_fwd_q1_kernel<4, true><<<qgrid, Q1<4>::kThreads, Q1<4>::kBytes, st>>>(mk, mv, (const __nv_bfloat16*)q, p);
-          break;
-      }
-      return launched("attn_fwd_sm100");
-    }
-  }
 #ifndef UL_FWD_PERSIST
 #define UL_FWD_PERSIST 1   // r73: -1.5% vs the one-shot grid; blocked-sparse keeps the one-shot kernel
 #endif
@@ -1398,10 +969,6 @@ int preload_fwd() {
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_kernel<128>));
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<64>));
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<128>));
-  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_q1_kernel<2, false>));
-  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_q1_kernel<2, true>));
-  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_q1_kernel<4, false>));
-  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_q1_kernel<4, true>));
   return UL_OK;
 }
 

@@ -133,6 +133,21 @@ __device__ __forceinline__ void mbar_wait_k(uint64_t* bar, uint32_t parity) {
     }
     return;
   }
+  if (kKind == 3) {
+    // poll, then back off with __nanosleep: a waiting producer / MMA-issuer
+    // thread must not take issue slots from the softmax warps of its SMSP
+    // (r2 trace: the MMA warp's SMSP ran its softmax warps ~700 cycles per
+    // kv step behind the other three)
+    if (mbar_try_wait(bar, parity)) return;
+    const uint64_t t0 = globaltimer();
+    uint32_t ns = 32;
+    while (!mbar_try_wait(bar, parity)) {
+      __nanosleep(ns);
+      if (ns < 256) ns <<= 1;
+      if (globaltimer() - t0 > 4000000000ull) mbar_timeout(bar, parity);
+    }
+    return;
+  }
   if (kKind == 2) {
     if (mbar_try_wait_sleep(bar, parity)) return;
   } else if (kKind == 1) {
@@ -165,6 +180,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) { mbar
 // the single MMA-issuing thread (the tensor pipe idles while it waits)
 __device__ __forceinline__ void mbar_wait_mma(uint64_t* bar, uint32_t parity) {
   mbar_wait_k<UL_WAIT_MMA_KIND>(bar, parity);
+}
+#ifndef UL_WAIT_PROD_KIND
+#define UL_WAIT_PROD_KIND 0
+#endif
+// the single TMA-producer thread
+__device__ __forceinline__ void mbar_wait_prod(uint64_t* bar, uint32_t parity) {
+  mbar_wait_k<UL_WAIT_PROD_KIND>(bar, parity);
 }
 
 // ---- TMA ----------------------------------------------------------------------
