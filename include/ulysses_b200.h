@@ -123,6 +123,19 @@ int ul_all_to_all(ul_comm* comm, int n_tensors, const void* const* in, void* con
                   const int64_t* shapes, int ndim, int dtype, int split_axis,
                   int concat_axis, uint64_t label_hash, void* stream);
 
+/* Seq->head exchange of ONE head group (extension: the pipelined layer
+ * exchanges group g+1 while group g is being attended).  in[t] is this
+ * rank's full sequence shard [nl, b, H_t, hd] (shapes[4t..4t+4), row-major);
+ * with Hg_t = H_t / (P * groups), rank i receives the heads
+ * { j*H_t/P + group*Hg_t + h : h < Hg_t } of every rank j's shard, rows in
+ * source-rank order: out[t] = [nl*P, b, Hg_t, hd].  Equal to ul_all_to_all
+ * (split 2, concat 0) of the [nl, b, P*Hg_t, hd] view holding those heads
+ * (same slot geometry and signature), read in place from the parent shard.
+ * groups = 1 is the plain seq->head flip. */
+int ul_all_to_all_head_group(ul_comm* comm, int n_tensors, const void* const* in, void* const* out,
+                             const int64_t* shapes, int dtype, int group, int groups,
+                             uint64_t label_hash, void* stream);
+
 /* Bytes of receive slot ul_all_to_all needs for these tensors. */
 size_t ul_all_to_all_slot_bytes(int n_tensors, const int64_t* shapes, int ndim, int dtype,
                                 int split_axis, int concat_axis, int world);
@@ -246,6 +259,18 @@ int ul_lse_merge(void* o_acc, float* lse_acc, const void* o_s, const float* lse_
 int ul_qkv_proj_exchange(ul_comm* comm, const void* x, const void* w, void* q4, void* k4, void* v4,
                          int64_t nl, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
                          uint64_t label_hash, void* stream);
+
+/* The general form (both directions): Y = X W (w
+ * row-major [d_in, N]) or Y = X W^T (w_transposed: w row-major [N, d_in],
+ * e.g. the backward's dc = g Wo^T, ulysses.py:207) with N = sum(heads)*hd,
+ * whose 128-column head blocks are stored straight into the head layout of
+ * their owner rank: outs[t] = [nl*P, b, heads[t]/P, hd] -- the GEMM fused
+ * with the seq->head exchange of its n_out (1..3) outputs.  x: [nl*b,
+ * d_in] bf16; d_in % 64 == 0, hd = 128.  A collective like ul_all_to_all.
+ * ul_qkv_proj_exchange == ul_proj_exchange(x, [wq|wk|wv], 0, 3, ...). */
+int ul_proj_exchange(ul_comm* comm, const void* x, const void* w, int w_transposed, int n_out,
+                     void* const* outs, const int64_t* heads, int64_t nl, int64_t b, int64_t d_in,
+                     int64_t hd, uint64_t label_hash, void* stream);
 
 /* Number of kernel launches the last ul_* call on this thread issued, and
  * the cumulative count since the library was loaded (all threads). */

@@ -36,7 +36,7 @@ EXPORTS = (
     "ul_abi_version", "ul_last_error", "ul_preload_kernels", "ul_comm_create", "ul_comm_export_handle",
     "ul_comm_open_peers", "ul_comm_validate_handles", "ul_comm_link_local", "ul_comm_destroy", "ul_comm_rank",
     "ul_comm_world", "ul_comm_slot_bytes", "ul_comm_set_timeout_ms", "ul_comm_status",
-    "ul_comm_ledger", "ul_all_to_all", "ul_all_to_all_slot_bytes", "ul_attn_fwd", "ul_attn_fwd_blocked", "ul_qkv_proj_exchange", "ul_ring_shift", "ul_lse_merge",
+    "ul_comm_ledger", "ul_all_to_all", "ul_all_to_all_head_group", "ul_all_to_all_slot_bytes", "ul_attn_fwd", "ul_attn_fwd_blocked", "ul_qkv_proj_exchange", "ul_proj_exchange", "ul_ring_shift", "ul_lse_merge",
     "ul_attn_bwd_workspace_bytes", "ul_attn_bwd_workspace_zero_bytes", "ul_attn_bwd", "ul_attn_bwd_stages", "ul_attn_fwd_exchange",
     "ul_attn_bwd_exchange", "ul_last_launch_count",
     "ul_total_launch_count", "ul_ulysses_volume",
@@ -70,6 +70,8 @@ def _declare(lib):
                                           P(ctypes.c_uint64)]),
         "ul_all_to_all": (ctypes.c_int, [c_vp, ctypes.c_int, P(c_vp), P(c_vp), P(c_i64), ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, c_vp]),
+        "ul_all_to_all_head_group": (ctypes.c_int, [c_vp, ctypes.c_int, P(c_vp), P(c_vp), P(c_i64), ctypes.c_int,
+                                                    ctypes.c_int, ctypes.c_int, ctypes.c_uint64, c_vp]),
         "ul_all_to_all_slot_bytes": (ctypes.c_size_t, [ctypes.c_int, P(c_i64), ctypes.c_int, ctypes.c_int,
                                                        ctypes.c_int, ctypes.c_int, ctypes.c_int]),
         "ul_lse_merge": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, ctypes.c_int,
@@ -78,6 +80,8 @@ def _declare(lib):
                                          ctypes.c_uint64, c_vp]),
         "ul_qkv_proj_exchange": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64,
                                                  c_i64, ctypes.c_uint64, c_vp]),
+        "ul_proj_exchange": (ctypes.c_int, [c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, P(c_vp), P(c_i64), c_i64,
+                                            c_i64, c_i64, c_i64, ctypes.c_uint64, c_vp]),
         "ul_attn_fwd_blocked": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64,
                                                 ctypes.c_int, c_i64, c_vp, c_i64, ctypes.c_float, c_vp]),
         "ul_attn_fwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64,

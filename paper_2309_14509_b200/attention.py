@@ -273,7 +273,8 @@ class FlashAttention:
         return dq, dk, dv
 
     # -- fused head->seq exchange (K2 in the kernels' epilogues) ------------
-    def forward_exchange(self, q, k, v, group: SequenceGroup, label: str = "attn.ctx.head2seq"):
+    def forward_exchange(self, q, k, v, group: SequenceGroup, label: str = "attn.ctx.head2seq",
+                         ledger_elements: int | None = None):
         """Forward on head-sharded q/k/v [N, b, h, hd] plus the head->seq
         exchange of O fused into the kernel epilogue.  Returns (o_head, lse,
         o_seq) with o_seq = seq layout [N/P, b, P*h, hd] of this rank."""
@@ -293,11 +294,12 @@ class FlashAttention:
                                                    o.data_ptr(), lse.data_ptr(), o_seq.data_ptr(), n, b, hq, hkv,
                                                    hd, _ATTN_DTYPES[q.dtype], self.mask_code, self._scale(hd),
                                                    label_hash(label), _sched_counter(q), _stream(q)))
-        group._record(label, o.numel())
+        if ledger_elements != 0:
+            group._record(label, o.numel() if ledger_elements is None else ledger_elements)
         return o, lse, o_seq
 
     def backward_exchange(self, q, k, v, o, lse, do, group: SequenceGroup, label: str = "bwd.qkv.head2seq",
-                          return_head: bool = False):
+                          return_head: bool = False, ledger_scale: int = 1):
         """Backward with the head->seq exchange of dQ/dK/dV fused into the
         epilogues.  Returns sequence-layout (dq, dk, dv) of this rank (and
         the head-layout gradients the kernels also wrote, if return_head)."""
@@ -321,8 +323,9 @@ class FlashAttention:
                                                    sq.data_ptr(), sk.data_ptr(), sv.data_ptr(), n, b, hq, hkv, hd,
                                                    dt, self.mask_code, self._scale(hd), label_hash(label),
                                                    self.flags | wflag, _stream(q)))
-        for name, t in (("bwd.q.head2seq", dq), ("bwd.k.head2seq", dk), ("bwd.v.head2seq", dv)):
-            group._record(name, t.numel())
+        if ledger_scale:   # (a pipelined layer records its G group calls once, scaled by G)
+            for name, t in (("bwd.q.head2seq", dq), ("bwd.k.head2seq", dk), ("bwd.v.head2seq", dv)):
+                group._record(name, t.numel() * ledger_scale)
         if return_head:
             return (sq, sk, sv), (dq, dk, dv)
         return sq, sk, sv
@@ -414,6 +417,99 @@ class _UlyssesAttnFn(torch.autograd.Function):
         return None, None, None, None, dq, dk, dv
 
 
+def _interleave(parts, p: int):
+    """Per-head-group sequence outputs [nl, b, P*Hg, hd] (heads ordered
+    (rank, h)) -> the layer's [nl, b, P*G*Hg, hd] with head r*Hl + g*Hg + h."""
+    nl, b, ph, hd = parts[0].shape
+    hg = ph // p
+    return torch.stack([x.view(nl, b, p, hg, hd) for x in parts], dim=3).view(nl, b, p * len(parts) * hg, hd)
+
+
+class _UlyssesAttnPipeFn(torch.autograd.Function):
+    """The layer node with the exchanges pipelined over G head groups
+    (north star item 3).  The seq->head exchange of group g+1 runs on the
+    group's second channel and stream while group g is attended on the
+    compute stream (its head->seq exchange fused into the attention
+    epilogue, main channel); the backward does the same with dO.  Every
+    group is the reference's layer on a subset of heads (attention is
+    independent per head, ulysses.py:148-152), so the result is the one of
+    _UlyssesAttnFn; the per-group sequence outputs are interleaved back into
+    the [s/P, b, h, hd] layout."""
+
+    @staticmethod
+    def forward(ctx, group, attn, G, q, k, v):
+        p = group.world
+        chan = group.channel
+        main = torch.cuda.current_stream(q.device)
+        cs = chan.stream
+        q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        cs.wait_stream(main)
+        heads, evs = [], []
+        with torch.cuda.stream(cs):
+            for t in (q, k, v):
+                t.record_stream(cs)
+            for gi in range(G):
+                heads.append(chan.all_to_all_head_group(
+                    [q, k, v], gi, G, label="attn.qkv.seq2head",
+                    labels=["attn.q.seq2head", "attn.k.seq2head", "attn.v.seq2head"]))
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                evs.append(ev)
+        outs, saved = [], []
+        for gi in range(G):
+            main.wait_event(evs[gi])
+            q4, k4, v4 = heads[gi]
+            for t in (q4, k4, v4):
+                t.record_stream(main)
+            o4, lse, o_seq = attn.forward_exchange(q4, k4, v4, group, label=f"attn.ctx.head2seq.{gi}/{G}",
+                                                   ledger_elements=q.numel() if gi == 0 else 0)
+            outs.append(o_seq)
+            saved += [q4, k4, v4, o4, lse]
+        ctx.group, ctx.attn, ctx.G = group, attn, G
+        ctx.save_for_backward(*saved)
+        return _interleave(outs, p)
+
+    @staticmethod
+    def backward(ctx, do):
+        group, attn, G = ctx.group, ctx.attn, ctx.G
+        p = group.world
+        chan = group.channel
+        main = torch.cuda.current_stream(do.device)
+        cs = chan.stream
+        saved = ctx.saved_tensors
+        do = do.contiguous()
+        cs.wait_stream(main)
+        dos, evs = [], []
+        with torch.cuda.stream(cs):
+            do.record_stream(cs)
+            for gi in range(G):
+                (do4,) = chan.all_to_all_head_group([do], gi, G, label="bwd.ctx.seq2head")
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                dos.append(do4)
+                evs.append(ev)
+        dq, dk, dv = [], [], []
+        for gi in range(G):
+            q4, k4, v4, o4, lse = saved[5 * gi:5 * gi + 5]
+            main.wait_event(evs[gi])
+            dos[gi].record_stream(main)
+            a, b_, c = attn.backward_exchange(q4, k4, v4, o4, lse, dos[gi], group, label=f"bwd.qkv.head2seq.{gi}/{G}",
+                                              ledger_scale=G if gi == 0 else 0)
+            dq.append(a)
+            dk.append(b_)
+            dv.append(c)
+        return None, None, None, _interleave(dq, p), _interleave(dk, p), _interleave(dv, p)
+
+
+def pipeline_groups(heads_local: int, kv_heads_local: int, want: int = 2) -> int:
+    """Head groups of the pipelined layer: the largest g <= want dividing
+    both this rank's query and kv head counts (1 = no pipelining)."""
+    for g in range(max(1, want), 0, -1):
+        if heads_local % g == 0 and kv_heads_local % g == 0:
+            return g
+    return 1
+
+
 class DistributedAttention(torch.nn.Module):
     """Ulysses sequence-parallel attention (arXiv 2309.14509 section 3.1).
 
@@ -423,12 +519,15 @@ class DistributedAttention(torch.nn.Module):
     """
 
     def __init__(self, local_attention, sequence_process_group=None, scatter_idx: int = 2,
-                 gather_idx: int = 0):
+                 gather_idx: int = 0, pipeline: int = 2):
         super().__init__()
         self.local_attn = local_attention
         self.spg = _group(sequence_process_group)
         self.scatter_idx = scatter_idx
         self.gather_idx = gather_idx
+        # head groups over which the fused route pipelines its exchanges with
+        # the attention (P > 1); 1 = one exchange of all heads, then attention
+        self.pipeline = int(pipeline)
 
     def _check(self, q, k, v):
         p = self.spg.world
@@ -455,6 +554,10 @@ class DistributedAttention(torch.nn.Module):
                 q, k, v = (x.reshape(x.shape[1], 1, x.shape[2], x.shape[3]) for x in (query, key, value))
                 o = _UlyssesAttnFn.apply(self.spg, self.local_attn, 2, 0, q, k, v)
                 return o.reshape(1, o.shape[0], o.shape[2], o.shape[3])
+            p = self.spg.world
+            G = pipeline_groups(query.shape[2] // p, key.shape[2] // p, self.pipeline) if p > 1 else 1
+            if G > 1 and (self.scatter_idx, self.gather_idx) == (2, 0):
+                return _UlyssesAttnPipeFn.apply(self.spg, self.local_attn, G, query, key, value)
             return _UlyssesAttnFn.apply(self.spg, self.local_attn, self.scatter_idx, self.gather_idx,
                                         query, key, value)
         # generic plugin: any callable local_attn(q, k, v) on head-sharded tensors

@@ -26,6 +26,7 @@ from .errors import GroupDesyncError, ShardError
 _DTYPES = {torch.float32: _lib.DTYPE_F32, torch.bfloat16: _lib.DTYPE_BF16}
 
 DEFAULT_SLOT_BYTES = 64 << 20
+CHANNEL_SLOT_BYTES = 1 << 20   # the prefetch channel starts small and grows on demand
 SLOT_GRANULE = 16 << 20      # receive slots grow in multiples of this
 
 
@@ -190,6 +191,9 @@ class SequenceGroup:
         self._pg = pg
         self._local = local                 # in-process group: every rank's SequenceGroup
         self._timeout_ms = None
+        # second exchange channel of the same ranks (own workspace, epochs and
+        # stream) for the pipelined layer's prefetch exchanges; see `channel`
+        self._channel = None
         self.records: CommLedger = CommLedger()   # the logical ledger (elements, reference schema)
         self.ledger = self.records
 
@@ -221,6 +225,10 @@ class SequenceGroup:
             return cls.single(device)
         h = cls._open_ipc(rank, world, device, slot_bytes, pg)
         g = cls(rank, world, device, h, int(_lib.lib().ul_comm_slot_bytes(h)), pg=pg)
+        hc = cls._open_ipc(rank, world, device, CHANNEL_SLOT_BYTES, pg)
+        g._channel = cls(rank, world, device, hc, int(_lib.lib().ul_comm_slot_bytes(hc)), pg=pg,
+                         stream=torch.cuda.Stream(device=device))
+        g._channel.records = g._channel.ledger = g.records   # one logical ledger for both channels
         if timeout_ms:
             g.set_timeout_ms(timeout_ms)
         dist.barrier(group=pg)
@@ -247,6 +255,15 @@ class SequenceGroup:
             device = torch.cuda.current_device()
         if world == 1:
             return [cls.single(device)]
+        local = cls._make_local(world, device, slot_bytes)
+        chans = cls._make_local(world, device, CHANNEL_SLOT_BYTES)
+        for g, c in zip(local, chans):
+            g._channel = c
+            c.records = c.ledger = g.records   # one logical ledger for both channels
+        return local
+
+    @classmethod
+    def _make_local(cls, world, device, slot_bytes):
         handles = cls._link_local(world, device, slot_bytes)
         sb = int(_lib.lib().ul_comm_slot_bytes(handles[0]))
         local = []
@@ -265,6 +282,22 @@ class SequenceGroup:
         if self._handle is not None:
             _lib.check(_lib.lib().ul_comm_set_timeout_ms(self._handle, int(ms)))
             self._timeout_ms = int(ms)
+        if self._channel is not None:
+            self._channel.set_timeout_ms(ms)
+
+    @property
+    def channel(self) -> "SequenceGroup":
+        """The group's second exchange channel: the same ranks with their own
+        workspace, epochs and stream (``channel.stream``).  The pipelined
+        layer issues the seq->head exchange of head group g+1 there while
+        the attention of group g (and its fused head->seq exchange on this,
+        the main channel) runs on the compute stream.  Each channel is used
+        from one stream, which is what the two-slot epoch protocol relies on
+        (csrc/a2a.cu: a sender reuses a slot only after passing the next
+        call's wait)."""
+        if self._channel is None:
+            raise RuntimeError("this SequenceGroup has no second channel (P = 1)")
+        return self._channel
 
     # -- receive-slot sizing -------------------------------------------------
     def ensure_slot(self, need: int):
@@ -286,7 +319,7 @@ class SequenceGroup:
             # call; the others have issued every earlier call already
             torch.cuda.synchronize(self.device)
             for g in self._local:
-                g.destroy()
+                g.destroy(with_channel=False)
             handles = self._link_local(self.world, self.device, new)
             sb = int(_lib.lib().ul_comm_slot_bytes(handles[0]))
             for g, h in zip(self._local, handles):
@@ -297,17 +330,19 @@ class SequenceGroup:
         import torch.distributed as dist
         torch.cuda.synchronize(self.device)
         dist.barrier(group=self._pg)           # every peer is done with the old slots
-        self.destroy()
+        self.destroy(with_channel=False)
         self._handle = self._open_ipc(self.rank, self.world, self.device, new, self._pg)
         self.slot_bytes = int(_lib.lib().ul_comm_slot_bytes(self._handle))
         if self._timeout_ms:
             self.set_timeout_ms(self._timeout_ms)
         dist.barrier(group=self._pg)
 
-    def destroy(self):
+    def destroy(self, with_channel: bool = True):
         if self._handle is not None:
             _lib.lib().ul_comm_destroy(self._handle)
             self._handle = None
+        if with_channel and self._channel is not None:
+            self._channel.destroy()
 
     def __del__(self):
         try:
@@ -339,6 +374,12 @@ class SequenceGroup:
         p = self.world
         self.records.append(CommRecord("all_to_all", label, p * local_elements,
                                        local_elements // p * (p - 1)))
+
+    def _record_full(self, label: str, parent_elements: int, group: int):
+        """Ledger for a head-group call: the G calls of one logical
+        all_to_all are recorded once, with the whole tensor's elements."""
+        if group == 0:
+            self._record(label, parent_elements)
 
     def total_egress(self) -> int:
         return sum(r.per_rank_egress_elements for r in self.records)
@@ -396,6 +437,71 @@ class SequenceGroup:
                                                    label_hash("attn.qkv.seq2head"), stream),
                    exc_override={-1: ShardError})
         return q4, k4, v4
+
+    def proj_exchange(self, x2: torch.Tensor, w: torch.Tensor, heads, b: int, transposed: bool = False,
+                      labels=None, label: str = "proj.seq2head"):
+        """GEMM fused with the seq->head exchange of its outputs
+        (ul_proj_exchange): Y = x2 @ w (w [d_in, N]) or x2 @ w.T (transposed,
+        w [N, d_in]); N = sum(heads)*hd is split into outputs of `heads[t]`
+        heads each, returned in this rank's head layout [nl*P, b, heads[t]/P,
+        hd].  x2 = this rank's [nl*b, d_in] shard; a collective."""
+        from .errors import ShardError
+        p = self.world
+        m, d_in = x2.shape
+        nl = m // b
+        n_cols = w.shape[0] if transposed else w.shape[1]
+        hd = n_cols // sum(heads)
+        for hh in heads:
+            if hh % p:
+                raise ShardError(f"p={p} does not divide head count {hh}")
+        outs = [torch.empty((nl * p, b, hh // p, hd), dtype=x2.dtype, device=x2.device) for hh in heads]
+        if p > 1:
+            self.ensure_slot(slot_need(o.numel() * o.element_size() for o in outs))
+        for lab, hh in zip(labels or [label] * len(heads), heads):
+            self._record(lab, nl * b * hh * hd)
+        op = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        hp = (ctypes.c_int64 * len(heads))(*heads)
+        stream = torch.cuda.current_stream(x2.device).cuda_stream
+        _lib.check(_lib.lib().ul_proj_exchange(self._handle, x2.data_ptr(), w.data_ptr(), int(transposed), len(outs),
+                                               op, hp, nl, b, d_in, hd, label_hash(label), stream),
+                   exc_override={-1: ShardError})
+        return outs
+
+    def all_to_all_head_group(self, tensors, group: int, groups: int, label: str = "attn.seq2head.group",
+                              labels=None, ledger_group=None):
+        """Seq->head exchange of head group `group` of `groups`
+        (ul_all_to_all_head_group): from each rank's full shard
+        [nl, b, H_t, hd] rank i receives heads i*H_t/P + group*Hg + [0, Hg)
+        of every rank, Hg = H_t / (P*groups), as [nl*P, b, Hg, hd].  The
+        `groups` calls of one tensor make one logical all_to_all in the
+        ledger (recorded at group 0, or at `ledger_group`)."""
+        tensors = [t.contiguous() for t in tensors]
+        if not tensors or len(tensors) > _lib.MAX_FUSED:
+            raise ValueError(f"all_to_all_head_group fuses 1..{_lib.MAX_FUSED} tensors, got {len(tensors)}")
+        p = self.world
+        dt = dtype_code(tensors[0].dtype)
+        outs = []
+        shapes = (ctypes.c_int64 * (4 * len(tensors)))()
+        for t, x in enumerate(tensors):
+            if x.dim() != 4 or x.dtype != tensors[0].dtype:
+                raise ValueError("all_to_all_head_group needs [nl, b, H, hd] tensors of one dtype")
+            nl, b, h, hd = x.shape
+            if h % (p * groups):
+                raise ShardError(f"p={p} x {groups} head groups does not divide head count {h}")
+            outs.append(torch.empty((nl * p, b, h // (p * groups), hd), dtype=x.dtype, device=x.device))
+            for kk in range(4):
+                shapes[4 * t + kk] = x.shape[kk]
+        if p > 1:
+            self.ensure_slot(slot_need(o.numel() * o.element_size() for o in outs))
+        for x, lab in zip(tensors, labels or [label] * len(tensors)):
+            self._record_full(lab, x.numel(), group if ledger_group is None else ledger_group)
+        inp = (ctypes.c_void_p * len(tensors))(*[x.data_ptr() for x in tensors])
+        outp = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+        stream = torch.cuda.current_stream(tensors[0].device).cuda_stream
+        _lib.check(_lib.lib().ul_all_to_all_head_group(self._handle, len(tensors), inp, outp, shapes, dt, group,
+                                                       groups, label_hash(f"{label}.{group}/{groups}"), stream),
+                   exc_override={-1: ShardError})
+        return outs
 
     def all_to_all(self, tensors, split_axis: int, concat_axis: int, label: str = "all_to_all",
                    labels=None):

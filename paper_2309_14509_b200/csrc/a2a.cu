@@ -719,38 +719,48 @@ int a2a_fused_finish(ul_comm* c, int n, void* const* seq_out, const int64_t* hea
 }
 
 int sm100_qkv_proj(const void* x, const void* w, int64_t M, int64_t K, int64_t N, const ProjEpilogue& ep,
-                   cudaStream_t st);
+                   cudaStream_t st, bool w_transposed);
 
 }  // namespace ul
 
 extern "C" {
 
-int ul_qkv_proj_exchange(ul_comm* c, const void* x, const void* w, void* q4, void* k4, void* v4, int64_t nl,
-                         int64_t b, int64_t hq, int64_t hkv, int64_t hd, uint64_t label, void* stream) {
+int ul_proj_exchange(ul_comm* c, const void* x, const void* w, int w_transposed, int n_out, void* const* outs,
+                     const int64_t* heads, int64_t nl, int64_t b, int64_t d_in, int64_t hd, uint64_t label,
+                     void* stream) {
   launch_count() = 0;
-  if ((!x || !q4 || !k4 || !v4) && nl * b > 0) return fail(UL_ERR_ARG, "ul_qkv_proj_exchange: NULL tensor");
-  if (!w) return fail(UL_ERR_ARG, "ul_qkv_proj_exchange: NULL weight");
-  if (nl < 0 || b < 1 || hq < 1 || hkv < 1 || hd < 1)
-    return fail(UL_ERR_SHAPE, "ul_qkv_proj_exchange: bad shape (nl=%lld, b=%lld, hq=%lld, hkv=%lld, hd=%lld)",
-                (long long)nl, (long long)b, (long long)hq, (long long)hkv, (long long)hd);
-  const int64_t d = hq * hd, dkv = hkv * hd;
-  // the fused all-to-all is the seq->head flip of the three projections' sequence shards
-  const int64_t shapes[12] = {nl, b, hq, hd, nl, b, hkv, hd, nl, b, hkv, hd};
-  void* outs[3] = {q4, k4, v4};
-  CallPlan pl;
-  UL_TRY(plan_call(c, 3, outs, shapes, 4, UL_DTYPE_BF16, 2, 0, label, &pl));
+  if (n_out < 1 || n_out > 3 || !outs || !heads) return fail(UL_ERR_ARG, "ul_proj_exchange: 1..3 outputs");
+  if (!w) return fail(UL_ERR_ARG, "ul_proj_exchange: NULL weight");
+  if (nl < 0 || b < 1 || d_in < 1 || hd < 1)
+    return fail(UL_ERR_SHAPE, "ul_proj_exchange: bad shape (nl=%lld, b=%lld, d_in=%lld, hd=%lld)", (long long)nl,
+                (long long)b, (long long)d_in, (long long)hd);
+  for (int t = 0; t < n_out; ++t) {
+    if (heads[t] < 1) return fail(UL_ERR_SHAPE, "ul_proj_exchange: head count %lld", (long long)heads[t]);
+    if (!outs[t] && nl * b > 0) return fail(UL_ERR_ARG, "ul_proj_exchange: NULL output %d", t);
+  }
+  if (!x && nl * b > 0) return fail(UL_ERR_ARG, "ul_proj_exchange: NULL input");
+  // the fused all-to-all is the seq->head flip of the projections' sequence shards
+  int64_t shapes[12];
+  int64_t N = 0;
   ProjEpilogue ep;
   memset(&ep, 0, sizeof(ep));
-  for (int t = 0; t < 3; ++t)
+  for (int t = 0; t < n_out; ++t) {
+    shapes[4 * t] = nl;
+    shapes[4 * t + 1] = b;
+    shapes[4 * t + 2] = heads[t];
+    shapes[4 * t + 3] = hd;
+    ep.col0[t] = (int)N;
+    N += heads[t] * hd;
+  }
+  for (int t = n_out; t < 4; ++t) ep.col0[t] = (int)N;
+  CallPlan pl;
+  UL_TRY(plan_call(c, n_out, outs, shapes, 4, UL_DTYPE_BF16, 2, 0, label, &pl));
+  for (int t = 0; t < n_out; ++t) {
     for (int r = 0; r < pl.P; ++r)
       ep.dst[t][r] = (r == pl.me || !c) ? (char*)outs[t]
                                         : c->peer_base[r] + (size_t)pl.slot * c->slot_bytes + pl.slot_off[t];
-  ep.col0[0] = 0;
-  ep.col0[1] = (int)d;
-  ep.col0[2] = (int)(d + dkv);
-  ep.col0[3] = (int)(d + 2 * dkv);
-  ep.hl[0] = (int)(hq / pl.P);
-  ep.hl[1] = ep.hl[2] = (int)(hkv / pl.P);
+    ep.hl[t] = (int)(heads[t] / pl.P);
+  }
   ep.nl = (int)nl;
   ep.b = (int)b;
   ep.hd = (int)hd;
@@ -772,31 +782,58 @@ int ul_qkv_proj_exchange(ul_comm* c, const void* x, const void* w, void* q4, voi
     // call -- peers still expect this rank's flag (a signal-only push)
     if (pl.P > 1) UL_TRY(signal_only(c, pl, st));
   } else {
-    UL_TRY(sm100_qkv_proj(x, w, nl * b, d, d + 2 * dkv, ep, st));
+    UL_TRY(sm100_qkv_proj(x, w, nl * b, d_in, N, ep, st, w_transposed != 0));
   }
   if (pl.P > 1) UL_TRY(wait_and_drain(c, pl, outs, st));
   return UL_OK;
 }
 
-int ul_all_to_all(ul_comm* c, int n, const void* const* in, void* const* out, const int64_t* shapes,
-                  int ndim, int dtype, int split, int concat, uint64_t label, void* stream) {
-  launch_count() = 0;
-  if (!in) return fail(UL_ERR_ARG, "all_to_all: NULL argument");
-  CallPlan pl;
-  UL_TRY(plan_call(c, n, out, shapes, ndim, dtype, split, concat, label, &pl));
-  for (int t = 0; t < n; ++t)
-    if (!in[t] && pl.g[t].in_bytes > 0) return fail(UL_ERR_ARG, "all_to_all: NULL tensor %d", t);
+int ul_qkv_proj_exchange(ul_comm* c, const void* x, const void* w, void* q4, void* k4, void* v4, int64_t nl,
+                         int64_t b, int64_t hq, int64_t hkv, int64_t hd, uint64_t label, void* stream) {
+  void* outs[3] = {q4, k4, v4};
+  const int64_t heads[3] = {hq, hkv, hkv};
+  return ul_proj_exchange(c, x, w, 0, 3, outs, heads, nl, b, hq * hd, hd, label, stream);
+}
+
+}  // extern "C"
+
+namespace ul {
+
+// Parent layout of a head-group exchange: box sources live inside this
+// rank's full [nl, b, H, hd] shard at head i * H / P + group * Hg (P, H per
+// tensor); nullptr for a plain contiguous all_to_all.
+struct HeadGroupSrc {
+  int64_t heads[UL_MAX_FUSED];   // H of each tensor
+  int group;                     // this call's head group
+};
+
+// the push (local chunk -> out, remote chunks -> peer slots, release
+// signal) + flag wait + drain of a planned call
+static int push_and_finish(ul_comm* c, const CallPlan& pl, const void* const* in, void* const* out,
+                           const HeadGroupSrc* hg, cudaStream_t st) {
   const int P = pl.P, me = pl.me, slot = pl.slot;
-  cudaStream_t st = (cudaStream_t)stream;
-  // push: local chunk -> out (local HBM), remote chunks -> peer slots (NVLink)
   CopyParams cp;
   memset(&cp, 0, sizeof(cp));
-  for (int t = 0; t < n; ++t) {
+  for (int t = 0; t < pl.n; ++t) {
     for (int k = 0; k < P; ++k) {
       const int i = (me + k) % P;  // rotate destinations to spread switch load
       char* dst = (i == me) ? (char*)out[t] : c->peer_base[i] + (size_t)slot * c->slot_bytes + pl.slot_off[t];
-      make_box(pl.g[t], me, i, P, (const char*)in[t], dst, &cp.box[cp.nbox]);
-      if (cp.box[cp.nbox].rows > 0) ++cp.nbox;
+      Box& b = cp.box[cp.nbox];
+      make_box(pl.g[t], me, i, P, (const char*)in[t], dst, &b);
+      if (hg && b.rows > 0) {
+        // the virtual [nl, b, P*Hg, hd] view of head group `group`: chunk i
+        // starts at head i*Hl + group*Hg of the parent shard, rows keep the
+        // parent's strides (run = Hg*hd elements, as for the view)
+        const Geom& g = pl.g[t];
+        const int64_t Hg = g.S[2] / P, Hl = hg->heads[t] / P, hd = g.S[3], esz = g.ss[3];
+        b.src = (const char*)in[t] + (i * Hl + (int64_t)hg->group * Hg) * hd * esz;
+        b.sst[1] = g.S[1] * hg->heads[t] * hd * esz;   // row s of the shard: b * H * hd elements
+        b.sst[2] = hg->heads[t] * hd * esz;             // batch entry: H * hd elements
+        uint64_t al = (uint64_t)b.run | (uint64_t)(uintptr_t)b.src | (uint64_t)(uintptr_t)b.dst;
+        for (int x = 0; x < 3; ++x) al |= (uint64_t)b.sst[x] | (uint64_t)b.dstr[x];
+        b.vec = (al % 16 == 0) ? 16 : (al % 8 == 0) ? 8 : (al % 4 == 0) ? 4 : (al % 2 == 0) ? 2 : 1;
+      }
+      if (b.rows > 0) ++cp.nbox;
     }
   }
   if (P > 1) {
@@ -817,6 +854,50 @@ int ul_all_to_all(ul_comm* c, int n, const void* const* in, void* const* out, co
   UL_TRY(launch_copy(cp, st, "a2a_push"));
   if (P == 1) return UL_OK;
   return wait_and_drain(c, pl, out, st);
+}
+
+}  // namespace ul
+
+extern "C" {
+
+int ul_all_to_all(ul_comm* c, int n, const void* const* in, void* const* out, const int64_t* shapes,
+                  int ndim, int dtype, int split, int concat, uint64_t label, void* stream) {
+  launch_count() = 0;
+  if (!in) return fail(UL_ERR_ARG, "all_to_all: NULL argument");
+  CallPlan pl;
+  UL_TRY(plan_call(c, n, out, shapes, ndim, dtype, split, concat, label, &pl));
+  for (int t = 0; t < n; ++t)
+    if (!in[t] && pl.g[t].in_bytes > 0) return fail(UL_ERR_ARG, "all_to_all: NULL tensor %d", t);
+  return push_and_finish(c, pl, in, out, nullptr, (cudaStream_t)stream);
+}
+
+int ul_all_to_all_head_group(ul_comm* c, int n, const void* const* in, void* const* out, const int64_t* shapes,
+                             int dtype, int group, int groups, uint64_t label, void* stream) {
+  launch_count() = 0;
+  if (!in || !shapes || n < 1 || n > UL_MAX_FUSED)
+    return fail(UL_ERR_ARG, "all_to_all_head_group: bad arguments");
+  const int P = c ? c->world : 1;
+  if (groups < 1 || group < 0 || group >= groups)
+    return fail(UL_ERR_ARG, "all_to_all_head_group: group %d of %d", group, groups);
+  HeadGroupSrc hg;
+  int64_t vshapes[4 * UL_MAX_FUSED];
+  for (int t = 0; t < n; ++t) {
+    const int64_t* sh = shapes + 4 * t;   // parent shard [nl, b, H, hd]
+    if (sh[2] % ((int64_t)P * groups) != 0)
+      return fail(UL_ERR_DIVISIBILITY, "all_to_all_head_group: p=%d x %d groups does not divide head count %lld", P,
+                  groups, (long long)sh[2]);
+    hg.heads[t] = sh[2];
+    vshapes[4 * t] = sh[0];
+    vshapes[4 * t + 1] = sh[1];
+    vshapes[4 * t + 2] = sh[2] / groups;   // the group's P*Hg heads
+    vshapes[4 * t + 3] = sh[3];
+  }
+  hg.group = group;
+  CallPlan pl;
+  UL_TRY(plan_call(c, n, out, vshapes, 4, dtype, 2, 0, label, &pl));
+  for (int t = 0; t < n; ++t)
+    if (!in[t] && pl.g[t].in_bytes > 0) return fail(UL_ERR_ARG, "all_to_all_head_group: NULL tensor %d", t);
+  return push_and_finish(c, pl, in, out, &hg, (cudaStream_t)stream);
 }
 
 // a flat byte range as rows of `run` bytes (so every warp of the copy gets rows)

@@ -53,6 +53,10 @@ struct Params {
   ProjEpilogue ep;
 };
 
+// kBKMajor: B is read from a row-major [N, K] matrix (Y = X W^T, e.g. the
+// backward's dc = g Wo^T): one 256-row x 64-column K-major box per stage;
+// otherwise from a row-major [K, N] matrix (Y = X W): four MN-major boxes.
+template <bool kBKMajor>
 __global__ void __launch_bounds__(kThreads, 1)
     qkv_proj_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, const Params p) {
   extern __shared__ uint8_t smem_raw[];
@@ -99,17 +103,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty[s], ((it / NSTAGE) & 1) ^ 1);
           mbar_expect_tx(&full[s], kATile + kBTile);
           tma_load_2d(sA + s * kATile, &tmX, &full[s], ks * BK, mt * BM);
+          if constexpr (kBKMajor) {
+            tma_load_2d(sB + s * kBTile, &tmW, &full[s], ks * BK, nt * BN);
+          } else {
 #pragma unroll
-          for (int a = 0; a < BN / 64; ++a)
-            tma_load_2d(sB + s * kBTile + a * (BK * 128), &tmW, &full[s], nt * BN + a * 64, ks * BK);
+            for (int a = 0; a < BN / 64; ++a)
+              tma_load_2d(sB + s * kBTile + a * (BK * 128), &tmW, &full[s], nt * BN + a * 64, ks * BK);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (elect_one()) {
-      constexpr uint32_t kId = idesc_bf16(BM, BN, 0, 1);   // A K-major, B MN-major
+      constexpr uint32_t kId = idesc_bf16(BM, BN, 0, kBKMajor ? 0 : 1);   // A K-major, B K- or MN-major
       const uint64_t dA0 = sdesc(smem_u32(sA), 16, 1024);
-      const uint64_t dB0 = sdesc(smem_u32(sB), BK * 128, 1024);
+      const uint64_t dB0 = kBKMajor ? sdesc(smem_u32(sB), 16, 1024) : sdesc(smem_u32(sB), BK * 128, 1024);
       int it = 0, tcount = 0;
       for (int tile = blockIdx.x; tile < ntile_total; tile += gridDim.x, ++tcount) {
         const int buf = tcount & 1;
@@ -125,7 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t da = dadd(dA0, s * kATile), db = dadd(dB0, s * kBTile);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
-            mma_ss(tacc, dadd(da, kk * 32), dadd(db, kk * 2048), kId, (ks > 0 || kk > 0) ? 1u : 0u);
+            mma_ss(tacc, dadd(da, kk * 32), dadd(db, kBKMajor ? kk * 32 : kk * 2048), kId, (ks > 0 || kk > 0) ? 1u : 0u);
           mma_commit(&empty[s]);
         }
         mma_commit(&acc_full[buf]);
@@ -189,14 +197,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 int preload_proj() {
   cudaFuncAttributes a;
-  UL_CUDA(cudaFuncGetAttributes(&a, proj::qkv_proj_kernel));
+  UL_CUDA(cudaFuncGetAttributes(&a, proj::qkv_proj_kernel<false>));
+  UL_CUDA(cudaFuncGetAttributes(&a, proj::qkv_proj_kernel<true>));
   return UL_OK;
 }
 
-// Y[M, N] = X[M, K] W[K, N] (bf16, fp32 accumulate) stored per 128-column
-// head block through `ep` (see above).  K % 64 == 0, N % 128 == 0.
+// Y[M, N] = X[M, K] W[K, N] (bf16, fp32 accumulate) -- or X W^T with W
+// stored [N, K] (w_transposed) -- stored per 128-column head block through
+// `ep` (see above).  K % 64 == 0, N % 128 == 0.
 int sm100_qkv_proj(const void* x, const void* w, int64_t M, int64_t K, int64_t N, const ProjEpilogue& ep,
-                   cudaStream_t st) {
+                   cudaStream_t st, bool w_transposed) {
   if (K % proj::BK != 0 || N % 128 != 0 || ep.hd != 128)
     return fail(UL_ERR_KERNEL, "qkv projection needs d %% 64 == 0, columns %% 128 == 0 and head_dim 128 "
                 "(K=%lld, N=%lld, hd=%d)", (long long)K, (long long)N, ep.hd);
@@ -204,7 +214,8 @@ int sm100_qkv_proj(const void* x, const void* w, int64_t M, int64_t K, int64_t N
   if (M == 0) return UL_OK;
   CUtensorMap mx, mw;
   UL_TRY(make_tmap_2d(&mx, x, M, K, proj::BM));
-  UL_TRY(make_tmap_2d(&mw, w, K, N, proj::BK));
+  if (w_transposed) UL_TRY(make_tmap_2d(&mw, w, N, K, proj::BN));
+  else UL_TRY(make_tmap_2d(&mw, w, K, N, proj::BK));
   proj::Params p;
   p.M = (int)M;
   p.K = (int)K;
@@ -212,11 +223,16 @@ int sm100_qkv_proj(const void* x, const void* w, int64_t M, int64_t K, int64_t N
   p.mtiles = (int)((M + proj::BM - 1) / proj::BM);
   p.ntiles = (int)((N + proj::BN - 1) / proj::BN);
   p.ep = ep;
-  static std::atomic<uint64_t> attr{0};
-  UL_TRY(smem_opt_in((const void*)proj::qkv_proj_kernel, proj::Smem::kBytes, attr));
+  static std::atomic<uint64_t> attr{0}, attr_t{0};
   const int tiles = p.mtiles * p.ntiles;
   const int grid = tiles < sm_count() ? tiles : sm_count();
-  proj::qkv_proj_kernel<<<grid, proj::kThreads, proj::Smem::kBytes, st>>>(mx, mw, p);
+  if (w_transposed) {
+    UL_TRY(smem_opt_in((const void*)proj::qkv_proj_kernel<true>, proj::Smem::kBytes, attr_t));
+    proj::qkv_proj_kernel<true><<<grid, proj::kThreads, proj::Smem::kBytes, st>>>(mx, mw, p);
+  } else {
+    UL_TRY(smem_opt_in((const void*)proj::qkv_proj_kernel<false>, proj::Smem::kBytes, attr));
+    proj::qkv_proj_kernel<false><<<grid, proj::kThreads, proj::Smem::kBytes, st>>>(mx, mw, p);
+  }
   return launched("qkv_proj_sm100");
 }
 

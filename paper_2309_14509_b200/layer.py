@@ -18,7 +18,9 @@ Mirrors the reference's layer (paths relative to /root/reference/pkg/src/seqlab)
 The attention core runs on this package's kernels and exchanges.  In bf16
 with hd = 128 the Q/K/V projection is this package's tcgen05 GEMM whose
 epilogue performs the seq->head exchange (csrc/proj_sm100.cu), and the layer
-is one autograd node; the O projection and the backward GEMMs are cuBLAS,
+is one autograd node; its backward's dc = g Wo^T is the same tcgen05 GEMM
+with the dO seq->head exchange in its epilogue (W read K-major); the
+remaining plain GEMMs (c Wo, dWo, dX, dW) are cuBLAS,
 and the row-wise pieces are torch ops -- off the hot path.  Weights are (d_in, d_out) like
 the reference's ``project``.
 """
@@ -87,14 +89,17 @@ class _UlyssesLayerFn(torch.autograd.Function):
         group, attn = ctx.group, ctx.attn
         nl, b, d, h, hkv = ctx.shape
         x2, wqkv, wo, q4, k4, v4, o4, lse, c2 = ctx.saved_tensors
-        g2 = gout.reshape(nl * b, d)
+        g2 = gout.reshape(nl * b, d).contiguous()
         dwo = c2.t() @ g2                                             # ulysses.py:206
-        dc = (g2 @ wo.t()).reshape(nl, b, h, d // h)                  # ulysses.py:207
+        # dc = g Wo^T (ulysses.py:207) as the tcgen05 GEMM whose epilogue
+        # stores each head block at its owner: the dctx seq->head flip
+        # (ulysses.py:213) fused into it, no dc round trip through HBM
+        (do4,) = group.proj_exchange(g2, wo.contiguous(), (h,), b, transposed=True, labels=("bwd.ctx.seq2head",),
+                                     label="bwd.ctx.seq2head")
         if group.world > 1:
-            (do4,) = group.all_to_all([dc], 2, 0, label="bwd.ctx.seq2head")
             dq, dk, dv = attn.backward_exchange(q4, k4, v4, o4, lse, do4, group, label="bwd.qkv.head2seq")
         else:
-            dq, dk, dv = attn.backward(q4, k4, v4, o4, lse, dc)
+            dq, dk, dv = attn.backward(q4, k4, v4, o4, lse, do4)
         dqkv = torch.cat([t.reshape(nl * b, -1) for t in (dq, dk, dv)], dim=1)
         dx = (dqkv @ wqkv.t()).reshape(nl, b, d)                      # ulysses.py:240
         dwqkv = x2.t() @ dqkv                                         # ulysses.py:234-238

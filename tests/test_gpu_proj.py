@@ -70,3 +70,26 @@ def test_layer_fused_path_is_taken_and_matches_unfused():
     bb = generic(x)
     err = float((a.float() - bb.float()).abs().max() / bb.float().abs().max())
     assert err <= 2e-2
+
+
+@pytest.mark.parametrize("p,nl,b,h", [(1, 200, 1, 3), (2, 128, 2, 4), (4, 64, 1, 8)])
+def test_transposed_projection_exchange_dc(p, nl, b, h):
+    # the backward's dc = g Wo^T (ulysses.py:207) with the dctx seq->head flip
+    # (ulysses.py:213) in the GEMM epilogue: W read K-major from its [N, d_in] rows
+    hd = 128
+    d = h * hd
+    n = nl * p
+    g = O.bf16_round(O.make_tensor((n, b, d), 43, 1))
+    wo = O.bf16_round(O.make_tensor((d, d), 43, 2) / np.sqrt(d))
+    groups = U().SequenceGroup.local_group(p, slot_bytes=1 << 20) if p > 1 else [U().SequenceGroup.single()]
+    warm_streams(groups)
+    wd = run_ranks(groups, lambda r: to_dev(wo, torch.bfloat16))
+    gs = run_ranks(groups, lambda r: to_dev(g[r * nl:(r + 1) * nl].reshape(nl * b, d), torch.bfloat16))
+    outs = run_ranks(groups, lambda r: groups[r].proj_exchange(gs[r], wd[r], (h,), b, transposed=True)[0])
+    seq = [O.matmul(g[r * nl:(r + 1) * nl].reshape(nl * b, d), wo.T, exact=False).reshape(nl, b, h, hd)
+           for r in range(p)]
+    heads = O.all_to_all(seq, 2, 0)
+    for r in range(p):
+        got, ref = to_np(outs[r]), heads[r]
+        assert got.shape == ref.shape
+        assert np.all(np.abs(got - ref) <= 2 * 2.0 ** -8 * np.abs(ref) + 1e-3 * np.abs(ref).max())
