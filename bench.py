@@ -568,12 +568,12 @@ def kernel_split(attn, q, k, v, do, args, dev):
     lse = torch.empty((b, h, n), dtype=torch.float32, device=dev)
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     wsb = int(lib.ul_attn_bwd_workspace_bytes(n, b, h, hkv, hd, 1))
-    ws = torch.zeros(wsb, dtype=torch.uint8, device=dev)   # left zero by every call: UL_ATTN_WS_ZEROED
+    ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
     sched = torch.zeros(2, dtype=torch.int32, device=dev)   # persistent-forward work counter (UL_ATTN_SCHED_BYTES)
     scale = 1.0 / math.sqrt(hd)
     fused = hd == 128 and not attn.deterministic
-    if fused:   # one kernel for dK, dV and dQ (incl. the dQ fp32 -> bf16 conversion)
-        names = ["attn_fwd_sm100", "attn_bwd_prep", "attn_bwd_fused_sm100"]
+    if fused:   # one kernel for dK, dV and dQ (+ the dQ fp32 -> bf16 pass)
+        names = ["attn_fwd_sm100", "attn_bwd_prep", "attn_bwd_fused_sm100", "attn_bwd_dq_convert"]
     else:
         names = ["attn_fwd_sm100", "attn_bwd_prep", "attn_bwd_dkdv_sm100", "attn_bwd_dq_sm100"]
     times = {nm: [] for nm in names}
@@ -594,7 +594,7 @@ def kernel_split(attn, q, k, v, do, args, dev):
             _lib.check(lib.ul_attn_bwd_stages(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                               do.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(),
                                               dv.data_ptr(), ws.data_ptr(), wsb, n, b, h, hkv, hd, 1, 1, scale,
-                                              stage, attn.flags | _lib.ATTN_WS_ZEROED, stream))
+                                              stage, attn.flags, stream))
 
     reps = max(3, min(args.steps, 10))
     for it in range(args.warmup + reps):

@@ -111,6 +111,12 @@ int ul_comm_status(ul_comm* comm, char* msg, size_t msg_len);
  * (CommLedger, simgroup.py:88-172). */
 int ul_comm_ledger(const ul_comm* comm, uint64_t* calls, uint64_t* egress_bytes,
                    uint64_t* aggregate_bytes);
+/* The same counts kept by the GPU: the signalling CTA of every call (the
+ * push kernel's last CTA, or the producing kernel's for fused exchanges)
+ * adds the call and its bytes to device counters in this rank's signal
+ * block.  A blocking read (call after the work has completed). */
+int ul_comm_ledger_device(const ul_comm* comm, uint64_t* calls, uint64_t* egress_bytes,
+                          uint64_t* aggregate_bytes);
 
 /* Fused all-to-all of n_tensors row-major tensors (each of rank `ndim`
  * <= 4, shape given per tensor in shapes[t*4 .. t*4+ndim)), identical
@@ -180,20 +186,11 @@ int ul_attn_fwd_blocked(const void* q, const void* k, const void* v, void* o, fl
  *      bits run to run);
  *   UL_ATTN_DETERMINISTIC: dK/dV kernel + a dQ kernel that recomputes S and
  *      dP, no atomics: bitwise reproducible (and bitwise P-invariant).
- *   UL_ATTN_WS_ZEROED: the first ul_attn_bwd_workspace_zero_bytes() bytes of
- *      `workspace` are zero (as every bf16 call leaves them: the fused
- *      kernel's dQ accumulator and sub-tile counters are cleared by the
- *      kernel itself), so the pre-pass does not clear them again -- for
- *      callers that keep one workspace per stream across calls.
  * hd 64 and fp32 always run the deterministic kernels. */
 #define UL_ATTN_DETERMINISTIC 1
-#define UL_ATTN_WS_ZEROED     2
 size_t ul_attn_bwd_workspace_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
                                    int dtype);
-/* Leading bytes of the workspace that must be zero on entry with
- * UL_ATTN_WS_ZEROED (and that every call leaves zero). */
-size_t ul_attn_bwd_workspace_zero_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd,
-                                        int dtype);
+
 int ul_attn_bwd(const void* q, const void* k, const void* v, const void* o,
                 const void* dout, const float* lse, void* dq, void* dk, void* dv,
                 void* workspace, size_t workspace_bytes,
@@ -202,8 +199,7 @@ int ul_attn_bwd(const void* q, const void* k, const void* v, const void* o,
 
 /* Same as ul_attn_bwd restricted to a subset of its launches (bit 0: D/LSE
  * pre-pass, bit 1: dK/dV kernel -- the fused dK/dV/dQ kernel in the default
- * hd-128 mode, which also converts dQ --, bit 2: dQ kernel -- nothing in
- * that mode),
+ * hd-128 mode --, bit 2: dQ kernel -- the dQ fp32->bf16 pass in that mode),
  * in that order; the stages must run in order over one workspace.  Lets
  * callers time or overlap the stages; ul_attn_bwd == stage_mask 7. */
 int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* o,
@@ -271,6 +267,26 @@ int ul_qkv_proj_exchange(ul_comm* comm, const void* x, const void* w, void* q4, 
 int ul_proj_exchange(ul_comm* comm, const void* x, const void* w, int w_transposed, int n_out,
                      void* const* outs, const int64_t* heads, int64_t nl, int64_t b, int64_t d_in,
                      int64_t hd, uint64_t label_hash, void* stream);
+
+/* ======================================================================
+ * The row-wise pieces of the transformer block around the attention
+ * (ulysses_block_forward ulysses.py:172-184), bf16 or
+ * fp32 rows of width d <= 4096, fp32 statistics:
+ *   ul_add_layernorm: s = x + r (r may be NULL: s = x; s_out may be NULL),
+ *     y = layernorm(s) * gain + bias (layers.py:106-110, population
+ *     variance, eps), stats[row] = {mean, rstd} (float2) for the backward;
+ *   ul_layernorm_bwd: dx, and dgain / dbias as deterministic column sums
+ *     (workspace >= ul_layernorm_bwd_workspace_bytes);
+ *   ul_gelu: exact erf GELU (layers.py:113-127); with dy != NULL the
+ *     backward dx = dy * gelu'(x).
+ * ==================================================================== */
+int ul_add_layernorm(const void* x, const void* r, const void* gain, const void* bias, void* s_out, void* y,
+                     float* stats, int64_t rows, int64_t d, float eps, int dtype, void* stream);
+size_t ul_layernorm_bwd_workspace_bytes(int64_t rows, int64_t d);
+int ul_layernorm_bwd(const void* dy, const void* s, const void* gain, const float* stats, void* dx, void* dgain,
+                     void* dbias, void* workspace, size_t workspace_bytes, int64_t rows, int64_t d, int dtype,
+                     void* stream);
+int ul_gelu(const void* x, const void* dy, void* out, int64_t n, int dtype, void* stream);
 
 /* Number of kernel launches the last ul_* call on this thread issued, and
  * the cumulative count since the library was loaded (all threads). */

@@ -29,17 +29,17 @@ IPC_HANDLE_BYTES = 128
 ABI_VERSION = 2
 ATTN_SCHED_BYTES = 8
 ATTN_DETERMINISTIC = 1
-ATTN_WS_ZEROED = 2
 
 # every symbol include/ulysses_b200.h declares (tests check the exports)
 EXPORTS = (
     "ul_abi_version", "ul_last_error", "ul_preload_kernels", "ul_comm_create", "ul_comm_export_handle",
     "ul_comm_open_peers", "ul_comm_validate_handles", "ul_comm_link_local", "ul_comm_destroy", "ul_comm_rank",
     "ul_comm_world", "ul_comm_slot_bytes", "ul_comm_set_timeout_ms", "ul_comm_status",
-    "ul_comm_ledger", "ul_all_to_all", "ul_all_to_all_head_group", "ul_all_to_all_slot_bytes", "ul_attn_fwd", "ul_attn_fwd_blocked", "ul_qkv_proj_exchange", "ul_proj_exchange", "ul_ring_shift", "ul_lse_merge",
-    "ul_attn_bwd_workspace_bytes", "ul_attn_bwd_workspace_zero_bytes", "ul_attn_bwd", "ul_attn_bwd_stages", "ul_attn_fwd_exchange",
+    "ul_comm_ledger", "ul_comm_ledger_device", "ul_all_to_all", "ul_all_to_all_head_group", "ul_all_to_all_slot_bytes", "ul_attn_fwd", "ul_attn_fwd_blocked", "ul_qkv_proj_exchange", "ul_proj_exchange", "ul_ring_shift", "ul_lse_merge",
+    "ul_attn_bwd_workspace_bytes", "ul_attn_bwd", "ul_attn_bwd_stages", "ul_attn_fwd_exchange",
     "ul_attn_bwd_exchange", "ul_last_launch_count",
-    "ul_total_launch_count", "ul_ulysses_volume",
+    "ul_total_launch_count", "ul_ulysses_volume", "ul_add_layernorm", "ul_layernorm_bwd_workspace_bytes",
+    "ul_layernorm_bwd", "ul_gelu",
 )
 
 _lib = None
@@ -68,6 +68,7 @@ def _declare(lib):
         "ul_comm_status": (ctypes.c_int, [c_vp, ctypes.c_char_p, ctypes.c_size_t]),
         "ul_comm_ledger": (ctypes.c_int, [c_vp, P(ctypes.c_uint64), P(ctypes.c_uint64),
                                           P(ctypes.c_uint64)]),
+        "ul_comm_ledger_device": (ctypes.c_int, [c_vp, P(ctypes.c_uint64), P(ctypes.c_uint64), P(ctypes.c_uint64)]),
         "ul_all_to_all": (ctypes.c_int, [c_vp, ctypes.c_int, P(c_vp), P(c_vp), P(c_i64), ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, c_vp]),
         "ul_all_to_all_head_group": (ctypes.c_int, [c_vp, ctypes.c_int, P(c_vp), P(c_vp), P(c_i64), ctypes.c_int,
@@ -87,7 +88,6 @@ def _declare(lib):
         "ul_attn_fwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64, c_i64,
                                        ctypes.c_int, ctypes.c_int, ctypes.c_float, c_vp, c_vp]),
         "ul_attn_bwd_workspace_bytes": (ctypes.c_size_t, [c_i64, c_i64, c_i64, c_i64, c_i64, ctypes.c_int]),
-        "ul_attn_bwd_workspace_zero_bytes": (ctypes.c_size_t, [c_i64, c_i64, c_i64, c_i64, c_i64, ctypes.c_int]),
         "ul_attn_bwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        ctypes.c_size_t, c_i64, c_i64, c_i64, c_i64, c_i64, ctypes.c_int,
                                        ctypes.c_int, ctypes.c_float, ctypes.c_int, c_vp]),
@@ -101,6 +101,12 @@ def _declare(lib):
                                                 ctypes.c_size_t, c_vp, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64,
                                                 c_i64, ctypes.c_int, ctypes.c_int, ctypes.c_float, ctypes.c_uint64,
                                                 ctypes.c_int, c_vp]),
+        "ul_add_layernorm": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, ctypes.c_float,
+                                            ctypes.c_int, c_vp]),
+        "ul_layernorm_bwd_workspace_bytes": (ctypes.c_size_t, [c_i64, c_i64]),
+        "ul_layernorm_bwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, c_i64,
+                                            c_i64, ctypes.c_int, c_vp]),
+        "ul_gelu": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i64, ctypes.c_int, c_vp]),
         "ul_last_launch_count": (ctypes.c_int, []),
         "ul_total_launch_count": (ctypes.c_uint64, []),
         "ul_ulysses_volume": (ctypes.c_int, [c_i64, c_i64, c_i64, c_i64, ctypes.c_int, P(c_i64), P(c_i64)]),

@@ -151,25 +151,10 @@ class FlashAttention:
             raise KernelError(f"block_size/pattern apply to the blocked kernel, not {mask!r}")
 
     def _workspace(self, t, n, b, hq, hkv, hd, dt):
-        """The backward workspace, kept per (device, stream) by this plugin.
-        Its leading ul_attn_bwd_workspace_zero_bytes are left zero by every
-        call (the fused kernel clears its dQ accumulator and counters), so
-        later calls pass UL_ATTN_WS_ZEROED and skip re-zeroing them.  Under
-        stream capture: a fresh workspace, zeroed by the call."""
-        L = _lib.lib()
-        need = max(int(L.ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dt)), 16)
-        zero = int(L.ul_attn_bwd_workspace_zero_bytes(n, b, hq, hkv, hd, dt))
-        if torch.cuda.is_current_stream_capturing():
-            return torch.empty(need, dtype=torch.uint8, device=t.device), 0
-        cache = self.__dict__.setdefault("_ws", {})
-        key = (t.device.index, torch.cuda.current_stream(t.device).stream_id)
-        ent = cache.get(key)
-        if ent is None or ent[0].numel() < need:
-            ent = [torch.zeros(need, dtype=torch.uint8, device=t.device), need]
-            cache[key] = ent
-        flag = _lib.ATTN_WS_ZEROED if zero <= ent[1] else 0
-        ent[1] = zero        # what the call leaves zero (its L2 / D rows follow)
-        return ent[0], flag
+        """The backward workspace (L2/D rows and, for the fused hd-128
+        kernel, its fp32 dQ accumulator), allocated on the calling stream."""
+        need = max(int(_lib.lib().ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dt)), 16)
+        return torch.empty(need, dtype=torch.uint8, device=t.device)
 
     @property
     def flags(self) -> int:
@@ -265,11 +250,11 @@ class FlashAttention:
         dk = torch.empty_like(k)
         dv = torch.empty_like(v)
         dt = _ATTN_DTYPES[q.dtype]
-        ws, wflag = self._workspace(q, n, b, hq, hkv, hd, dt)
+        ws = self._workspace(q, n, b, hq, hkv, hd, dt)
         _lib.check(_lib.lib().ul_attn_bwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(),
                                           do.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(),
                                           dv.data_ptr(), ws.data_ptr(), ws.numel(), n, b, hq, hkv, hd,
-                                          dt, self.mask_code, self._scale(hd), self.flags | wflag, _stream(q)))
+                                          dt, self.mask_code, self._scale(hd), self.flags, _stream(q)))
         return dq, dk, dv
 
     # -- fused head->seq exchange (K2 in the kernels' epilogues) ------------
@@ -315,14 +300,14 @@ class FlashAttention:
         sk = torch.empty((n // p, b, hkv * p, hd), dtype=q.dtype, device=q.device)
         sv = torch.empty_like(sk)
         dt = _ATTN_DTYPES[q.dtype]
-        ws, wflag = self._workspace(q, n, b, hq, hkv, hd, dt)
+        ws = self._workspace(q, n, b, hq, hkv, hd, dt)
         group.ensure_slot(slot_need(t.numel() * t.element_size() for t in (sq, sk, sv)))
         _lib.check(_lib.lib().ul_attn_bwd_exchange(group._handle, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                                    o.data_ptr(), do.data_ptr(), lse.data_ptr(), dq.data_ptr(),
                                                    dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), ws.numel(),
                                                    sq.data_ptr(), sk.data_ptr(), sv.data_ptr(), n, b, hq, hkv, hd,
                                                    dt, self.mask_code, self._scale(hd), label_hash(label),
-                                                   self.flags | wflag, _stream(q)))
+                                                   self.flags, _stream(q)))
         if ledger_scale:   # (a pipelined layer records its G group calls once, scaled by G)
             for name, t in (("bwd.q.head2seq", dq), ("bwd.k.head2seq", dk), ("bwd.v.head2seq", dv)):
                 group._record(name, t.numel() * ledger_scale)

@@ -189,7 +189,11 @@ class SequenceGroup:
         self.slot_bytes = slot_bytes
         self.stream = stream
         self._pg = pg
-        self._local = local                 # in-process group: every rank's SequenceGroup
+        # in-process group: weak references to every rank's SequenceGroup (no
+        # reference cycle: a group must be freed by refcount, deterministically
+        # -- a cyclic-GC collection that destroys a group (device sync) while
+        # another group's ranks are being issued would deadlock them)
+        self._local = local
         self._timeout_ms = None
         # second exchange channel of the same ranks (own workspace, epochs and
         # stream) for the pipelined layer's prefetch exchanges; see `channel`
@@ -264,12 +268,14 @@ class SequenceGroup:
 
     @classmethod
     def _make_local(cls, world, device, slot_bytes):
+        import weakref
         handles = cls._link_local(world, device, slot_bytes)
         sb = int(_lib.lib().ul_comm_slot_bytes(handles[0]))
-        local = []
-        local.extend(cls(r, world, device, handles[r], sb, stream=torch.cuda.Stream(device=device), local=local)
-                     for r in range(world))
-        return local
+        refs = []
+        groups = [cls(r, world, device, handles[r], sb, stream=torch.cuda.Stream(device=device), local=refs)
+                  for r in range(world)]
+        refs.extend(weakref.ref(g) for g in groups)
+        return groups
 
     @classmethod
     def _link_local(cls, world, device, slot_bytes):
@@ -317,12 +323,15 @@ class SequenceGroup:
         if self._local is not None:
             # in-process: this rank is the first of the group to reach the
             # call; the others have issued every earlier call already
+            peers = [ref() for ref in self._local]
+            if any(g is None for g in peers):
+                raise RuntimeError("in-process group: a rank's SequenceGroup was freed; cannot regrow")
             torch.cuda.synchronize(self.device)
-            for g in self._local:
+            for g in peers:
                 g.destroy(with_channel=False)
             handles = self._link_local(self.world, self.device, new)
             sb = int(_lib.lib().ul_comm_slot_bytes(handles[0]))
-            for g, h in zip(self._local, handles):
+            for g, h in zip(peers, handles):
                 g._handle, g.slot_bytes = h, sb
                 if g._timeout_ms:
                     g.set_timeout_ms(g._timeout_ms)
@@ -367,6 +376,16 @@ class SequenceGroup:
             return {"calls": 0, "egress_bytes": 0, "aggregate_bytes": 0}
         c, e, a = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
         _lib.check(_lib.lib().ul_comm_ledger(self._handle, ctypes.byref(c), ctypes.byref(e), ctypes.byref(a)))
+        return {"calls": c.value, "egress_bytes": e.value, "aggregate_bytes": a.value}
+
+    def device_ledger(self) -> dict:
+        """The byte ledger the GPU kept itself: every call's signalling CTA
+        (push kernel or fused epilogue) adds the call and its bytes to this
+        rank's device counters (ul_comm_ledger_device).  Read after a sync."""
+        if self._handle is None:
+            return {"calls": 0, "egress_bytes": 0, "aggregate_bytes": 0}
+        c, e, a = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+        _lib.check(_lib.lib().ul_comm_ledger_device(self._handle, ctypes.byref(c), ctypes.byref(e), ctypes.byref(a)))
         return {"calls": c.value, "egress_bytes": e.value, "aggregate_bytes": a.value}
 
     def _record(self, label: str, local_elements: int):

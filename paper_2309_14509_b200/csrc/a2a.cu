@@ -52,6 +52,8 @@ struct CopyParams {
   uint64_t epoch, sig;
   Signals* peer_sig[UL_MAX_RANKS];
   unsigned int* counter;    // local, reset by the last CTA
+  unsigned long long* ledger;   // this rank's device ledger (or nullptr)
+  uint64_t egress, aggregate;   // bytes of the call, added by the last CTA
 };
 
 }  // namespace ul
@@ -189,6 +191,11 @@ __global__ void __launch_bounds__(256) a2a_copy_kernel(const __grid_constant__ C
     unsigned int ticket = atomicAdd(p.counter, 1u);
     if (ticket == total - 1) {
       *p.counter = 0;  // every CTA has arrived; safe to rearm for the next call
+      if (p.ledger) {
+        atomicAdd(p.ledger, 1ull);
+        atomicAdd(p.ledger + 1, (unsigned long long)p.egress);
+        atomicAdd(p.ledger + 2, (unsigned long long)p.aggregate);
+      }
       __threadfence_system();
       for (int i = 0; i < p.world; ++i) {
         if (i == p.rank) continue;
@@ -546,6 +553,17 @@ int ul_comm_ledger(const ul_comm* c, uint64_t* calls, uint64_t* egress, uint64_t
   return UL_OK;
 }
 
+int ul_comm_ledger_device(const ul_comm* c, uint64_t* calls, uint64_t* egress, uint64_t* aggregate) {
+  if (!c) return fail(UL_ERR_ARG, "ul_comm_ledger_device: NULL comm");
+  unsigned long long v[3] = {0, 0, 0};
+  UL_CUDA(cudaSetDevice(c->device));
+  UL_CUDA(cudaMemcpy(v, ((Signals*)(c->base + 2 * c->slot_bytes))->ledger, sizeof(v), cudaMemcpyDeviceToHost));
+  if (calls) *calls = v[0];
+  if (egress) *egress = v[1];
+  if (aggregate) *aggregate = v[2];
+  return UL_OK;
+}
+
 size_t ul_all_to_all_slot_bytes(int n, const int64_t* shapes, int ndim, int dtype, int split,
                                 int concat, int world) {
   size_t tot = 0;
@@ -569,7 +587,12 @@ struct CallPlan {
   Geom g[UL_MAX_FUSED];
   size_t slot_off[UL_MAX_FUSED];
   uint64_t sig = 0, epoch = 0;
+  uint64_t egress = 0, aggregate = 0;   // this rank's bytes (simgroup.py:329-332 metering)
 };
+
+static unsigned long long* dev_ledger(ul_comm* c) {
+  return c ? ((Signals*)(c->base + 2 * c->slot_bytes))->ledger : nullptr;
+}
 
 static int plan_call(ul_comm* c, int n, void* const* out, const int64_t* shapes, int ndim, int dtype, int split,
                      int concat, uint64_t label, CallPlan* pl) {
@@ -618,6 +641,8 @@ static int plan_call(ul_comm* c, int n, void* const* out, const int64_t* shapes,
     c->aggregate += (uint64_t)P * in_total;
     c->egress += in_total / P * (P - 1);
   }
+  pl->aggregate = (uint64_t)P * in_total;
+  pl->egress = in_total / P * (P - 1);
   return UL_OK;
 }
 
@@ -654,6 +679,9 @@ static int signal_only(ul_comm* c, const CallPlan& pl, cudaStream_t st) {
   cp.sig = pl.sig;
   for (int r = 0; r < pl.P; ++r) cp.peer_sig[r] = (Signals*)(c->peer_base[r] + 2 * c->slot_bytes);
   cp.counter = &((Signals*)(c->base + 2 * c->slot_bytes))->counter[pl.slot];
+  cp.ledger = dev_ledger(c);
+  cp.egress = pl.egress;
+  cp.aggregate = pl.aggregate;
   cp.box[0].rows = 0;
   cp.box[0].vec = 16;
   cp.nbox = 1;
@@ -683,6 +711,9 @@ int a2a_fused_begin(ul_comm* c, int n, void* const* seq_out, const int64_t* head
       if (c) e.sig[r] = (Signals*)(c->peer_base[r] + 2 * c->slot_bytes);
     }
     if (c) e.counter = &((Signals*)(c->base + 2 * c->slot_bytes))->counter[pl.slot];
+    e.ledger = dev_ledger(c);
+    e.egress = pl.egress;
+    e.aggregate = pl.aggregate;
   }
   *handle_slot = pl.slot;
   *handle_epoch = pl.epoch;
@@ -775,6 +806,9 @@ int ul_proj_exchange(ul_comm* c, const void* x, const void* w, int w_transposed,
   if (c) {
     for (int r = 0; r < pl.P; ++r) sg.sig[r] = (Signals*)(c->peer_base[r] + 2 * c->slot_bytes);
     sg.counter = &((Signals*)(c->base + 2 * c->slot_bytes))->counter[pl.slot];
+    sg.ledger = dev_ledger(c);
+    sg.egress = pl.egress;
+    sg.aggregate = pl.aggregate;
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (nl * b == 0) {
@@ -845,6 +879,9 @@ static int push_and_finish(ul_comm* c, const CallPlan& pl, const void* const* in
     cp.sig = pl.sig;
     for (int r = 0; r < P; ++r) cp.peer_sig[r] = (Signals*)(c->peer_base[r] + 2 * c->slot_bytes);
     cp.counter = &((Signals*)(c->base + 2 * c->slot_bytes))->counter[slot];
+    cp.ledger = dev_ledger(c);
+    cp.egress = pl.egress;
+    cp.aggregate = pl.aggregate;
     if (cp.nbox == 0) {  // nothing to move (empty tensors) -- still signal
       make_box(pl.g[0], me, me, P, (const char*)in[0], (char*)out[0], &cp.box[0]);
       cp.box[0].rows = 0;
@@ -973,6 +1010,9 @@ int ul_ring_shift(ul_comm* c, int n, const void* const* in, void* const* out, co
   cp.sig = sig;
   for (int r = 0; r < P; ++r) cp.peer_sig[r] = (Signals*)(c->peer_base[r] + 2 * c->slot_bytes);
   cp.counter = &((Signals*)(c->base + 2 * c->slot_bytes))->counter[slot];
+  cp.ledger = dev_ledger(c);
+  cp.egress = total * (uint64_t)steps;
+  cp.aggregate = (uint64_t)P * total;
   if (cp.nbox == 0) {
     flat_box((const char*)in[0], (char*)out[0], 0, &cp.box[0]);
     cp.nbox = 1;

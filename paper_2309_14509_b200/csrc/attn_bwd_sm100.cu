@@ -134,11 +134,6 @@ struct Params {
   // their destination rank's sequence layout; the dQ kernel (launched last)
   // publishes the call once all its CTAs and the dK/dV kernel are done
   PeerEpilogue ep_dq, ep_dk, ep_dv;
-  // fused kernel: per (head, 64-row query sub-tile) count of kv-tile CTAs
-  // whose dQ^T partials have been added; the last one converts the
-  // sub-tile's fp32 accumulator rows into bf16 dQ and zeroes them again
-  int* dq_cnt;
-  int nsub_pad;
 };
 
 // ---- pre-pass ----------------------------------------------------------------
@@ -146,7 +141,8 @@ template <int HD>
 __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                                        const __nv_bfloat16* __restrict__ dout,
                                                        const float* __restrict__ lse, float* __restrict__ L2,
-                                                       float* __restrict__ Dv, int n, int n_pad, int b, int hq) {
+                                                       float* __restrict__ Dv, int n, int n_pad, int b, int hq,
+                                                       float* __restrict__ dq_acc) {
   // HD/8 threads per row, rows in memory order ((i*b + bb)*hq + h): every
   // warp streams contiguous 16-byte chunks of O and dO
   constexpr int TPR = HD / 8;
@@ -176,6 +172,11 @@ __global__ void __launch_bounds__(256) bwd_prep_kernel(const __nv_bfloat16* __re
     if (sub == 0) {
       Dv[bh * n_pad + i] = s;
       L2[bh * n_pad + i] = lse[bh * n + i] * 1.4426950408889634f;
+    }
+    if (dq_acc) {   // fused backward: zero this row's slice of the fp32 dQ accumulator
+      float4* z = reinterpret_cast<float4*>(dq_acc + (bh * n_pad + i) * HD + sub * 8);
+      z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+      z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
   // rows n..n_pad of every head: masked-out padding (P = 0, D = 0)
@@ -920,10 +921,7 @@ __global__ void __launch_bounds__(kFuThreads, 1)
     const int grp = (int)(blockIdx.x / (ktiles * G)), rem = (int)(blockIdx.x % (ktiles * G));
     kt = rem / G;
     bg = grp * G + rem % G;
-    if (bg >= kheads) {   // partial last group (before any barrier or TMEM use)
-      if (p.ep_dq.active && threadIdx.x == 0) peer_signal_last_cta(p.ep_dq, gridDim.x);   // still counted
-      return;
-    }
+    if (bg >= kheads) return;   // partial last group (before any barrier or TMEM use)
   } else {
     kt = (int)(blockIdx.x / kheads);
     bg = (int)(blockIdx.x % kheads);
@@ -1073,8 +1071,6 @@ __global__ void __launch_bounds__(kFuThreads, 1)
     const int quarter = warp & 3;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const int d = quarter * 32 + lane;
-    const int dt = threadIdx.x - 64;   // 0..127 over the four drain warps (thread = hd column)
-    volatile int* s_last = reinterpret_cast<volatile int*>(tmem_slot + 1);
     int h = g * group, qi = i0;
     for (int it = 0; it < total; ++it) {
       const int b = it & 1;
@@ -1097,45 +1093,11 @@ __global__ void __launch_bounds__(kFuThreads, 1)
 #pragma unroll
       for (int c = 0; c < 64; ++c) red_add_f32(dst + c * HD, __uint_as_float(v[c]));
       if (lane == 0 && warp == 2) UL_EV(15, it);
-      // count this CTA's contribution to (h, qi); the last contributor turns
-      // the accumulated rows into bf16 dQ (and its fused head->seq copy) and
-      // zeroes them for the next call -- no separate conversion pass.
-      // (bar.sync orders the four warps' reductions before thread 0's
-      // gpu-scope fence + counter atomic: the release pattern of a
-      // cross-CTA semaphore)
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (dt == 0) {
-        __threadfence();
-        const int need = p.causal ? min(ktiles, (qi * BS + BS - 1) / BT + 1) : ktiles;
-        int* cnt = p.dq_cnt + ((int64_t)bb * p.hq + h) * p.nsub_pad + qi;
-        const int old = atomicAdd(cnt, 1);
-        *s_last = old == need - 1;
-        if (old == need - 1) *cnt = 0;
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (*s_last) {
-        __threadfence();
-        float* src = dq_acc + (((int64_t)bb * p.hq + h) * p.n_pad + (int64_t)qi * BS) * HD + dt;
-        const int rows = min(BS, p.n - qi * BS);
-#pragma unroll 4
-        for (int r = 0; r < BS; ++r) {
-          const float x = __ldcg(src + (int64_t)r * HD);
-          __stcg(src + (int64_t)r * HD, 0.f);
-          if (r < rows) {
-            const int qrow = qi * BS + r;
-            const __nv_bfloat16 y = __float2bfloat16_rn(x * p.scale);
-            p.dq[(((int64_t)qrow * p.b + bb) * p.hq + h) * HD + dt] = y;
-            if (p.ep_dq.active)
-              reinterpret_cast<__nv_bfloat16*>(peer_row_ptr(p.ep_dq, qrow, bb, p.b, h, HD, 2))[dt] = y;
-          }
-        }
-      }
       if (++qi == nsub) {
         qi = i0;
         ++h;
       }
     }
-    if (p.ep_dq.active) __threadfence_system();
   } else {
     const int quarter = warp & 3;
     const int part = (warp - 6) >> 2;        // which kFuCols-column part of the sub-tile
@@ -1273,9 +1235,6 @@ __global__ void __launch_bounds__(kFuThreads, 1)
     UL_CTA(3, globaltimer());
     UL_CTA(6, clock64());
   }
-  // the last CTA publishes the fused dQ/dK/dV head->seq exchange: every dK/dV
-  // row and every converted dQ sub-tile of the launch has been stored
-  if (p.ep_dq.active && threadIdx.x == 0) peer_signal_last_cta(p.ep_dq, gridDim.x);
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
@@ -1283,50 +1242,50 @@ __global__ void __launch_bounds__(kFuThreads, 1)
   }
 }
 
-static int64_t pad_n(int64_t n) { return (n + 127) / 128 * 128; }
-
-// Workspace (hd 128): [fp32 dQ accumulator rows*HD | per (head, 64-row
-// sub-tile) counters | L2 rows | D rows], rows = b*hq*npad; the first two
-// parts (`zero_bytes`) must be zero when the fused kernel starts and are
-// left zero by it (its last contributor per sub-tile zeroes them), so a
-// caller that keeps its workspace across calls passes UL_ATTN_WS_ZEROED and
-// the prep pass skips re-zeroing them.  hd 64: [L2 | D].
-struct WsLayout {
-  size_t acc, cnt, l2, dv, zero_bytes, total;
-};
-static WsLayout ws_layout(int64_t n, int64_t b, int64_t hq, int64_t hd) {
-  const size_t rows = (size_t)b * hq * pad_n(n);
-  WsLayout w;
-  const size_t acc_bytes = hd == 128 ? rows * hd * sizeof(float) : 0;
-  const size_t cnt_bytes = hd == 128 ? ((size_t)b * hq * (pad_n(n) / BS) * sizeof(int) + 255) / 256 * 256 : 0;
-  w.acc = 0;
-  w.cnt = acc_bytes;
-  w.zero_bytes = acc_bytes + cnt_bytes;
-  w.l2 = w.zero_bytes;
-  w.dv = w.l2 + rows * sizeof(float);
-  w.total = w.dv + rows * sizeof(float);
-  return w;
+// dQ = scale * acc in bf16 rows of the head layout (+ the fused head->seq
+// stores and, as the last launch of the backward, the exchange signal)
+template <int HD>
+__global__ void __launch_bounds__(256) bwd_dq_convert_kernel(const float* __restrict__ acc,
+                                                             __nv_bfloat16* __restrict__ dq, int n, int n_pad, int b,
+                                                             int hq, float scale, PeerEpilogue ep) {
+  constexpr int TPR = HD / 8;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r = tid / TPR;   // output row (i*b + bb)*hq + h
+  const int sub = (int)(tid % TPR);
+  if (r < (int64_t)n * b * hq) {
+    const int h = (int)(r % hq);
+    const int64_t ib = r / hq;
+    const int bb = (int)(ib % b), i = (int)(ib / b);
+    const float4* src = reinterpret_cast<const float4*>(acc + (((int64_t)bb * hq + h) * n_pad + i) * HD + sub * 8);
+    const float4 x = __ldg(src), y = __ldg(src + 1);
+    const uint4 o = make_uint4(pack_bf16(x.x * scale, x.y * scale), pack_bf16(x.z * scale, x.w * scale),
+                               pack_bf16(y.x * scale, y.y * scale), pack_bf16(y.z * scale, y.w * scale));
+    reinterpret_cast<uint4*>(dq + r * HD)[sub] = o;
+    if (ep.active) reinterpret_cast<uint4*>(peer_row_ptr(ep, i, bb, b, h, HD, 2))[sub] = o;
+  }
+  if (ep.active) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) peer_signal_last_cta(ep, gridDim.x);
+  }
 }
+
+static int64_t pad_n(int64_t n) { return (n + 127) / 128 * 128; }
 
 template <int HD>
 static int launch(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
                   void* dq, void* dk, void* dv, void* ws, int64_t n, int64_t b, int64_t hq, int64_t hkv, int causal,
-                  float scale, int stages, int deterministic, int ws_zeroed, const PeerEpilogue* eps,
-                  cudaStream_t st) {
+                  float scale, int stages, int deterministic, const PeerEpilogue* eps, cudaStream_t st) {
   const int64_t npad = pad_n(n);
-  const WsLayout wl = ws_layout(n, b, hq, HD);
-  char* wsb = reinterpret_cast<char*>(ws);
-  float* L2 = reinterpret_cast<float*>(wsb + wl.l2);
-  float* Dv = reinterpret_cast<float*>(wsb + wl.dv);
+  float* L2 = reinterpret_cast<float*>(ws);
+  float* Dv = L2 + b * hq * npad;
   const bool fused = HD == 128 && !deterministic;
-  float* dq_acc = fused ? reinterpret_cast<float*>(wsb + wl.acc) : nullptr;   // [b*hq][npad][HD] f32
-  int* dq_cnt = fused ? reinterpret_cast<int*>(wsb + wl.cnt) : nullptr;
+  float* dq_acc = fused ? Dv + b * hq * npad : nullptr;   // [b*hq][npad][HD] f32
   if (stages & 1) {
-    if (fused && !ws_zeroed) UL_CUDA(cudaMemsetAsync(wsb, 0, wl.zero_bytes, st));
     const int64_t threads = std::max<int64_t>(n * b * hq * (HD / 8), b * hq * (npad - n));
     const unsigned blocks = (unsigned)((threads + 255) / 256);
     bwd_prep_kernel<HD><<<blocks, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout, lse, L2, Dv,
-                                                (int)n, (int)npad, (int)b, (int)hq);
+                                                (int)n, (int)npad, (int)b, (int)hq, dq_acc);
     UL_TRY(launched("attn_bwd_prep"));
   }
   Params p;
@@ -1348,8 +1307,6 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
   p.dq = (__nv_bfloat16*)dq;
   p.dk = (__nv_bfloat16*)dk;
   p.dv = (__nv_bfloat16*)dv;
-  p.dq_cnt = dq_cnt;
-  p.nsub_pad = (int)(npad / BS);
   if (eps) {   // [dq, dk, dv]
     p.ep_dq = eps[0];
     p.ep_dk = eps[1];
@@ -1392,7 +1349,12 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
         bwd_fused_kernel<HD><<<grid, kFuThreads, FusedSmem<HD>::kBytes, st>>>(mq, mk, mv, mo, mdk, mdv, pf, dq_acc);
         UL_TRY(launched("attn_bwd_fused_sm100"));
       }
-      // (stage bit 2, the dQ conversion, happens inside the fused kernel)
+      if (stages & 4) {
+        const int64_t threads = n * b * hq * (HD / 8);
+        bwd_dq_convert_kernel<HD><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+            dq_acc, (__nv_bfloat16*)dq, (int)n, (int)npad, (int)b, (int)hq, scale, p.ep_dq);
+        UL_TRY(launched("attn_bwd_dq_convert"));
+      }
       return UL_OK;
     }
   }
@@ -1451,35 +1413,33 @@ int preload_bwd() {
   UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dq_kernel<64>));
   UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dq_kernel<128>));
   UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_fused_kernel<128>));
+  UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dq_convert_kernel<128>));
   return UL_OK;
 }
 
 
 size_t sm100_bwd_workspace(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd) {
   (void)hkv;
-  // L2 + D rows, and the fp32 dQ accumulator + counters of the fused hd-128
-  // kernel (sized whether or not deterministic mode is on, so a workspace
-  // stays valid across mode switches)
-  return bwd::ws_layout(n, b, hq, hd).total;
-}
-size_t sm100_bwd_workspace_zero(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd) {
-  (void)hkv;
-  return bwd::ws_layout(n, b, hq, hd).zero_bytes;
+  // L2 + D rows, and the fp32 dQ accumulator of the fused hd-128 kernel
+  // (sized whether or not deterministic mode is on, so a workspace stays valid
+  // across mode switches)
+  const size_t rows = (size_t)b * hq * bwd::pad_n(n);
+  return rows * 2 * sizeof(float) + (hd == 128 ? rows * hd * sizeof(float) : 0);
 }
 
 int sm100_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
               void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n, int64_t b, int64_t hq,
-              int64_t hkv, int64_t hd, int causal, float scale, int stages, int deterministic, int ws_zeroed,
-              cudaStream_t st, const PeerEpilogue* eps) {
+              int64_t hkv, int64_t hd, int causal, float scale, int stages, int deterministic, cudaStream_t st,
+              const PeerEpilogue* eps) {
   (void)ws_bytes;
   if (n > INT32_MAX / 2) return fail(UL_ERR_SHAPE, "attention: sequence too long (n=%lld)", (long long)n);
   switch (hd) {
     case 64:
       return bwd::launch<64>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, deterministic,
-                             ws_zeroed, eps, st);
+                             eps, st);
     case 128:
       return bwd::launch<128>(q, k, v, o, dout, lse, dq, dk, dv, ws, n, b, hq, hkv, causal, scale, stages, deterministic,
-                              ws_zeroed, eps, st);
+                              eps, st);
     default:
       return fail(UL_ERR_KERNEL, "bf16 attention supports head_dim 64 or 128, got %lld", (long long)hd);
   }

@@ -36,16 +36,16 @@ int sm100_fwd(const void* q, const void* k, const void* v, void* o, float* lse, 
               int64_t blk_words = 0, void* sched = nullptr);
 int sm100_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
               void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n, int64_t b, int64_t hq,
-              int64_t hkv, int64_t hd, int causal, float scale, int stages, int deterministic, int ws_zeroed,
-              cudaStream_t st, const PeerEpilogue* eps = nullptr);
+              int64_t hkv, int64_t hd, int causal, float scale, int stages, int deterministic, cudaStream_t st,
+              const PeerEpilogue* eps = nullptr);
 size_t sm100_bwd_workspace(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd);
-size_t sm100_bwd_workspace_zero(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd);
 int preload_a2a();
 int preload_simt();
 int preload_fwd();
 int preload_bwd();
 int preload_proj();
 int preload_merge();
+int preload_block();
 
 static int check_attn(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask) {
   if (mask != UL_MASK_NONE && mask != UL_MASK_CAUSAL)
@@ -81,6 +81,7 @@ int ul_preload_kernels(void) {
   UL_TRY(preload_fwd());
   UL_TRY(preload_proj());
   UL_TRY(preload_merge());
+  UL_TRY(preload_block());
 
   return preload_bwd();
 }
@@ -135,10 +136,6 @@ size_t ul_attn_bwd_workspace_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv
   return sm100_bwd_workspace(n, b, hq, hkv, hd);
 }
 
-size_t ul_attn_bwd_workspace_zero_bytes(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype) {
-  if (dtype == UL_DTYPE_F32) return 0;
-  return sm100_bwd_workspace_zero(n, b, hq, hkv, hd);
-}
 
 int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* o, const void* dout,
                        const float* lse, void* dq, void* dk, void* dv, void* ws, size_t ws_bytes, int64_t n,
@@ -152,8 +149,7 @@ int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* 
   if (!lse) return fail(UL_ERR_STATE, "backward needs the LSE saved by the forward pass");
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(UL_ERR_ARG, "scale must be finite and > 0");
   if (stages < 1 || stages > 7) return fail(UL_ERR_ARG, "stage mask must be in [1, 7], got %d", stages);
-  if (flags & ~(UL_ATTN_DETERMINISTIC | UL_ATTN_WS_ZEROED))
-    return fail(UL_ERR_ARG, "unknown backward flags 0x%x", flags);
+  if (flags & ~UL_ATTN_DETERMINISTIC) return fail(UL_ERR_ARG, "unknown backward flags 0x%x", flags);
   const size_t need = ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dtype);
   if (!ws || ws_bytes < need)
     return fail(UL_ERR_ARG, "ul_attn_bwd: workspace of %zu bytes < required %zu", ws_bytes, need);
@@ -165,7 +161,7 @@ int ul_attn_bwd_stages(const void* q, const void* k, const void* v, const void* 
                     (float*)dq, (float*)dk, (float*)dv, (float*)ws, n, b, hq, hkv, hd, causal, scale, st);
   }
   return sm100_bwd(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, causal, scale, stages,
-                   flags & UL_ATTN_DETERMINISTIC, (flags & UL_ATTN_WS_ZEROED) != 0, st);
+                   flags & UL_ATTN_DETERMINISTIC, st);
 }
 
 int ul_attn_bwd(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
@@ -234,8 +230,7 @@ int ul_attn_bwd_exchange(ul_comm* comm, const void* q, const void* k, const void
   if (!q || !k || !v || !o || !dout || !dq || !dk || !dv) return fail(UL_ERR_ARG, "ul_attn_bwd_exchange: NULL tensor");
   if (!lse) return fail(UL_ERR_STATE, "backward needs the LSE saved by the forward pass");
   if (!(scale > 0.f) || !std::isfinite(scale)) return fail(UL_ERR_ARG, "scale must be finite and > 0");
-  if (flags & ~(UL_ATTN_DETERMINISTIC | UL_ATTN_WS_ZEROED))
-    return fail(UL_ERR_ARG, "unknown backward flags 0x%x", flags);
+  if (flags & ~UL_ATTN_DETERMINISTIC) return fail(UL_ERR_ARG, "unknown backward flags 0x%x", flags);
   const size_t need = ul_attn_bwd_workspace_bytes(n, b, hq, hkv, hd, dtype);
   if (!ws || ws_bytes < need)
     return fail(UL_ERR_ARG, "ul_attn_bwd: workspace of %zu bytes < required %zu", ws_bytes, need);
@@ -246,7 +241,7 @@ int ul_attn_bwd_exchange(ul_comm* comm, const void* q, const void* k, const void
   UL_TRY(a2a_fused_begin(comm, 3, outs, shapes, dtype, label, eps, &slot, &epoch));
   if (n * b * hq > 0)
     UL_TRY(sm100_bwd(q, k, v, o, dout, lse, dq, dk, dv, ws, ws_bytes, n, b, hq, hkv, hd, mask == UL_MASK_CAUSAL,
-                     scale, 7, flags & UL_ATTN_DETERMINISTIC, (flags & UL_ATTN_WS_ZEROED) != 0, st, eps));
+                     scale, 7, flags & UL_ATTN_DETERMINISTIC, st, eps));
   return a2a_fused_finish(comm, 3, outs, shapes, dtype, label, slot, epoch, st);
 }
 

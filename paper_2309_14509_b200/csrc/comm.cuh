@@ -26,6 +26,10 @@ struct Signals {           // lives at base + 2*slot_bytes on every rank
   unsigned int counter[2];
   unsigned int pad[2];
   ErrWord err;              // device-side error accumulator (local use)
+  // device ledger (CommLedger, simgroup.py:145-172, counted on the GPU): the
+  // last CTA of every call's producing kernel adds 1 call, the call's
+  // per-rank egress bytes and its aggregate bytes
+  unsigned long long ledger[3];
 };
 
 // Fused head->seq epilogue: a kernel that produces head-layout rows
@@ -44,6 +48,8 @@ struct PeerEpilogue {
   int heads_seq;                // heads of the sequence-layout tensor (H)
   int head_offset;              // rank * H / P
   int active;                   // 0: plain kernel (P = 1 or unfused)
+  unsigned long long* ledger;   // this rank's device ledger (Signals::ledger) or nullptr
+  uint64_t egress, aggregate;   // the call's bytes, added once by the signalling CTA
 };
 
 // Fused seq->head epilogue of the Q/K/V projection GEMM (csrc/proj_sm100.cu):
@@ -79,6 +85,11 @@ __device__ __forceinline__ void peer_signal_last_cta(const PeerEpilogue& ep, uns
   const unsigned int ticket = atomicAdd(ep.counter, 1u);
   if (ticket == total_ctas - 1) {
     *ep.counter = 0;
+    if (ep.ledger) {
+      atomicAdd(ep.ledger, 1ull);
+      atomicAdd(ep.ledger + 1, (unsigned long long)ep.egress);
+      atomicAdd(ep.ledger + 2, (unsigned long long)ep.aggregate);
+    }
     __threadfence_system();
     for (int i = 0; i < ep.world; ++i) {
       if (i == ep.rank) continue;

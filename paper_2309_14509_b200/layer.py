@@ -140,6 +140,114 @@ class UlyssesAttention(torch.nn.Module):
         return (c.reshape(nl * b, d) @ self.wo).reshape(nl, b, d)        # ulysses.py:155
 
 
+# ---------------------------------------------------------------------------
+# the block's row-wise kernels (csrc/block.cu): fused residual + layernorm,
+# exact GELU -- forward and backward
+# ---------------------------------------------------------------------------
+
+_BLOCK_DTYPES = {torch.float32: _lib.DTYPE_F32, torch.bfloat16: _lib.DTYPE_BF16}
+
+
+def _st(t):
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _ln_forward(x, r, gain, bias, eps):
+    d = x.shape[-1]
+    rows = x.numel() // d
+    s = torch.empty_like(x) if r is not None else None
+    y = torch.empty_like(x)
+    stats = torch.empty((rows, 2), dtype=torch.float32, device=x.device)
+    _lib.check(_lib.lib().ul_add_layernorm(x.data_ptr(), r.data_ptr() if r is not None else None, gain.data_ptr(),
+                                           bias.data_ptr(), s.data_ptr() if s is not None else None, y.data_ptr(),
+                                           stats.data_ptr(), rows, d, eps, _BLOCK_DTYPES[x.dtype], _st(x)))
+    return s, y, stats
+
+
+def _ln_backward(dy, s, gain, stats):
+    d = s.shape[-1]
+    rows = s.numel() // d
+    dy = dy.contiguous()
+    dx = torch.empty_like(s)
+    dgain, dbias = torch.empty_like(gain), torch.empty_like(gain)
+    wsb = int(_lib.lib().ul_layernorm_bwd_workspace_bytes(rows, d))
+    ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=s.device)
+    _lib.check(_lib.lib().ul_layernorm_bwd(dy.data_ptr(), s.data_ptr(), gain.data_ptr(), stats.data_ptr(),
+                                           dx.data_ptr(), dgain.data_ptr(), dbias.data_ptr(), ws.data_ptr(),
+                                           ws.numel(), rows, d, _BLOCK_DTYPES[s.dtype], _st(s)))
+    return dx, dgain, dbias
+
+
+class _LayerNormFn(torch.autograd.Function):
+    """y = layernorm(x) * gain + bias (layers.py:106-110)."""
+
+    @staticmethod
+    def forward(ctx, x, gain, bias, eps):
+        x = x.contiguous()
+        _, y, stats = _ln_forward(x, None, gain, bias, eps)
+        ctx.save_for_backward(x, gain, stats)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        x, gain, stats = ctx.saved_tensors
+        dx, dgain, dbias = _ln_backward(dy, x, gain, stats)
+        return dx, dgain, dbias, None
+
+
+class _AddLayerNormFn(torch.autograd.Function):
+    """(s, y) = (x + r, layernorm(x + r) * gain + bias) in one pass: the
+    residual of ulysses.py:179 fused into the layernorm after it."""
+
+    @staticmethod
+    def forward(ctx, x, r, gain, bias, eps):
+        s, y, stats = _ln_forward(x.contiguous(), r.contiguous(), gain, bias, eps)
+        ctx.save_for_backward(s, gain, stats)
+        return s, y
+
+    @staticmethod
+    def backward(ctx, ds, dy):
+        s, gain, stats = ctx.saved_tensors
+        dx, dgain, dbias = _ln_backward(dy, s, gain, stats)
+        if ds is not None:
+            dx = dx + ds
+        return dx, dx, dgain, dbias, None
+
+
+class _GeluFn(torch.autograd.Function):
+    """Exact erf GELU (layers.py:113-127) on the GPU, forward and backward."""
+
+    @staticmethod
+    def forward(ctx, x):
+        x = x.contiguous()
+        y = torch.empty_like(x)
+        _lib.check(_lib.lib().ul_gelu(x.data_ptr(), None, y.data_ptr(), x.numel(), _BLOCK_DTYPES[x.dtype], _st(x)))
+        ctx.save_for_backward(x)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        (x,) = ctx.saved_tensors
+        dy = dy.contiguous()
+        dx = torch.empty_like(x)
+        _lib.check(_lib.lib().ul_gelu(x.data_ptr(), dy.data_ptr(), dx.data_ptr(), x.numel(), _BLOCK_DTYPES[x.dtype],
+                                      _st(x)))
+        return dx
+
+
+def layernorm(x, gain, bias, eps: float = LN_EPS):
+    return _LayerNormFn.apply(x, gain, bias, eps)
+
+
+def add_layernorm(x, r, gain, bias, eps: float = LN_EPS):
+    """(x + r, layernorm(x + r))."""
+    return _AddLayerNormFn.apply(x, r, gain, bias, eps)
+
+
+def gelu(x):
+    return _GeluFn.apply(x)
+
+
 class UlyssesBlock(torch.nn.Module):
     """Pre-LN transformer block on sequence shards (ulysses.py:172-184)."""
 
@@ -154,11 +262,12 @@ class UlyssesBlock(torch.nn.Module):
         self.ln2_gain, self.ln2_bias = _param(w["ln2_gain"], dtype, device), _param(w["ln2_bias"], dtype, device)
 
     def forward(self, x):
-        d = x.shape[-1]
-        t1 = F.layer_norm(x, (d,), self.ln1_gain, self.ln1_bias, eps=LN_EPS)    # layers.py:106-110
-        x1 = x + self.attn(t1)
-        t2 = F.layer_norm(x1, (d,), self.ln2_gain, self.ln2_bias, eps=LN_EPS)
-        return x1 + F.gelu(t2 @ self.w1, approximate="none") @ self.w2           # layers.py:113-127
+        # ulysses.py:172-184 on this package's kernels: LN (csrc/block.cu),
+        # the attention layer, residual + LN fused, GELU MLP (cuBLAS GEMMs
+        # around the GELU kernel), residual; only the attention communicates
+        t1 = layernorm(x, self.ln1_gain, self.ln1_bias)                           # layers.py:106-110
+        x1, t2 = add_layernorm(x, self.attn(t1), self.ln2_gain, self.ln2_bias)   # x1 = x + attn(t1)
+        return x1 + gelu(t2 @ self.w1) @ self.w2                                  # layers.py:113-127
 
 
 # ---------------------------------------------------------------------------

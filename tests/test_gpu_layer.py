@@ -112,3 +112,5 @@ def test_layer_ledger_law_and_device_bytes():
         nat = g.native_ledger()
         assert nat["egress_bytes"] == 2 * g.ledger.total_egress()     # bf16
         assert nat["aggregate_bytes"] == 2 * g.ledger.total_aggregate()
+        # counted on the device by each call's signalling CTA: the same bytes
+        assert g.device_ledger() == nat
