@@ -484,7 +484,7 @@ def run_ours(args):
     mk4 = lambda h: torch.randn((n_seq, 1, h, hd), generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
     kt = kernel_split(attn, mk4(H // P), mk4(HKV // P), mk4(HKV // P), mk4(H // P), args, dev)
     attn_only_ms = sum(x["ms"] for x in kt["kernels"])
-    a2a = bench_a2a(dev, n_seq, H, hd, P, group, HKV)
+    a2a = bench_a2a(dev, n_seq, H, hd, P, group, HKV, inproc=not args.quick)
     extras = {}
     if P == 1 and not args.quick:
         extras["blocked_sparse_fwd"] = bench_blocked(kt_inputs=(lambda: mk4(H), n_seq, H, hd), args=args, dev=dev)
@@ -698,7 +698,7 @@ def bench_blocked(kt_inputs, args, dev, bs=128, bandwidth=15):
             "tflops_visible": round(flops / (ms / 1e3) / 1e12, 1)}
 
 
-def bench_a2a(dev, n_seq, H, hd, P, group, HKV=None, reps=10):
+def bench_a2a(dev, n_seq, H, hd, P, group, HKV=None, reps=10, inproc=True):
     """All-to-all throughput of the fused Q/K/V seq->head exchange (K1).
 
     P > 1: this rank's real exchange over NVLink peer memory; GB/s = exact
@@ -722,8 +722,8 @@ def bench_a2a(dev, n_seq, H, hd, P, group, HKV=None, reps=10):
             read_flush(flush)
             torch.cuda.synchronize()
             ev = []
-            for _ in range(len(streams) - 1):   # keep the GPU busy while the host enqueues every rank
-                read_flush(flush)
+            for _ in range(len(streams)):   # keep the GPU busy while the host enqueues every rank
+                read_flush(flush)               # (the first event must not time the host's issue latency)
             for s in streams:
                 s.wait_stream(torch.cuda.current_stream(dev))
             for fn, s in zip(fn_list, streams):
@@ -796,7 +796,9 @@ def bench_a2a(dev, n_seq, H, hd, P, group, HKV=None, reps=10):
     b1 = 2 * 3 * n_seq * H * hd * 2
     out["p1_permute"] = {"ms": round(ms1, 4), "hbm_gbs": round(b1 / (ms1 / 1e3) / 1e9, 1)}
     P8 = 8
-    if H % P8 == 0 and n_seq % P8 == 0:
+    # (skipped by --quick: under ncu the serialised kernels would leave every
+    # rank's flag wait spinning until its timeout)
+    if inproc and H % P8 == 0 and n_seq % P8 == 0:
         groups = U.SequenceGroup.local_group(P8, device=dev.index)
         xl = [[t[r * (n_seq // P8):(r + 1) * (n_seq // P8)].contiguous() for t in xs] for r in range(P8)]
         torch.cuda.synchronize()

@@ -146,7 +146,7 @@ class FlashAttention:
                 raise KernelError("blocked kernel needs block_size and pattern")
             self.block_size = int(block_size)
             self.pattern = frozenset((int(a), int(b)) for a, b in pattern)
-            self._bits = {}
+            self._build_bits()
         elif block_size is not None or pattern is not None:
             raise KernelError(f"block_size/pattern apply to the blocked kernel, not {mask!r}")
 
@@ -168,12 +168,15 @@ class FlashAttention:
     def _pattern_bits(self, n: int, device) -> torch.Tensor:
         """Validate the pattern for sequence length n with blocked_kernel's
         rules and order (kernels.py:63-80) and return its device bitmap
-        (uint32 rows of ceil(nb/32) words, include/ulysses_b200.h).  One
-        device copy per (n, device, stream): the copy is stream-ordered on the
-        stream that reads it, so no other stream can see it unfinished."""
-        key = (n, str(device), torch.cuda.current_stream(device).stream_id)
-        if key in self._bits:
-            return self._bits[key]
+        (uint32 rows of ceil(nb/32) words, include/ulysses_b200.h).
+
+        A valid call has exactly nb = (largest block index + 1) blocks (every
+        index < nb, every query block present), so the bitmap depends on the
+        pattern alone: it is built at construction (``_device_bits``) and
+        copied to a device at most once, outside any call when the device is
+        current at construction.  No host allocation or copy happens while an
+        in-process group's ranks are being issued (a pinned allocation there
+        can serialize the device's streams behind a spinning flag wait)."""
         bs = self.block_size
         if bs < 1 or n % bs != 0:
             raise DivisibilityError(f"block_size {bs} does not divide sequence length {n}")
@@ -185,17 +188,33 @@ class FlashAttention:
         empty = [qb for qb in range(nb) if qb not in seen]
         if empty:
             raise DegenerateRowError(f"query block {empty[0]} has no visible key blocks (invalid sparse pattern)")
-        words = (nb + 31) // 32
-        bits = [0] * (nb * words)
+        assert nb == self._nb
+        return self._device_bits(device), self._words, self._host_bits
+
+    def _build_bits(self):
+        nb = 1 + max((max(a, b) for a, b in self.pattern), default=-1)
+        words = max(1, (nb + 31) // 32)
+        bits = [0] * (max(nb, 1) * words)
         for qb, kb in self.pattern:
-            bits[qb * words + kb // 32] |= 1 << (kb % 32)
-        host = torch.tensor(bits, dtype=torch.int64).to(torch.int32).pin_memory()   # (bit 31 wraps: same bits)
-        # stream-ordered, non-blocking: under an in-process group this rank's
-        # stream may still be waiting for its peers' pushes, and a blocking
-        # copy would stall the host thread that has yet to issue them
-        t = host.to(device, non_blocking=True)
-        self._bits[key] = (t, words, host)
-        return self._bits[key]
+            if qb >= 0 and kb >= 0:
+                bits[qb * words + kb // 32] |= 1 << (kb % 32)
+        self._nb, self._words = nb, words
+        self._host_bits = torch.tensor(bits, dtype=torch.int64).to(torch.int32)   # (bit 31 wraps: same bits)
+        self._bits = {}
+        if torch.cuda.is_available():
+            self._device_bits(torch.device("cuda", torch.cuda.current_device()))
+
+    def _device_bits(self, device) -> torch.Tensor:
+        device = torch.device(device)
+        t = self._bits.get(device.index)
+        if t is None:
+            # (a blocking copy from pageable memory, on a private stream)
+            side = torch.cuda.Stream(device=device)
+            with torch.cuda.stream(side):
+                t = self._host_bits.to(device)
+            side.synchronize()
+            self._bits[device.index] = t
+        return t
 
     def _check(self, q, k, v):
         if q.dim() != 4 or k.dim() != 4 or v.dim() != 4:

@@ -14,6 +14,7 @@ setup); the data path never calls NCCL.
 
 from __future__ import annotations
 
+import atexit
 import ctypes
 import struct
 from dataclasses import dataclass
@@ -176,6 +177,20 @@ def check_ledger(ledger, n: int, b: int, d: int, p: int, layers: int = 1, backwa
     return bool(measured == predicted and counts_ok and records_ok), int(measured), int(predicted)
 
 
+_GRAVEYARD = []   # workspaces of collected SequenceGroups, released at a safe point
+
+
+def reap_workspaces():
+    """Release the workspaces of garbage-collected groups (a device sync).
+    Called when a group is created and at exit -- points where no rank of an
+    in-process group is half issued."""
+    while _GRAVEYARD:
+        _lib.lib().ul_comm_destroy(_GRAVEYARD.pop())
+
+
+atexit.register(reap_workspaces)
+
+
 class SequenceGroup:
     """One rank of a P-way Ulysses sequence-parallel group."""
 
@@ -198,6 +213,9 @@ class SequenceGroup:
         # second exchange channel of the same ranks (own workspace, epochs and
         # stream) for the pipelined layer's prefetch exchanges; see `channel`
         self._channel = None
+        # in-process regrowth: workspaces this rank switched away from, and
+        # new generations prepared by a peer that this rank has not reached
+        self._retired, self._pending = [], []
         self.records: CommLedger = CommLedger()   # the logical ledger (elements, reference schema)
         self.ledger = self.records
 
@@ -221,6 +239,7 @@ class SequenceGroup:
         """Collective: every rank of ``pg`` (a torch.distributed group, any
         backend) allocates its workspace and maps every peer's over CUDA IPC."""
         import torch.distributed as dist
+        reap_workspaces()
         rank = dist.get_rank(pg)
         world = dist.get_world_size(pg)
         if device is None:
@@ -259,6 +278,7 @@ class SequenceGroup:
             device = torch.cuda.current_device()
         if world == 1:
             return [cls.single(device)]
+        reap_workspaces()
         local = cls._make_local(world, device, slot_bytes)
         chans = cls._make_local(world, device, CHANNEL_SLOT_BYTES)
         for g, c in zip(local, chans):
@@ -321,20 +341,7 @@ class SequenceGroup:
             return
         new = (int(need) + SLOT_GRANULE - 1) // SLOT_GRANULE * SLOT_GRANULE
         if self._local is not None:
-            # in-process: this rank is the first of the group to reach the
-            # call; the others have issued every earlier call already
-            peers = [ref() for ref in self._local]
-            if any(g is None for g in peers):
-                raise RuntimeError("in-process group: a rank's SequenceGroup was freed; cannot regrow")
-            torch.cuda.synchronize(self.device)
-            for g in peers:
-                g.destroy(with_channel=False)
-            handles = self._link_local(self.world, self.device, new)
-            sb = int(_lib.lib().ul_comm_slot_bytes(handles[0]))
-            for g, h in zip(peers, handles):
-                g._handle, g.slot_bytes = h, sb
-                if g._timeout_ms:
-                    g.set_timeout_ms(g._timeout_ms)
+            self._grow_local(need, new)
             return
         import torch.distributed as dist
         torch.cuda.synchronize(self.device)
@@ -346,7 +353,45 @@ class SequenceGroup:
             self.set_timeout_ms(self._timeout_ms)
         dist.barrier(group=self._pg)
 
+    def _grow_local(self, need: int, new: int):
+        """In-process regrowth without a device sync.  The host issues the
+        ranks of a local group one after the other, so when this rank reaches
+        the call, its peers may not have issued their earlier calls yet, and
+        this rank's own streams may hold flag waits that only those calls
+        satisfy: a synchronize here would deadlock them (and a swap of every
+        rank's handle now would move the peers' earlier calls onto the new
+        workspace).  Instead each regrowth creates one new generation of
+        linked workspaces; every rank switches to the next generation when
+        IT reaches a call that does not fit -- the same call on every rank,
+        since all ranks issue the same calls from the same slot size -- and
+        the replaced workspaces are released with the group (their last
+        calls may still be in flight)."""
+        while self._pending and need > self.slot_bytes:
+            self._switch(*self._pending.pop(0))
+        if need <= self.slot_bytes:
+            return
+        peers = [ref() for ref in self._local]
+        if any(g is None for g in peers):
+            raise RuntimeError("in-process group: a rank's SequenceGroup was freed; cannot regrow")
+        handles = self._link_local(self.world, self.device, new)
+        sb = int(_lib.lib().ul_comm_slot_bytes(handles[0]))
+        for g, h in zip(peers, handles):
+            if g is self:
+                self._switch(h, sb)
+            else:
+                g._pending.append((h, sb))
+
+    def _switch(self, handle, slot_bytes: int):
+        if self._handle is not None:
+            self._retired.append(self._handle)
+        self._handle, self.slot_bytes = handle, slot_bytes
+        if self._timeout_ms:
+            _lib.check(_lib.lib().ul_comm_set_timeout_ms(self._handle, int(self._timeout_ms)))
+
     def destroy(self, with_channel: bool = True):
+        for h in self._retired + [h for h, _ in self._pending]:
+            _lib.lib().ul_comm_destroy(h)
+        self._retired, self._pending = [], []
         if self._handle is not None:
             _lib.lib().ul_comm_destroy(self._handle)
             self._handle = None
@@ -354,8 +399,16 @@ class SequenceGroup:
             self._channel.destroy()
 
     def __del__(self):
+        # no CUDA call here: a collection can run while the ranks of another
+        # in-process group are being issued, and releasing a workspace
+        # (cudaFree) synchronizes the device -- which would wait on flag waits
+        # that only the not-yet-issued ranks satisfy.  The handles go to the
+        # graveyard, released at the next group creation or at exit.
         try:
-            self.destroy()
+            _GRAVEYARD.extend(self._retired + [h for h, _ in self._pending])
+            if self._handle is not None:
+                _GRAVEYARD.append(self._handle)
+            self._retired, self._pending, self._handle = [], [], None
         except Exception:
             pass
 
@@ -364,6 +417,8 @@ class SequenceGroup:
         """Raise GroupDesyncError if a device-side wait saw a signature
         mismatch or timed out (simgroup.py:265-298).  Errors are reported
         asynchronously, like NCCL's: poll after a synchronize."""
+        if self._channel is not None:
+            self._channel.check()
         if self._handle is None:
             return
         buf = ctypes.create_string_buffer(512)

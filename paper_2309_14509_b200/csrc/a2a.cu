@@ -23,6 +23,7 @@
 #include <cmath>
 
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "comm.cuh"
@@ -380,6 +381,44 @@ extern "C" {
 
 int ul_preload_kernels(void);
 
+// Mapped host error words come from one pinned pool, allocated at the first
+// group creation: cudaHostAlloc can serialize the device's streams, and an
+// in-process group creates workspaces (regrowth) while its ranks' flag waits
+// may be spinning on peers the host has yet to issue.
+namespace {
+constexpr int kErrPool = 4096;
+std::mutex g_err_mu;
+ul::ErrWord* g_err_host = nullptr;
+std::vector<int> g_err_free;
+}  // namespace
+
+static cudaError_t err_word_take(ul::ErrWord** host, ul::ErrWord** dev) {
+  std::lock_guard<std::mutex> lock(g_err_mu);
+  if (!g_err_host) {
+    cudaError_t e = cudaHostAlloc((void**)&g_err_host, kErrPool * sizeof(ul::ErrWord),
+                                  cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+      g_err_host = nullptr;
+      return e;
+    }
+    for (int i = kErrPool - 1; i >= 0; --i) g_err_free.push_back(i);
+  }
+  if (g_err_free.empty()) return cudaErrorMemoryAllocation;
+  const int i = g_err_free.back();
+  g_err_free.pop_back();
+  memset((void*)(g_err_host + i), 0, sizeof(ul::ErrWord));
+  *host = g_err_host + i;
+  // mapped pinned memory: the device address equals the host address under UVA
+  cudaError_t e = cudaHostGetDevicePointer((void**)dev, (void*)*host, 0);
+  if (e != cudaSuccess) g_err_free.push_back(i);
+  return e;
+}
+
+static void err_word_give(ul::ErrWord* host) {
+  std::lock_guard<std::mutex> lock(g_err_mu);
+  if (g_err_host && host >= g_err_host && host < g_err_host + kErrPool) g_err_free.push_back((int)(host - g_err_host));
+}
+
 int ul_comm_create(int rank, int world, int device, size_t slot_bytes, ul_comm** out) {
   if (!out) return fail(UL_ERR_ARG, "ul_comm_create: out is NULL");
   *out = nullptr;
@@ -399,13 +438,16 @@ int ul_comm_create(int rank, int world, int device, size_t slot_bytes, ul_comm**
     delete c;
     return fail(UL_ERR_CUDA, "ul_comm_create: cudaMalloc(%zu): %s", total, cudaGetErrorString(e));
   }
-  e = cudaMemset(c->base + 2 * c->slot_bytes, 0, sizeof(Signals));
-  if (e == cudaSuccess) e = cudaHostAlloc((void**)&c->err_host, sizeof(ErrWord), cudaHostAllocMapped);
-  if (e == cudaSuccess) {
-    memset((void*)c->err_host, 0, sizeof(ErrWord));
-    e = cudaHostGetDevicePointer((void**)&c->err_dev, (void*)c->err_host, 0);
-  }
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  // zero the signals on a private non-blocking stream and wait for that
+  // stream only: an in-process group creates workspaces (regrowth) while
+  // its ranks' streams may hold flag waits that the host has yet to satisfy,
+  // so neither a device sync nor the legacy default stream may be used here
+  cudaStream_t zs = nullptr;
+  e = cudaStreamCreateWithFlags(&zs, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->base + 2 * c->slot_bytes, 0, sizeof(Signals), zs);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(zs);
+  if (zs) cudaStreamDestroy(zs);
+  if (e == cudaSuccess) e = err_word_take(&c->err_host, &c->err_dev);
   if (e != cudaSuccess) {
     cudaFree(c->base);
     delete c;
@@ -499,7 +541,7 @@ int ul_comm_destroy(ul_comm* c) {
   for (int r = 0; r < c->world; ++r)
     if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->peer_base[r]);
   cudaFree(c->base);
-  if (c->err_host) cudaFreeHost((void*)c->err_host);
+  if (c->err_host) err_word_give(c->err_host);
   delete c;
   return UL_OK;
 }

@@ -36,12 +36,12 @@ def child(n, H, hd, reps):
     def run(stage):
         if stage == 0:
             _lib.check(lib.ul_attn_fwd(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), lse.data_ptr(),
-                                       n, 1, H, H, hd, 1, 1, scale, st))
+                                       n, 1, H, H, hd, 1, 1, scale, None, st))
         else:
             _lib.check(lib.ul_attn_bwd_stages(q.data_ptr(), k.data_ptr(), v.data_ptr(), o.data_ptr(), do.data_ptr(),
                                               lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
-                                              ws.data_ptr(), wsb, n, 1, H, H, hd, 1, 1, scale, stage, st))
-    lib.ul_attn_set_deterministic(int(os.environ.get("AB_DET", "0")))
+                                              ws.data_ptr(), wsb, n, 1, H, H, hd, 1, 1, scale, stage,
+                                              int(os.environ.get("AB_DET", "0")), st))
     names = {0: "fwd", 1: "prep", 2: "dkdv", 4: "dq"}
     t = {s: [] for s in names}
     for it in range(3 + reps):

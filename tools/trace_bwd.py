@@ -26,7 +26,6 @@ from paper_2309_14509_b200 import _lib  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 lib = ctypes.CDLL(os.path.join(ROOT, os.environ.get("TRACE_LIB", "ab_libs/trace/libulysses_b200.so")))
 _lib._declare(lib)
-lib.ul_attn_set_deterministic.argtypes = [ctypes.c_int]
 lib.ul_debug_trace.restype = ctypes.c_int
 lib.ul_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 
@@ -51,14 +50,15 @@ def chk(rc):
         raise RuntimeError(lib.ul_last_error().decode())
 
 
-chk(lib.ul_attn_fwd(P(q), P(k), P(v), P(o), P(lse), n, 1, H, H, hd, 1, 1, ctypes.c_float(scale), st))
+chk(lib.ul_attn_fwd(P(q), P(k), P(v), P(o), P(lse), n, 1, H, H, hd, 1, 1, ctypes.c_float(scale), None, st))
+FLAGS = 0   # per-call backward flags (UL_ATTN_DETERMINISTIC = 1)
 wsb = lib.ul_attn_bwd_workspace_bytes(n, 1, H, H, hd, 1)
 ws = torch.empty(wsb, device=dev, dtype=torch.uint8)
 
 
 def run(stages):
     chk(lib.ul_attn_bwd_stages(P(q), P(k), P(v), P(o), P(do), P(lse), P(dq), P(dk), P(dv), P(ws), ctypes.c_size_t(wsb),
-                               n, 1, H, H, hd, 1, 1, ctypes.c_float(scale), stages, st))
+                               n, 1, H, H, hd, 1, 1, ctypes.c_float(scale), stages, FLAGS, st))
     torch.cuda.synchronize()
     buf = np.zeros(8 * 16 * 256, dtype=np.uint64)
     chk(lib.ul_debug_trace(buf.ctypes.data, buf.nbytes))
@@ -131,7 +131,7 @@ def timeline_fused(tr, j0=60, span=3):
             print(f"  {t:6d}  {nm}")
 
 
-lib.ul_attn_set_deterministic(0)
+FLAGS = 0
 run(1 | 2)
 tr = run(1 | 2)
 report_fused(tr)
@@ -146,7 +146,7 @@ for j in (59, 60, 61):
     print(f"  arrivals [{j}] (rel. MMA top 60): p_full " +
           " ".join(f"w{x}:{w[x][j] - ref}" for x in range(6, 22)) + "  dq_free " +
           " ".join(f"w{x}:{w[x][j] - ref}" for x in range(2, 6)))
-lib.ul_attn_set_deterministic(1)
+FLAGS = 1
 for stages, name in ((1 | 2, "dkdv"), (4, "dq")):
     run(stages)  # warm
     report(name, run(stages))
@@ -216,6 +216,6 @@ if os.environ.get("CTA"):
 
 
 if os.environ.get("CTA_FUSED"):
-    lib.ul_attn_set_deterministic(0)
+    FLAGS = 0
     run(1 | 2)
     cta_report("fused")

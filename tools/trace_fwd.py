@@ -40,6 +40,7 @@ q, k, v = mk(), mk(), mk()
 o = torch.empty_like(q)
 lse = torch.empty((1, H, n), device=dev, dtype=torch.float32)
 st = torch.cuda.current_stream().cuda_stream
+sched = torch.zeros(4, dtype=torch.int32, device=dev)   # persistent-forward work counter
 P = lambda t: ctypes.c_void_p(t.data_ptr())
 
 
@@ -49,7 +50,8 @@ def chk(rc):
 
 
 def run():
-    chk(lib.ul_attn_fwd(P(q), P(k), P(v), P(o), P(lse), n, 1, H, H, hd, 1, 1, ctypes.c_float(hd ** -0.5), st))
+    chk(lib.ul_attn_fwd(P(q), P(k), P(v), P(o), P(lse), n, 1, H, H, hd, 1, 1, ctypes.c_float(hd ** -0.5),
+                        P(sched) if os.environ.get("PERSIST", "1") == "1" else None, st))
     torch.cuda.synchronize()
 
 
