@@ -383,11 +383,36 @@ def get_kernel(name: str, **mask_args):
 # DistributedAttention
 # ---------------------------------------------------------------------------
 
+def _bytes(shape, dtype) -> int:
+    n = 1
+    for x in shape:
+        n *= int(x)
+    return n * torch.empty((), dtype=dtype).element_size()
+
+
+def _presize(group: SequenceGroup, main_need: int, chan_need: int = 0):
+    """Size the receive slots of every exchange a layer call will issue
+    BEFORE issuing the first one: a regrowth then never happens while this
+    rank already has flag waits queued (for an in-process group those waits
+    can only be satisfied by peers the host has not issued yet, and the
+    workspace allocation of a regrowth may serialize the device behind them)."""
+    group.ensure_slot(main_need)
+    if chan_need:
+        group.channel.ensure_slot(chan_need)
+
+
 class _UlyssesAttnFn(torch.autograd.Function):
     """Whole-layer node: fused QKV seq->head, local attention, O head->seq."""
 
     @staticmethod
     def forward(ctx, group, attn, scatter_idx, gather_idx, q, k, v):
+        if group.world > 1 and (scatter_idx, gather_idx) == (2, 0):
+            p = group.world
+            nl, b, hq, hd = q.shape
+            hkv = k.shape[2]
+            _presize(group, max(slot_need([_bytes((nl * p, b, hq // p, hd), q.dtype)] +
+                                          [_bytes((nl * p, b, hkv // p, hd), q.dtype)] * 2),
+                                slot_need([_bytes(q.shape, q.dtype)])))
         if group.world > 1:
             q4, k4, v4 = group.all_to_all([q, k, v], scatter_idx, gather_idx, label="attn.qkv.seq2head",
                                           labels=["attn.q.seq2head", "attn.k.seq2head", "attn.v.seq2head"])
@@ -409,6 +434,9 @@ class _UlyssesAttnFn(torch.autograd.Function):
         scatter_idx, gather_idx = ctx.idx
         q4, k4, v4, o4, lse = ctx.saved_tensors
         do = do.contiguous()
+        if group.world > 1 and (scatter_idx, gather_idx) == (2, 0):
+            _presize(group, max(slot_need([_bytes(q4.shape, q4.dtype)]),
+                                slot_need([_bytes(q4.shape, q4.dtype)] + [_bytes(k4.shape, k4.dtype)] * 2)))
         if group.world > 1:
             (do4,) = group.all_to_all([do], scatter_idx, gather_idx, label="bwd.ctx.seq2head")
         else:
@@ -447,6 +475,11 @@ class _UlyssesAttnPipeFn(torch.autograd.Function):
         main = torch.cuda.current_stream(q.device)
         cs = chan.stream
         q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+        nl, b, hq, hd = q.shape
+        hkv = k.shape[2]
+        hg, hkg = hq // (p * G), hkv // (p * G)
+        _presize(group, slot_need([_bytes((nl, b, p * hg, hd), q.dtype)]),
+                 slot_need([_bytes((nl * p, b, hg, hd), q.dtype)] + [_bytes((nl * p, b, hkg, hd), q.dtype)] * 2))
         cs.wait_stream(main)
         heads, evs = [], []
         with torch.cuda.stream(cs):
@@ -482,6 +515,11 @@ class _UlyssesAttnPipeFn(torch.autograd.Function):
         cs = chan.stream
         saved = ctx.saved_tensors
         do = do.contiguous()
+        nl, b, hq, hd = do.shape
+        hkv = saved[1].shape[2] * p * G
+        hg, hkg = hq // (p * G), hkv // (p * G)
+        _presize(group, slot_need([_bytes((nl, b, p * hg, hd), do.dtype)] + [_bytes((nl, b, p * hkg, hd), do.dtype)] * 2),
+                 slot_need([_bytes((nl * p, b, hg, hd), do.dtype)]))
         cs.wait_stream(main)
         dos, evs = [], []
         with torch.cuda.stream(cs):

@@ -869,6 +869,383 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Half-unit forward (default for hd 128, dense / causal): the persistent
+// kernel above with every 128-column K/V tile processed as two 64-column
+// units, each query tile's S region split into two 64-column buffers.
+//
+// Why: in the kernel above S_t(j+1) overwrites the TMEM columns PV_t(j) reads
+// P_t(j) from, so each query tile runs the serial chain softmax(j) -> PV(j)
+// -> S(j+1) -> softmax(j+1) and the tensor pipe idles whenever a softmax
+// takes longer than the other tile's two GEMMs (ncu: tensor pipe 53% active).
+// Here unit u lives in buffer u & 1: S_t(u + 1) is computed while
+// softmax_t(u) runs, and only S_t(u + 2) waits for PV_t(u).  Per 128 kv
+// columns the pipe then runs 2 x (2 PV + 2 S) with no chain bubble; the
+// N = 64 S MMAs read 6 KB of shared memory per 32-cycle K-step (2/3 rate) --
+// ~2560 instead of 2048 tensor cycles, against ~3900 measured for the chain.
+//   MMA order per unit u:  PV_A(u), S_A(u + 2), PV_B(u), S_B(u + 2).
+//   TMEM: tile t: S buffers t*128 + {0, 64} (P packed over the consumed S),
+//         O_t at 256 + t*128.
+//   Softmax: 8 warps per tile, two per TMEM lane quarter, each owning 32 of
+//   the unit's 64 columns (row max combined through shared memory); O is
+//   rescaled lazily (after PV_t(u - 1), which then has to be complete).
+constexpr int kUN = 64;   // kv columns per unit
+
+template <int HD>
+struct SmemH2 {
+  static constexpr int kTile = (HD / 64) * kAtom;
+  static constexpr int kQ = 0;                    // [2] (tile A, tile B)
+  static constexpr int kK = kQ + 2 * kTile;       // [NS]
+  static constexpr int kV = kK + NS * kTile;      // [NS]
+  static constexpr int kBar = kV + NS * kTile;    // 512 B of barriers
+  static constexpr int kX = kBar + 512;           // row max / sum exchange [3][2 tiles][128][2]
+  static constexpr int kBytes = kX + 3 * 2 * 128 * 2 * 4 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_h2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                       const __grid_constant__ CUtensorMap tmV, const Params p) {
+  static_assert(HD == 128, "half-unit forward: TMEM holds 2 x (2 x 64 S + HD O) columns");
+  using S = SmemH2<HD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + S::kQ;
+  uint8_t* sK = smem + S::kK;
+  uint8_t* sV = smem + S::kV;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::kBar);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;              // [NS]
+  uint64_t* k_empty = bars + 2 + NS;        // [NS]
+  uint64_t* v_full = bars + 2 + 2 * NS;     // [NS]
+  uint64_t* v_empty = bars + 2 + 3 * NS;    // [NS]
+  uint64_t* s_full = bars + 2 + 4 * NS;     // [tile][buffer]
+  uint64_t* p_full = bars + 6 + 4 * NS;     // [tile][buffer]
+  uint64_t* o_done = bars + 10 + 4 * NS;    // [tile]: one phase per PV
+  uint64_t* o_free = bars + 12 + 4 * NS;    // [tile]: O read out by the epilogue
+  uint64_t* it_full = bars + 14 + 4 * NS;   // [4] dynamic item ring
+  uint64_t* it_empty = bars + 18 + 4 * NS;  // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22 + 4 * NS);
+  volatile int* sitem = reinterpret_cast<volatile int*>(bars + 23 + 4 * NS);
+  static_assert((25 + 4 * NS) * 8 <= 512, "barrier area");
+  auto item = [&](int k, int& pair, int& bh, int role) {
+    return p.ctr ? fwd_item_dyn<HD>(p, k, pair, bh, role, it_full, it_empty, sitem) : fwd_item<HD>(p, k, pair, bh);
+  };
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nkv_all = (p.n + BN - 1) / BN;
+  auto item_kv = [&](int pair, int t) {
+    const int qt = 2 * pair + t;
+    return qt >= p.qtiles ? 0 : (p.causal ? min(nkv_all, (qt * BM + BM - 1) / BN + 1) : nkv_all);
+  };
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], kSoftPerTile);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&o_done[t], 1);
+      mbar_init(&o_free[t], kSoftPerTile);
+    }
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&it_full[s], 1);
+      mbar_init(&it_empty[s], 1 + 2 * kSoftPerTile);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    UL_CTA(0, globaltimer());
+    UL_CTA(1, globaltimer());
+    UL_CTA(4, smid());
+    UL_CTA(5, clock64());
+  }
+  tc_fence_after();
+  if (*tmem_slot != 0u) __trap();
+  constexpr uint32_t tbase = 0;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (128-row K / V tiles, as above) ----------------
+    if (lane == 0) {
+      tma_prefetch_desc(&tmQ);
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      int pair, bh, gk = 0;
+      for (int k = 0; item(k, pair, bh, 0); ++k) {
+        const int bb = bh / p.hq, h = bh % p.hq, g = h / (p.hq / p.hkv);
+        const int n0 = item_kv(pair, 0), n1 = item_kv(pair, 1);
+        const int nkv = max(n0, n1), ntiles = n1 > 0 ? 2 : 1;
+        if (k > 0) mbar_wait(q_empty, (k - 1) & 1);
+        mbar_expect_tx(q_full, ntiles * BM * HD * 2);
+        for (int t = 0; t < ntiles; ++t)
+#pragma unroll
+          for (int a = 0; a < HD / 64; ++a)
+            tma_load_3d(sQ + t * S::kTile + a * kAtom, &tmQ, q_full, a * 64, bb * p.hq + h, (2 * pair + t) * BM);
+        for (int j = 0; j < nkv; ++j, ++gk) {
+          const int s = gk % NS;
+          const uint32_t ph = (gk / NS) & 1;
+          mbar_wait_prod(&k_empty[s], ph ^ 1);
+          UL_EV(8, gk);
+          mbar_expect_tx(&k_full[s], BN * HD * 2);
+#pragma unroll
+          for (int a = 0; a < HD / 64; ++a)
+            tma_load_3d(sK + s * S::kTile + a * kAtom, &tmK, &k_full[s], a * 64, bb * p.hkv + g, j * BN);
+          mbar_wait_prod(&v_empty[s], ph ^ 1);
+          UL_EV(9, gk);
+          mbar_expect_tx(&v_full[s], BN * HD * 2);
+#pragma unroll
+          for (int a = 0; a < HD / 64; ++a)
+            tma_load_3d(sV + s * S::kTile + a * kAtom, &tmV, &v_full[s], a * 64, bb * p.hkv + g, j * BN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (elect_one()) {
+      constexpr uint32_t kIdQK = idesc_bf16(BM, kUN, 0, 0);   // S unit: M = 128 q rows, N = 64 kv
+      constexpr uint32_t kIdPV = idesc_bf16(BM, HD, 0, 1);    // O += P V: K = 64 kv per unit
+      const uint64_t dQ0 = sdesc(smem_u32(sQ), 16, 1024);
+      const uint64_t dK0 = sdesc(smem_u32(sK), 16, 1024);
+      const uint64_t dV0 = sdesc(smem_u32(sV), kAtom, 1024);
+      int cp[4] = {0, 0, 0, 0};   // p_full waits per (tile, buffer)
+      int items_t[2] = {0, 0};    // items in which the tile existed so far
+      // S_t(unit) from K rows (unit & 1) * 64 of stage `stage`
+      auto issue_s = [&](int t, int unit, int stage) {
+        const int bf = unit & 1;
+        const uint64_t dk = dadd(dK0, stage * S::kTile + bf * (kUN * 128));
+        const uint64_t dq = dadd(dQ0, t * S::kTile);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
+          mma_ss(tbase + t * 128 + bf * kUN, dadd(dq, off), dadd(dk, off), kIdQK, kk > 0 ? 1u : 0u);
+        }
+        mma_commit(&s_full[t * 2 + bf]);
+      };
+      // O_t += P_t(unit) V rows (unit & 1) * 64 of stage `stage`
+      auto issue_pv = [&](int t, int unit, int stage) {
+        const int bf = unit & 1;
+        if (unit == 0 && items_t[t] > 0) mbar_wait_mma(&o_free[t], (items_t[t] - 1) & 1);
+        mbar_wait_mma(&p_full[t * 2 + bf], cp[t * 2 + bf] & 1);
+        ++cp[t * 2 + bf];
+        tc_fence_after();
+        const uint64_t dv = dadd(dV0, stage * S::kTile + bf * (kUN * 128));
+#pragma unroll
+        for (int kk = 0; kk < kUN / 16; ++kk)
+          mma_ts(tbase + 256 + t * HD, tbase + t * 128 + bf * kUN + kk * 8, dadd(dv, kk * 2048), kIdPV,
+                 (unit > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&o_done[t]);
+      };
+      int pair, bh, gk = 0;
+      for (int k = 0; item(k, pair, bh, 1); ++k) {
+        const int nU0 = 2 * item_kv(pair, 0), nU1 = 2 * item_kv(pair, 1);
+        const int nU = max(nU0, nU1);
+        mbar_wait_mma(q_full, k & 1);
+        mbar_wait_mma(&k_full[gk % NS], (gk / NS) & 1);
+        tc_fence_after();
+        for (int t = 0; t < 2; ++t) {
+          const int nUt = t ? nU1 : nU0;
+          if (nUt > 0) issue_s(t, 0, gk % NS);
+          if (nUt > 1) issue_s(t, 1, gk % NS);
+        }
+        mma_commit(&k_empty[gk % NS]);
+        if (nU <= 2) mma_commit(q_empty);
+        for (int u = 0; u < nU; ++u) {
+          const int j = u >> 1;
+          const int s = (gk + j) % NS;
+          const int nu = u + 2;                       // the unit whose S follows PV(u) into the same buffer
+          const int sn = (gk + (nu >> 1)) % NS;
+          if ((u & 1) == 0) {
+            mbar_wait_mma(&v_full[s], ((gk + j) / NS) & 1);
+            if (nu < nU) mbar_wait_mma(&k_full[sn], ((gk + (nu >> 1)) / NS) & 1);
+            tc_fence_after();
+          }
+          UL_EV(0, gk + j);
+          if (u < nU0) issue_pv(0, u, s);
+          if (nu < nU0) issue_s(0, nu, sn);
+          if (u < nU1) issue_pv(1, u, s);
+          if (nu < nU1) issue_s(1, nu, sn);
+          if (u & 1) mma_commit(&v_empty[s]);        // both halves of V_j read by both tiles
+          if (nu < nU && (nu & 1)) mma_commit(&k_empty[sn]);
+          if (nu == nU - 1) mma_commit(q_empty);      // the item's last S MMAs: Q may be replaced
+          UL_EV(7, gk + j);
+        }
+        if (nU0 > 0) ++items_t[0];
+        if (nU1 > 0) ++items_t[1];
+        gk += nU >> 1;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax / lazy correction / epilogue ----------------
+    const int idx = warp - 2;
+    const int t = idx >> 3;
+    const int quarter = warp & 3;
+    const int half = (idx & 7) >> 2;           // which 32 of the unit's 64 columns
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t tS = tbase + t * 128 + lane_off;
+    const uint32_t tO = tbase + 256 + t * HD + lane_off;
+    const uint32_t bar_id = 1 + t * 4 + quarter;
+    float* xch = reinterpret_cast<float*>(smem + S::kX);
+    auto xslot = [&](int sl, int hh) { return smem_u32(xch + ((sl * 2 + t) * 128 + row) * 2 + hh); };
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
+    int cs[2] = {0, 0};   // S units of each buffer consumed so far (s_full phases)
+    int base = 0;         // PVs of this tile before the current item (o_done phases)
+    int pair, bh;
+    for (int k = 0; item(k, pair, bh, 2); ++k) {
+      const int my_nU = 2 * item_kv(pair, t);
+      if (my_nU == 0) continue;
+      const int bb = bh / p.hq, h = bh % p.hq;
+      const int q0 = (2 * pair + t) * BM;
+      const int qrow = q0 + row;
+      float m = -INFINITY, l = 0.f;
+      for (int u = 0; u < my_nU; ++u) {
+        const int bf = u & 1;
+        const int kv0 = u * kUN;
+        mbar_wait(&s_full[t * 2 + bf], cs[bf] & 1);
+        ++cs[bf];
+        if (lane == 0 && warp == 2) UL_EV(3, u);
+        tc_fence_after();
+        uint32_t r[32];
+        tmem_ld32(tS + bf * kUN + half * 32, r);
+        tmem_wait_ld();
+        const bool masked = (p.causal && kv0 + kUN - 1 > q0) || kv0 + kUN > p.n;
+        if (masked) {
+          int limit = p.n - kv0;
+          if (p.causal) limit = min(limit, qrow - kv0 + 1);
+          limit -= half * 32;
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (c >= limit) r[c] = __float_as_uint(-INFINITY);
+        }
+        float mx[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) mx[x] = __uint_as_float(r[x]);
+#pragma unroll
+        for (int c = 8; c < 32; c += 8) {
+#pragma unroll
+          for (int x = 0; x < 8; ++x) mx[x] = fmaxf(mx[x], __uint_as_float(r[c + x]));
+        }
+        const float mh =
+            fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(bf, half)), "f"(mh) : "memory");
+        pair_sync();   // (also: both warps have loaded their S before either stores P over it)
+        float other;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(xslot(bf, half ^ 1)) : "memory");
+        const float mt = fmaxf(mh, other) * p.scale_log2;
+        float alpha = 1.f;
+        bool rescale = false;
+        if (mt > m + kLazy) {
+          alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - mt);
+          rescale = (u > 0);
+          m = mt;
+        }
+        const float mu = (m == -INFINITY) ? 0.f : m;
+        float2 rsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                          make_float2(0.f, 0.f)};
+        uint32_t pk[16];
+        exp_chunk<false>(r, p.scale_log2, mu, pk, rsum);
+        tmem_st16(tS + bf * kUN + half * 16, pk);   // P (bf16 pairs) over consumed S columns
+        const float2 rs = __fadd2_rn(__fadd2_rn(rsum[0], rsum[1]), __fadd2_rn(rsum[2], rsum[3]));
+        l = l * alpha + (rs.x + rs.y);
+        if (__any_sync(0xffffffffu, rescale)) {
+          // O holds PV(0..u-1): wait for PV(u-1) (PV(u-2) completed before S(u))
+          mbar_wait(&o_done[t], (base + u - 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < HD / 64; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(tO + half * (HD / 2) + c * 32, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int x = 0; x < 32; ++x) ov[x] = __float_as_uint(__uint_as_float(ov[x]) * alpha);
+            tmem_st32(tO + half * (HD / 2) + c * 32, ov);
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t * 2 + bf]);
+        if (lane == 0 && warp == 2) UL_EV(4, u);
+      }
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(2, half)), "f"(l) : "memory");
+      pair_sync();
+      float lo;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lo) : "r"(xslot(2, half ^ 1)) : "memory");
+      pair_sync();   // (the sum slot is rewritten by the next item)
+      const float lrow = l + lo;
+      base += my_nU;
+      mbar_wait(&o_done[t], (base - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / lrow;
+      const bool valid = qrow < p.n;
+      uint32_t pkd[HD / 64][16];
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(tO + half * (HD / 2) + c * 32, ov);
+        tmem_wait_ld();
+#pragma unroll
+        for (int x = 0; x < 16; ++x)
+          pkd[c][x] = pack_bf16(__uint_as_float(ov[2 * x]) * inv, __uint_as_float(ov[2 * x + 1]) * inv);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_free[t]);
+      if (valid) {
+        __nv_bfloat16* orow = p.o + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD + half * (HD / 2);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+            dst[x] = make_uint4(pkd[c][4 * x], pkd[c][4 * x + 1], pkd[c][4 * x + 2], pkd[c][4 * x + 3]);
+          if (p.ep.active) {
+            uint4* pd = reinterpret_cast<uint4*>(peer_row_ptr(p.ep, qrow, bb, p.b, h, HD, 2) + half * HD) + c * 4;
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              pd[x] = make_uint4(pkd[c][4 * x], pkd[c][4 * x + 1], pkd[c][4 * x + 2], pkd[c][4 * x + 3]);
+          }
+        }
+        if (half == 0) p.lse[((int64_t)bb * p.hq + h) * p.n + qrow] = (m + log2f(lrow)) * 0.69314718055994531f;
+      }
+    }
+    if (p.ep.active) __threadfence_system();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    UL_CTA(2, globaltimer());
+    UL_CTA(3, globaltimer());
+    UL_CTA(6, clock64());
+  }
+  if (p.ctr && threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1) {
+      atomicExch(p.ctr, 0);
+      atomicExch(p.ctr + 1, 0);
+    }
+  }
+  if (p.ep.active && threadIdx.x == 0) peer_signal_last_cta(p.ep, gridDim.x);
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc<512>(tbase);
+  }
+}
+
 // The persistent forward's [next item, CTAs done] counter pair is caller
 // memory (`sched`, UL_ATTN_SCHED_BYTES, zeroed once; the kernel leaves it
 // zero): launches sharing one pair must be stream-ordered.  No counter, or a
@@ -885,6 +1262,15 @@ static int* schedule_counter(void* sched, cudaStream_t st) {
     return nullptr;
   }
   return reinterpret_cast<int*>(sched);
+}
+
+// UL_FWD_H2=0 in the environment selects the full-tile persistent kernel (A/B)
+static bool fwd_h2_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("UL_FWD_H2");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 template <int HD>
@@ -935,6 +1321,14 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
   if (UL_FWD_PERSIST && !blk) {
     p.ctr = schedule_counter(sched, st);
     if (p.ctr || !p.head_major) {
+      if (HD == 128 && fwd_h2_enabled()) {
+        static std::atomic<uint64_t> hattr{0};
+        const int hsmem = SmemH2<128>::kBytes;
+        UL_TRY(smem_opt_in((const void*)attn_fwd_h2_kernel<128>, hsmem, hattr));
+        const int64_t pgrid = grid < sm_count() ? grid : sm_count();
+        attn_fwd_h2_kernel<128><<<(unsigned)pgrid, kThreads, hsmem, st>>>(mq, mk, mv, p);
+        return launched("attn_fwd_sm100");
+      }
       UL_TRY(smem_opt_in((const void*)attn_fwd_persist_kernel<HD>, smem, pattr));
       const int64_t pgrid = grid < sm_count() ? grid : sm_count();
       attn_fwd_persist_kernel<HD><<<(unsigned)pgrid, kThreads, smem, st>>>(mq, mk, mv, p);
@@ -969,6 +1363,7 @@ int preload_fwd() {
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_kernel<128>));
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<64>));
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<128>));
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_h2_kernel<128>));
   return UL_OK;
 }
 

@@ -14,10 +14,33 @@ def to_np(t):
     return t.detach().to(torch.float64).cpu().numpy()
 
 
+_WARMED = set()
+
+
+def _warm_stream(s):
+    """Reserve caching-allocator memory on a rank's stream once: a cudaMalloc
+    issued while an earlier rank's flag wait spins can serialize the device
+    behind it (implicit synchronization) -- a deadlock for in-process groups,
+    whose peers are issued by the same host thread afterwards."""
+    if s is None or s.stream_id in _WARMED:
+        return
+    _WARMED.add(s.stream_id)
+    with torch.cuda.stream(s):
+        small = [torch.empty(n, dtype=torch.uint8, device="cuda") for n in (512, 1 << 16, 1 << 19)]
+        big = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        del small, big
+
+
 def run_ranks(groups, fn):
     """Issue fn(rank) for every rank of an in-process group, each on its own
     stream (ranks of a local group must not share a stream: their device
     waits would serialise), then synchronise and surface desync errors."""
+    torch.cuda.synchronize()
+    for g in groups:
+        _warm_stream(g.stream)
+        ch = getattr(g, "_channel", None)
+        if ch is not None:
+            _warm_stream(ch.stream)
     torch.cuda.synchronize()
     out = []
     for g in groups:
