@@ -36,6 +36,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the in-process P = 8 exchange leg runs 8 ranks on 8 streams of one GPU with
+# device-side flag waits: give every stream its own hardware queue
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 SEQ_PER_GPU = 8192
 HEADS = 16

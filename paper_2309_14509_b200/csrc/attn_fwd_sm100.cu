@@ -98,7 +98,15 @@ struct Params {
   // persistent kernel: [next item, CTAs done] counters (per stream, zero at
   // rest: the last CTA resets them), or nullptr for the static zig-zag waves
   int* ctr;
+  // ping-pong of the two query tiles' exponential phases (named barriers
+  // 9/10): tile A's exponentials of a step run while tile B's MMAs do and
+  // vice versa, instead of both softmaxes sharing the MUFU in lockstep
+  int alt;
 };
+
+// named-barrier hand-off between the two tiles' softmax warp groups (8 warps each)
+__device__ __forceinline__ void alt_sync(int id) { asm volatile("bar.sync %0, 512;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void alt_arrive(int id) { asm volatile("bar.arrive %0, 512;" ::"r"(id) : "memory"); }
 
 __device__ __forceinline__ bool blk_bit(const Params& p, int qb, int kb) {
   return (__ldg(p.blk + (int64_t)qb * p.blk_words + (kb >> 5)) >> (kb & 31)) & 1u;
@@ -733,12 +741,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int k = 0; item(k, pair, bh, 2); ++k) {
       const int my_nkv = item_kv(pair, t);
       if (my_nkv == 0) continue;
+      const int na = item_kv(pair, 0);
+      const bool alt_item = p.alt && na > 0 && item_kv(pair, 1) > 0;
+      if (alt_item && t == 1) alt_arrive(9);   // tile A goes first
       const int bb = bh / p.hq, h = bh % p.hq;
       const int q0 = (2 * pair + t) * BM;
       const int qrow = q0 + row;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < my_nkv; ++j, ++cs) {
         const int kv0 = j * BN;
+        const bool alt = alt_item && j < na;
         mbar_wait(&s_full[t], cs & 1);
         tc_fence_after();
         uint32_t r[BN / 2];
@@ -779,12 +791,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mu = (m == -INFINITY) ? 0.f : m;
         float2 rsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                           make_float2(0.f, 0.f)};
+        if (alt) alt_sync(9 + t);   // the other tile's exponentials are done
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           uint32_t pk[16];
           exp_chunk<false>(r + c * 32, p.scale_log2, mu, pk, rsum);
           tmem_st16(tS + (2 * half + c) * 16, pk);
         }
+        if (alt && (t == 0 || j + 1 < na)) alt_arrive(9 + (t ^ 1));
         const float2 rs = __fadd2_rn(__fadd2_rn(rsum[0], rsum[1]), __fadd2_rn(rsum[2], rsum[3]));
         l = l * alpha + (rs.x + rs.y);
         if (__any_sync(0xffffffffu, rescale)) {
@@ -922,13 +936,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* v_empty = bars + 2 + 3 * NS;    // [NS]
   uint64_t* s_full = bars + 2 + 4 * NS;     // [tile][buffer]
   uint64_t* p_full = bars + 6 + 4 * NS;     // [tile][buffer]
-  uint64_t* o_done = bars + 10 + 4 * NS;    // [tile]: one phase per PV
-  uint64_t* o_free = bars + 12 + 4 * NS;    // [tile]: O read out by the epilogue
-  uint64_t* it_full = bars + 14 + 4 * NS;   // [4] dynamic item ring
-  uint64_t* it_empty = bars + 18 + 4 * NS;  // [4]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22 + 4 * NS);
-  volatile int* sitem = reinterpret_cast<volatile int*>(bars + 23 + 4 * NS);
-  static_assert((25 + 4 * NS) * 8 <= 512, "barrier area");
+  // [tile][buffer]: one phase per PV of that buffer's units.  Per buffer, a
+  // waiter is never more than one phase behind: s_full(u) implies PV(u - 2)
+  // (same buffer) completed, because S(u) was issued after it.
+  uint64_t* o_done = bars + 10 + 4 * NS;
+  uint64_t* o_free = bars + 14 + 4 * NS;    // [tile]: O read out by the epilogue
+  uint64_t* it_full = bars + 16 + 4 * NS;   // [4] dynamic item ring
+  uint64_t* it_empty = bars + 20 + 4 * NS;  // [4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24 + 4 * NS);
+  volatile int* sitem = reinterpret_cast<volatile int*>(bars + 25 + 4 * NS);
+  static_assert((27 + 4 * NS) * 8 <= 512, "barrier area");
   auto item = [&](int k, int& pair, int& bh, int role) {
     return p.ctr ? fwd_item_dyn<HD>(p, k, pair, bh, role, it_full, it_empty, sitem) : fwd_item<HD>(p, k, pair, bh);
   };
@@ -952,11 +969,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], kSoftPerTile);
+      mbar_init(&o_done[i], 1);
     }
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&o_done[t], 1);
-      mbar_init(&o_free[t], kSoftPerTile);
-    }
+    for (int t = 0; t < 2; ++t) mbar_init(&o_free[t], kSoftPerTile);
     for (int s = 0; s < 4; ++s) {
       mbar_init(&it_full[s], 1);
       mbar_init(&it_empty[s], 1 + 2 * kSoftPerTile);
@@ -1039,13 +1054,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (unit == 0 && items_t[t] > 0) mbar_wait_mma(&o_free[t], (items_t[t] - 1) & 1);
         mbar_wait_mma(&p_full[t * 2 + bf], cp[t * 2 + bf] & 1);
         ++cp[t * 2 + bf];
+        UL_EV(t == 0 ? 0 : 2, cp[t * 2] + cp[t * 2 + 1] - 1);
         tc_fence_after();
         const uint64_t dv = dadd(dV0, stage * S::kTile + bf * (kUN * 128));
 #pragma unroll
         for (int kk = 0; kk < kUN / 16; ++kk)
           mma_ts(tbase + 256 + t * HD, tbase + t * 128 + bf * kUN + kk * 8, dadd(dv, kk * 2048), kIdPV,
                  (unit > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&o_done[t]);
+        mma_commit(&o_done[t * 2 + bf]);
+        UL_EV(t == 0 ? 1 : 3, cp[t * 2] + cp[t * 2 + 1] - 1);
       };
       int pair, bh, gk = 0;
       for (int k = 0; item(k, pair, bh, 1); ++k) {
@@ -1071,7 +1088,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (nu < nU) mbar_wait_mma(&k_full[sn], ((gk + (nu >> 1)) / NS) & 1);
             tc_fence_after();
           }
-          UL_EV(0, gk + j);
           if (u < nU0) issue_pv(0, u, s);
           if (nu < nU0) issue_s(0, nu, sn);
           if (u < nU1) issue_pv(1, u, s);
@@ -1079,7 +1095,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (u & 1) mma_commit(&v_empty[s]);        // both halves of V_j read by both tiles
           if (nu < nU && (nu & 1)) mma_commit(&k_empty[sn]);
           if (nu == nU - 1) mma_commit(q_empty);      // the item's last S MMAs: Q may be replaced
-          UL_EV(7, gk + j);
         }
         if (nU0 > 0) ++items_t[0];
         if (nU1 > 0) ++items_t[1];
@@ -1102,11 +1117,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto xslot = [&](int sl, int hh) { return smem_u32(xch + ((sl * 2 + t) * 128 + row) * 2 + hh); };
     auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory"); };
     int cs[2] = {0, 0};   // S units of each buffer consumed so far (s_full phases)
-    int base = 0;         // PVs of this tile before the current item (o_done phases)
+    int base = 0;         // PVs per buffer of this tile before the current item (o_done phases)
     int pair, bh;
     for (int k = 0; item(k, pair, bh, 2); ++k) {
       const int my_nU = 2 * item_kv(pair, t);
       if (my_nU == 0) continue;
+      const int nUa = 2 * item_kv(pair, 0);   // units both tiles have (tile A's <= tile B's)
+      const bool alt_item = p.alt && nUa > 0 && item_kv(pair, 1) > 0;
+      if (alt_item && t == 1) alt_arrive(9);   // tile A goes first
       const int bb = bh / p.hq, h = bh % p.hq;
       const int q0 = (2 * pair + t) * BM;
       const int qrow = q0 + row;
@@ -1114,9 +1132,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int u = 0; u < my_nU; ++u) {
         const int bf = u & 1;
         const int kv0 = u * kUN;
+        const bool alt = alt_item && u < nUa;
         mbar_wait(&s_full[t * 2 + bf], cs[bf] & 1);
         ++cs[bf];
-        if (lane == 0 && warp == 2) UL_EV(3, u);
+        const int ev_i = cs[0] + cs[1] - 1;   // this tile's unit index across items (traces)
+        (void)ev_i;
+        if (lane == 0 && (warp == 2 || warp == 10)) UL_EV(warp == 2 ? 4 : 7, ev_i);
         tc_fence_after();
         uint32_t r[32];
         tmem_ld32(tS + bf * kUN + half * 32, r);
@@ -1156,13 +1177,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         float2 rsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                           make_float2(0.f, 0.f)};
         uint32_t pk[16];
+        if (alt) alt_sync(9 + t);                   // the other tile's exponentials are done
+        if (lane == 0 && (warp == 2 || warp == 10)) UL_EV(warp == 2 ? 5 : 8, ev_i);
         exp_chunk<false>(r, p.scale_log2, mu, pk, rsum);
+        if (alt && (t == 0 || u + 1 < nUa)) alt_arrive(9 + (t ^ 1));
         tmem_st16(tS + bf * kUN + half * 16, pk);   // P (bf16 pairs) over consumed S columns
         const float2 rs = __fadd2_rn(__fadd2_rn(rsum[0], rsum[1]), __fadd2_rn(rsum[2], rsum[3]));
         l = l * alpha + (rs.x + rs.y);
         if (__any_sync(0xffffffffu, rescale)) {
-          // O holds PV(0..u-1): wait for PV(u-1) (PV(u-2) completed before S(u))
-          mbar_wait(&o_done[t], (base + u - 1) & 1);
+          // O holds PV(0..u-1): wait for PV(u-1), the ((u-1)/2)-th of its buffer
+          mbar_wait(&o_done[t * 2 + ((u - 1) & 1)], (base + ((u - 1) >> 1)) & 1);
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < HD / 64; ++c) {
@@ -1178,7 +1202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t * 2 + bf]);
-        if (lane == 0 && warp == 2) UL_EV(4, u);
+        if (lane == 0 && (warp == 2 || warp == 10)) UL_EV(warp == 2 ? 6 : 9, ev_i);
       }
       asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(2, half)), "f"(l) : "memory");
       pair_sync();
@@ -1186,8 +1210,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lo) : "r"(xslot(2, half ^ 1)) : "memory");
       pair_sync();   // (the sum slot is rewritten by the next item)
       const float lrow = l + lo;
-      base += my_nU;
-      mbar_wait(&o_done[t], (base - 1) & 1);
+      base += my_nU >> 1;   // (my_nU is even: the same count of PVs in both buffers)
+      mbar_wait(&o_done[t * 2 + 0], (base - 1) & 1);
+      mbar_wait(&o_done[t * 2 + 1], (base - 1) & 1);
       tc_fence_after();
       const float inv = 1.f / lrow;
       const bool valid = qrow < p.n;
@@ -1264,6 +1289,15 @@ static int* schedule_counter(void* sched, cudaStream_t st) {
   return reinterpret_cast<int*>(sched);
 }
 
+// UL_FWD_ALT=0 in the environment turns the tiles' softmax ping-pong off (A/B)
+static int fwd_alt_enabled() {
+  static const int on = [] {
+    const char* e = getenv("UL_FWD_ALT");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return on;
+}
+
 // UL_FWD_H2=0 in the environment selects the full-tile persistent kernel (A/B)
 static bool fwd_h2_enabled() {
   static const bool on = [] {
@@ -1304,6 +1338,7 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
   p.blk_words = (int)blk_words;
   p.blk_nb = blk ? (int)(n / blk_bs) : 0;
   p.ctr = nullptr;
+  p.alt = fwd_alt_enabled();
   if (blk) p.causal = 0;
   const int smem = Smem<HD>::kBytes;
   static std::atomic<uint64_t> attr{0}, pattr{0};

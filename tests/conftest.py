@@ -6,6 +6,12 @@ import sys
 # lands: streams must not share a hardware work queue, or the push queues
 # behind the spin.  32 connections (read at CUDA context creation).
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# ... and no kernel may be loaded lazily while ranks are being issued: the
+# first launch of a not-yet-loaded kernel (torch's own included, e.g. the
+# first fp32 torch.stack of a pipelined layer) loads its module, which can
+# stall the device behind a rank's spinning flag wait whose peer the same
+# host thread has yet to issue.  Load every module at context creation.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 import pytest  # noqa: E402
 

@@ -1,5 +1,5 @@
 """A/B of the forward kernels (UL_FWD_H2=1 half-unit kernel vs =0 full-tile
-persistent kernel): device time per launch (CUDA events, L2 flushed by a
+persistent kernel; UL_FWD_ALT=1/0 softmax ping-pong on/off): device time per launch (CUDA events, L2 flushed by a
 read before each), TF/s, and max error of O / LSE against a torch fp32
 reference on a few heads.  Each variant runs in its own process (the env
 switch is read once).
@@ -44,7 +44,8 @@ def child(n, h, causal, reps=20):
         lref = torch.logsumexp(s, -1)
         errs[hh] = {"o": float((o[:, 0, hh].float() - ref).abs().max() / ref.abs().max()),
                     "lse": float((lse[0, hh] - lref).abs().max())}
-    print(json.dumps({"h2": os.environ.get("UL_FWD_H2", "1"), "ms": round(ms, 4),
+    print(json.dumps({"h2": os.environ.get("UL_FWD_H2", "1"), "alt": os.environ.get("UL_FWD_ALT", "1"),
+                      "ms": round(ms, 4),
                       "tflops": round(flops / ms / 1e9, 1), "err": errs}))
 
 
@@ -55,8 +56,8 @@ if __name__ == "__main__":
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
     h = int(sys.argv[2]) if len(sys.argv) > 2 else 16
     causal = int(sys.argv[3]) if len(sys.argv) > 3 else 1
-    for var in ("1", "0", "1"):
-        env = dict(os.environ, UL_FWD_H2=var)
+    for h2, alt in (("1", "1"), ("1", "0"), ("0", "1"), ("0", "0"), ("1", "1")):
+        env = dict(os.environ, UL_FWD_H2=h2, UL_FWD_ALT=alt)
         r = subprocess.run([sys.executable, __file__, "--child", str(n), str(h), str(causal)], env=env,
                            capture_output=True, text=True)
         print(r.stdout.strip() or r.stderr[-2000:], flush=True)
