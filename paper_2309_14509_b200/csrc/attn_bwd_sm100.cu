@@ -1023,9 +1023,11 @@ __global__ void __launch_bounds__(kFuThreads, 1)
         mma_commit(&q_empty[s]);
         // dQ^T(i) over the dP^T / dS^T columns dK(i) just read (in-order pipe)
         const uint64_t dds = dadd(dDS0, (i % NDS) * kAtomT);
+#ifndef UL_BWD_XP_NO_DQMMA   // (what-if flag, r2: no dQ^T GEMM -> only -1.3%; results wrong)
 #pragma unroll
         for (int kk = 0; kk < BT / 16; ++kk)
           mma_ss(tdPt, dadd(dKt0, kk * 2048), dadd(dds, kk * 2048), kIdQ, kk > 0 ? 1u : 0u);
+#endif
         mma_commit(&dq_full[b]);
         mma_commit(&ds_free[i % NDS]);
         UL_EV(6, i);
@@ -1090,8 +1092,12 @@ __global__ void __launch_bounds__(kFuThreads, 1)
       if (lane == 0) mbar_arrive(&dq_free[b]);
       UL_WARP(it);
       if (lane == 0 && warp == 2) UL_EV(11, it);
+#ifndef UL_BWD_XP_NO_RED   // (what-if flag, r2: drop the dQ atomics -> -4.7%; results wrong)
 #pragma unroll
       for (int c = 0; c < 64; ++c) red_add_f32(dst + c * HD, __uint_as_float(v[c]));
+#else
+      if (v[0] == 0x7fffffffu && v[63] == 0x7fffffffu) dst[0] = 0.f;
+#endif
       if (lane == 0 && warp == 2) UL_EV(15, it);
       if (++qi == nsub) {
         qi = i0;
@@ -1169,9 +1175,13 @@ __global__ void __launch_bounds__(kFuThreads, 1)
       if (it >= NDS) mbar_wait(&ds_free[ib], ((it - NDS) / NDS) & 1);
       if (lane == 0 && warp == 6) UL_EV(14, it);
       const uint32_t dsb = ds_row + ib * kAtomT;
+#ifndef UL_BWD_XP_NO_DSSTS   // (what-if flag, r2: skip the dS^T smem tile -> -7%; results wrong.
+                             //  Moving the copy to the drain warps, or after the p_full
+                             //  arrival, made the kernel 37% / 2.6% slower: dQ^T then waits)
 #pragma unroll
       for (int j = 0; j < kFuCols / 8; ++j)
         sts_u4(dsb + (((chunk0 + j) ^ (row & 7)) << 4), dsk[4 * j], dsk[4 * j + 1], dsk[4 * j + 2], dsk[4 * j + 3]);
+#endif
       fence_proxy_async_smem();
       if constexpr (kFuCols == 16) tmem_st8(tdPt + lane_off + c0 + 8, dsk);
       else tmem_st16(tdPt + lane_off + c0 + 16, dsk);

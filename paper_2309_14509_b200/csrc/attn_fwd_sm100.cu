@@ -1289,11 +1289,15 @@ static int* schedule_counter(void* sched, cudaStream_t st) {
   return reinterpret_cast<int*>(sched);
 }
 
-// UL_FWD_ALT=0 in the environment turns the tiles' softmax ping-pong off (A/B)
+// UL_FWD_ALT=1 in the environment turns the tiles' softmax ping-pong on (A/B;
+// off by default -- r2 at N = 4K/8K/32K: 0.3-0.8% slower with it; neither a
+// quarter of the exponentials on the FMA pipe (4.5% slower) nor 64-row K/V
+// unit rings of 4-5 stages (12% slower) helped: the kernel is not MUFU- or
+// K/V-latency-bound)
 static int fwd_alt_enabled() {
   static const int on = [] {
     const char* e = getenv("UL_FWD_ALT");
-    return (e && e[0] == '0') ? 0 : 1;
+    return (e && e[0] == '1') ? 1 : 0;
   }();
   return on;
 }

@@ -46,8 +46,9 @@ buf = np.zeros(8 * 16 * 256, dtype=np.uint64)
 assert lib.ul_debug_trace_fwd(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes)) == 0
 tr = buf.reshape(8, 16, 256).astype(np.int64)
 names = {0: "MMA p_full(A) seen", 1: "MMA PV(A)+S issued", 2: "MMA p_full(B) seen", 3: "MMA PV(B)+S issued",
-         4: "A s_full seen", 5: "A exps start", 6: "A p_full arrive",
-         7: "B s_full seen", 8: "B exps start", 9: "B p_full arrive"}
+         4: "A s_full seen", 5: "A exps start", 6: "A p_full arrive (w2, SMSP2)",
+         7: "B s_full seen", 10: "MMA K/V landed (step)", 11: "A arrive w3 (SMSP3)",
+         12: "A arrive w4 (SMSP0, +TMA warp)", 13: "A arrive w5 (SMSP1, +MMA warp)", 14: "A arrive w6 (SMSP2, half 1)"}
 for cta in range(2):
     ev = tr[cta]
     t0 = ev[4][U0]
@@ -63,5 +64,5 @@ for cta in range(2):
     med = lambda a, b, sa=0: int(np.median(ev[a][j + sa] - ev[b][j]))
     print(f"  medians: A unit period={med(4, 4, 1)}  A s_full->exps={med(5, 4)} A exps->arrive={med(6, 5)}"
           f"  A arrive->MMA sees={med(0, 6)}  MMA sees->issued={med(1, 0)}  A arrive->next s_full seen={med(4, 6, 1)}")
-    print(f"           B s_full->exps={med(8, 7)} B exps->arrive={med(9, 8)} B arrive->MMA sees={med(2, 9)}"
-          f"  A exps start - B exps start (same unit)={med(5, 8)}")
+    print(f"           A arrivals rel. w2: w3 {med(11, 6)} w4 {med(12, 6)} w5 {med(13, 6)} w6 {med(14, 6)}"
+          f"  last A arrival -> MMA sees: {int(np.median(ev[0][j] - np.max(ev[[6, 11, 12, 13, 14]][:, j], 0)))}")
