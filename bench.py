@@ -69,8 +69,8 @@ def make_flush(dev):
     return torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
 
-NCU_PROFILE = os.path.join(ROOT, "profiles", "r1_ncu_full_r80.json")
-NCU_NAMES = {"attn_fwd_sm100": "fwd::attn_fwd_persist_kernel<128>", "attn_bwd_dkdv_sm100": "bwd::bwd_dkdv_kernel<128>",
+NCU_PROFILE = os.path.join(ROOT, "profiles", "r2_ncu_full.json")   # tools/ncu_r2_summary.py of the r2 capture
+NCU_NAMES = {"attn_fwd_sm100": "fwd::attn_fwd_h2_kernel<128>", "attn_bwd_dkdv_sm100": "bwd::bwd_dkdv_kernel<128>",
              "attn_bwd_dq_sm100": "bwd::bwd_dq_kernel<128>", "attn_bwd_fused_sm100": "bwd::bwd_fused_kernel<128>"}
 
 
@@ -80,6 +80,8 @@ def ncu_traffic(kernel):
     try:
         with open(NCU_PROFILE) as f:
             d = json.load(f)[NCU_NAMES[kernel]]
+        if isinstance(d, list):   # (one record per captured launch: the first)
+            d = d[0]
         mb = lambda v: float(v.split()[0]) * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3}[v.split()[1]]
         return {"bytes": int(mb(d["dram__bytes_read.sum"]) + mb(d["dram__bytes_write.sum"])),
                 "source": os.path.relpath(NCU_PROFILE, ROOT)}
