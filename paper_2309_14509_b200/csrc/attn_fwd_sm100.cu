@@ -147,6 +147,11 @@ __device__ __forceinline__ void blk_row_mask(const Params& p, int qrow, int kv0,
 #endif
 constexpr bool kH2 = UL_FWD_EXP_H2 != 0;
 constexpr int kH2Sel = UL_FWD_EXP_H2 == 2 ? 2 : 0;
+// FMA-pipe exponentials on element pairs x with (x & mask) == mask: 6 -> 1/4,
+// 14 -> 1/8, 30 -> 1/16 of the pairs (when kPoly)
+#ifndef UL_FWD_POLY_MASK
+#define UL_FWD_POLY_MASK 6
+#endif
 template <bool kPoly>
 __device__ __forceinline__ void exp_chunk(const uint32_t* r, float scale_log2, float mu, uint32_t* pk,
                                           float2* rsum) {
@@ -156,7 +161,7 @@ __device__ __forceinline__ void exp_chunk(const uint32_t* r, float scale_log2, f
     // packed f32x2 FMA / add: half the issue slots of the scalar forms
     const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[x]), __uint_as_float(r[x + 1])), sc, nm);
     float2 e;
-    if (kPoly && (x & 6) == 6) {
+    if (kPoly && (x & UL_FWD_POLY_MASK) == UL_FWD_POLY_MASK) {
       e = poly_exp2x2(a);
     } else if (kH2 && (x & 2) == kH2Sel) {
       e = exp2_h2(a);
@@ -916,11 +921,20 @@ struct SmemH2 {
   static constexpr int kBytes = kX + 3 * 2 * 128 * 2 * 4 + 1024;
 };
 
-template <int HD>
-__global__ void __launch_bounds__(kThreads, 1)
+// WPR: softmax warps per query row (2: two warps per TMEM lane quarter, 32
+// of a unit's 64 columns each, row max exchanged through shared memory;
+// 1: one thread per row, all 64 columns, no exchange)
+template <int WPR>
+constexpr int h2_threads() { return 64 + 2 * 4 * WPR * 32; }
+
+template <int HD, int WPR>
+__global__ void __launch_bounds__(h2_threads<WPR>(), 1)
     attn_fwd_h2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                        const __grid_constant__ CUtensorMap tmV, const Params p) {
   static_assert(HD == 128, "half-unit forward: TMEM holds 2 x (2 x 64 S + HD O) columns");
+  constexpr int kSoft = 4 * WPR;         // softmax warps per query tile
+  constexpr int kC = kUN / WPR;          // unit columns per softmax thread
+  constexpr int kOC = HD / WPR;          // O columns per softmax thread
   using S = SmemH2<HD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -968,13 +982,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], kSoftPerTile);
+      mbar_init(&p_full[i], kSoft);
       mbar_init(&o_done[i], 1);
     }
-    for (int t = 0; t < 2; ++t) mbar_init(&o_free[t], kSoftPerTile);
+    for (int t = 0; t < 2; ++t) mbar_init(&o_free[t], kSoft);
     for (int s = 0; s < 4; ++s) {
       mbar_init(&it_full[s], 1);
-      mbar_init(&it_empty[s], 1 + 2 * kSoftPerTile);
+      mbar_init(&it_empty[s], 1 + 2 * kSoft);
     }
     fence_barrier_init();
   }
@@ -1105,9 +1119,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ---------------- softmax / lazy correction / epilogue ----------------
     const int idx = warp - 2;
-    const int t = idx >> 3;
+    const int t = idx / kSoft;
     const int quarter = warp & 3;
-    const int half = (idx & 7) >> 2;           // which 32 of the unit's 64 columns
+    const int half = (idx % kSoft) >> 2;       // which kC of the unit's 64 columns (WPR = 2)
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const uint32_t tS = tbase + t * 128 + lane_off;
@@ -1139,33 +1153,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         (void)ev_i;
         if (lane == 0 && (warp == 2 || warp == 10)) UL_EV(warp == 2 ? 4 : 7, ev_i);
         tc_fence_after();
-        uint32_t r[32];
-        tmem_ld32(tS + bf * kUN + half * 32, r);
+        uint32_t r[kC];
+#pragma unroll
+        for (int c = 0; c < kC; c += 32) tmem_ld32(tS + bf * kUN + half * kC + c, r + c);
         tmem_wait_ld();
         const bool masked = (p.causal && kv0 + kUN - 1 > q0) || kv0 + kUN > p.n;
         if (masked) {
           int limit = p.n - kv0;
           if (p.causal) limit = min(limit, qrow - kv0 + 1);
-          limit -= half * 32;
+          limit -= half * kC;
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
+          for (int c = 0; c < kC; ++c)
             if (c >= limit) r[c] = __float_as_uint(-INFINITY);
         }
         float mx[8];
 #pragma unroll
         for (int x = 0; x < 8; ++x) mx[x] = __uint_as_float(r[x]);
 #pragma unroll
-        for (int c = 8; c < 32; c += 8) {
+        for (int c = 8; c < kC; c += 8) {
 #pragma unroll
           for (int x = 0; x < 8; ++x) mx[x] = fmaxf(mx[x], __uint_as_float(r[c + x]));
         }
-        const float mh =
+        float mh =
             fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(bf, half)), "f"(mh) : "memory");
-        pair_sync();   // (also: both warps have loaded their S before either stores P over it)
-        float other;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(xslot(bf, half ^ 1)) : "memory");
-        const float mt = fmaxf(mh, other) * p.scale_log2;
+        if constexpr (WPR == 2) {
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(bf, half)), "f"(mh) : "memory");
+          pair_sync();   // (also: both warps have loaded their S before either stores P over it)
+          float other;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(xslot(bf, half ^ 1)) : "memory");
+          mh = fmaxf(mh, other);
+        }
+        const float mt = mh * p.scale_log2;
         float alpha = 1.f;
         bool rescale = false;
         if (mt > m + kLazy) {
@@ -1176,12 +1194,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mu = (m == -INFINITY) ? 0.f : m;
         float2 rsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                           make_float2(0.f, 0.f)};
-        uint32_t pk[16];
         if (alt) alt_sync(9 + t);                   // the other tile's exponentials are done
         if (lane == 0 && (warp == 2 || warp == 10)) UL_EV(warp == 2 ? 5 : 8, ev_i);
-        exp_chunk<false>(r, p.scale_log2, mu, pk, rsum);
+#pragma unroll
+        for (int c = 0; c < kC; c += 32) {
+          uint32_t pk[16];
+#ifdef UL_FWD_POLY
+          if (!masked) exp_chunk<true>(r + c, p.scale_log2, mu, pk, rsum);
+          else
+#endif
+          exp_chunk<false>(r + c, p.scale_log2, mu, pk, rsum);
+          tmem_st16(tS + bf * kUN + (half * kC + c) / 2, pk);   // P (bf16 pairs) over consumed S columns
+        }
         if (alt && (t == 0 || u + 1 < nUa)) alt_arrive(9 + (t ^ 1));
-        tmem_st16(tS + bf * kUN + half * 16, pk);   // P (bf16 pairs) over consumed S columns
         const float2 rs = __fadd2_rn(__fadd2_rn(rsum[0], rsum[1]), __fadd2_rn(rsum[2], rsum[3]));
         l = l * alpha + (rs.x + rs.y);
         if (__any_sync(0xffffffffu, rescale)) {
@@ -1189,13 +1214,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&o_done[t * 2 + ((u - 1) & 1)], (base + ((u - 1) >> 1)) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < HD / 64; ++c) {
+          for (int c = 0; c < kOC / 32; ++c) {
             uint32_t ov[32];
-            tmem_ld32(tO + half * (HD / 2) + c * 32, ov);
+            tmem_ld32(tO + half * kOC + c * 32, ov);
             tmem_wait_ld();
 #pragma unroll
             for (int x = 0; x < 32; ++x) ov[x] = __float_as_uint(__uint_as_float(ov[x]) * alpha);
-            tmem_st32(tO + half * (HD / 2) + c * 32, ov);
+            tmem_st32(tO + half * kOC + c * 32, ov);
           }
         }
         tmem_wait_st();
@@ -1204,11 +1229,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&p_full[t * 2 + bf]);
         if (lane == 0 && (warp == 2 || warp == 10)) UL_EV(warp == 2 ? 6 : 9, ev_i);
       }
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(2, half)), "f"(l) : "memory");
-      pair_sync();
-      float lo;
-      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lo) : "r"(xslot(2, half ^ 1)) : "memory");
-      pair_sync();   // (the sum slot is rewritten by the next item)
+      float lo = 0.f;
+      if constexpr (WPR == 2) {
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(2, half)), "f"(l) : "memory");
+        pair_sync();
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lo) : "r"(xslot(2, half ^ 1)) : "memory");
+        pair_sync();   // (the sum slot is rewritten by the next item)
+      }
       const float lrow = l + lo;
       base += my_nU >> 1;   // (my_nU is even: the same count of PVs in both buffers)
       mbar_wait(&o_done[t * 2 + 0], (base - 1) & 1);
@@ -1216,11 +1243,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const float inv = 1.f / lrow;
       const bool valid = qrow < p.n;
-      uint32_t pkd[HD / 64][16];
+      uint32_t pkd[kOC / 32][16];
 #pragma unroll
-      for (int c = 0; c < HD / 64; ++c) {
+      for (int c = 0; c < kOC / 32; ++c) {
         uint32_t ov[32];
-        tmem_ld32(tO + half * (HD / 2) + c * 32, ov);
+        tmem_ld32(tO + half * kOC + c * 32, ov);
         tmem_wait_ld();
 #pragma unroll
         for (int x = 0; x < 16; ++x)
@@ -1230,15 +1257,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[t]);
       if (valid) {
-        __nv_bfloat16* orow = p.o + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD + half * (HD / 2);
+        __nv_bfloat16* orow = p.o + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD + half * kOC;
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c) {
+        for (int c = 0; c < kOC / 32; ++c) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
           for (int x = 0; x < 4; ++x)
             dst[x] = make_uint4(pkd[c][4 * x], pkd[c][4 * x + 1], pkd[c][4 * x + 2], pkd[c][4 * x + 3]);
           if (p.ep.active) {
-            uint4* pd = reinterpret_cast<uint4*>(peer_row_ptr(p.ep, qrow, bb, p.b, h, HD, 2) + half * HD) + c * 4;
+            uint4* pd = reinterpret_cast<uint4*>(peer_row_ptr(p.ep, qrow, bb, p.b, h, HD, 2) + half * kOC * 2) + c * 4;
 #pragma unroll
             for (int x = 0; x < 4; ++x)
               pd[x] = make_uint4(pkd[c][4 * x], pkd[c][4 * x + 1], pkd[c][4 * x + 2], pkd[c][4 * x + 3]);
@@ -1302,6 +1329,17 @@ static int fwd_alt_enabled() {
   return on;
 }
 
+// UL_FWD_WPR=1 / 2: softmax warps per query row of the half-unit kernel (A/B;
+// default 1 -- r2: one thread per row, 10 warps, 168 registers, no row-max
+// exchange: -1.8% at N = 8K, -2.2% at N = 32K vs two warps per row)
+static int fwd_wpr() {
+  static const int w = [] {
+    const char* e = getenv("UL_FWD_WPR");
+    return (e && e[0] == '2') ? 2 : 1;
+  }();
+  return w;
+}
+
 // UL_FWD_H2=0 in the environment selects the full-tile persistent kernel (A/B)
 static bool fwd_h2_enabled() {
   static const bool on = [] {
@@ -1361,11 +1399,16 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
     p.ctr = schedule_counter(sched, st);
     if (p.ctr || !p.head_major) {
       if (HD == 128 && fwd_h2_enabled()) {
-        static std::atomic<uint64_t> hattr{0};
+        static std::atomic<uint64_t> hattr1{0}, hattr2{0};
         const int hsmem = SmemH2<128>::kBytes;
-        UL_TRY(smem_opt_in((const void*)attn_fwd_h2_kernel<128>, hsmem, hattr));
         const int64_t pgrid = grid < sm_count() ? grid : sm_count();
-        attn_fwd_h2_kernel<128><<<(unsigned)pgrid, kThreads, hsmem, st>>>(mq, mk, mv, p);
+        if (fwd_wpr() == 1) {
+          UL_TRY(smem_opt_in((const void*)attn_fwd_h2_kernel<128, 1>, hsmem, hattr1));
+          attn_fwd_h2_kernel<128, 1><<<(unsigned)pgrid, h2_threads<1>(), hsmem, st>>>(mq, mk, mv, p);
+        } else {
+          UL_TRY(smem_opt_in((const void*)attn_fwd_h2_kernel<128, 2>, hsmem, hattr2));
+          attn_fwd_h2_kernel<128, 2><<<(unsigned)pgrid, h2_threads<2>(), hsmem, st>>>(mq, mk, mv, p);
+        }
         return launched("attn_fwd_sm100");
       }
       UL_TRY(smem_opt_in((const void*)attn_fwd_persist_kernel<HD>, smem, pattr));
@@ -1402,7 +1445,8 @@ int preload_fwd() {
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_kernel<128>));
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<64>));
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<128>));
-  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_h2_kernel<128>));
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_h2_kernel<128, 1>));
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_h2_kernel<128, 2>));
   return UL_OK;
 }
 

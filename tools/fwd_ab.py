@@ -44,7 +44,8 @@ def child(n, h, causal, reps=20):
         lref = torch.logsumexp(s, -1)
         errs[hh] = {"o": float((o[:, 0, hh].float() - ref).abs().max() / ref.abs().max()),
                     "lse": float((lse[0, hh] - lref).abs().max())}
-    print(json.dumps({"h2": os.environ.get("UL_FWD_H2", "1"), "alt": os.environ.get("UL_FWD_ALT", "1"),
+    print(json.dumps({"h2": os.environ.get("UL_FWD_H2", "1"), "alt": os.environ.get("UL_FWD_ALT", "0"),
+                      "wpr": os.environ.get("UL_FWD_WPR", "2"),
                       "ms": round(ms, 4),
                       "tflops": round(flops / ms / 1e9, 1), "err": errs}))
 
@@ -56,8 +57,10 @@ if __name__ == "__main__":
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
     h = int(sys.argv[2]) if len(sys.argv) > 2 else 16
     causal = int(sys.argv[3]) if len(sys.argv) > 3 else 1
-    for h2, alt in (("1", "1"), ("1", "0"), ("0", "1"), ("0", "0"), ("1", "1")):
-        env = dict(os.environ, UL_FWD_H2=h2, UL_FWD_ALT=alt)
+    variants = os.environ.get("AB_VARIANTS", "1:0:2,1:0:1,0:0:2,1:0:2,1:0:1").split(",")
+    for var in variants:
+        h2, alt, wpr = var.split(":")
+        env = dict(os.environ, UL_FWD_H2=h2, UL_FWD_ALT=alt, UL_FWD_WPR=wpr)
         r = subprocess.run([sys.executable, __file__, "--child", str(n), str(h), str(causal)], env=env,
                            capture_output=True, text=True)
         print(r.stdout.strip() or r.stderr[-2000:], flush=True)
