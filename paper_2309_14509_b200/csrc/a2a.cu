@@ -170,8 +170,13 @@ __device__ __forceinline__ void copy_box(const Box& bx, int64_t warp0, int64_t n
   }
 }
 
-// grid (blocks_per_box, nbox); 256 threads
-__global__ void __launch_bounds__(256) a2a_copy_kernel(const __grid_constant__ CopyParams p) {
+// grid (blocks_per_box, nbox); kCopyThreads threads.  128-thread CTAs of
+// <= 64 registers (8192 registers) fit beside a resident attention CTA
+// (forward: 320 threads x 168 registers; fused backward: 704 x 80), so the
+// pipelined layer's prefetch exchange runs on the SMs the attention of the
+// previous head group occupies instead of waiting for its tail.
+constexpr int kCopyThreads = 128;
+__global__ void __launch_bounds__(kCopyThreads) a2a_copy_kernel(const __grid_constant__ CopyParams p) {
   const Box& bx = p.box[blockIdx.y];
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -356,13 +361,13 @@ static int launch_copy(CopyParams& p, cudaStream_t st, const char* name) {
     if (w > maxwork) maxwork = w;
   }
   // ~one 512-byte warp-row per warp per pass; cap the grid at a few waves
-  const int warps_per_block = 8;
+  const int warps_per_block = kCopyThreads / 32;
   int64_t bpb = (maxwork + warps_per_block - 1) / warps_per_block;
-  const int64_t cap = (int64_t)sm_count() * 8 / p.nbox + 1;
+  const int64_t cap = (int64_t)sm_count() * (2048 / kCopyThreads / 2) / p.nbox + 1;   // ~32 warps per SM
   if (bpb > cap) bpb = cap;
   if (bpb < 1) bpb = 1;
   dim3 grid((unsigned)bpb, (unsigned)p.nbox);
-  a2a_copy_kernel<<<grid, 256, 0, st>>>(p);
+  a2a_copy_kernel<<<grid, kCopyThreads, 0, st>>>(p);
   return launched(name);
 }
 
