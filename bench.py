@@ -7,13 +7,17 @@
 (torch.distributed.run on 127.0.0.1, one process per GPU); under torchrun it
 runs as the rank it is.
 
-Workloads (BASELINE.json configs): at N = 1, config 2 -- local attention
+Workloads (BASELINE.json configs): config 2's problem -- local attention
 fwd+bwd of one GPT-1.3B layer shape (16 heads x 128), N = 8192 tokens, bf16,
-causal.  At N > 1, config 5 -- weak scaling N = 64K x P, 56 heads x 128
-(constant per-GPU exchange volume), the Ulysses layer over N ranks with the
-seq->head / head->seq exchanges on the peer-memory kernels (csrc/a2a.cu), no
-NCCL on the data path; --config 3 / 4 select the 7B (32 heads, N = 32K..256K
-via --seq) and GQA (32 q / 8 kv, N = 128K) workloads.
+causal -- at every N: N = 1 is the metric's single-GPU workload, N > 1 runs
+the same problem through the Ulysses layer over N ranks (strong scaling:
+the driver's per-N values compare one problem), the seq->head / head->seq
+exchanges on the peer-memory kernels (csrc/a2a.cu), no NCCL on the data path.
+Beside it (`config5_weak`, skipped by --quick): config 5, weak scaling N =
+64K x P, 56 heads x 128 -- per-GPU TF/s, exposed exchange and the constant
+per-GPU exchange volume.  --config 3 / 4 / 5 select the 7B (32 heads, N =
+32K..256K via --seq), GQA (32 q / 8 kv, N = 128K) or config-5 workload as
+the main line instead.
 
 One JSON line on rank 0.  `value` = tokens/s of the whole job with inputs
 resident in HBM (device time from CUDA events, max over ranks; L2 flushed by
@@ -310,8 +314,8 @@ def cpu_baseline(n_seq, heads, hd, procs=1, n_sample=1024, heads_sample=1):
 
 CONFIGS = {
     # name: (query heads, kv heads, sequence length for P ranks, description)
-    "2": (16, 16, lambda P: SEQ_PER_GPU * P,
-          "config2: single-GPU local attention fwd+bwd, GPT-1.3B layer 16 heads x 128, N={n} bf16 causal"),
+    "2": (16, 16, lambda P: SEQ_PER_GPU,
+          "config2: local attention fwd+bwd, GPT-1.3B layer 16 heads x 128, N={n} bf16 causal, Ulysses P={P}"),
     "3": (32, 32, lambda P: 32768,
           "config3: Ulysses attention layer P={P}, 7B shape 32 heads x 128, N={n} bf16 causal fwd+bwd"),
     "4": (32, 8, lambda P: 131072,
@@ -322,9 +326,11 @@ CONFIGS = {
 
 
 def pick_config(args, P):
-    """N = 1: config 2 (the metric's single-GPU workload); N > 1: config 5
-    (the metric's 1/2/4/8-GPU weak-scaling sweep), unless --config says."""
-    name = args.config or ("2" if P == 1 else "5")
+    """Every N runs config 2's problem (16 heads x 128, N = 8192: the metric's
+    single-GPU workload) -- strong scaling over Ulysses P = N, so the
+    driver's per-N values compare one problem; config 5 (weak scaling, N =
+    64K x P) is measured beside it (`config5_weak`).  --config overrides."""
+    name = args.config or "2"
     hq, hkv, seq, desc = CONFIGS[name]
     if args.heads:
         hq = hkv = args.heads
@@ -491,6 +497,8 @@ def run_ours(args):
     attn_only_ms = sum(x["ms"] for x in kt["kernels"])
     a2a = bench_a2a(dev, n_seq, H, hd, P, group, HKV, inproc=not args.quick)
     extras = {}
+    if not args.quick and not args.config:
+        extras["config5_weak"] = bench_config5(P, rank, dev, group, args)
     if P == 1 and not args.quick:
         extras["blocked_sparse_fwd"] = bench_blocked(kt_inputs=(lambda: mk4(H), n_seq, H, hd), args=args, dev=dev)
         extras["layer"] = bench_layer(group, nl, H, hd, args, dev)
@@ -516,7 +524,7 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True,
-            "scaling": "weak" if cfg_name in ("5", "2") else "strong",
+            "scaling": "weak" if cfg_name == "5" else "strong",
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic N(0,1) q/k/v/dO, seed 2024 (no dataset)",
@@ -557,6 +565,66 @@ def run_ours(args):
     if P > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bench_config5(P, rank, dev, group, args):
+    """BASELINE config 5 beside the headline: weak scaling N = 64K x P, 56
+    heads x 128, the Ulysses layer fwd+bwd over this job's P ranks (device
+    time, L2 read-flushed before every step, max over ranks), per-GPU
+    TFLOP/s and roofline fraction, the exposed exchange (step minus this
+    rank's attention kernels alone) and the exact per-GPU exchange egress,
+    which N proportional to P keeps constant per link (costmodel.py:82-87)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2309_14509_b200 as U
+    H, hd = 56, HEAD_DIM
+    n_seq = 65536 * P
+    nl = n_seq // P
+    g = torch.Generator(device=dev)
+    g.manual_seed(2024 + rank)
+    mk = lambda shape: torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(torch.bfloat16)
+    q, k, v, do = (mk((nl, 1, H, hd)) for _ in range(4))
+    attn = U.FlashAttention("causal")
+    layer = U.DistributedAttention(attn, group)
+    flush = make_flush(dev)
+
+    def step():
+        qq, kk, vv = (x.detach().requires_grad_(True) for x in (q, k, v))
+        torch.autograd.backward([layer(qq, kk, vv)], [do])
+    steps, warm = max(2, min(args.steps, 5)), max(1, min(args.warmup, 2))
+    for _ in range(warm):
+        step()
+    torch.cuda.synchronize()
+    if P > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        read_flush(flush)
+        ev[i][0].record()
+        step()
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    t = sum(a.elapsed_time(b) for a, b in ev) / steps
+    if P > 1:
+        tt = torch.tensor([t], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    del q, k, v, do
+    kt = kernel_split(attn, mk((n_seq, 1, H // P, hd)), mk((n_seq, 1, H // P, hd)), mk((n_seq, 1, H // P, hd)),
+                      mk((n_seq, 1, H // P, hd)), argparse.Namespace(steps=2, warmup=1), dev)
+    att = sum(x["ms"] for x in kt["kernels"])
+    f_fwd, f_bwd = attn_flops(n_seq, H // P, hd, True)
+    pk, _ = peaks()
+    local = nl * H * hd * 2
+    egress = 8 * local // P * (P - 1)      # fwd: q, k, v, o; bwd: do, dq, dk, dv
+    tf = (f_fwd + f_bwd) / (t / 1e3) / 1e12
+    return {"workload": f"config5: 56 heads x 128, N={n_seq}, P={P}, bf16 causal fwd+bwd", "seq_len": n_seq,
+            "ms_per_step": round(t, 3), "tokens_per_s": round(n_seq / (t / 1e3), 1),
+            "tflops_per_gpu": round(tf, 1), "frac_of_burst_peak": round(tf / pk["bf16_tflops"], 4),
+            "attention_only_ms": round(att, 3), "exposed_exchange_ms": round(t - att, 3),
+            "exposed_exchange_pct": round(100.0 * (t - att) / t, 2),
+            "exchange_egress_bytes_per_gpu": egress, "local_bytes_per_tensor": local,
+            "steps": steps, "scaling": "weak"}
 
 
 def kernel_split(attn, q, k, v, do, args, dev):

@@ -52,10 +52,11 @@ def _dry(gpus, extra=()):
                           capture_output=True, text=True, timeout=300)
 
 
-def test_bench_self_launches_n_ranks_on_config5():
+def test_bench_self_launches_n_ranks_strong_scaling_config2():
     # `bench.py --gpus 2` outside torchrun starts 2 ranks itself (gloo here, no
-    # CUDA in --dry-run), picks config 5 (weak scaling N = 64K x P) and reduces
-    # the timing as the max over ranks; rank 0 alone prints
+    # CUDA in --dry-run), runs config 2's problem over Ulysses P = 2 (strong
+    # scaling: the same N = 8192 at every N, so per-N values are comparable)
+    # and reduces the timing as the max over ranks; rank 0 alone prints
     r = _dry(2)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -63,8 +64,11 @@ def test_bench_self_launches_n_ranks_on_config5():
     d = json.loads(lines[0])
     assert d["dry_run"] and d["n_gpus"] == 2 and d["max_over_ranks"] == 2.0
     c = d["config"]
-    assert c["baseline_config"] == 5 and c["heads"] == 56 and c["seq_len"] == 65536 * 2
+    assert c["baseline_config"] == 2 and c["heads"] == 16 and c["seq_len"] == 8192
     assert c["parallelism"] == "ulysses-sp2"
+    r = _dry(2, ("--config", "5"))
+    c = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])["config"]
+    assert c["baseline_config"] == 5 and c["heads"] == 56 and c["seq_len"] == 65536 * 2
 
 
 def test_bench_config_selection():
