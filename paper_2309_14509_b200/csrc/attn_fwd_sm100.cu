@@ -104,9 +104,14 @@ struct Params {
   int alt;
 };
 
-// named-barrier hand-off between the two tiles' softmax warp groups (8 warps each)
-__device__ __forceinline__ void alt_sync(int id) { asm volatile("bar.sync %0, 512;" ::"r"(id) : "memory"); }
-__device__ __forceinline__ void alt_arrive(int id) { asm volatile("bar.arrive %0, 512;" ::"r"(id) : "memory"); }
+// named-barrier hand-off between the two tiles' softmax warp groups (`nthr`:
+// the softmax threads of both tiles)
+__device__ __forceinline__ void alt_sync(int id, int nthr = 512) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthr) : "memory");
+}
+__device__ __forceinline__ void alt_arrive(int id, int nthr = 512) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthr) : "memory");
+}
 
 __device__ __forceinline__ bool blk_bit(const Params& p, int qb, int kb) {
   return (__ldg(p.blk + (int64_t)qb * p.blk_words + (kb >> 5)) >> (kb & 31)) & 1u;
@@ -1138,7 +1143,7 @@ __global__ void __launch_bounds__(h2_threads<WPR>(), 1)
       if (my_nU == 0) continue;
       const int nUa = 2 * item_kv(pair, 0);   // units both tiles have (tile A's <= tile B's)
       const bool alt_item = p.alt && nUa > 0 && item_kv(pair, 1) > 0;
-      if (alt_item && t == 1) alt_arrive(9);   // tile A goes first
+      if (alt_item && t == 1) alt_arrive(9, 64 * kSoft);   // tile A goes first
       const int bb = bh / p.hq, h = bh % p.hq;
       const int q0 = (2 * pair + t) * BM;
       const int qrow = q0 + row;
@@ -1194,7 +1199,7 @@ __global__ void __launch_bounds__(h2_threads<WPR>(), 1)
         const float mu = (m == -INFINITY) ? 0.f : m;
         float2 rsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                           make_float2(0.f, 0.f)};
-        if (alt) alt_sync(9 + t);                   // the other tile's exponentials are done
+        if (alt) alt_sync(9 + t, 64 * kSoft);       // the other tile's exponentials are done
         if (lane == 0 && (warp == 2 || warp == 10)) UL_EV(warp == 2 ? 5 : 8, ev_i);
 #pragma unroll
         for (int c = 0; c < kC; c += 32) {
@@ -1206,7 +1211,7 @@ __global__ void __launch_bounds__(h2_threads<WPR>(), 1)
           exp_chunk<false>(r + c, p.scale_log2, mu, pk, rsum);
           tmem_st16(tS + bf * kUN + (half * kC + c) / 2, pk);   // P (bf16 pairs) over consumed S columns
         }
-        if (alt && (t == 0 || u + 1 < nUa)) alt_arrive(9 + (t ^ 1));
+        if (alt && (t == 0 || u + 1 < nUa)) alt_arrive(9 + (t ^ 1), 64 * kSoft);
         const float2 rs = __fadd2_rn(__fadd2_rn(rsum[0], rsum[1]), __fadd2_rn(rsum[2], rsum[3]));
         l = l * alpha + (rs.x + rs.y);
         if (__any_sync(0xffffffffu, rescale)) {

@@ -1,0 +1,50 @@
+"""Every selectable forward kernel stays correct: the default half-unit
+kernel (one softmax thread per row), its two-warps-per-row form
+(UL_FWD_WPR=2), the full-tile persistent kernel (UL_FWD_H2=0) and the
+softmax ping-pong (UL_FWD_ALT=1), each in its own process (the switches are
+read once per process), against the f64 oracle (causal and dense, a ragged
+tail, GQA)."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+from helpers import BF16_MAXREL
+
+pytestmark = pytest.mark.gpu
+
+CHILD = r"""
+import json, sys
+import numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2309_14509_b200 as U
+from oracle import ulysses_oracle as O
+out = {}
+for n, hq, hkv, mask in ((1000, 4, 2, "causal"), (640, 2, 2, "none")):
+    q = O.make_tensor((n, 1, hq, 128), 5, 1, "bfloat16")
+    k = O.make_tensor((n, 1, hkv, 128), 5, 2, "bfloat16")
+    v = O.make_tensor((n, 1, hkv, 128), 5, 3, "bfloat16")
+    dev = lambda x: torch.tensor(x, dtype=torch.float32).to(torch.bfloat16).cuda()
+    o, lse = U.FlashAttention(mask).forward_with_lse(dev(q), dev(k), dev(v))
+    ref, ref_lse = O.local_attention(q, k, v, mask, exact=False)
+    o = o.float().cpu().numpy()
+    out[f"{n}-{mask}"] = {"o": float(np.abs(o - ref).max() / np.abs(ref).max()),
+                          "lse": float(np.abs(lse.cpu().numpy() - ref_lse).max())}
+print("RESULT " + json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", [{}, {"UL_FWD_WPR": "2"}, {"UL_FWD_H2": "0"}, {"UL_FWD_ALT": "1"},
+                                 {"UL_FWD_ALT": "1", "UL_FWD_WPR": "2"}])
+def test_forward_kernel_variants_vs_oracle(env):
+    r = subprocess.run([sys.executable, "-c", CHILD, ROOT], cwd=ROOT, env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=300)
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("RESULT ")]
+    assert line, r.stderr[-3000:]
+    for case, e in json.loads(line[0][7:]).items():
+        assert e["o"] <= BF16_MAXREL, (env, case, e)
+        assert e["lse"] <= 2e-2, (env, case, e)
