@@ -543,13 +543,33 @@ class _UlyssesAttnPipeFn(torch.autograd.Function):
         return None, None, None, _interleave(dq, p), _interleave(dk, p), _interleave(dv, p)
 
 
-def pipeline_groups(heads_local: int, kv_heads_local: int, want: int = 2) -> int:
+def pipeline_groups(heads_local: int, kv_heads_local: int, want: int = 2, n: int | None = None,
+                    sms: int | None = None) -> int:
     """Head groups of the pipelined layer: the largest g <= want dividing
-    both this rank's query and kv head counts (1 = no pipelining)."""
+    both this rank's query and kv head counts (1 = no pipelining) -- and,
+    when the full sequence length n is given, only if every group's
+    attention still fills the GPU (>= 2 forward work items of two 128-row
+    query tiles per SM): splitting a small problem costs more than the
+    hidden exchange (r2, tools/inproc_layer.py: P = 4, 16 heads, N = 8K,
+    2.49 -> 4.70 ms)."""
     for g in range(max(1, want), 0, -1):
         if heads_local % g == 0 and kv_heads_local % g == 0:
+            if g > 1 and n is not None:
+                items = ((n + 255) // 256) * (heads_local // g)
+                if items < 2 * (sms or _sm_count()):
+                    continue
             return g
     return 1
+
+
+_SMS = {}
+
+
+def _sm_count() -> int:
+    d = torch.cuda.current_device()
+    if d not in _SMS:
+        _SMS[d] = torch.cuda.get_device_properties(d).multi_processor_count
+    return _SMS[d]
 
 
 class DistributedAttention(torch.nn.Module):
@@ -561,7 +581,7 @@ class DistributedAttention(torch.nn.Module):
     """
 
     def __init__(self, local_attention, sequence_process_group=None, scatter_idx: int = 2,
-                 gather_idx: int = 0, pipeline: int = 2):
+                 gather_idx: int = 0, pipeline: int = 2, adaptive_pipeline: bool = True):
         super().__init__()
         self.local_attn = local_attention
         self.spg = _group(sequence_process_group)
@@ -570,6 +590,9 @@ class DistributedAttention(torch.nn.Module):
         # head groups over which the fused route pipelines its exchanges with
         # the attention (P > 1); 1 = one exchange of all heads, then attention
         self.pipeline = int(pipeline)
+        # pipeline only problems whose head groups still fill the GPU (False:
+        # always split into `pipeline` groups when the head counts allow)
+        self.adaptive_pipeline = bool(adaptive_pipeline)
 
     def _check(self, q, k, v):
         p = self.spg.world
@@ -597,7 +620,8 @@ class DistributedAttention(torch.nn.Module):
                 o = _UlyssesAttnFn.apply(self.spg, self.local_attn, 2, 0, q, k, v)
                 return o.reshape(1, o.shape[0], o.shape[2], o.shape[3])
             p = self.spg.world
-            G = pipeline_groups(query.shape[2] // p, key.shape[2] // p, self.pipeline) if p > 1 else 1
+            G = pipeline_groups(query.shape[2] // p, key.shape[2] // p, self.pipeline,
+                                n=query.shape[0] * p if self.adaptive_pipeline else None) if p > 1 else 1
             if G > 1 and (self.scatter_idx, self.gather_idx) == (2, 0):
                 return _UlyssesAttnPipeFn.apply(self.spg, self.local_attn, G, query, key, value)
             return _UlyssesAttnFn.apply(self.spg, self.local_attn, self.scatter_idx, self.gather_idx,

@@ -375,6 +375,18 @@ int preload_a2a() {
   cudaFuncAttributes a;
   UL_CUDA(cudaFuncGetAttributes(&a, a2a_copy_kernel));
   UL_CUDA(cudaFuncGetAttributes(&a, a2a_wait_kernel));
+  // An SM runs a new CTA beside resident ones only if its L1 / shared-memory
+  // carveout has room.  The flag wait spins for as long as a peer takes, and
+  // the exchange copies are meant to run beside an attention CTA (~200 KB of
+  // shared memory): both ask for the max-shared carveout, so the SM hosting
+  // them can still take an attention CTA.  (With the default carveout the
+  // last CTA of a persistent attention grid could not start on the SM of a
+  // spinning wait -- whose peer signal that very grid's last CTA sends: an
+  // in-process group deadlocked at its first layer call.)
+  UL_CUDA(cudaFuncSetAttribute(a2a_copy_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared));
+  UL_CUDA(cudaFuncSetAttribute(a2a_wait_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared));
   return UL_OK;
 }
 

@@ -1326,10 +1326,9 @@ static int launch(const void* q, const void* k, const void* v, const void* o, co
     memset(&p.ep_dk, 0, sizeof(PeerEpilogue));
     memset(&p.ep_dv, 0, sizeof(PeerEpilogue));
   }
-  static std::atomic<uint64_t> attr_dkdv{0}, attr_dq{0}, attr_fused{0};
-  UL_TRY(smem_opt_in((const void*)bwd_dkdv_kernel<HD>, DkdvSmem<HD>::kBytes, attr_dkdv));
-  UL_TRY(smem_opt_in((const void*)bwd_dq_kernel<HD>, DqSmem<HD>::kBytes, attr_dq));
-  if constexpr (HD == 128) UL_TRY(smem_opt_in((const void*)bwd_fused_kernel<HD>, FusedSmem<HD>::kBytes, attr_fused));
+  UL_TRY(smem_opt_in((const void*)bwd_dkdv_kernel<HD>, DkdvSmem<HD>::kBytes));
+  UL_TRY(smem_opt_in((const void*)bwd_dq_kernel<HD>, DqSmem<HD>::kBytes));
+  if constexpr (HD == 128) UL_TRY(smem_opt_in((const void*)bwd_fused_kernel<HD>, FusedSmem<HD>::kBytes));
   const int64_t tiles = (n + BT - 1) / BT;
   if constexpr (HD == 128) {
     if (fused) {
@@ -1424,6 +1423,12 @@ int preload_bwd() {
   UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dq_kernel<128>));
   UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_fused_kernel<128>));
   UL_CUDA(cudaFuncGetAttributes(&a, bwd::bwd_dq_convert_kernel<128>));
+  // dynamic shared-memory opt-ins now, not at the first launch (common.cuh)
+  UL_TRY(smem_opt_in((const void*)bwd::bwd_dkdv_kernel<64>, bwd::DkdvSmem<64>::kBytes));
+  UL_TRY(smem_opt_in((const void*)bwd::bwd_dkdv_kernel<128>, bwd::DkdvSmem<128>::kBytes));
+  UL_TRY(smem_opt_in((const void*)bwd::bwd_dq_kernel<64>, bwd::DqSmem<64>::kBytes));
+  UL_TRY(smem_opt_in((const void*)bwd::bwd_dq_kernel<128>, bwd::DqSmem<128>::kBytes));
+  UL_TRY(smem_opt_in((const void*)bwd::bwd_fused_kernel<128>, bwd::FusedSmem<128>::kBytes));
   return UL_OK;
 }
 

@@ -1388,8 +1388,7 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
   p.alt = fwd_alt_enabled();
   if (blk) p.causal = 0;
   const int smem = Smem<HD>::kBytes;
-  static std::atomic<uint64_t> attr{0}, pattr{0};
-  UL_TRY(smem_opt_in((const void*)attn_fwd_kernel<HD>, smem, attr));
+  UL_TRY(smem_opt_in((const void*)attn_fwd_kernel<HD>, smem));
   const int64_t grid = (int64_t)p.pairs * b * hq;
 #ifndef UL_FWD_PERSIST
 #define UL_FWD_PERSIST 1   // r73: -1.5% vs the one-shot grid; blocked-sparse keeps the one-shot kernel
@@ -1404,19 +1403,18 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
     p.ctr = schedule_counter(sched, st);
     if (p.ctr || !p.head_major) {
       if (HD == 128 && fwd_h2_enabled()) {
-        static std::atomic<uint64_t> hattr1{0}, hattr2{0};
         const int hsmem = SmemH2<128>::kBytes;
         const int64_t pgrid = grid < sm_count() ? grid : sm_count();
         if (fwd_wpr() == 1) {
-          UL_TRY(smem_opt_in((const void*)attn_fwd_h2_kernel<128, 1>, hsmem, hattr1));
+          UL_TRY(smem_opt_in((const void*)attn_fwd_h2_kernel<128, 1>, hsmem));
           attn_fwd_h2_kernel<128, 1><<<(unsigned)pgrid, h2_threads<1>(), hsmem, st>>>(mq, mk, mv, p);
         } else {
-          UL_TRY(smem_opt_in((const void*)attn_fwd_h2_kernel<128, 2>, hsmem, hattr2));
+          UL_TRY(smem_opt_in((const void*)attn_fwd_h2_kernel<128, 2>, hsmem));
           attn_fwd_h2_kernel<128, 2><<<(unsigned)pgrid, h2_threads<2>(), hsmem, st>>>(mq, mk, mv, p);
         }
         return launched("attn_fwd_sm100");
       }
-      UL_TRY(smem_opt_in((const void*)attn_fwd_persist_kernel<HD>, smem, pattr));
+      UL_TRY(smem_opt_in((const void*)attn_fwd_persist_kernel<HD>, smem));
       const int64_t pgrid = grid < sm_count() ? grid : sm_count();
       attn_fwd_persist_kernel<HD><<<(unsigned)pgrid, kThreads, smem, st>>>(mq, mk, mv, p);
       return launched("attn_fwd_sm100");
@@ -1452,6 +1450,13 @@ int preload_fwd() {
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<128>));
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_h2_kernel<128, 1>));
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_h2_kernel<128, 2>));
+  // dynamic shared-memory opt-ins now, not at the first launch (common.cuh)
+  UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_kernel<64>, fwd::Smem<64>::kBytes));
+  UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_kernel<128>, fwd::Smem<128>::kBytes));
+  UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_persist_kernel<64>, fwd::Smem<64>::kBytes));
+  UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_persist_kernel<128>, fwd::Smem<128>::kBytes));
+  UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_h2_kernel<128, 1>, fwd::SmemH2<128>::kBytes));
+  UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_h2_kernel<128, 2>, fwd::SmemH2<128>::kBytes));
   return UL_OK;
 }
 

@@ -47,6 +47,57 @@ int preload_proj();
 int preload_merge();
 int preload_block();
 
+// First launch of each attention kernel variant, once per device, at group
+// creation.  Measured (r2, tools/debug_pipe.py): the first in-process layer
+// call of a process deadlocked until the flag wait's timeout -- rank 1's
+// attention kernel could not start while rank 0's wait spun -- and any P = 1
+// attention launch earlier in the process avoided it; setting the kernels'
+// attributes, the shared-memory carveout and the local-memory pool up front
+// did not.  Whatever the driver does at a kernel's first launch, it happens
+// here, where no rank of an in-process group has work queued.
+static int launch_warmup() {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  UL_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return UL_OK;
+  const int64_t n = 256, hq = 2, hkv = 1;
+  const size_t tens = (size_t)n * hq * 128 * 4;            // one q-sized tensor (fp32 upper bound)
+  const size_t ws = sm100_bwd_workspace(n, 1, hq, hkv, 128);
+  char* buf = nullptr;
+  UL_CUDA(cudaMalloc(&buf, 8 * tens + ws + 4096));
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, 8 * tens + ws + 4096, s);
+  int rc = UL_OK;
+  if (e == cudaSuccess) {
+    char *q = buf, *k = buf + tens, *v = buf + 2 * tens, *o = buf + 3 * tens, *dout = buf + 4 * tens;
+    char *dq = buf + 5 * tens, *dk = buf + 6 * tens, *dv = buf + 7 * tens, *w = buf + 8 * tens;
+    float* lse = reinterpret_cast<float*>(w + ws);            // n * hq floats (2 KB)
+    void* sched = w + ws + 2048;                                 // zeroed, left zero by the kernel
+    for (int hd : {64, 128}) {
+      for (int causal : {0, 1}) {
+        if (rc == UL_OK) rc = sm100_fwd(q, k, v, o, lse, n, 1, hq, hkv, hd, causal, 0.1f, s);
+        if (rc == UL_OK) rc = sm100_fwd(q, k, v, o, lse, n, 1, hq, hkv, hd, causal, 0.1f, s, nullptr, nullptr, 0, 0,
+                                        sched);   // (persistent grid with the dynamic schedule)
+        for (int det : {0, 1})
+          if (rc == UL_OK)
+            rc = sm100_bwd(q, k, v, o, dout, lse, dq, dk, dv, w, ws, n, 1, hq, hkv, hd, causal, 0.1f, 7, det, s);
+      }
+    }
+    if (rc == UL_OK)
+      rc = simt_fwd((const float*)q, (const float*)k, (const float*)v, (float*)o, lse, 64, 1, hq, hkv, 64, 1, 0.1f, s);
+    e = cudaStreamSynchronize(s);
+  }
+  if (s) cudaStreamDestroy(s);
+  cudaFree(buf);
+  cudaGetLastError();
+  if (rc != UL_OK) return rc;
+  if (e != cudaSuccess) return fail(UL_ERR_CUDA, "kernel warm-up: %s", cudaGetErrorString(e));
+  done.fetch_or(bit, std::memory_order_release);
+  return UL_OK;
+}
+
 static int check_attn(int64_t n, int64_t b, int64_t hq, int64_t hkv, int64_t hd, int dtype, int mask) {
   if (mask != UL_MASK_NONE && mask != UL_MASK_CAUSAL)
     return fail(UL_ERR_KERNEL, "kernel supports dense/causal masks only, got mask kind %d", mask);
@@ -82,8 +133,8 @@ int ul_preload_kernels(void) {
   UL_TRY(preload_proj());
   UL_TRY(preload_merge());
   UL_TRY(preload_block());
-
-  return preload_bwd();
+  UL_TRY(preload_bwd());
+  return launch_warmup();
 }
 
 int ul_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int64_t n, int64_t b,

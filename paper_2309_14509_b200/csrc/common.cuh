@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 #include <atomic>
+#include <mutex>
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
@@ -74,12 +75,34 @@ inline int sm_count() {
 }
 
 // Dynamic shared-memory opt-in of `fn` on the CURRENT device.  The attribute
-// is per device context, so it is tracked per device (`done` is one bit per
-// device, owned by the call site).
-inline int smem_opt_in(const void* fn, int bytes, std::atomic<uint64_t>& done) {
+// is per device context, so it is tracked per (kernel, device) in one
+// registry.  The preload functions opt every large-smem kernel in when a
+// group is created: cudaFuncSetAttribute at a kernel's first launch could
+// otherwise run while an in-process rank's flag wait is spinning on a peer
+// the host has not issued yet (observed: the first layer call of a process
+// deadlocked until the wait's timeout).
+struct SmemOptIn {
+  const void* fn = nullptr;
+  std::atomic<uint64_t> mask{0};
+};
+inline std::atomic<uint64_t>& smem_mask(const void* fn) {
+  static SmemOptIn table[64];
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : table) {
+    if (e.fn == fn) return e.mask;
+    if (!e.fn) {
+      e.fn = fn;
+      return e.mask;
+    }
+  }
+  return table[63].mask;   // (not reached: fewer than 64 kernels)
+}
+inline int smem_opt_in(const void* fn, int bytes) {
   int dev = 0;
   UL_CUDA(cudaGetDevice(&dev));
   const uint64_t bit = 1ull << (dev & 63);
+  std::atomic<uint64_t>& done = smem_mask(fn);
   if (done.load(std::memory_order_acquire) & bit) return UL_OK;
   UL_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   done.fetch_or(bit, std::memory_order_release);

@@ -199,6 +199,9 @@ int preload_proj() {
   cudaFuncAttributes a;
   UL_CUDA(cudaFuncGetAttributes(&a, proj::qkv_proj_kernel<false>));
   UL_CUDA(cudaFuncGetAttributes(&a, proj::qkv_proj_kernel<true>));
+  // dynamic shared-memory opt-ins now, not at the first launch (common.cuh)
+  UL_TRY(smem_opt_in((const void*)proj::qkv_proj_kernel<false>, proj::Smem::kBytes));
+  UL_TRY(smem_opt_in((const void*)proj::qkv_proj_kernel<true>, proj::Smem::kBytes));
   return UL_OK;
 }
 
@@ -223,14 +226,13 @@ int sm100_qkv_proj(const void* x, const void* w, int64_t M, int64_t K, int64_t N
   p.mtiles = (int)((M + proj::BM - 1) / proj::BM);
   p.ntiles = (int)((N + proj::BN - 1) / proj::BN);
   p.ep = ep;
-  static std::atomic<uint64_t> attr{0}, attr_t{0};
   const int tiles = p.mtiles * p.ntiles;
   const int grid = tiles < sm_count() ? tiles : sm_count();
   if (w_transposed) {
-    UL_TRY(smem_opt_in((const void*)proj::qkv_proj_kernel<true>, proj::Smem::kBytes, attr_t));
+    UL_TRY(smem_opt_in((const void*)proj::qkv_proj_kernel<true>, proj::Smem::kBytes));
     proj::qkv_proj_kernel<true><<<grid, proj::kThreads, proj::Smem::kBytes, st>>>(mx, mw, p);
   } else {
-    UL_TRY(smem_opt_in((const void*)proj::qkv_proj_kernel<false>, proj::Smem::kBytes, attr));
+    UL_TRY(smem_opt_in((const void*)proj::qkv_proj_kernel<false>, proj::Smem::kBytes));
     proj::qkv_proj_kernel<false><<<grid, proj::kThreads, proj::Smem::kBytes, st>>>(mx, mw, p);
   }
   return launched("qkv_proj_sm100");

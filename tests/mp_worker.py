@@ -37,14 +37,14 @@ def main():
                    ((1, hq), (2, hkv), (3, hkv), (4, hq)))
     sh = lambda x: torch.tensor(x[rank * nl:(rank + 1) * nl], dtype=torch.float32).to(torch.bfloat16).cuda()
     if mode == "pg":
-        layer = U.DistributedAttention(U.FlashAttention("causal"), dist.group.WORLD)
+        layer = U.DistributedAttention(U.FlashAttention("causal"), dist.group.WORLD, adaptive_pipeline=False)
         group = layer.spg
         assert U.DistributedAttention(U.FlashAttention("causal"), dist.group.WORLD).spg is group   # cached wrapper
         group.set_timeout_ms(60000)
     else:
         slot = 64 << 10 if mode == "grow" else 3 * nl * hq * hd * 2 + (1 << 20)
         group = U.SequenceGroup.from_process_group(None, slot_bytes=slot, timeout_ms=60000)
-        layer = U.DistributedAttention(U.FlashAttention("causal"), group)
+        layer = U.DistributedAttention(U.FlashAttention("causal"), group, adaptive_pipeline=False)
     res = {"rank": rank, "device": torch.cuda.current_device()}
     tq, tk, tv = (sh(x).requires_grad_(True) for x in (q, k, v))
     try:

@@ -25,7 +25,7 @@ def _layer(p, q, k, v, do, pipeline, deterministic=True):
     nl = n // p
     groups = U().SequenceGroup.local_group(p, slot_bytes=1 << 20)
     attn = U().FlashAttention("causal", deterministic=deterministic)
-    layers = [U().DistributedAttention(attn, g, pipeline=pipeline) for g in groups]
+    layers = [U().DistributedAttention(attn, g, pipeline=pipeline, adaptive_pipeline=False) for g in groups]
     sh = lambda x, r: to_dev(x[r * nl:(r + 1) * nl], torch.bfloat16).requires_grad_(True)
     ins = run_ranks(groups, lambda r: [sh(x, r) for x in (q, k, v)])
     dos = run_ranks(groups, lambda r: to_dev(do[r * nl:(r + 1) * nl], torch.bfloat16))
@@ -46,6 +46,8 @@ def test_pipelined_equals_unpipelined_bitwise(p, hq, hkv, want):
     o1, g1, groups1 = _layer(p, q, k, v, do, pipeline=1)
     o2, g2, groups2 = _layer(p, q, k, v, do, pipeline=want)
     assert U().attention.pipeline_groups(hq // p, hkv // p, want) > 1
+    # (the default layer would not split a problem this small)
+    assert U().attention.pipeline_groups(hq // p, hkv // p, want, n=n, sms=148) == 1
     assert torch.equal(o1, o2)
     for a, b in zip(g1, g2):
         assert torch.equal(a, b)
