@@ -19,6 +19,9 @@ import os
 import statistics
 import sys
 
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
@@ -43,7 +46,7 @@ def main():
     import paper_2309_14509_b200 as U
 
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_sweep.json"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r2_sweep.json"))
     ap.add_argument("--quick", action="store_true", help="skip the 256K/512K points")
     ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
@@ -89,12 +92,16 @@ def main():
                   for _ in range(P)]
             torch.cuda.synchronize()
             times = []
+            cover = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
             for it in range(1 + args.reps):
                 torch.cuda.synchronize()
+                for _ in range(P):   # keep the GPU busy while the host enqueues every rank
+                    cover.view(torch.int64).sum()
                 evs = []
                 for r in range(P):
                     with torch.cuda.stream(groups[r].stream):
                         a, b = ev(), ev()
+                        groups[r].stream.wait_stream(torch.cuda.current_stream(dev))
                         a.record()
                         groups[r].all_to_all(xs[r], 2, 0)
                         b.record()
@@ -113,8 +120,11 @@ def main():
             # whole layer fwd+bwd: q,k,v,o then dO,dq,dk,dv cross the group once each
             layer_egress = (2 * (Hq + 2 * Hkv) + 2 * Hq) * nl * hd * 2 // P * (P - 1)
             rec["a2a_layer_egress_bytes_per_gpu"] = layer_egress
-            rec["a2a_layer_time_at_770GBs_ms"] = round(layer_egress / 770e9 * 1e3, 3)
-            rec["a2a_layer_share_at_770GBs"] = round(layer_egress / 770e9 * 1e3 / (step_ms + layer_egress / 770e9 * 1e3), 4)
+            # (770 GB/s: the pool's measured B200 peer copy per direction, B200_PROFILING.md --
+            #  not measured by this tool, which has one GPU)
+            rec["a2a_layer_time_at_guide_peer_copy_770GBs_ms"] = round(layer_egress / 770e9 * 1e3, 3)
+            rec["a2a_layer_share_at_guide_peer_copy_770GBs"] = round(
+                layer_egress / 770e9 * 1e3 / (step_ms + layer_egress / 770e9 * 1e3), 4)
             for gr in groups:
                 gr.destroy()
             del xs
