@@ -74,7 +74,7 @@ def make_flush(dev):
 
 
 NCU_PROFILE = os.path.join(ROOT, "profiles", "r2_ncu_full.json")   # tools/ncu_r2_summary.py of the r2 capture
-NCU_NAMES = {"attn_fwd_sm100": "fwd::attn_fwd_h2_kernel<128>", "attn_bwd_dkdv_sm100": "bwd::bwd_dkdv_kernel<128>",
+NCU_NAMES = {"attn_fwd_sm100": "fwd::attn_fwd_persist_kernel<128", "attn_bwd_dkdv_sm100": "bwd::bwd_dkdv_kernel<128>",
              "attn_bwd_dq_sm100": "bwd::bwd_dq_kernel<128>", "attn_bwd_fused_sm100": "bwd::bwd_fused_kernel<128>"}
 
 
@@ -83,7 +83,9 @@ def ncu_traffic(kernel):
     `ncu --set full` capture of the same workload (profiles/), or None."""
     try:
         with open(NCU_PROFILE) as f:
-            d = json.load(f)[NCU_NAMES[kernel]]
+            prof = json.load(f)
+        # (keys are ncu's demangled names; match on the name up to the template arguments given)
+        d = next(v for k_, v in prof.items() if k_.startswith(NCU_NAMES[kernel]))
         if isinstance(d, list):   # (one record per captured launch: the first)
             d = d[0]
         mb = lambda v: float(v.split()[0]) * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3}[v.split()[1]]

@@ -65,6 +65,23 @@ constexpr int NS = 2;               // K/V pipeline stages
 constexpr int kSoftPerTile = 8;
 constexpr int kThreads = 64 + 2 * kSoftPerTile * 32;
 constexpr float kLazy = 8.0f;       // log2 headroom before O is rescaled
+// Full-tile persistent kernel (r2 A/B at config 2 / N = 32K x 4 heads, WPR = 1):
+// split P arrive 0.2662 -> 0.2519 ms with a 1/8 FMA-pipe share; 1/16: 0.249 /
+// 0.905 ms vs the half-unit kernel's 0.267 / 0.996.  The chain softmax(j) ->
+// PV(j) -> S(j+1) of a tile hides under the other tile's 1024 tensor cycles
+// only if the softmax is shorter: its 4096 exponentials per SMSP are exactly
+// 1024 MUFU cycles, so a share goes to the FMA pipe and the first 3/4 of P
+// is handed to the PV MMAs before the last quarter's exponentials run.
+#ifndef UL_FWD_SPLITP
+#define UL_FWD_SPLITP 1
+#endif
+#ifndef UL_FWD_SPLIT_AT
+#define UL_FWD_SPLIT_AT 96
+#endif
+constexpr int kSplitAt = UL_FWD_SPLIT_AT;   // split P arrive: kv columns announced first (multiple of 32)
+#ifndef UL_FWD_FULL_POLY_MASK
+#define UL_FWD_FULL_POLY_MASK 30           // FMA-pipe exp2 on 1/16 of the element pairs (0: none)
+#endif
 constexpr int kAtom = 128 * 128;    // SW128 atom column of a 128-row tile
 constexpr int kMaxTiles = 8192;     // kv tiles per head in blocked-sparse mode (n <= 1M)
 
@@ -157,7 +174,7 @@ constexpr int kH2Sel = UL_FWD_EXP_H2 == 2 ? 2 : 0;
 #ifndef UL_FWD_POLY_MASK
 #define UL_FWD_POLY_MASK 6
 #endif
-template <bool kPoly>
+template <bool kPoly, int kMask = UL_FWD_POLY_MASK>
 __device__ __forceinline__ void exp_chunk(const uint32_t* r, float scale_log2, float mu, uint32_t* pk,
                                           float2* rsum) {
   const float2 sc = make_float2(scale_log2, scale_log2), nm = make_float2(-mu, -mu);
@@ -166,7 +183,7 @@ __device__ __forceinline__ void exp_chunk(const uint32_t* r, float scale_log2, f
     // packed f32x2 FMA / add: half the issue slots of the scalar forms
     const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[x]), __uint_as_float(r[x + 1])), sc, nm);
     float2 e;
-    if (kPoly && (x & UL_FWD_POLY_MASK) == UL_FWD_POLY_MASK) {
+    if (kPoly && (x & kMask) == kMask) {
       e = poly_exp2x2(a);
     } else if (kH2 && (x & 2) == kH2Sel) {
       e = exp2_h2(a);
@@ -567,11 +584,20 @@ __device__ __forceinline__ bool fwd_item_dyn(const Params& p, int k, int& pair, 
   return true;
 }
 
-template <int HD>
-__global__ void __launch_bounds__(kThreads, 1)
+// WPR: softmax warps per query row (2: two warps per TMEM lane quarter, 64
+// of the 128 columns each, row max / sum exchanged through shared memory;
+// 1: one thread per row owning all 128 columns, 10 warps, no exchange)
+template <int WPR>
+constexpr int persist_threads() { return 64 + 2 * 4 * WPR * 32; }
+
+template <int HD, int WPR>
+__global__ void __launch_bounds__(persist_threads<WPR>(), 1)
     attn_fwd_persist_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                             const __grid_constant__ CUtensorMap tmV, const Params p) {
   using S = Smem<HD>;
+  constexpr int kSoft = 4 * WPR;     // softmax warps per query tile
+  constexpr int kC = BN / WPR;       // S columns per softmax thread
+  constexpr int kOC = HD / WPR;      // O columns per softmax thread
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem + S::kQ;
@@ -592,7 +618,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* it_full = bars + 11 + 4 * NS;   // [4] dynamic item ring
   uint64_t* it_empty = bars + 15 + 4 * NS;  // [4]
   volatile int* sitem = reinterpret_cast<volatile int*>(bars + 19 + 4 * NS);
-  static_assert((21 + 4 * NS) * 8 <= 256, "barrier area");
+  // [2] per tile (split P arrive): P of kv columns < kSplitAt stored (and O
+  // rescaled) -- the first six PV K-steps may start while the last 32
+  // columns' exponentials are still running
+  uint64_t* p_part = bars + 21 + 4 * NS;
+  static_assert((23 + 4 * NS) * 8 <= 256, "barrier area");
   auto item = [&](int k, int& pair, int& bh, int role) {
     return p.ctr ? fwd_item_dyn<HD>(p, k, pair, bh, role, it_full, it_empty, sitem) : fwd_item<HD>(p, k, pair, bh);
   };
@@ -615,13 +645,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], kSoftPerTile);
+      mbar_init(&p_full[t], kSoft);
+      mbar_init(&p_part[t], kSoft);
       mbar_init(&o_done[t], 1);
-      mbar_init(&o_free[t], kSoftPerTile);
+      mbar_init(&o_free[t], kSoft);
     }
     for (int s = 0; s < 4; ++s) {
       mbar_init(&it_full[s], 1);
-      mbar_init(&it_empty[s], 1 + 2 * kSoftPerTile);
+      mbar_init(&it_empty[s], 1 + 2 * kSoft);
     }
     fence_barrier_init();
   }
@@ -691,13 +722,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       auto issue_pv = [&](int t, int j, int stage) {
         if (j == 0 && items_t[t] > 0) mbar_wait_mma(&o_free[t], (items_t[t] - 1) & 1);
+        const uint64_t dv = dadd(dV0, stage * S::kTile);
+#if UL_FWD_SPLITP
+        mbar_wait_mma(&p_part[t], cpv[t] & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kSplitAt / 16; ++kk)
+          mma_ts(tbase + 256 + t * HD, tbase + t * 128 + kk * 8, dadd(dv, kk * 2048), kIdPV,
+                 (j > 0 || kk > 0) ? 1u : 0u);
         mbar_wait_mma(&p_full[t], cpv[t] & 1);
         tc_fence_after();
-        const uint64_t dv = dadd(dV0, stage * S::kTile);
+#pragma unroll
+        for (int kk = kSplitAt / 16; kk < BN / 16; ++kk)
+          mma_ts(tbase + 256 + t * HD, tbase + t * 128 + kk * 8, dadd(dv, kk * 2048), kIdPV, 1u);
+#else
+        mbar_wait_mma(&p_full[t], cpv[t] & 1);
+        tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)
           mma_ts(tbase + 256 + t * HD, tbase + t * 128 + kk * 8, dadd(dv, kk * 2048), kIdPV,
                  (j > 0 || kk > 0) ? 1u : 0u);
+#endif
         mma_commit(&o_done[t]);
         ++cpv[t];
       };
@@ -734,9 +779,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     const int idx = warp - 2;
-    const int t = idx >> 3;
+    const int t = idx / kSoft;
     const int quarter = warp & 3;
-    const int half = (idx & 7) >> 2;
+    const int half = (idx % kSoft) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const uint32_t tS = tbase + t * 128 + lane_off;
@@ -753,7 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (my_nkv == 0) continue;
       const int na = item_kv(pair, 0);
       const bool alt_item = p.alt && na > 0 && item_kv(pair, 1) > 0;
-      if (alt_item && t == 1) alt_arrive(9);   // tile A goes first
+      if (alt_item && t == 1) alt_arrive(9, 64 * kSoft);   // tile A goes first
       const int bb = bh / p.hq, h = bh % p.hq;
       const int q0 = (2 * pair + t) * BM;
       const int qrow = q0 + row;
@@ -762,35 +807,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kv0 = j * BN;
         const bool alt = alt_item && j < na;
         mbar_wait(&s_full[t], cs & 1);
+#ifdef UL_FWD_XP_NOSOFT   // (what-if flag: no softmax work at all; results wrong)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&p_part[t]);
+          mbar_arrive(&p_full[t]);
+        }
+        continue;
+#endif
         tc_fence_after();
-        uint32_t r[BN / 2];
-        tmem_ld32(tS + half * 64, r);
-        tmem_ld32(tS + half * 64 + 32, r + 32);
+        uint32_t r[kC];
+#pragma unroll
+        for (int c = 0; c < kC; c += 32) tmem_ld32(tS + half * kC + c, r + c);
         tmem_wait_ld();
         const bool masked = (p.causal && kv0 + BN - 1 > q0) || kv0 + BN > p.n;
         if (masked) {
           int limit = p.n - kv0;
           if (p.causal) limit = min(limit, qrow - kv0 + 1);
-          limit -= half * 64;
+          limit -= half * kC;
 #pragma unroll
-          for (int c = 0; c < BN / 2; ++c)
+          for (int c = 0; c < kC; ++c)
             if (c >= limit) r[c] = __float_as_uint(-INFINITY);
         }
         float mx[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) mx[u] = __uint_as_float(r[u]);
 #pragma unroll
-        for (int c = 8; c < BN / 2; c += 8) {
+        for (int c = 8; c < kC; c += 8) {
 #pragma unroll
           for (int u = 0; u < 8; ++u) mx[u] = fmaxf(mx[u], __uint_as_float(r[c + u]));
         }
-        const float mh =
+        float mh =
             fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(cs & 1, half)), "f"(mh) : "memory");
-        pair_sync();
-        float other;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(xslot(cs & 1, half ^ 1)) : "memory");
-        const float mt = fmaxf(mh, other) * p.scale_log2;
+        if constexpr (WPR == 2) {
+          asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(cs & 1, half)), "f"(mh) : "memory");
+          pair_sync();
+          float other;
+          asm volatile("ld.shared.f32 %0, [%1];" : "=f"(other) : "r"(xslot(cs & 1, half ^ 1)) : "memory");
+          mh = fmaxf(mh, other);
+        }
+        const float mt = mh * p.scale_log2;
         float alpha = 1.f;
         bool rescale = false;
         if (mt > m + kLazy) {
@@ -801,47 +858,70 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mu = (m == -INFINITY) ? 0.f : m;
         float2 rsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                           make_float2(0.f, 0.f)};
-        if (alt) alt_sync(9 + t);   // the other tile's exponentials are done
+        // O holds PV(0..j-1); S(j) completing implies PV(j-1) did (in-order tensor pipe)
+        auto rescale_o = [&]() {
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t pk[16];
-          exp_chunk<false>(r + c * 32, p.scale_log2, mu, pk, rsum);
-          tmem_st16(tS + (2 * half + c) * 16, pk);
-        }
-        if (alt && (t == 0 || j + 1 < na)) alt_arrive(9 + (t ^ 1));
-        const float2 rs = __fadd2_rn(__fadd2_rn(rsum[0], rsum[1]), __fadd2_rn(rsum[2], rsum[3]));
-        l = l * alpha + (rs.x + rs.y);
-        if (__any_sync(0xffffffffu, rescale)) {
-#pragma unroll
-          for (int c = 0; c < HD / 64; ++c) {
+          for (int c = 0; c < kOC / 32; ++c) {
             uint32_t ov[32];
-            tmem_ld32(tO + half * (HD / 2) + c * 32, ov);
+            tmem_ld32(tO + half * kOC + c * 32, ov);
             tmem_wait_ld();
 #pragma unroll
             for (int x = 0; x < 32; ++x) ov[x] = __float_as_uint(__uint_as_float(ov[x]) * alpha);
-            tmem_st32(tO + half * (HD / 2) + c * 32, ov);
+            tmem_st32(tO + half * kOC + c * 32, ov);
           }
+        };
+        // a warp whose rows need O rescaled announces the split only after it
+        // (rare: lazy rescale); the others as soon as P of kv < 96 is stored
+        const bool any_rs = __any_sync(0xffffffffu, rescale);
+        if (alt) alt_sync(9 + t, 64 * kSoft);   // the other tile's exponentials are done
+#pragma unroll
+        for (int c = 0; c < kC; c += 32) {
+          uint32_t pk[16];
+          if (UL_FWD_FULL_POLY_MASK != 0 && !masked)
+            exp_chunk<UL_FWD_FULL_POLY_MASK != 0, UL_FWD_FULL_POLY_MASK>(r + c, p.scale_log2, mu, pk, rsum);
+          else
+            exp_chunk<false>(r + c, p.scale_log2, mu, pk, rsum);
+          tmem_st16(tS + (half * kC + c) / 2, pk);   // P (bf16 pairs) over consumed S columns
+#if UL_FWD_SPLITP
+          // P of kv columns < kSplitAt complete after this chunk: announce it
+          if (!any_rs &&
+              (half * kC + c + 32 == kSplitAt || (half * kC + c + 32 < kSplitAt && c + 32 == kC))) {
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_part[t]);
+          }
+#endif
         }
+        if (alt && (t == 0 || j + 1 < na)) alt_arrive(9 + (t ^ 1), 64 * kSoft);
+        const float2 rs = __fadd2_rn(__fadd2_rn(rsum[0], rsum[1]), __fadd2_rn(rsum[2], rsum[3]));
+        l = l * alpha + (rs.x + rs.y);
+        if (any_rs) rescale_o();
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
+#if UL_FWD_SPLITP
+        if (any_rs && lane == 0) mbar_arrive(&p_part[t]);
+#endif
         if (lane == 0) mbar_arrive(&p_full[t]);
       }
-      asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(2, half)), "f"(l) : "memory");
-      pair_sync();
-      float lo;
-      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lo) : "r"(xslot(2, half ^ 1)) : "memory");
-      pair_sync();   // (the sum slot is rewritten by the next item)
+      float lo = 0.f;
+      if constexpr (WPR == 2) {
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot(2, half)), "f"(l) : "memory");
+        pair_sync();
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(lo) : "r"(xslot(2, half ^ 1)) : "memory");
+        pair_sync();   // (the sum slot is rewritten by the next item)
+      }
       const float lrow = l + lo;
       mbar_wait(&o_done[t], (cs - 1) & 1);
       tc_fence_after();
       const float inv = 1.f / lrow;
       const bool valid = qrow < p.n;
-      uint32_t pkd[HD / 64][16];
+      uint32_t pkd[kOC / 32][16];
 #pragma unroll
-      for (int c = 0; c < HD / 64; ++c) {
+      for (int c = 0; c < kOC / 32; ++c) {
         uint32_t ov[32];
-        tmem_ld32(tO + half * (HD / 2) + c * 32, ov);
+        tmem_ld32(tO + half * kOC + c * 32, ov);
         tmem_wait_ld();
 #pragma unroll
         for (int x = 0; x < 16; ++x)
@@ -852,15 +932,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_free[t]);
       if (valid) {
-        __nv_bfloat16* orow = p.o + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD + half * (HD / 2);
+        __nv_bfloat16* orow = p.o + (((int64_t)qrow * p.b + bb) * p.hq + h) * HD + half * kOC;
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c) {
+        for (int c = 0; c < kOC / 32; ++c) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
           for (int x = 0; x < 4; ++x)
             dst[x] = make_uint4(pkd[c][4 * x], pkd[c][4 * x + 1], pkd[c][4 * x + 2], pkd[c][4 * x + 3]);
           if (p.ep.active) {
-            uint4* pd = reinterpret_cast<uint4*>(peer_row_ptr(p.ep, qrow, bb, p.b, h, HD, 2) + half * HD) + c * 4;
+            uint4* pd = reinterpret_cast<uint4*>(peer_row_ptr(p.ep, qrow, bb, p.b, h, HD, 2) + half * kOC * 2) + c * 4;
 #pragma unroll
             for (int x = 0; x < 4; ++x)
               pd[x] = make_uint4(pkd[c][4 * x], pkd[c][4 * x + 1], pkd[c][4 * x + 2], pkd[c][4 * x + 3]);
@@ -1031,13 +1111,13 @@ __global__ void __launch_bounds__(h2_threads<WPR>(), 1)
           const int s = gk % NS;
           const uint32_t ph = (gk / NS) & 1;
           mbar_wait_prod(&k_empty[s], ph ^ 1);
-          UL_EV(8, gk);
+          UL_EV(13, gk);
           mbar_expect_tx(&k_full[s], BN * HD * 2);
 #pragma unroll
           for (int a = 0; a < HD / 64; ++a)
             tma_load_3d(sK + s * S::kTile + a * kAtom, &tmK, &k_full[s], a * 64, bb * p.hkv + g, j * BN);
           mbar_wait_prod(&v_empty[s], ph ^ 1);
-          UL_EV(9, gk);
+          UL_EV(14, gk);
           mbar_expect_tx(&v_full[s], BN * HD * 2);
 #pragma unroll
           for (int a = 0; a < HD / 64; ++a)
@@ -1102,11 +1182,14 @@ __global__ void __launch_bounds__(h2_threads<WPR>(), 1)
           const int s = (gk + j) % NS;
           const int nu = u + 2;                       // the unit whose S follows PV(u) into the same buffer
           const int sn = (gk + (nu >> 1)) % NS;
+          UL_EV(10, cp[0] + cp[1]);   // (trace builds) loop top of tile A's unit
           if ((u & 1) == 0) {
             mbar_wait_mma(&v_full[s], ((gk + j) / NS) & 1);
+            UL_EV(11, cp[0] + cp[1]);
             if (nu < nU) mbar_wait_mma(&k_full[sn], ((gk + (nu >> 1)) / NS) & 1);
             tc_fence_after();
           }
+          UL_EV(12, cp[0] + cp[1]);   // K / V of the unit landed
           if (u < nU0) issue_pv(0, u, s);
           if (nu < nU0) issue_s(0, nu, sn);
           if (u < nU1) issue_pv(1, u, s);
@@ -1154,9 +1237,15 @@ __global__ void __launch_bounds__(h2_threads<WPR>(), 1)
         const bool alt = alt_item && u < nUa;
         mbar_wait(&s_full[t * 2 + bf], cs[bf] & 1);
         ++cs[bf];
+#ifdef UL_FWD_XP_NOSOFT   // (what-if flag: no softmax work at all -- the MMA / TMA pipeline alone; results wrong)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t * 2 + bf]);
+        continue;
+#endif
         const int ev_i = cs[0] + cs[1] - 1;   // this tile's unit index across items (traces)
         (void)ev_i;
-        if (lane == 0 && (warp == 2 || warp == 10)) UL_EV(warp == 2 ? 4 : 7, ev_i);
+        if (lane == 0 && (warp == 2 || warp == 2 + kSoft)) UL_EV(warp == 2 ? 4 : 7, ev_i);
         tc_fence_after();
         uint32_t r[kC];
 #pragma unroll
@@ -1200,10 +1289,16 @@ __global__ void __launch_bounds__(h2_threads<WPR>(), 1)
         float2 rsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                           make_float2(0.f, 0.f)};
         if (alt) alt_sync(9 + t, 64 * kSoft);       // the other tile's exponentials are done
-        if (lane == 0 && (warp == 2 || warp == 10)) UL_EV(warp == 2 ? 5 : 8, ev_i);
+        if (lane == 0 && (warp == 2 || warp == 2 + kSoft)) UL_EV(warp == 2 ? 5 : 8, ev_i);
 #pragma unroll
         for (int c = 0; c < kC; c += 32) {
           uint32_t pk[16];
+#ifdef UL_FWD_XP_NOEXP   // (what-if flag: TMEM traffic and row max, no exponentials; results wrong)
+#pragma unroll
+          for (int x = 0; x < 16; ++x) pk[x] = r[c + 2 * x] ^ r[c + 2 * x + 1];
+          tmem_st16(tS + bf * kUN + (half * kC + c) / 2, pk);
+          continue;
+#endif
 #ifdef UL_FWD_POLY
           if (!masked) exp_chunk<true>(r + c, p.scale_log2, mu, pk, rsum);
           else
@@ -1232,7 +1327,7 @@ __global__ void __launch_bounds__(h2_threads<WPR>(), 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[t * 2 + bf]);
-        if (lane == 0 && (warp == 2 || warp == 10)) UL_EV(warp == 2 ? 6 : 9, ev_i);
+        if (lane == 0 && (warp == 2 || warp == 2 + kSoft)) UL_EV(warp == 2 ? 6 : 9, ev_i);
       }
       float lo = 0.f;
       if constexpr (WPR == 2) {
@@ -1345,11 +1440,24 @@ static int fwd_wpr() {
   return w;
 }
 
-// UL_FWD_H2=0 in the environment selects the full-tile persistent kernel (A/B)
+// UL_FWD_FULL_WPR=1 / 2: softmax warps per row of the full-tile persistent
+// kernel (default: 1 for hd 128 -- r2: 0.249 vs 0.266 ms at config 2 with the
+// split P arrive; 2 for hd 64)
+static int fwd_full_wpr(int hd) {
+  static const int w = [] {
+    const char* e = getenv("UL_FWD_FULL_WPR");
+    return (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
+  }();
+  return w ? w : (hd == 128 ? 1 : 2);
+}
+
+// UL_FWD_H2=1 in the environment selects the half-unit kernel for hd 128 (A/B;
+// default off since r2: the full-tile kernel with the split P arrive and the
+// FMA-pipe exponential share is 7% faster at config 2, 9% at N = 32K)
 static bool fwd_h2_enabled() {
   static const bool on = [] {
     const char* e = getenv("UL_FWD_H2");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
   return on;
 }
@@ -1414,9 +1522,14 @@ static int launch(const void* q, const void* k, const void* v, void* o, float* l
         }
         return launched("attn_fwd_sm100");
       }
-      UL_TRY(smem_opt_in((const void*)attn_fwd_persist_kernel<HD>, smem));
       const int64_t pgrid = grid < sm_count() ? grid : sm_count();
-      attn_fwd_persist_kernel<HD><<<(unsigned)pgrid, kThreads, smem, st>>>(mq, mk, mv, p);
+      if (fwd_full_wpr(HD) == 1) {
+        UL_TRY(smem_opt_in((const void*)attn_fwd_persist_kernel<HD, 1>, smem));
+        attn_fwd_persist_kernel<HD, 1><<<(unsigned)pgrid, persist_threads<1>(), smem, st>>>(mq, mk, mv, p);
+      } else {
+        UL_TRY(smem_opt_in((const void*)attn_fwd_persist_kernel<HD, 2>, smem));
+        attn_fwd_persist_kernel<HD, 2><<<(unsigned)pgrid, persist_threads<2>(), smem, st>>>(mq, mk, mv, p);
+      }
       return launched("attn_fwd_sm100");
     }
     p.ctr = nullptr;
@@ -1446,15 +1559,19 @@ int preload_fwd() {
   cudaFuncAttributes a;
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_kernel<64>));
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_kernel<128>));
-  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<64>));
-  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<128>));
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<64, 1>));
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<64, 2>));
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<128, 1>));
+  UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_persist_kernel<128, 2>));
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_h2_kernel<128, 1>));
   UL_CUDA(cudaFuncGetAttributes(&a, fwd::attn_fwd_h2_kernel<128, 2>));
   // dynamic shared-memory opt-ins now, not at the first launch (common.cuh)
   UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_kernel<64>, fwd::Smem<64>::kBytes));
   UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_kernel<128>, fwd::Smem<128>::kBytes));
-  UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_persist_kernel<64>, fwd::Smem<64>::kBytes));
-  UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_persist_kernel<128>, fwd::Smem<128>::kBytes));
+  UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_persist_kernel<64, 1>, fwd::Smem<64>::kBytes));
+  UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_persist_kernel<64, 2>, fwd::Smem<64>::kBytes));
+  UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_persist_kernel<128, 1>, fwd::Smem<128>::kBytes));
+  UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_persist_kernel<128, 2>, fwd::Smem<128>::kBytes));
   UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_h2_kernel<128, 1>, fwd::SmemH2<128>::kBytes));
   UL_TRY(smem_opt_in((const void*)fwd::attn_fwd_h2_kernel<128, 2>, fwd::SmemH2<128>::kBytes));
   return UL_OK;

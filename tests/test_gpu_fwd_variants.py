@@ -1,9 +1,10 @@
-"""Every selectable forward kernel stays correct: the default half-unit
-kernel (one softmax thread per row), its two-warps-per-row form
-(UL_FWD_WPR=2), the full-tile persistent kernel (UL_FWD_H2=0) and the
-softmax ping-pong (UL_FWD_ALT=1), each in its own process (the switches are
-read once per process), against the f64 oracle (causal and dense, a ragged
-tail, GQA)."""
+"""Every selectable forward kernel stays correct: the default full-tile
+persistent kernel (one softmax thread per row for hd 128, split P arrive,
+FMA-pipe exponential share), its two-warps-per-row form (UL_FWD_FULL_WPR),
+the half-unit kernel (UL_FWD_H2=1, both WPR forms) and the softmax
+ping-pong (UL_FWD_ALT=1), each in its own process (the switches are read
+once per process), against the f64 oracle (causal and dense, a ragged tail,
+GQA, hd 64 and 128)."""
 
 import json
 import os
@@ -24,22 +25,23 @@ sys.path.insert(0, sys.argv[1])
 import paper_2309_14509_b200 as U
 from oracle import ulysses_oracle as O
 out = {}
-for n, hq, hkv, mask in ((1000, 4, 2, "causal"), (640, 2, 2, "none")):
-    q = O.make_tensor((n, 1, hq, 128), 5, 1, "bfloat16")
-    k = O.make_tensor((n, 1, hkv, 128), 5, 2, "bfloat16")
-    v = O.make_tensor((n, 1, hkv, 128), 5, 3, "bfloat16")
+for n, hq, hkv, mask, hd in ((1000, 4, 2, "causal", 128), (640, 2, 2, "none", 128), (700, 2, 1, "causal", 64)):
+    q = O.make_tensor((n, 1, hq, hd), 5, 1, "bfloat16")
+    k = O.make_tensor((n, 1, hkv, hd), 5, 2, "bfloat16")
+    v = O.make_tensor((n, 1, hkv, hd), 5, 3, "bfloat16")
     dev = lambda x: torch.tensor(x, dtype=torch.float32).to(torch.bfloat16).cuda()
     o, lse = U.FlashAttention(mask).forward_with_lse(dev(q), dev(k), dev(v))
     ref, ref_lse = O.local_attention(q, k, v, mask, exact=False)
     o = o.float().cpu().numpy()
-    out[f"{n}-{mask}"] = {"o": float(np.abs(o - ref).max() / np.abs(ref).max()),
+    out[f"{n}-{mask}-{hd}"] = {"o": float(np.abs(o - ref).max() / np.abs(ref).max()),
                           "lse": float(np.abs(lse.cpu().numpy() - ref_lse).max())}
 print("RESULT " + json.dumps(out))
 """
 
 
-@pytest.mark.parametrize("env", [{}, {"UL_FWD_WPR": "2"}, {"UL_FWD_H2": "0"}, {"UL_FWD_ALT": "1"},
-                                 {"UL_FWD_ALT": "1", "UL_FWD_WPR": "2"}])
+@pytest.mark.parametrize("env", [{}, {"UL_FWD_FULL_WPR": "2"}, {"UL_FWD_FULL_WPR": "1"}, {"UL_FWD_ALT": "1"},
+                                 {"UL_FWD_H2": "1"}, {"UL_FWD_H2": "1", "UL_FWD_WPR": "2"},
+                                 {"UL_FWD_H2": "1", "UL_FWD_ALT": "1"}])
 def test_forward_kernel_variants_vs_oracle(env):
     r = subprocess.run([sys.executable, "-c", CHILD, ROOT], cwd=ROOT, env=dict(os.environ, **env),
                        capture_output=True, text=True, timeout=300)

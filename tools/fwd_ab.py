@@ -1,5 +1,6 @@
 """A/B of the forward kernels (UL_FWD_H2=1 half-unit kernel vs =0 full-tile
-persistent kernel; UL_FWD_ALT=1/0 softmax ping-pong on/off): device time per launch (CUDA events, L2 flushed by a
+persistent kernel; UL_FWD_ALT=1/0 softmax ping-pong on/off; softmax warps per
+row, UL_FWD_WPR / UL_FWD_FULL_WPR): device time per launch (CUDA events, L2 flushed by a
 read before each), TF/s, and max error of O / LSE against a torch fp32
 reference on a few heads.  Each variant runs in its own process (the env
 switch is read once).
@@ -60,7 +61,7 @@ if __name__ == "__main__":
     variants = os.environ.get("AB_VARIANTS", "1:0:2,1:0:1,0:0:2,1:0:2,1:0:1").split(",")
     for var in variants:
         h2, alt, wpr = var.split(":")
-        env = dict(os.environ, UL_FWD_H2=h2, UL_FWD_ALT=alt, UL_FWD_WPR=wpr)
+        env = dict(os.environ, UL_FWD_H2=h2, UL_FWD_ALT=alt, UL_FWD_WPR=wpr, UL_FWD_FULL_WPR=wpr)
         r = subprocess.run([sys.executable, __file__, "--child", str(n), str(h), str(causal)], env=env,
                            capture_output=True, text=True)
         print(r.stdout.strip() or r.stderr[-2000:], flush=True)

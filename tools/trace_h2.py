@@ -47,8 +47,9 @@ assert lib.ul_debug_trace_fwd(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size
 tr = buf.reshape(8, 16, 256).astype(np.int64)
 names = {0: "MMA p_full(A) seen", 1: "MMA PV(A)+S issued", 2: "MMA p_full(B) seen", 3: "MMA PV(B)+S issued",
          4: "A s_full seen", 5: "A exps start", 6: "A p_full arrive (w2, SMSP2)",
-         7: "B s_full seen", 10: "MMA K/V landed (step)", 11: "A arrive w3 (SMSP3)",
-         12: "A arrive w4 (SMSP0, +TMA warp)", 13: "A arrive w5 (SMSP1, +MMA warp)", 14: "A arrive w6 (SMSP2, half 1)"}
+         7: "B s_full seen", 8: "B exps start", 9: "B p_full arrive",
+         10: "MMA loop top", 11: "MMA V landed", 12: "MMA K+V landed"}
+# producer events (indexed by kv tile, not unit): 13 K slot free, 14 V slot free
 for cta in range(2):
     ev = tr[cta]
     t0 = ev[4][U0]
@@ -64,5 +65,6 @@ for cta in range(2):
     med = lambda a, b, sa=0: int(np.median(ev[a][j + sa] - ev[b][j]))
     print(f"  medians: A unit period={med(4, 4, 1)}  A s_full->exps={med(5, 4)} A exps->arrive={med(6, 5)}"
           f"  A arrive->MMA sees={med(0, 6)}  MMA sees->issued={med(1, 0)}  A arrive->next s_full seen={med(4, 6, 1)}")
-    print(f"           A arrivals rel. w2: w3 {med(11, 6)} w4 {med(12, 6)} w5 {med(13, 6)} w6 {med(14, 6)}"
-          f"  last A arrival -> MMA sees: {int(np.median(ev[0][j] - np.max(ev[[6, 11, 12, 13, 14]][:, j], 0)))}")
+    print(f"           B: s_full->exps={med(8, 7)} exps->arrive={med(9, 8)} B arrive->MMA sees={med(2, 9)}"
+          f"  MMA: loop top->K+V landed={med(12, 10)} K+V landed->p_full(A) seen={med(0, 12)}"
+          f"  PV(A) issued->p_full(B) seen={med(2, 1)} PV(B) issued->next loop top={med(10, 3, 1)}")
