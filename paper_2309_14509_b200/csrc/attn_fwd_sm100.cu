@@ -725,12 +725,14 @@ __global__ void __launch_bounds__(persist_threads<WPR>(), 1)
         const uint64_t dv = dadd(dV0, stage * S::kTile);
 #if UL_FWD_SPLITP
         mbar_wait_mma(&p_part[t], cpv[t] & 1);
+        UL_EV(t == 0 ? 0 : 2, cpv[t]);   // (trace) p_part seen
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kSplitAt / 16; ++kk)
           mma_ts(tbase + 256 + t * HD, tbase + t * 128 + kk * 8, dadd(dv, kk * 2048), kIdPV,
                  (j > 0 || kk > 0) ? 1u : 0u);
         mbar_wait_mma(&p_full[t], cpv[t] & 1);
+        UL_EV(t == 0 ? 12 : 13, cpv[t]);   // (trace) p_full seen (after the first K-steps)
         tc_fence_after();
 #pragma unroll
         for (int kk = kSplitAt / 16; kk < BN / 16; ++kk)
@@ -744,6 +746,7 @@ __global__ void __launch_bounds__(persist_threads<WPR>(), 1)
                  (j > 0 || kk > 0) ? 1u : 0u);
 #endif
         mma_commit(&o_done[t]);
+        UL_EV(t == 0 ? 1 : 3, cpv[t]);   // (trace) PV issued
         ++cpv[t];
       };
       int pair, bh, gk = 0;
@@ -760,6 +763,7 @@ __global__ void __launch_bounds__(persist_threads<WPR>(), 1)
         for (int j = 0; j < nkv; ++j) {
           const int s = (gk + j) % NS, s1 = (gk + j + 1) % NS;
           const bool next = j + 1 < nkv;
+          UL_EV(10, gk + j);   // (trace) MMA loop top
           mbar_wait_mma(&v_full[s], ((gk + j) / NS) & 1);
           if (next) mbar_wait_mma(&k_full[s1], ((gk + j + 1) / NS) & 1);
           tc_fence_after();
@@ -807,6 +811,7 @@ __global__ void __launch_bounds__(persist_threads<WPR>(), 1)
         const int kv0 = j * BN;
         const bool alt = alt_item && j < na;
         mbar_wait(&s_full[t], cs & 1);
+        if (lane == 0 && (warp == 2 || warp == 2 + kSoft)) UL_EV(warp == 2 ? 4 : 7, cs);   // (trace) s_full seen
 #ifdef UL_FWD_XP_NOSOFT   // (what-if flag: no softmax work at all; results wrong)
         tc_fence_before();
         __syncwarp();
@@ -873,6 +878,7 @@ __global__ void __launch_bounds__(persist_threads<WPR>(), 1)
         // a warp whose rows need O rescaled announces the split only after it
         // (rare: lazy rescale); the others as soon as P of kv < 96 is stored
         const bool any_rs = __any_sync(0xffffffffu, rescale);
+        if (lane == 0 && (warp == 2 || warp == 2 + kSoft)) UL_EV(warp == 2 ? 5 : 8, cs);   // (trace) exps start
         if (alt) alt_sync(9 + t, 64 * kSoft);   // the other tile's exponentials are done
 #pragma unroll
         for (int c = 0; c < kC; c += 32) {
@@ -890,6 +896,7 @@ __global__ void __launch_bounds__(persist_threads<WPR>(), 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_part[t]);
+            if (lane == 0 && (warp == 2 || warp == 2 + kSoft)) UL_EV(warp == 2 ? 11 : 14, cs);   // (trace) p_part arrive
           }
 #endif
         }
@@ -904,6 +911,7 @@ __global__ void __launch_bounds__(persist_threads<WPR>(), 1)
         if (any_rs && lane == 0) mbar_arrive(&p_part[t]);
 #endif
         if (lane == 0) mbar_arrive(&p_full[t]);
+        if (lane == 0 && (warp == 2 || warp == 2 + kSoft)) UL_EV(warp == 2 ? 6 : 9, cs);   // (trace) p_full arrive
       }
       float lo = 0.f;
       if constexpr (WPR == 2) {
