@@ -1449,14 +1449,16 @@ static int fwd_wpr() {
 }
 
 // UL_FWD_FULL_WPR=1 / 2: softmax warps per row of the full-tile persistent
-// kernel (default: 1 for hd 128 -- r2: 0.249 vs 0.266 ms at config 2 with the
-// split P arrive; 2 for hd 64)
-static int fwd_full_wpr(int hd) {
+// kernel (default 1 -- r2 with the split P arrive: hd 128 config 2 0.250 vs
+// 0.261-0.266 ms, hd 64 32 heads x 8K 0.424 vs 0.438 ms; two warps per row
+// with interleaved 32-column blocks and the split at 64 columns: 0.261 /
+// 0.441, not kept)
+static int fwd_full_wpr(int /*hd*/) {
   static const int w = [] {
     const char* e = getenv("UL_FWD_FULL_WPR");
-    return (e && (e[0] == '1' || e[0] == '2')) ? e[0] - '0' : 0;
+    return (e && e[0] == '2') ? 2 : 1;
   }();
-  return w ? w : (hd == 128 ? 1 : 2);
+  return w;
 }
 
 // UL_FWD_H2=1 in the environment selects the half-unit kernel for hd 128 (A/B;

@@ -82,7 +82,7 @@ if __name__ == "__main__":
     for rnd in range(int(os.environ.get("AB_ROUNDS", "2"))):
         for path in sys.argv[1:]:
             env = dict(os.environ, UL_LIB=os.path.join(os.path.abspath(path), "libulysses_b200.so"))
-            out = subprocess.run([sys.executable, __file__, "--child", str(n), str(H), "128", str(reps)],
+            out = subprocess.run([sys.executable, __file__, "--child", str(n), str(H), os.environ.get("AB_HD", "128"), str(reps)],
                                  env=env, capture_output=True, text=True)
             line = [l for l in out.stdout.splitlines() if l.startswith("RESULT ")]
             print(rnd, os.path.basename(path.rstrip("/")), line[0][7:] if line else out.stderr[-2000:], flush=True)
