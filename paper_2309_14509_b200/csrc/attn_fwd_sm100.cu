@@ -75,6 +75,17 @@ constexpr float kLazy = 8.0f;       // log2 headroom before O is rescaled
 #ifndef UL_FWD_SPLITP
 #define UL_FWD_SPLITP 1
 #endif
+// the full-tile forward's MMA thread waits (UL_FWD_MMA_WAIT: 0 plain try_wait,
+// 2 try_wait with the suspend hint -- the other kernels' default, which the
+// compiler turns into a NANOSLEEP.SYNCS back-off; 3 nanosleep polling).  r2,
+// config 2: 0.2478 / 0.2509-0.2519 / 0.254 ms -- the thread is woken ~400
+// cycles late from the back-off (trace), on the chain p_full -> PV -> S
+#ifndef UL_FWD_MMA_WAIT
+#define UL_FWD_MMA_WAIT 0
+#endif
+__device__ __forceinline__ void mbar_wait_fmma(uint64_t* bar, uint32_t parity) {
+  mbar_wait_k<UL_FWD_MMA_WAIT>(bar, parity);
+}
 #ifndef UL_FWD_SPLIT_AT
 #define UL_FWD_SPLIT_AT 96
 #endif
@@ -721,24 +732,24 @@ __global__ void __launch_bounds__(persist_threads<WPR>(), 1)
         mma_commit(&s_full[t]);
       };
       auto issue_pv = [&](int t, int j, int stage) {
-        if (j == 0 && items_t[t] > 0) mbar_wait_mma(&o_free[t], (items_t[t] - 1) & 1);
+        if (j == 0 && items_t[t] > 0) mbar_wait_fmma(&o_free[t], (items_t[t] - 1) & 1);
         const uint64_t dv = dadd(dV0, stage * S::kTile);
 #if UL_FWD_SPLITP
-        mbar_wait_mma(&p_part[t], cpv[t] & 1);
+        mbar_wait_fmma(&p_part[t], cpv[t] & 1);
         UL_EV(t == 0 ? 0 : 2, cpv[t]);   // (trace) p_part seen
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kSplitAt / 16; ++kk)
           mma_ts(tbase + 256 + t * HD, tbase + t * 128 + kk * 8, dadd(dv, kk * 2048), kIdPV,
                  (j > 0 || kk > 0) ? 1u : 0u);
-        mbar_wait_mma(&p_full[t], cpv[t] & 1);
+        mbar_wait_fmma(&p_full[t], cpv[t] & 1);
         UL_EV(t == 0 ? 12 : 13, cpv[t]);   // (trace) p_full seen (after the first K-steps)
         tc_fence_after();
 #pragma unroll
         for (int kk = kSplitAt / 16; kk < BN / 16; ++kk)
           mma_ts(tbase + 256 + t * HD, tbase + t * 128 + kk * 8, dadd(dv, kk * 2048), kIdPV, 1u);
 #else
-        mbar_wait_mma(&p_full[t], cpv[t] & 1);
+        mbar_wait_fmma(&p_full[t], cpv[t] & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)
@@ -753,8 +764,8 @@ __global__ void __launch_bounds__(persist_threads<WPR>(), 1)
       for (int k = 0; item(k, pair, bh, 1); ++k) {
         const int nT0 = item_kv(pair, 0), nT1 = item_kv(pair, 1);
         const int nkv = max(nT0, nT1);
-        mbar_wait_mma(q_full, k & 1);
-        mbar_wait_mma(&k_full[gk % NS], (gk / NS) & 1);
+        mbar_wait_fmma(q_full, k & 1);
+        mbar_wait_fmma(&k_full[gk % NS], (gk / NS) & 1);
         tc_fence_after();
         if (nT0 > 0) issue_s(0, gk % NS);
         if (nT1 > 0) issue_s(1, gk % NS);
@@ -764,8 +775,8 @@ __global__ void __launch_bounds__(persist_threads<WPR>(), 1)
           const int s = (gk + j) % NS, s1 = (gk + j + 1) % NS;
           const bool next = j + 1 < nkv;
           UL_EV(10, gk + j);   // (trace) MMA loop top
-          mbar_wait_mma(&v_full[s], ((gk + j) / NS) & 1);
-          if (next) mbar_wait_mma(&k_full[s1], ((gk + j + 1) / NS) & 1);
+          mbar_wait_fmma(&v_full[s], ((gk + j) / NS) & 1);
+          if (next) mbar_wait_fmma(&k_full[s1], ((gk + j + 1) / NS) & 1);
           tc_fence_after();
           if (j < nT0) issue_pv(0, j, s);
           if (next && j + 1 < nT0) issue_s(0, s1);
