@@ -267,3 +267,41 @@ def test_fwd_under_cuda_graph_capture(n, hq):
     else:
         assert rel_max_err(to_np(o_g), to_np(o_ref)) <= 1e-2
         assert float((lse_g - lse_ref).abs().max()) <= 1e-2
+
+
+def test_layer_fwd_bwd_under_cuda_graph_capture():
+    # the whole DistributedAttention step (forward + autograd backward, P = 1)
+    # captured in one CUDA graph (tools/graph_step.py): replays equal the
+    # eager step -- O and dK / dV exactly (same kernels, per-tile math), dQ
+    # within the fused kernel's atomic-order rounding
+    n, h, hd = 2048, 4, 128
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    mk = lambda: torch.randn((n, 1, h, hd), generator=g, device="cuda").to(torch.bfloat16)
+    q, k, v, do = mk(), mk(), mk(), mk()
+    layer = U().DistributedAttention(U().FlashAttention("causal"), U().SequenceGroup.single())
+    eq, ek, ev = (x.detach().clone().requires_grad_(True) for x in (q, k, v))
+    o_ref = layer(eq, ek, ev)
+    torch.autograd.backward([o_ref], [do])
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        # fresh leaves: their AccumulateGrad nodes belong to the capture stream
+        cq, ck, cv = (x.detach().clone().requires_grad_(True) for x in (q, k, v))
+        o_w = layer(cq, ck, cv)
+        torch.autograd.backward([o_w], [do])
+        del o_w
+        torch.cuda.synchronize()
+        for t in (cq, ck, cv):
+            t.grad = None
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            o_g = layer(cq, ck, cv)
+            torch.autograd.backward([o_g], [do])
+    torch.cuda.current_stream().wait_stream(side)
+    for _ in range(2):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(o_g, o_ref)
+    assert torch.equal(ck.grad, ek.grad) and torch.equal(cv.grad, ev.grad)
+    assert rel_max_err(to_np(cq.grad), to_np(eq.grad)) <= 1e-2
