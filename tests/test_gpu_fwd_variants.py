@@ -4,7 +4,8 @@ FMA-pipe exponential share), its two-warps-per-row form (UL_FWD_FULL_WPR),
 the half-unit kernel (UL_FWD_H2=1, both WPR forms) and the softmax
 ping-pong (UL_FWD_ALT=1), each in its own process (the switches are read
 once per process), against the f64 oracle (causal and dense, a ragged tail,
-GQA, hd 64 and 128)."""
+GQA, hd 64 and 128, and scores that force the lazy O rescale at almost every
+key tile)."""
 
 import json
 import os
@@ -35,6 +36,21 @@ for n, hq, hkv, mask, hd in ((1000, 4, 2, "causal", 128), (640, 2, 2, "none", 12
     o = o.float().cpu().numpy()
     out[f"{n}-{mask}-{hd}"] = {"o": float(np.abs(o - ref).max() / np.abs(ref).max()),
                           "lse": float(np.abs(lse.cpu().numpy() - ref_lse).max())}
+# scores that grow along the key axis by ~8 log2 units per 128-key tile: the
+# running row max jumps past the lazy-rescale threshold at almost every tile,
+# so O is rescaled (and the split P hand-off waits for it) over and over
+bf = lambda x: torch.tensor(x, dtype=torch.float32).to(torch.bfloat16).double().numpy()
+for n, mask in ((1024, "causal"), (896, "none")):
+    ramp = (1.0 + 4.0 * np.arange(n) / n)[:, None, None, None]
+    q = bf(O.make_tensor((n, 1, 2, 128), 9, 1, "bfloat16") * 0.5 + 1.0)
+    k = bf((O.make_tensor((n, 1, 2, 128), 9, 2, "bfloat16") * 0.5 + 1.0) * ramp)
+    v = bf(O.make_tensor((n, 1, 2, 128), 9, 3, "bfloat16"))
+    dev = lambda x: torch.tensor(x, dtype=torch.float32).to(torch.bfloat16).cuda()
+    o, lse = U.FlashAttention(mask).forward_with_lse(dev(q), dev(k), dev(v))
+    ref, ref_lse = O.local_attention(q, k, v, mask, exact=False)
+    o = o.float().cpu().numpy()
+    out[f"ramp-{n}-{mask}"] = {"o": float(np.abs(o - ref).max() / np.abs(ref).max()),
+                               "lse": float(np.abs(lse.cpu().numpy() - ref_lse).max() / max(1.0, np.abs(ref_lse).max()))}
 print("RESULT " + json.dumps(out))
 """
 
