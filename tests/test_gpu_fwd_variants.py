@@ -26,7 +26,8 @@ sys.path.insert(0, sys.argv[1])
 import paper_2309_14509_b200 as U
 from oracle import ulysses_oracle as O
 out = {}
-for n, hq, hkv, mask, hd in ((1000, 4, 2, "causal", 128), (640, 2, 2, "none", 128), (700, 2, 1, "causal", 64)):
+for n, hq, hkv, mask, hd in ((1000, 4, 2, "causal", 128), (640, 2, 2, "none", 128), (700, 2, 1, "causal", 64),
+                             (1, 1, 1, "causal", 128), (37, 2, 2, "none", 128), (129, 1, 1, "causal", 128)):
     q = O.make_tensor((n, 1, hq, hd), 5, 1, "bfloat16")
     k = O.make_tensor((n, 1, hkv, hd), 5, 2, "bfloat16")
     v = O.make_tensor((n, 1, hkv, hd), 5, 3, "bfloat16")
