@@ -595,9 +595,11 @@ __device__ __forceinline__ bool fwd_item_dyn(const Params& p, int k, int& pair, 
   return true;
 }
 
-// WPR: softmax warps per query row (2: two warps per TMEM lane quarter, 64
-// of the 128 columns each, row max / sum exchanged through shared memory;
-// 1: one thread per row owning all 128 columns, 10 warps, no exchange)
+// WPR: softmax warps per query row (1, the default: one thread per row
+// owning all 128 columns, 10 warps, no exchange; 2: two warps per TMEM lane
+// quarter, 64 of the 128 columns each, row max / sum exchanged through shared
+// memory).  Each tile's softmax hands P to the PV MMAs in two parts (p_part:
+// kv columns < kSplitAt, then p_full) -- see the UL_FWD_SPLITP note above.
 template <int WPR>
 constexpr int persist_threads() { return 64 + 2 * 4 * WPR * 32; }
 
@@ -993,7 +995,8 @@ __global__ void __launch_bounds__(persist_threads<WPR>(), 1)
 }
 
 // ---------------------------------------------------------------------------
-// Half-unit forward (default for hd 128, dense / causal): the persistent
+// Half-unit forward (UL_FWD_H2=1, A/B; the hd-128 default until r2, now
+// slower than the split-P full-tile kernel above): the persistent
 // kernel above with every 128-column K/V tile processed as two 64-column
 // units, each query tile's S region split into two 64-column buffers.
 //
