@@ -121,6 +121,7 @@ print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=Tr
 out = []
 period = float(sys.argv[2])
 idle = os.environ.get("UL_BENCH_CLOCK_IDLE") == "1"   # diagnostics: NVML initialised, no queries
+max_clk = int(os.environ.get("UL_BENCH_CLOCK_SM_SAMPLES", "2"))   # SM-clock queries once the steps are enqueued
 clocks = False
 last_clk, n_clk = -1e9, 0
 while True:
@@ -142,7 +143,7 @@ while True:
         except Exception:
             rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
         mhz = -1
-        if clocks and n_clk < 2:
+        if clocks and n_clk < max_clk:
             mhz = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)   # each query stalls the GPU ~20 us (r90)
             last_clk, n_clk = time.perf_counter(), n_clk + 1
         out.append("%d %d" % (mhz, rs))
